@@ -1,0 +1,124 @@
+// K3 (CUDA-core path): fp32 implicit-GEMM convolution over NHWC views.
+//
+// Numerics follow refiner.py:330-396 (float32 cross-correlation + bias,
+// leaky ReLU 0.01, nearest up2) with fp32 FMA accumulation.  GEMM view:
+// M = output pixels of the window (x batch), N = C_out, K = k*k*C_in.
+// CTA tile 64x64, K step 16, 4x4 register micro-tile per thread; the A
+// tile is gathered im2col-style straight from the (optionally upsampled)
+// input, zero outside the image (padding), the B tile from weights packed
+// [K][C_out].  Used for layers the tensor-core path does not take and as
+// the reference implementation of ts_conv2d.
+#include "conv.cuh"
+#include "ts_common.cuh"
+
+namespace ts {
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16;
+
+__global__ void __launch_bounds__(256)
+conv_simt_kernel(ConvOp op) {
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN];
+  const int tid = threadIdx.x;
+  const int wy = op.oy1 - op.oy0, wx = op.ox1 - op.ox0;
+  const int64_t M = (int64_t)op.batch * wy * wx;
+  const int Cin = op.in.C, Cout = op.out.C;
+  const int K = op.k * op.k * Cin;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
+  const int Hl = op.up2 ? 2 * op.in.H : op.in.H;
+  const int Wl = op.up2 ? 2 * op.in.W : op.in.W;
+
+  // this thread's A-load pixel (fixed across the K loop)
+  const int am = tid & (BM - 1);
+  const int ak = tid >> 6;  // 0..3, rows ak, ak+4, ak+8, ak+12
+  const int64_t gm = m0 + am;
+  const bool mvalid = gm < M;
+  int b = 0, oy = 0, ox = 0;
+  if (mvalid) {
+    b = (int)(gm / ((int64_t)wy * wx));
+    const int r = (int)(gm - (int64_t)b * wy * wx);
+    oy = op.oy0 + r / wx;
+    ox = op.ox0 + r % wx;
+  }
+  const int iy0 = oy * op.stride - op.pad, ix0 = ox * op.stride - op.pad;
+  const float* inb = op.in.base + (int64_t)b * op.in.H * op.in.W * op.in.cstride + op.in.coff;
+
+  const int tx = tid & 15, ty = tid >> 4;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+  for (int k0 = 0; k0 < K; k0 += BK) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int kk = ak + 4 * r;
+      const int k = k0 + kk;
+      float v = 0.f;
+      if (mvalid && k < K) {
+        const int tap = k / Cin, ci = k - tap * Cin;
+        const int ky = tap / op.k, kx = tap - ky * op.k;
+        int iy = iy0 + ky, ix = ix0 + kx;
+        if (iy >= 0 && iy < Hl && ix >= 0 && ix < Wl) {
+          if (op.up2) { iy >>= 1; ix >>= 1; }
+          v = inb[((int64_t)iy * op.in.W + ix) * op.in.cstride + ci];
+        }
+      }
+      As[kk][am] = v;
+    }
+    for (int e = tid; e < BK * BN; e += 256) {
+      const int kk = e / BN, nn = e - kk * BN;
+      const int k = k0 + kk, n = n0 + nn;
+      Bs[kk][nn] = (k < K && n < Cout) ? op.w[(int64_t)k * Cout + n] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[4], bb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bb[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  // epilogue: bias (+ leaky ReLU), scatter to the output window
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t gmo = m0 + ty * 4 + i;
+    if (gmo >= M) continue;
+    const int bo = (int)(gmo / ((int64_t)wy * wx));
+    const int r = (int)(gmo - (int64_t)bo * wy * wx);
+    const int y = op.oy0 + r / wx, x = op.ox0 + r % wx;
+    float* o = op.out.base +
+               (((int64_t)bo * op.out.H + y) * op.out.W + x) * op.out.cstride + op.out.coff;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= Cout) continue;
+      float v = acc[i][j] + op.bias[n];
+      if (op.lrelu) v = v >= 0.f ? v : 0.01f * v;
+      o[n] = v;
+    }
+  }
+}
+
+}  // namespace
+
+int launch_conv_simt(const ConvOp& op, void* stream) {
+  const int64_t M = (int64_t)op.batch * (op.oy1 - op.oy0) * (op.ox1 - op.ox0);
+  if (M <= 0) return TS_OK;
+  dim3 grid((unsigned)ceil_div<int64_t>(M, BM), (unsigned)ceil_div(op.out.C, BN));
+  conv_simt_kernel<<<grid, 256, 0, as_stream(stream)>>>(op);
+  TS_LAUNCH_CHECK();
+  return TS_OK;
+}
+
+}  // namespace ts

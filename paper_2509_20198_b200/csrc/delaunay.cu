@@ -1,0 +1,171 @@
+// K2a: per-patch Delaunay triangulation on the GPU (one warp per patch).
+//
+// Replaces scipy.spatial.Delaunay (Qhull) + _ccw in interpolate_patch
+// (patches.py:316-326).  Incremental Bowyer-Watson: start from the padding
+// square split into two triangles, insert points 0..N-1 in index order.  For
+// each point the warp tests every live triangle's circumcircle in parallel
+// (exact incircle), compacts the cavity with ballots, finds its boundary
+// edges and re-fans them to the new point, reusing the cavity's slots.
+// Exact predicates keep the cavity star-shaped, so the mesh stays valid;
+// an exact duplicate of an earlier point has an empty cavity and is
+// skipped (the lowest index survives as the vertex).
+//
+// Compiled with --fmad=false: the predicate error bounds assume one
+// rounding per operation.
+#include "predicates.cuh"
+#include "ts_common.cuh"
+
+namespace ts {
+namespace {
+
+constexpr int kWarpsPerBlock = 4;
+constexpr int kMaxCavity = 512;
+
+struct PatchPts {
+  const double* xy;
+  int n;
+  __device__ __forceinline__ void get(int v, double& x, double& y) const {
+    if (v < n) { x = xy[2 * v]; y = xy[2 * v + 1]; }
+    else {
+      const int c = v - n;  // (-1,-1), (1,-1), (-1,1), (1,1)
+      x = (c & 1) ? 1.0 : -1.0;
+      y = (c & 2) ? 1.0 : -1.0;
+    }
+  }
+};
+
+__device__ __forceinline__ bool has_edge(const int* t, int a, int b) {
+  return (t[0] == a && t[1] == b) || (t[1] == a && t[2] == b) ||
+         (t[2] == a && t[0] == b);
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+delaunay_kernel(const double* __restrict__ xy_all,
+                const int64_t* __restrict__ pts_off, int n_patches,
+                int32_t* tri_all, int32_t* ntri_out, int32_t* status) {
+  __shared__ int s_bad[kWarpsPerBlock][kMaxCavity];
+  __shared__ int2 s_edge[kWarpsPerBlock][kMaxCavity + 8];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p = blockIdx.x * kWarpsPerBlock + wib;
+  if (p >= n_patches) return;
+  const int64_t off = pts_off[p];
+  const int n = (int)(pts_off[p + 1] - off);
+  int* tri = tri_all + 2 * off + 8 * (int64_t)p;
+  if (n == 0) {
+    if (lane == 0) { ntri_out[p] = 0; status[p] = TS_E_EMPTY_PATCH; }
+    return;
+  }
+  const PatchPts P{xy_all + 2 * off, n};
+  int* bad = s_bad[wib];
+  int2* edge = s_edge[wib];
+  const int cap = 2 * n + 8;
+  if (lane == 0) {
+    tri[0] = n; tri[1] = n + 1; tri[2] = n + 3;
+    tri[3] = n; tri[4] = n + 3; tri[5] = n + 2;
+  }
+  int ntri = 2;
+  int st = TS_OK;
+  __syncwarp();
+  for (int v = 0; v < n; ++v) {
+    double px, py;
+    P.get(v, px, py);
+    // 1. cavity: triangles whose circumcircle strictly contains v
+    int nb = 0;
+    for (int b0 = 0; b0 < ntri; b0 += 32) {
+      const int t = b0 + lane;
+      bool in = false;
+      if (t < ntri) {
+        const int a = tri[3 * t], b = tri[3 * t + 1], c = tri[3 * t + 2];
+        double ax, ay, bx, by, cx, cy;
+        P.get(a, ax, ay);
+        P.get(b, bx, by);
+        P.get(c, cx, cy);
+        in = pred::incircle(ax, ay, bx, by, cx, cy, px, py) > 0;
+      }
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, in);
+      if (in) {
+        const int slot = nb + __popc(m & ((1u << lane) - 1));
+        if (slot < kMaxCavity) bad[slot] = t;
+      }
+      nb += __popc(m);
+    }
+    if (nb == 0) continue;  // exact duplicate of an inserted vertex
+    if (nb > kMaxCavity) { st = TS_E_INVALID; break; }
+    __syncwarp();
+    // 2. boundary edges of the cavity (edges without a bad twin)
+    int ne = 0;
+    for (int e0 = 0; e0 < 3 * nb; e0 += 32) {
+      const int e = e0 + lane;
+      bool keep = false;
+      int u = 0, w = 0;
+      if (e < 3 * nb) {
+        const int i = e / 3, j = e - 3 * i;
+        const int* t = tri + 3 * bad[i];
+        u = t[j];
+        w = t[j == 2 ? 0 : j + 1];
+        keep = true;
+        for (int k = 0; k < nb && keep; ++k)
+          if (k != i && has_edge(tri + 3 * bad[k], w, u)) keep = false;
+        if (keep) {
+          double ux, uy, wx, wy;
+          P.get(u, ux, uy);
+          P.get(w, wx, wy);
+          // v on a hull edge: no zero-area triangle (patches.py:238 would
+          // give it inv_det = 0)
+          if (pred::orient(ux, uy, wx, wy, px, py) == 0) keep = false;
+        }
+      }
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
+      if (keep) {
+        const int slot = ne + __popc(m & ((1u << lane) - 1));
+        if (slot < kMaxCavity + 8) edge[slot] = make_int2(u, w);
+      }
+      ne += __popc(m);
+    }
+    if (ne < nb || ne > kMaxCavity + 8 || ntri + ne - nb > cap) {
+      st = TS_E_INVALID;
+      break;
+    }
+    __syncwarp();
+    // 3. fan the boundary to v: reuse cavity slots, then append
+    for (int i = lane; i < ne; i += 32) {
+      const int slot = i < nb ? bad[i] : ntri + (i - nb);
+      const int2 ed = edge[i];
+      tri[3 * slot] = ed.x;
+      tri[3 * slot + 1] = ed.y;
+      tri[3 * slot + 2] = v;
+    }
+    ntri += ne - nb;
+    __syncwarp();
+  }
+  if (lane == 0) {
+    ntri_out[p] = st == TS_OK ? ntri : 0;
+    status[p] = st;
+  }
+}
+
+}  // namespace
+}  // namespace ts
+
+using namespace ts;
+
+extern "C" int ts_triangulate(const double* d_xy, const int64_t* d_pts_off,
+                              int n_patches, int32_t* d_tri, int32_t* d_ntri,
+                              int32_t* d_status, void* stream) {
+  if (n_patches <= 0) return TS_OK;
+  delaunay_kernel<<<ceil_div(n_patches, kWarpsPerBlock), kWarpsPerBlock * 32, 0,
+                    as_stream(stream)>>>(d_xy, d_pts_off, n_patches, d_tri,
+                                         d_ntri, d_status);
+  TS_LAUNCH_CHECK();
+  return TS_OK;
+}
+
+extern "C" int ts_incircle_sign(const double a[2], const double b[2],
+                                const double c[2], const double d[2]) {
+  return pred::incircle(a[0], a[1], b[0], b[1], c[0], c[1], d[0], d[1]);
+}
+
+extern "C" int ts_orient_sign(const double a[2], const double b[2],
+                              const double c[2]) {
+  return pred::orient(a[0], a[1], b[0], b[1], c[0], c[1]);
+}

@@ -1,0 +1,232 @@
+// LASzip-2 arithmetic decoder + 32-bit IntegerCompressor for chunk tables.
+//
+// Device code (one thread decodes one tile's table).  Follows the
+// published LASzip coder the reference restates in
+// pkg/src/terrascout/lasio/codec.py:43-281 (models, decoder) and
+// :441-484 (IntegerCompressor.decompress, bits=32, bits_high=8).
+// Model state lives in a per-thread scratch pool (global memory) because a
+// table may touch up to 31 corrector models of up to 256 symbols.
+#pragma once
+
+#include <stdint.h>
+
+namespace ts {
+namespace laz {
+
+constexpr uint32_t kMinLen = 0x01000000u;
+constexpr uint32_t kMaxLen = 0xFFFFFFFFu;
+
+struct BitModel {
+  uint32_t c0, n, p0, cyc, left;
+  __device__ void init() { c0 = 1; n = 2; p0 = 1u << 12; cyc = left = 4; }
+  __device__ void update() {
+    n += cyc;
+    if (n >= 8192u) {
+      n = (n + 1) >> 1;
+      c0 = (c0 + 1) >> 1;
+      if (c0 == n) ++n;
+    }
+    p0 = (c0 * (0x80000000u / n)) >> 18;
+    cyc = min((5u * cyc) >> 2, 64u);
+    left = cyc;
+  }
+};
+
+// Adaptive symbol model, decoder flavour (lookup table when n > 16).
+struct SymModel {
+  uint32_t n, tot, cyc, left, tbits, tshift;
+  uint16_t* dist;   // n
+  uint16_t* cnt;    // n
+  uint16_t* table;  // (1 << tbits) + 2, only if tbits
+  __device__ static uint32_t table_bits(uint32_t n) {
+    if (n <= 16) return 0;
+    uint32_t tb = 3;
+    while (n > (1u << (tb + 2))) ++tb;
+    return tb;
+  }
+  __device__ static uint32_t words16(uint32_t n) {
+    uint32_t tb = table_bits(n);
+    return 2 * n + (tb ? (1u << tb) + 2 : 0);
+  }
+  __device__ void init(uint32_t nsym, uint16_t* mem) {
+    n = nsym;
+    tbits = table_bits(n);
+    tshift = tbits ? 15 - tbits : 0;
+    dist = mem;
+    cnt = mem + n;
+    table = tbits ? mem + 2 * n : nullptr;
+    for (uint32_t k = 0; k < n; ++k) cnt[k] = 1;
+    tot = 0;
+    cyc = n;
+    update();
+    cyc = left = (n + 6) >> 1;
+  }
+  __device__ void update() {
+    tot += cyc;
+    if (tot > 32768u) {
+      tot = 0;
+      for (uint32_t k = 0; k < n; ++k) {
+        cnt[k] = (uint16_t)((cnt[k] + 1u) >> 1);
+        tot += cnt[k];
+      }
+    }
+    const uint32_t scale = 0x80000000u / tot;
+    uint32_t acc = 0;
+    if (!tbits) {
+      for (uint32_t k = 0; k < n; ++k) {
+        dist[k] = (uint16_t)((scale * acc) >> 16);
+        acc += cnt[k];
+      }
+    } else {
+      uint32_t s = 0;
+      for (uint32_t k = 0; k < n; ++k) {
+        const uint32_t d = (scale * acc) >> 16;
+        dist[k] = (uint16_t)d;
+        acc += cnt[k];
+        const uint32_t w = d >> tshift;
+        while (s < w) table[++s] = (uint16_t)(k - 1);
+      }
+      table[0] = 0;
+      const uint32_t size = 1u << tbits;
+      while (s <= size) table[++s] = (uint16_t)(n - 1);
+    }
+    cyc = min((5u * cyc) >> 2, (n + 6) << 3);
+    left = cyc;
+  }
+};
+
+struct Decoder {
+  const uint8_t* buf;
+  int64_t pos, end;
+  uint32_t value, length;
+  bool desync;
+
+  __device__ bool start(const uint8_t* b, int64_t p, int64_t e) {
+    buf = b; pos = p; end = e; desync = false;
+    if (pos + 4 > end) { desync = true; return false; }
+    value = ((uint32_t)buf[pos] << 24) | ((uint32_t)buf[pos + 1] << 16) |
+            ((uint32_t)buf[pos + 2] << 8) | (uint32_t)buf[pos + 3];
+    pos += 4;
+    length = kMaxLen;
+    return true;
+  }
+  __device__ void renorm() {
+    while (length < kMinLen) {
+      if (pos >= end) { desync = true; length = kMaxLen; return; }
+      value = (value << 8) | buf[pos++];
+      length <<= 8;
+    }
+  }
+  __device__ uint32_t bit(BitModel& m) {
+    const uint32_t x = m.p0 * (length >> 13);
+    uint32_t s;
+    if (value < x) { s = 0; length = x; ++m.c0; }
+    else { s = 1; value -= x; length -= x; }
+    if (length < kMinLen) renorm();
+    if (--m.left == 0) m.update();
+    return s;
+  }
+  __device__ uint32_t symbol(SymModel& m) {
+    uint32_t hi = length;
+    uint32_t lo, s;
+    const uint32_t unit = length >> 15;
+    length = unit;
+    if (m.tbits) {
+      const uint32_t dv = value / unit;
+      const uint32_t t = dv >> m.tshift;
+      s = m.table[t];
+      uint32_t n = (uint32_t)m.table[t + 1] + 1;
+      while (n > s + 1) {
+        const uint32_t k = (s + n) >> 1;
+        if (m.dist[k] > dv) n = k; else s = k;
+      }
+      lo = m.dist[s] * unit;
+      if (s != m.n - 1) hi = m.dist[s + 1] * unit;
+    } else {
+      lo = 0; s = 0;
+      uint32_t n = m.n, k = n >> 1;
+      do {
+        const uint32_t z = unit * m.dist[k];
+        if (z > value) { n = k; hi = z; } else { s = k; lo = z; }
+        k = (s + n) >> 1;
+      } while (k != s);
+    }
+    value -= lo;
+    length = hi - lo;
+    if (length < kMinLen) renorm();
+    ++m.cnt[s];
+    if (--m.left == 0) m.update();
+    return s;
+  }
+  __device__ uint32_t raw_bits(uint32_t nb) {
+    if (nb > 19) {
+      const uint32_t lo = raw_bits(16);
+      return (raw_bits(nb - 16) << 16) | lo;
+    }
+    length >>= nb;
+    const uint32_t s = value / length;
+    value -= length * s;
+    if (length < kMinLen) renorm();
+    return s;
+  }
+};
+
+// Model pool of one decoding thread: k-models for 2 contexts, the k = 0
+// bit model and corrector models k = 1..31, allocated on first use.
+struct ChunkTableCoder {
+  SymModel kmod[2];
+  bool kmod_live[2];
+  BitModel cbit;
+  bool cbit_live;
+  SymModel cmod[32];
+  bool cmod_live[32];
+  uint16_t* pool;
+  uint32_t used;
+
+  __device__ static uint32_t pool_words() {
+    uint32_t w = 2 * SymModel::words16(33);
+    for (uint32_t k = 1; k < 32; ++k) w += SymModel::words16(1u << (k < 8 ? k : 8));
+    return w;
+  }
+  __device__ void init(uint16_t* mem) {
+    pool = mem; used = 0;
+    kmod_live[0] = kmod_live[1] = false;
+    cbit_live = false;
+    for (int k = 0; k < 32; ++k) cmod_live[k] = false;
+  }
+  __device__ SymModel& alloc(SymModel& m, bool& live, uint32_t n) {
+    if (!live) {
+      m.init(n, pool + used);
+      used += SymModel::words16(n);
+      live = true;
+    }
+    return m;
+  }
+  // IntegerCompressor.decompress(pred, ctx) with 32-bit wraparound.
+  __device__ int32_t decompress(Decoder& d, int32_t pred, int ctx) {
+    const uint32_t k = d.symbol(alloc(kmod[ctx], kmod_live[ctx], 33));
+    int64_t c;
+    if (k == 0) {
+      if (!cbit_live) { cbit.init(); cbit_live = true; }
+      c = d.bit(cbit);
+    } else if (k < 32) {
+      SymModel& m = alloc(cmod[k], cmod_live[k], 1u << (k < 8 ? k : 8));
+      if (k <= 8) {
+        c = d.symbol(m);
+      } else {
+        const uint32_t lowb = k - 8;
+        const uint32_t hi = d.symbol(m);
+        const uint32_t lo = d.raw_bits(lowb);
+        c = ((int64_t)hi << lowb) | lo;
+      }
+      if (c >= (int64_t(1) << (k - 1))) c += 1;
+      else c -= (int64_t(1) << k) - 1;
+    } else {
+      c = -(int64_t)0x80000000LL;
+    }
+    return (int32_t)(uint32_t)((int64_t)pred + c);
+  }
+};
+
+}  // namespace laz
+}  // namespace ts

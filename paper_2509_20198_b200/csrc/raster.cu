@@ -1,0 +1,385 @@
+// K2b: Algorithm 1 rasterisation of one patch per CTA.
+//
+// Replaces interpolate_patch after the triangulation
+// (patches.py:306-405):
+//   * NN raster: exact d^2 = dx*dx + dy*dy argmin over the patch points,
+//     strict '<' so the lowest index wins ties (_nn_assign, :180-199);
+//   * face map: every triangle's clipped cell bbox (_cell_range, :283-287)
+//     is tested with the _TriGeom barycentric formulas and 1e-9 tolerance
+//     (:227-253); the lowest triangle id claims a cell (what the two flood
+//     fill passes :330-349 compute; pinned by test_acceptance.py:165-191);
+//   * padding-triangle blanking (:351-358), barycentric hm/rgb (:360-380),
+//     re-centring on cell [48,48] and the float32 casts (_finish :386-405).
+// Triangles are _ccw-normalised here (:215-224) so Qhull simplices can be
+// fed in as well as ts_triangulate output.  Compiled with --fmad=false and
+// explicit _rn intrinsics: every fp64 op rounds like numpy.
+//
+// Work split: the face map is rasterised over a flattened (triangle, cell)
+// index space so one huge padding triangle does not serialise a thread; the
+// NN search keeps the patch points in shared memory and scans them for
+// four cells at a time.
+#include <cfloat>
+#include <climits>
+
+#include "ts_common.cuh"
+
+namespace ts {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kCells = kRes * kRes;
+constexpr int kSmemPts = 512;          // points cached in shared memory
+constexpr int kSmemTri = 2 * kSmemPts + 8;
+
+struct Tri {
+  int v0, v1, v2;
+};
+
+struct Geo {
+  double ax, ay, abx, aby, acx, acy, inv;
+};
+
+template <typename PT>
+__device__ __forceinline__ void vtx(const PT* xy, int n, int v, double& x,
+                                    double& y) {
+  if (v < n) { x = xy[2 * v]; y = xy[2 * v + 1]; }
+  else {
+    const int c = v - n;
+    x = (c & 1) ? 1.0 : -1.0;
+    y = (c & 2) ? 1.0 : -1.0;
+  }
+}
+
+// _ccw (patches.py:215-224) then _TriGeom (:230-239)
+template <typename PT>
+__device__ __forceinline__ Geo tri_geo(const PT* xy, int n, Tri& t) {
+  double ax, ay, bx, by, cx, cy;
+  vtx(xy, n, t.v0, ax, ay);
+  vtx(xy, n, t.v1, bx, by);
+  vtx(xy, n, t.v2, cx, cy);
+  const double d = dsub(dmul(dsub(bx, ax), dsub(cy, ay)),
+                        dmul(dsub(by, ay), dsub(cx, ax)));
+  if (d < 0.0) {
+    const int tmp = t.v1; t.v1 = t.v2; t.v2 = tmp;
+    double tx = bx, ty = by;
+    bx = cx; by = cy; cx = tx; cy = ty;
+  }
+  Geo g;
+  g.ax = ax; g.ay = ay;
+  g.abx = dsub(bx, ax); g.aby = dsub(by, ay);
+  g.acx = dsub(cx, ax); g.acy = dsub(cy, ay);
+  double det = dsub(dmul(g.abx, g.acy), dmul(g.aby, g.acx));
+  if (det == 0.0) det = INFINITY;  // patches.py:238 -> inv_det = 0
+  g.inv = ddiv(1.0, det);
+  return g;
+}
+
+__device__ __forceinline__ void bary(const Geo& g, double qx, double qy,
+                                     double& w0, double& w1, double& w2) {
+  const double px = dsub(qx, g.ax), py = dsub(qy, g.ay);
+  w1 = dmul(dsub(dmul(px, g.acy), dmul(py, g.acx)), g.inv);
+  w2 = dmul(dsub(dmul(g.abx, py), dmul(g.aby, px)), g.inv);
+  w0 = dsub(dsub(1.0, w1), w2);
+}
+
+__device__ __forceinline__ bool contains(const Geo& g, double qx, double qy) {
+  double w0, w1, w2;
+  bary(g, qx, qy, w0, w1, w2);
+  const double lo = -kBaryTol, hi = 1.0 + kBaryTol;
+  return w0 >= lo && w0 <= hi && w1 >= lo && w1 <= hi && w2 >= lo && w2 <= hi;
+}
+
+// _cell_range (patches.py:283-287) for res = 96
+__device__ __forceinline__ void cell_range(double lo, double hi, int& a, int& b) {
+  const double r = (double)kRes;
+  a = (int)ceil(dsub(ddiv(dmul(dadd(lo, 1.0), r), 2.0), 0.5));
+  b = (int)floor(dsub(ddiv(dmul(dadd(hi, 1.0), r), 2.0), 0.5));
+  a = a < 0 ? 0 : a;
+  b = b > kRes - 1 ? kRes - 1 : b;
+}
+
+struct RasterArgs {
+  const double* xy;
+  const double* h;
+  const float* prgb;
+  const int64_t* pts_off;
+  const int32_t* tri;
+  const int64_t* tri_off;
+  const int32_t* ntri;
+  const double* cz_in;
+  int recenter;
+  float* cnn_in;
+  float* hm_nn;
+  float* hm_lin;
+  float* rgb_nn;
+  float* rgb_lin;
+  int32_t* face;
+  double* cz_out;
+  int32_t* status;
+};
+
+__global__ void __launch_bounds__(kThreads)
+raster_kernel(RasterArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int* s_face = reinterpret_cast<int*>(smem);                       // 9216
+  double* s_xy = reinterpret_cast<double*>(s_face + kCells);        // 2*512
+  double* s_h = s_xy + 2 * kSmemPts;                                // 512
+  int* s_pref = reinterpret_cast<int*>(s_h + kSmemPts);             // 1033
+  uint32_t* s_rng = reinterpret_cast<uint32_t*>(s_pref + kSmemTri + 1);  // 1032
+  __shared__ double s_shift;
+  __shared__ int s_total;
+  __shared__ int s_wsum[kThreads / 32];
+
+  const int p = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int64_t off = A.pts_off[p];
+  const int n = (int)(A.pts_off[p + 1] - off);
+  if (n == 0) {
+    if (tid == 0) {
+      A.status[p] = TS_E_EMPTY_PATCH;
+      if (A.cz_out) A.cz_out[p] = 0.0;
+    }
+    return;
+  }
+  const bool cached = n <= kSmemPts;
+  const double* g_xy = A.xy + 2 * off;
+  const double* g_h = A.h + off;
+  const float* g_rgb = A.prgb ? A.prgb + 3 * off : nullptr;
+  for (int i = tid; i < kCells; i += kThreads) s_face[i] = INT_MAX;
+  if (cached) {
+    for (int i = tid; i < n; i += kThreads) {
+      s_xy[2 * i] = g_xy[2 * i];
+      s_xy[2 * i + 1] = g_xy[2 * i + 1];
+      s_h[i] = g_h[i];
+    }
+  }
+  const double* xy = cached ? s_xy : g_xy;
+  const double* hh = cached ? s_h : g_h;
+  const int T = A.ntri ? A.ntri[p] : 0;
+  const int32_t* tri = A.tri + A.tri_off[p];
+  const bool tri_cached = T <= kSmemTri;
+  __syncthreads();
+
+  // ---- face map: lowest triangle id wins ----
+  if (tri_cached) {
+    // per-triangle clipped cell ranges + flattened work prefix
+    int local = 0;
+    const int per = ceil_div(T, kThreads);
+    const int t0 = tid * per, t1 = min(T, t0 + per);
+    for (int t = t0; t < t1; ++t) {
+      Tri tr{tri[3 * t], tri[3 * t + 1], tri[3 * t + 2]};
+      double x[3], y[3];
+      vtx(xy, n, tr.v0, x[0], y[0]);
+      vtx(xy, n, tr.v1, x[1], y[1]);
+      vtx(xy, n, tr.v2, x[2], y[2]);
+      const double xl = fmax(fmin(fmin(x[0], x[1]), x[2]), -1.0);
+      const double xh = fmin(fmax(fmax(x[0], x[1]), x[2]), 1.0);
+      const double yl = fmax(fmin(fmin(y[0], y[1]), y[2]), -1.0);
+      const double yh = fmin(fmax(fmax(y[0], y[1]), y[2]), 1.0);
+      int gx0, gx1, gy0, gy1;
+      cell_range(xl, xh, gx0, gx1);
+      cell_range(yl, yh, gy0, gy1);
+      int cnt = 0;
+      if (gx1 >= gx0 && gy1 >= gy0) cnt = (gx1 - gx0 + 1) * (gy1 - gy0 + 1);
+      else { gx0 = gy0 = 0; gx1 = gy1 = -1; }
+      s_rng[t] = (uint32_t)gx0 | ((uint32_t)(gx1 - gx0 + 1) << 8) |
+                 ((uint32_t)gy0 << 16);
+      s_pref[t] = cnt;  // temporarily the count
+      local += cnt;
+    }
+    // block exclusive scan of per-thread totals
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if ((tid & 31) >= o) incl += v;
+    }
+    if ((tid & 31) == 31) s_wsum[tid >> 5] = incl;
+    __syncthreads();
+    int wbase = 0;
+    for (int w = 0; w < (tid >> 5); ++w) wbase += s_wsum[w];
+    if (tid == kThreads - 1) s_total = wbase + incl;
+    int run = wbase + incl - local;
+    for (int t = t0; t < t1; ++t) {
+      const int c = s_pref[t];
+      s_pref[t] = run;
+      run += c;
+    }
+    __syncthreads();
+    if (tid == 0) s_pref[T] = s_total;
+    __syncthreads();
+    const int total = s_total;
+    for (int w = tid; w < total; w += kThreads) {
+      int lo = 0, hi = T;  // largest t with s_pref[t] <= w
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_pref[mid] <= w) lo = mid; else hi = mid;
+      }
+      const int t = lo;
+      const uint32_t rg = s_rng[t];
+      const int width = (rg >> 8) & 0xFF;
+      const int k = w - s_pref[t];
+      const int gy = (int)(rg >> 16) + k / width;
+      const int gx = (int)(rg & 0xFF) + k % width;
+      Tri tr{tri[3 * t], tri[3 * t + 1], tri[3 * t + 2]};
+      const Geo g = tri_geo(xy, n, tr);
+      if (contains(g, cell_center(gx, kRes), cell_center(gy, kRes)))
+        atomicMin(&s_face[gy * kRes + gx], t);
+    }
+  } else {
+    for (int t = tid; t < T; t += kThreads) {
+      Tri tr{tri[3 * t], tri[3 * t + 1], tri[3 * t + 2]};
+      double x[3], y[3];
+      vtx(xy, n, tr.v0, x[0], y[0]);
+      vtx(xy, n, tr.v1, x[1], y[1]);
+      vtx(xy, n, tr.v2, x[2], y[2]);
+      int gx0, gx1, gy0, gy1;
+      cell_range(fmax(fmin(fmin(x[0], x[1]), x[2]), -1.0),
+                 fmin(fmax(fmax(x[0], x[1]), x[2]), 1.0), gx0, gx1);
+      cell_range(fmax(fmin(fmin(y[0], y[1]), y[2]), -1.0),
+                 fmin(fmax(fmax(y[0], y[1]), y[2]), 1.0), gy0, gy1);
+      const Geo g = tri_geo(xy, n, tr);
+      for (int gy = gy0; gy <= gy1; ++gy)
+        for (int gx = gx0; gx <= gx1; ++gx)
+          if (contains(g, cell_center(gx, kRes), cell_center(gy, kRes)))
+            atomicMin(&s_face[gy * kRes + gx], t);
+    }
+  }
+  __syncthreads();
+
+  // ---- per-cell values ----
+  auto cell_value = [&](int j, int nn, double& hl, double* rl, int& f) {
+    f = s_face[j];
+    hl = hh[nn];
+    if (g_rgb) {
+      rl[0] = g_rgb[3 * nn]; rl[1] = g_rgb[3 * nn + 1]; rl[2] = g_rgb[3 * nn + 2];
+    }
+    if (f == INT_MAX) { f = -1; return; }
+    Tri tr{tri[3 * f], tri[3 * f + 1], tri[3 * f + 2]};
+    const Geo g = tri_geo(xy, n, tr);
+    if (tr.v0 >= n || tr.v1 >= n || tr.v2 >= n) { f = -1; return; }
+    double w0, w1, w2;
+    bary(g, cell_center(j % kRes, kRes), cell_center(j / kRes, kRes), w0, w1, w2);
+    hl = dadd(dadd(dmul(w0, hh[tr.v0]), dmul(w1, hh[tr.v1])), dmul(w2, hh[tr.v2]));
+    if (g_rgb) {
+      for (int c = 0; c < 3; ++c)
+        rl[c] = dadd(dadd(dmul(w0, (double)g_rgb[3 * tr.v0 + c]),
+                          dmul(w1, (double)g_rgb[3 * tr.v1 + c])),
+                     dmul(w2, (double)g_rgb[3 * tr.v2 + c]));
+    }
+  };
+  auto nn_of = [&](double qx, double qy) {
+    double best = DBL_MAX;
+    int bi = 0;
+    for (int i = 0; i < n; ++i) {
+      const double dx = dsub(qx, xy[2 * i]), dy = dsub(qy, xy[2 * i + 1]);
+      const double d2 = dadd(dmul(dx, dx), dmul(dy, dy));
+      if (d2 < best) { best = d2; bi = i; }
+    }
+    return bi;
+  };
+
+  if (tid == 0) {
+    double shift = 0.0;
+    if (A.recenter) {
+      const int j = (kRes / 2) * kRes + kRes / 2;
+      double hl, rl[3];
+      int f;
+      cell_value(j, nn_of(cell_center(kRes / 2, kRes), cell_center(kRes / 2, kRes)),
+                 hl, rl, f);
+      shift = hl;
+    }
+    s_shift = shift;
+    if (A.cz_out)
+      A.cz_out[p] = A.recenter ? dadd(A.cz_in[p], dmul(shift, kRadius)) : A.cz_in[p];
+    A.status[p] = TS_OK;
+  }
+  __syncthreads();
+  const double shift = s_shift;
+
+  for (int j0 = tid; j0 < kCells; j0 += 4 * kThreads) {
+    int jj[4], bi[4];
+    double qx[4], qy[4], best[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      jj[u] = min(j0 + u * kThreads, kCells - 1);
+      qx[u] = cell_center(jj[u] % kRes, kRes);
+      qy[u] = cell_center(jj[u] / kRes, kRes);
+      best[u] = DBL_MAX;
+      bi[u] = 0;
+    }
+    for (int i = 0; i < n; ++i) {
+      const double px = xy[2 * i], py = xy[2 * i + 1];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double dx = dsub(qx[u], px), dy = dsub(qy[u], py);
+        const double d2 = dadd(dmul(dx, dx), dmul(dy, dy));
+        if (d2 < best[u]) { best[u] = d2; bi[u] = i; }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u * kThreads;
+      if (j >= kCells) continue;
+      double hl, rl[3] = {0.0, 0.0, 0.0};
+      int f;
+      cell_value(j, bi[u], hl, rl, f);
+      const float fnn = __double2float_rn(dsub(hh[bi[u]], shift));
+      const float flin = __double2float_rn(dsub(hl, shift));
+      float rn[3] = {0.f, 0.f, 0.f}, rli[3] = {0.f, 0.f, 0.f};
+      if (g_rgb) {
+        for (int c = 0; c < 3; ++c) {
+          rn[c] = g_rgb[3 * bi[u] + c];
+          rli[c] = __double2float_rn(rl[c]);
+        }
+      }
+      const int64_t o = (int64_t)p * kCells + j;
+      if (A.cnn_in) {
+        float4* d = reinterpret_cast<float4*>(A.cnn_in + 8 * o);
+        d[0] = make_float4(fnn, flin, rn[0], rn[1]);
+        d[1] = make_float4(rn[2], rli[0], rli[1], rli[2]);
+      }
+      if (A.hm_nn) A.hm_nn[o] = fnn;
+      if (A.hm_lin) A.hm_lin[o] = flin;
+      if (A.face) A.face[o] = f;
+      if (g_rgb && A.rgb_nn) {
+        A.rgb_nn[3 * o] = rn[0]; A.rgb_nn[3 * o + 1] = rn[1]; A.rgb_nn[3 * o + 2] = rn[2];
+      }
+      if (g_rgb && A.rgb_lin) {
+        A.rgb_lin[3 * o] = rli[0]; A.rgb_lin[3 * o + 1] = rli[1];
+        A.rgb_lin[3 * o + 2] = rli[2];
+      }
+    }
+  }
+}
+
+constexpr size_t kRasterSmem = sizeof(int) * kCells + sizeof(double) * 3 * kSmemPts +
+                               sizeof(int) * (kSmemTri + 1) + sizeof(uint32_t) * kSmemTri;
+
+}  // namespace
+}  // namespace ts
+
+using namespace ts;
+
+extern "C" int ts_raster(const double* d_xy, const double* d_h, const float* d_prgb,
+                         const int64_t* d_pts_off, const int32_t* d_tri,
+                         const int64_t* d_tri_off, const int32_t* d_ntri,
+                         const double* d_cz_in, int n_patches, int recenter,
+                         float* d_cnn_in, float* d_hm_nn, float* d_hm_lin,
+                         float* d_rgb_nn, float* d_rgb_lin, int32_t* d_face,
+                         double* d_cz_out, int32_t* d_status, void* stream) {
+  if (n_patches <= 0) return TS_OK;
+  static bool configured = false;
+  if (!configured) {
+    TS_CUDA_TRY(cudaFuncSetAttribute(raster_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kRasterSmem));
+    configured = true;
+  }
+  RasterArgs a{d_xy, d_h, d_prgb, d_pts_off, d_tri, d_tri_off, d_ntri, d_cz_in,
+               recenter, d_cnn_in, d_hm_nn, d_hm_lin, d_rgb_nn, d_rgb_lin, d_face,
+               d_cz_out, d_status};
+  raster_kernel<<<n_patches, kThreads, kRasterSmem, as_stream(stream)>>>(a);
+  TS_LAUNCH_CHECK();
+  return TS_OK;
+}

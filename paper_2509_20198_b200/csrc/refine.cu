@@ -1,0 +1,603 @@
+// K3: refiner CNN -- weight bundle, execution plan and refine epilogue.
+//
+//   ts_weights_create  <- load_weights + ArchDescriptor.from_text/validate +
+//                         WeightBundle.validate (refiner.py:92-311)
+//   ts_refine          <- refine_batch (refiner.py:475-528) / _Forward.run
+//                         (refiner.py:430-441)
+//   ts_conv2d          <- conv2d / _conv_batched (refiner.py:330-388)
+//
+// The topology is the reference's fixed one (4 encoders -> concat -> merge
+// -> two decoders -> concat with the 8 raw input channels -> fuse -> crop);
+// the descriptor fixes the layer sizes.  Activations are NHWC float32.
+// Execution is crop-aware: the needed window of every layer is propagated
+// backwards from the 64x64 crop, so decoder/fuse layers compute only the
+// rows/columns that reach the crop (2.28 vs 3.59 GFLOP per tile for the
+// default descriptor); results on the crop are unchanged.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "conv.cuh"
+#include "ts_common.cuh"
+
+namespace ts {
+
+int launch_conv_tc(const ConvOp& op, int precision, void* stream);
+bool conv_tc_supported(const ConvOp& op, int precision);
+
+namespace {
+
+const char* kStages[8] = {"enc_hm_nn", "enc_hm_lin", "enc_rgb_nn", "enc_rgb_lin",
+                          "merge", "dec_height", "dec_color", "fuse"};
+
+struct LayerDesc {
+  bool up2 = false;
+  int ci = 0, co = 0, k = 0, s = 1, p = 0;
+  bool lrelu = false;
+};
+
+struct Win {
+  int y0, y1, x0, x1;
+};
+
+struct ConvLayer {
+  int stage;            // index into kStages
+  int index;            // position inside the stage's layer list
+  bool up2;             // preceded by an Upsample2
+  LayerDesc d;
+  int Hin, Win_, Hout, Wout;  // physical input dims, output dims
+  Win out_win;
+  float* w = nullptr;   // device [K][Cout]
+  float* b = nullptr;   // device [Cout]
+  size_t out_off = 0;   // workspace offset (floats) of the output buffer
+  int out_cstride = 0, out_coff = 0;
+  int in_src = -1;      // -1: external/concat buffers handled by the planner
+};
+
+}  // namespace
+}  // namespace ts
+
+struct ts_weights {
+  bool identity = false;
+  int precision = 0;
+  std::vector<ts::ConvLayer> layers;
+  // per-tile float counts of the planner's buffers
+  size_t cat_floats = 0, fuse_in_floats = 0, per_tile_floats = 0;
+  int enc_out_c = 0, dec_h_c = 0, dec_c_c = 0, fuse_in_c = 0;
+  int enc_hw = 0;
+  size_t cat_off = 0, fuse_in_off = 0;
+  std::vector<void*> device_allocs;
+};
+
+namespace ts {
+namespace {
+
+int parse_descriptor(const std::string& text, bool& identity,
+                     std::map<std::string, std::vector<LayerDesc>>& stages,
+                     long long& declared) {
+  std::vector<std::string> lines;
+  std::istringstream is(text);
+  std::string ln;
+  while (std::getline(is, ln)) {
+    if (!ln.empty() && ln[0] == '#') continue;
+    size_t a = ln.find_first_not_of(" \t\r\n");
+    if (a == std::string::npos) continue;
+    size_t b = ln.find_last_not_of(" \t\r\n");
+    lines.push_back(ln.substr(a, b - a + 1));
+  }
+  if (lines.empty() || lines[0].rfind("arch ", 0) != 0) return TS_E_SHAPE;
+  if (lines[0] != "arch 1") return TS_E_VERSION;
+  identity = lines.size() > 1 && lines[1] == "identity";
+  declared = -1;
+  if (identity) return TS_OK;
+  std::vector<LayerDesc>* cur = nullptr;
+  bool pending_up = false;
+  for (size_t i = 1; i < lines.size(); ++i) {
+    std::istringstream ls(lines[i]);
+    std::string kw;
+    ls >> kw;
+    if (kw == "params") {
+      ls >> declared;
+    } else if (kw == "stage") {
+      std::string name;
+      ls >> name;
+      cur = &stages[name];
+      pending_up = false;
+    } else if (kw == "up2") {
+      if (!cur || pending_up) return TS_E_SHAPE;
+      pending_up = true;
+    } else if (kw == "conv") {
+      if (!cur) return TS_E_SHAPE;
+      LayerDesc d;
+      std::string act;
+      ls >> d.ci >> d.co >> d.k >> d.s >> d.p >> act;
+      if (ls.fail()) return TS_E_SHAPE;
+      d.up2 = pending_up;
+      d.lrelu = act == "lrelu";
+      pending_up = false;
+      cur->push_back(d);
+    } else {
+      return TS_E_SHAPE;
+    }
+  }
+  if (pending_up) return TS_E_SHAPE;
+  return TS_OK;
+}
+
+int conv_out(int n, const LayerDesc& d) {
+  const int nl = d.up2 ? 2 * n : n;
+  return (nl + 2 * d.p - d.k) / d.s + 1;
+}
+
+// input window needed (physical coords) for an output window
+Win need_in(const Win& o, const LayerDesc& d, int Hin, int Win_) {
+  const int Hl = d.up2 ? 2 * Hin : Hin, Wl = d.up2 ? 2 * Win_ : Win_;
+  Win w;
+  w.y0 = std::max(0, o.y0 * d.s - d.p);
+  w.y1 = std::min(Hl, (o.y1 - 1) * d.s - d.p + d.k);
+  w.x0 = std::max(0, o.x0 * d.s - d.p);
+  w.x1 = std::min(Wl, (o.x1 - 1) * d.s - d.p + d.k);
+  if (d.up2) {
+    w.y0 >>= 1; w.x0 >>= 1;
+    w.y1 = ((w.y1 - 1) >> 1) + 1;
+    w.x1 = ((w.x1 - 1) >> 1) + 1;
+  }
+  return w;
+}
+
+Win unite(const Win& a, const Win& b) {
+  return Win{std::min(a.y0, b.y0), std::max(a.y1, b.y1), std::min(a.x0, b.x0),
+             std::max(a.x1, b.x1)};
+}
+
+__global__ void copy_inputs_kernel(const float* __restrict__ in, int64_t pixels,
+                                   float* __restrict__ out, int cstride) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pixels;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4* s = reinterpret_cast<const float4*>(in + 8 * i);
+    float4* d = reinterpret_cast<float4*>(out + (int64_t)cstride * i);
+    d[0] = s[0];
+    d[1] = s[1];
+  }
+}
+
+// Crop, denormalise, clamp and the non-finite fallback (refiner.py:491-527).
+__global__ void __launch_bounds__(256)
+refine_epilogue_kernel(const float* __restrict__ fused, int fcs, int identity,
+                       const float* __restrict__ in, float* __restrict__ out,
+                       uint8_t* __restrict__ nonfinite) {
+  const int b = blockIdx.x;
+  const float* F = fused + (int64_t)b * kRes * kRes * fcs;
+  const float* I = in + (int64_t)b * kRes * kRes * 8;
+  int bad = 0;
+  if (!identity) {
+    for (int i = threadIdx.x; i < kOut * kOut; i += blockDim.x) {
+      const int y = i / kOut + kCrop, x = i % kOut + kCrop;
+      const float* v = F + ((int64_t)y * kRes + x) * fcs;
+      bad |= !(isfinite(v[0]) && isfinite(v[1]) && isfinite(v[2]) && isfinite(v[3]));
+    }
+  }
+  bad = __syncthreads_or(bad);
+  for (int i = threadIdx.x; i < kOut * kOut; i += blockDim.x) {
+    const int y = i / kOut + kCrop, x = i % kOut + kCrop;
+    const float* src = I + ((int64_t)y * kRes + x) * 8;
+    float4 o;
+    if (identity || bad) {
+      o.x = src[1] * 480.0f;
+      o.y = src[5]; o.z = src[6]; o.w = src[7];
+      if (identity) {
+        o.y = fminf(fmaxf(o.y, 0.f), 1.f);
+        o.z = fminf(fmaxf(o.z, 0.f), 1.f);
+        o.w = fminf(fmaxf(o.w, 0.f), 1.f);
+      }
+    } else {
+      const float* v = F + ((int64_t)y * kRes + x) * fcs;
+      o.x = v[0] * 480.0f;
+      o.y = fminf(fmaxf(v[1], 0.f), 1.f);
+      o.z = fminf(fmaxf(v[2], 0.f), 1.f);
+      o.w = fminf(fmaxf(v[3], 0.f), 1.f);
+    }
+    reinterpret_cast<float4*>(out)[(int64_t)b * kOut * kOut + i] = o;
+  }
+  if (threadIdx.x == 0 && nonfinite) nonfinite[b] = (uint8_t)(bad && !identity);
+}
+
+struct Blob {
+  const uint8_t* p;
+  size_t n, off = 0;
+  bool ok = true;
+  template <typename T>
+  T get() {
+    T v{};
+    if (off + sizeof(T) > n) { ok = false; return v; }
+    memcpy(&v, p + off, sizeof(T));
+    off += sizeof(T);
+    return v;
+  }
+};
+
+constexpr int kSubBatch = 1024;
+
+int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
+               std::map<std::string, std::pair<std::vector<int>, std::vector<float>>>& tensors) {
+  for (const char* s : kStages)
+    if (!st.count(s) || st[s].empty()) return TS_E_SHAPE;
+  const int enc_in[4] = {1, 1, 3, 3};
+  // spatial forward pass + channel checks (ArchDescriptor.validate)
+  int enc_hw = -1, enc_c = 0;
+  for (int e = 0; e < 4; ++e) {
+    auto& L = st[kStages[e]];
+    if (L[0].ci != enc_in[e]) return TS_E_SHAPE;
+    int hw = kRes, c = enc_in[e];
+    for (auto& d : L) {
+      if (d.ci != c) return TS_E_SHAPE;
+      hw = conv_out(hw, d);
+      c = d.co;
+    }
+    if (enc_hw >= 0 && hw != enc_hw) return TS_E_SHAPE;
+    enc_hw = hw;
+    enc_c += c;
+  }
+  int hw = enc_hw, c = enc_c;
+  for (auto& d : st["merge"]) {
+    if (d.ci != c) return TS_E_SHAPE;
+    hw = conv_out(hw, d);
+    c = d.co;
+  }
+  const int merge_hw = hw, merge_c = c;
+  int dec_c_out[2];
+  for (int k = 0; k < 2; ++k) {
+    int h2 = merge_hw, c2 = merge_c;
+    for (auto& d : st[kStages[5 + k]]) {
+      if (d.ci != c2) return TS_E_SHAPE;
+      h2 = conv_out(h2, d);
+      c2 = d.co;
+    }
+    if (h2 != kRes) return TS_E_SHAPE;
+    dec_c_out[k] = c2;
+  }
+  const int fin = 8 + dec_c_out[0] + dec_c_out[1];
+  c = fin;
+  hw = kRes;
+  for (auto& d : st["fuse"]) {
+    if (d.ci != c) return TS_E_SHAPE;
+    hw = conv_out(hw, d);
+    c = d.co;
+  }
+  if (c != 4 || hw != kRes) return TS_E_SHAPE;
+  W->enc_out_c = enc_c;
+  W->dec_h_c = dec_c_out[0];
+  W->dec_c_c = dec_c_out[1];
+  W->fuse_in_c = fin;
+  W->enc_hw = enc_hw;
+
+  // ---- layers in execution order with physical dims ----
+  std::vector<ConvLayer> layers;
+  auto add_stage = [&](int s, int Hin) {
+    int h = Hin, li = 0;
+    for (auto& d : st[kStages[s]]) {
+      if (d.up2) ++li;  // the Upsample2 entry occupies a layer index
+      ConvLayer L;
+      L.stage = s;
+      L.index = li++;
+      L.up2 = d.up2;
+      L.d = d;
+      L.Hin = h; L.Win_ = h;
+      L.Hout = conv_out(h, d); L.Wout = L.Hout;
+      h = L.Hout;
+      layers.push_back(L);
+    }
+  };
+  for (int s = 0; s < 4; ++s) add_stage(s, kRes);
+  add_stage(4, enc_hw);
+  add_stage(5, merge_hw);
+  add_stage(6, merge_hw);
+  add_stage(7, kRes);
+
+  // ---- backward window propagation from the crop ----
+  const int nL = (int)layers.size();
+  std::vector<int> stage_first(8, -1), stage_last(8, -1);
+  for (int i = 0; i < nL; ++i) {
+    if (stage_first[layers[i].stage] < 0) stage_first[layers[i].stage] = i;
+    stage_last[layers[i].stage] = i;
+  }
+  auto back = [&](int s, Win w) {  // returns needed window of the stage input
+    for (int i = stage_last[s]; i >= stage_first[s]; --i) {
+      layers[i].out_win = w;
+      w = need_in(w, layers[i].d, layers[i].Hin, layers[i].Win_);
+    }
+    return w;
+  };
+  Win crop{kCrop, kCrop + kOut, kCrop, kCrop + kOut};
+  const Win fuse_in_need = back(7, crop);
+  Win merge_need = unite(back(5, fuse_in_need), back(6, fuse_in_need));
+  Win enc_need = back(4, merge_need);
+  for (int s = 0; s < 4; ++s) back(s, enc_need);
+
+  // ---- weights upload + buffer offsets (floats per tile) ----
+  size_t off = 0;
+  auto alloc = [&](size_t floats) {
+    const size_t o = off;
+    off += (floats + 63) & ~size_t(63);
+    return o;
+  };
+  W->cat_off = alloc((size_t)enc_hw * enc_hw * enc_c);
+  W->fuse_in_off = alloc((size_t)kRes * kRes * fin);
+  int enc_coff = 0;
+  size_t params = 0;
+  for (int i = 0; i < nL; ++i) {
+    ConvLayer& L = layers[i];
+    const bool last = i == stage_last[L.stage];
+    if (L.stage < 4 && last) {
+      L.out_off = W->cat_off; L.out_cstride = enc_c; L.out_coff = enc_coff;
+      enc_coff += L.d.co;
+    } else if ((L.stage == 5 || L.stage == 6) && last) {
+      L.out_off = W->fuse_in_off; L.out_cstride = fin;
+      L.out_coff = L.stage == 5 ? 8 : 8 + dec_c_out[0];
+    } else {
+      L.out_off = alloc((size_t)L.Hout * L.Wout * L.d.co);
+      L.out_cstride = L.d.co; L.out_coff = 0;
+    }
+    const std::string base = std::string(kStages[L.stage]) + "." + std::to_string(L.index);
+    auto wi = tensors.find(base + ".weight");
+    auto bi = tensors.find(base + ".bias");
+    if (wi == tensors.end() || bi == tensors.end()) return TS_E_SHAPE;
+    const auto& ws = wi->second.first;
+    if (ws.size() != 4 || ws[0] != L.d.co || ws[1] != L.d.ci || ws[2] != L.d.k ||
+        ws[3] != L.d.k)
+      return TS_E_SHAPE;
+    if (bi->second.first.size() != 1 || bi->second.first[0] != L.d.co) return TS_E_SHAPE;
+    const int K = L.d.k * L.d.k * L.d.ci, Co = L.d.co;
+    std::vector<float> packed((size_t)K * Co);
+    const std::vector<float>& src = wi->second.second;
+    for (int o = 0; o < Co; ++o)
+      for (int ci = 0; ci < L.d.ci; ++ci)
+        for (int ky = 0; ky < L.d.k; ++ky)
+          for (int kx = 0; kx < L.d.k; ++kx)
+            packed[(size_t)((ky * L.d.k + kx) * L.d.ci + ci) * Co + o] =
+                src[(((size_t)o * L.d.ci + ci) * L.d.k + ky) * L.d.k + kx];
+    params += packed.size() + Co;
+    TS_CUDA_TRY(cudaMalloc(&L.w, packed.size() * sizeof(float)));
+    TS_CUDA_TRY(cudaMalloc(&L.b, Co * sizeof(float)));
+    W->device_allocs.push_back(L.w);
+    W->device_allocs.push_back(L.b);
+    TS_CUDA_TRY(cudaMemcpy(L.w, packed.data(), packed.size() * sizeof(float),
+                           cudaMemcpyHostToDevice));
+    TS_CUDA_TRY(cudaMemcpy(L.b, bi->second.second.data(), Co * sizeof(float),
+                           cudaMemcpyHostToDevice));
+  }
+  (void)params;
+  if (tensors.size() != (size_t)nL * 2) return TS_E_SHAPE;  // unexpected tensors
+  W->per_tile_floats = off;
+  W->layers = std::move(layers);
+  return TS_OK;
+}
+
+}  // namespace
+}  // namespace ts
+
+using namespace ts;
+
+extern "C" int ts_weights_create(const uint8_t* lswb, size_t n_bytes, int precision,
+                                 ts_weights** out) {
+  if (!lswb || !out) return TS_E_INVALID;
+  *out = nullptr;
+  if (n_bytes < 4 || memcmp(lswb, "LSWB", 4) != 0) return TS_E_BAD_MAGIC;
+  Blob bl{lswb, n_bytes, 4};
+  const uint32_t version = bl.get<uint32_t>();
+  const uint32_t count = bl.get<uint32_t>();
+  if (!bl.ok) return TS_E_SHAPE;
+  if (version != 1) return TS_E_VERSION;
+  std::map<std::string, std::pair<std::vector<int>, std::vector<float>>> tensors;
+  for (uint32_t t = 0; t < count; ++t) {
+    const uint16_t nl = bl.get<uint16_t>();
+    if (!bl.ok || bl.off + nl > n_bytes) return TS_E_SHAPE;
+    std::string name(reinterpret_cast<const char*>(lswb + bl.off), nl);
+    bl.off += nl;
+    const uint8_t rank = bl.get<uint8_t>();
+    std::vector<int> dims(rank);
+    size_t cnt = 1;
+    for (int r = 0; r < rank; ++r) { dims[r] = (int)bl.get<uint32_t>(); cnt *= dims[r]; }
+    if (!bl.ok || bl.off + 4 * cnt > n_bytes) return TS_E_SHAPE;
+    std::vector<float> data(cnt);
+    memcpy(data.data(), lswb + bl.off, 4 * cnt);
+    bl.off += 4 * cnt;
+    tensors[name] = {dims, std::move(data)};
+  }
+  const uint32_t dl = bl.get<uint32_t>();
+  if (!bl.ok || bl.off + dl > n_bytes) return TS_E_SHAPE;
+  std::string text(reinterpret_cast<const char*>(lswb + bl.off), dl);
+  bool identity = false;
+  long long declared = -1;
+  std::map<std::string, std::vector<LayerDesc>> stages;
+  int st = parse_descriptor(text, identity, stages, declared);
+  if (st != TS_OK) return st;
+  std::unique_ptr<ts_weights> W(new ts_weights());
+  W->identity = identity;
+  W->precision = precision;
+  if (identity) {
+    if (!tensors.empty()) return TS_E_SHAPE;
+    *out = W.release();
+    return TS_OK;
+  }
+  long long params = 0;
+  for (auto& kv : stages)
+    for (auto& d : kv.second) params += (long long)d.co * d.ci * d.k * d.k + d.co;
+  if (declared >= 0 && declared != params) return TS_E_SHAPE;
+  st = build_plan(W.get(), stages, tensors);
+  if (st != TS_OK) {
+    for (void* p : W->device_allocs) cudaFree(p);
+    return st;
+  }
+  *out = W.release();
+  return TS_OK;
+}
+
+extern "C" int ts_weights_destroy(ts_weights* w) {
+  if (!w) return TS_OK;
+  for (void* p : w->device_allocs) cudaFree(p);
+  delete w;
+  return TS_OK;
+}
+
+extern "C" int ts_weights_is_identity(const ts_weights* w) { return w && w->identity; }
+
+extern "C" size_t ts_refine_workspace(const ts_weights* w, int batch) {
+  if (!w || w->identity) return 256;
+  const int sb = std::min(batch, kSubBatch);
+  return (w->per_tile_floats * (size_t)std::max(sb, 1)) * sizeof(float) + 256;
+}
+
+extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, float* d_out,
+                         uint8_t* d_nonfinite, void* d_workspace, void* stream) {
+  if (!W || batch < 0) return TS_E_INVALID;
+  if (batch == 0) return TS_E_SHAPE;  // refine_batch requires a non-empty batch
+  cudaStream_t s = as_stream(stream);
+  if (W->identity) {
+    refine_epilogue_kernel<<<batch, 256, 0, s>>>(d_in, 8, 1, d_in, d_out, d_nonfinite);
+    TS_LAUNCH_CHECK();
+    return TS_OK;
+  }
+  float* ws = reinterpret_cast<float*>(d_workspace);
+  const int fcs = W->layers.back().d.co;
+  for (int b0 = 0; b0 < batch; b0 += kSubBatch) {
+    const int B = std::min(kSubBatch, batch - b0);
+    const float* in = d_in + (size_t)b0 * kRes * kRes * 8;
+    auto buf = [&](size_t off) { return ws + off * B; };
+    // raw inputs -> channels [0, 8) of the fuse input (skip concat)
+    {
+      const int64_t px = (int64_t)B * kRes * kRes;
+      copy_inputs_kernel<<<(int)std::min<int64_t>(ceil_div<int64_t>(px, 256), 148 * 16),
+                           256, 0, s>>>(in, px, buf(W->fuse_in_off), W->fuse_in_c);
+      TS_LAUNCH_CHECK();
+    }
+    const int enc_ch0[4] = {0, 1, 2, 5};
+    const int enc_cin[4] = {1, 1, 3, 3};
+    const float* prev_base = nullptr;
+    int prev_H = 0, prev_cs = 0, prev_coff = 0, prev_C = 0;
+    int prev_stage = -1;
+    for (size_t i = 0; i < W->layers.size(); ++i) {
+      const ConvLayer& L = W->layers[i];
+      ConvOp op{};
+      const bool first = (int)L.stage != prev_stage;
+      if (first) {
+        if (L.stage < 4) {
+          op.in = ActView{const_cast<float*>(in), kRes, kRes, 8, enc_ch0[L.stage],
+                          enc_cin[L.stage]};
+        } else if (L.stage == 4) {
+          op.in = ActView{buf(W->cat_off), W->enc_hw, W->enc_hw, W->enc_out_c, 0,
+                          W->enc_out_c};
+        } else if (L.stage == 5 || L.stage == 6) {
+          // merge output = the last merge layer's buffer
+          size_t mi = 0;
+          for (size_t j = 0; j < W->layers.size(); ++j)
+            if (W->layers[j].stage == 4) mi = j;
+          const ConvLayer& M = W->layers[mi];
+          op.in = ActView{buf(M.out_off), M.Hout, M.Wout, M.out_cstride, M.out_coff, M.d.co};
+        } else {
+          op.in = ActView{buf(W->fuse_in_off), kRes, kRes, W->fuse_in_c, 0, W->fuse_in_c};
+        }
+      } else {
+        op.in = ActView{const_cast<float*>(prev_base), prev_H, prev_H, prev_cs, prev_coff,
+                        prev_C};
+      }
+      op.out = ActView{buf(L.out_off), L.Hout, L.Wout, L.out_cstride, L.out_coff, L.d.co};
+      op.up2 = L.up2;
+      op.k = L.d.k; op.stride = L.d.s; op.pad = L.d.p;
+      op.lrelu = L.d.lrelu;
+      op.oy0 = L.out_win.y0; op.oy1 = L.out_win.y1;
+      op.ox0 = L.out_win.x0; op.ox1 = L.out_win.x1;
+      op.w = L.w; op.bias = L.b;
+      op.batch = B;
+      int st;
+      if (W->precision != 0 && conv_tc_supported(op, W->precision))
+        st = launch_conv_tc(op, W->precision, stream);
+      else
+        st = launch_conv_simt(op, stream);
+      if (st != TS_OK) return st;
+      prev_base = op.out.base; prev_H = L.Hout; prev_cs = L.out_cstride;
+      prev_coff = L.out_coff; prev_C = L.d.co;
+      prev_stage = L.stage;
+    }
+    const ConvLayer& last = W->layers.back();
+    refine_epilogue_kernel<<<B, 256, 0, s>>>(buf(last.out_off), fcs, 0, in,
+                                             d_out + (size_t)b0 * kOut * kOut * 4,
+                                             d_nonfinite ? d_nonfinite + b0 : nullptr);
+    TS_LAUNCH_CHECK();
+  }
+  return TS_OK;
+}
+
+namespace ts {
+namespace {
+
+__global__ void nchw_to_nhwc(const float* __restrict__ x, int B, int C, int H, int W,
+                             float* __restrict__ y) {
+  const int64_t n = (int64_t)B * C * H * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i % C, r = i / C;  // r = (b*H + y)*W + x
+    const int64_t b = r / ((int64_t)H * W), yx = r % ((int64_t)H * W);
+    y[i] = x[(b * C + c) * H * W + yx];
+  }
+}
+
+__global__ void nhwc_to_nchw(const float* __restrict__ x, int B, int C, int H, int W,
+                             float* __restrict__ y) {
+  const int64_t n = (int64_t)B * C * H * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t yx = i % ((int64_t)H * W), r = i / ((int64_t)H * W);
+    const int64_t c = r % C, b = r / C;
+    y[i] = x[(b * H * W + yx) * C + c];
+  }
+}
+
+// OIKK -> [K][C_out] with K = (ky*k + kx)*C_in + ci
+__global__ void pack_weights(const float* __restrict__ w, int Co, int Ci, int k,
+                             float* __restrict__ out) {
+  const int n = Co * Ci * k * k;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int kx = i % k, ky = (i / k) % k, ci = (i / (k * k)) % Ci, o = i / (k * k * Ci);
+    out[(size_t)((ky * k + kx) * Ci + ci) * Co + o] = w[i];
+  }
+}
+
+}  // namespace
+}  // namespace ts
+
+extern "C" int ts_conv2d(const float* d_x, int batch, int c_in, int h, int w,
+                         const float* d_weight, int c_out, int k, const float* d_bias,
+                         int stride, int padding, float* d_y, void* stream) {
+  if (batch <= 0 || c_in <= 0 || c_out <= 0 || k <= 0 || stride <= 0 || padding < 0)
+    return TS_E_SHAPE;
+  const int ho = (h + 2 * padding - k) / stride + 1;
+  const int wo = (w + 2 * padding - k) / stride + 1;
+  if (ho <= 0 || wo <= 0) return TS_E_SHAPE;
+  cudaStream_t s = as_stream(stream);
+  const size_t nin = (size_t)batch * c_in * h * w, nout = (size_t)batch * c_out * ho * wo;
+  const size_t nw = (size_t)c_out * c_in * k * k;
+  float* buf = nullptr;
+  TS_CUDA_TRY(cudaMallocAsync(&buf, sizeof(float) * (nin + nout + nw), s));
+  float *xin = buf, *yout = buf + nin, *wp = buf + nin + nout;
+  const int g = 148 * 4;
+  nchw_to_nhwc<<<g, 256, 0, s>>>(d_x, batch, c_in, h, w, xin);
+  pack_weights<<<g, 256, 0, s>>>(d_weight, c_out, c_in, k, wp);
+  ConvOp op{};
+  op.in = ActView{xin, h, w, c_in, 0, c_in};
+  op.out = ActView{yout, ho, wo, c_out, 0, c_out};
+  op.up2 = 0; op.k = k; op.stride = stride; op.pad = padding; op.lrelu = 0;
+  op.oy0 = 0; op.oy1 = ho; op.ox0 = 0; op.ox1 = wo;
+  op.w = wp; op.bias = d_bias; op.batch = batch;
+  int st = launch_conv_simt(op, stream);
+  if (st != TS_OK) return st;
+  nhwc_to_nchw<<<g, 256, 0, s>>>(yout, batch, c_out, ho, wo, d_y);
+  TS_LAUNCH_CHECK();
+  TS_CUDA_TRY(cudaFreeAsync(buf, s));
+  return TS_OK;
+}

@@ -1,0 +1,416 @@
+"""Heightmap refinement network on the GPU (descriptor-driven CNN).
+
+Drop-in for ``pkg/src/terrascout/refiner.py``.  Host side keeps the
+reference's types and containers -- ``ArchDescriptor`` text format
+(:59-189), ``default_descriptor``/``identity_descriptor`` (:192-224),
+``WeightBundle`` + LSWB ``save_weights``/``load_weights`` (:227-311),
+He-init ``random_weights`` (:314-327).  The numerics run in CUDA:
+``refine_batch`` -> ``ts_refine`` (all conv layers, fused up2/concat,
+crop-aware windows, crop/denormalise/clamp/non-finite fallback), and
+``conv2d`` -> ``ts_conv2d``.  Device weight handles are built once per
+bundle (``ts_weights_create`` parses the same LSWB bytes) and cached.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import logging
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as D
+from ._lib import lib
+from .errors import (BadMagic, ShapeMismatch, UnsupportedVersion,
+                     raise_for_status)
+from .patches import OUTPUT_RES, PAD_RADIUS, RASTER_RES, PatchKey, RawPatch
+
+log = logging.getLogger(__name__)
+
+MAGIC = b"LSWB"
+BUNDLE_VERSION = 1
+STAGES = ("enc_hm_nn", "enc_hm_lin", "enc_rgb_nn", "enc_rgb_lin",
+          "merge", "dec_height", "dec_color", "fuse")
+ENC_IN = {"enc_hm_nn": 1, "enc_hm_lin": 1, "enc_rgb_nn": 3, "enc_rgb_lin": 3}
+CROP = (RASTER_RES - OUTPUT_RES) // 2
+
+PROV_INTERPOLATED = "interpolated-only"
+PROV_REFINED = "refined"
+PROV_BAKED = "fullres-baked"
+
+# ts_weights_create precision modes
+PRECISION_FP32 = 0      # CUDA-core fp32 implicit GEMM
+PRECISION_TF32X3 = 1    # tcgen05 kind::tf32, 3-pass split (fp32-accurate)
+PRECISION_BF16 = 2      # tcgen05 kind::f16 (bf16 operands, fp32 accumulate)
+
+
+@dataclass
+class ConvLayer:
+    c_in: int
+    c_out: int
+    kernel: int
+    stride: int
+    padding: int
+    activation: str
+
+
+class Upsample2:
+    """Nearest-neighbour x2 upsampling; no parameters."""
+
+
+@dataclass
+class ArchDescriptor:
+    identity: bool
+    stages: dict
+    declared_params: int | None = None
+
+    def parameter_count(self) -> int:
+        return sum(l.c_out * l.c_in * l.kernel ** 2 + l.c_out
+                   for ls in self.stages.values() for l in ls
+                   if isinstance(l, ConvLayer))
+
+    def to_text(self) -> str:
+        out = ["arch 1"]
+        if self.identity:
+            out.append("identity")
+        else:
+            out.append(f"params {self.parameter_count()}")
+            for name in STAGES:
+                out.append(f"stage {name}")
+                for l in self.stages[name]:
+                    out.append("up2" if isinstance(l, Upsample2) else
+                               f"conv {l.c_in} {l.c_out} {l.kernel} "
+                               f"{l.stride} {l.padding} {l.activation}")
+        return "\n".join(out) + "\n"
+
+    @classmethod
+    def from_text(cls, text: str) -> "ArchDescriptor":
+        lines = [ln.strip() for ln in text.splitlines()
+                 if ln.strip() and not ln.startswith("#")]
+        if not lines or not lines[0].startswith("arch "):
+            raise ShapeMismatch("descriptor missing arch line")
+        if lines[0] != "arch 1":
+            raise UnsupportedVersion(f"descriptor {lines[0]!r}")
+        if len(lines) > 1 and lines[1] == "identity":
+            return cls(identity=True, stages={})
+        stages: dict = {}
+        declared = None
+        cur = None
+        for ln in lines[1:]:
+            f = ln.split()
+            if f[0] == "params":
+                declared = int(f[1])
+            elif f[0] == "stage":
+                cur = stages.setdefault(f[1], [])
+            elif f[0] == "up2":
+                cur.append(Upsample2())
+            elif f[0] == "conv":
+                cur.append(ConvLayer(*map(int, f[1:6]), f[6]))
+            else:
+                raise ShapeMismatch(f"unknown descriptor line {ln!r}")
+        d = cls(identity=False, stages=stages, declared_params=declared)
+        d.validate()
+        return d
+
+    def _convs(self, s):
+        return [l for l in self.stages[s] if isinstance(l, ConvLayer)]
+
+    def validate(self):
+        if self.identity:
+            return
+        missing = [s for s in STAGES if s not in self.stages]
+        if missing:
+            raise ShapeMismatch(f"descriptor missing stages {missing}")
+        for name, cin in ENC_IN.items():
+            if self._convs(name)[0].c_in != cin:
+                raise ShapeMismatch(f"{name} must take {cin} channels")
+        merged = sum(self._convs(n)[-1].c_out for n in ENC_IN)
+        if self._convs("merge")[0].c_in != merged:
+            raise ShapeMismatch("merge input != encoder outputs")
+        for dec in ("dec_height", "dec_color"):
+            if self._convs(dec)[0].c_in != self._convs("merge")[-1].c_out:
+                raise ShapeMismatch(f"{dec} input != merge output")
+        skip = 8 + self._convs("dec_height")[-1].c_out + \
+            self._convs("dec_color")[-1].c_out
+        if self._convs("fuse")[0].c_in != skip:
+            raise ShapeMismatch("fuse input != skip concat")
+        if self._convs("fuse")[-1].c_out != 4:
+            raise ShapeMismatch("fuse must emit 4 channels (1 h + 3 rgb)")
+        size = RASTER_RES
+        for stage in ("enc_hm_nn", "merge", "dec_height"):
+            for l in self.stages[stage]:
+                if isinstance(l, Upsample2):
+                    size *= 2
+                else:
+                    size = (size + 2 * l.padding - l.kernel) // l.stride + 1
+        if size != RASTER_RES:
+            raise ShapeMismatch(f"decoder output {size}, expected "
+                                f"{RASTER_RES}")
+        if self.declared_params is not None and \
+                self.declared_params != self.parameter_count():
+            raise ShapeMismatch("declared parameter count mismatch")
+
+    def tensor_shapes(self) -> dict:
+        shapes = {}
+        for name in STAGES:
+            for li, l in enumerate(self.stages[name]):
+                if isinstance(l, ConvLayer):
+                    shapes[f"{name}.{li}.weight"] = (l.c_out, l.c_in,
+                                                     l.kernel, l.kernel)
+                    shapes[f"{name}.{li}.bias"] = (l.c_out,)
+        return shapes
+
+
+def default_descriptor() -> ArchDescriptor:
+    """Default sizes (~2.4M parameters), refiner.py:192-219."""
+    def enc(cin):
+        return [ConvLayer(cin, 48, 3, 2, 1, "lrelu"),
+                ConvLayer(48, 96, 3, 2, 1, "lrelu"),
+                ConvLayer(96, 192, 3, 2, 1, "lrelu")]
+
+    def dec():
+        return [Upsample2(), ConvLayer(320, 96, 3, 1, 1, "lrelu"),
+                Upsample2(), ConvLayer(96, 64, 3, 1, 1, "lrelu"),
+                Upsample2(), ConvLayer(64, 32, 3, 1, 1, "lrelu")]
+    d = ArchDescriptor(False, {
+        "enc_hm_nn": enc(1), "enc_hm_lin": enc(1),
+        "enc_rgb_nn": enc(3), "enc_rgb_lin": enc(3),
+        "merge": [ConvLayer(768, 768, 1, 1, 0, "lrelu"),
+                  ConvLayer(768, 320, 1, 1, 0, "lrelu")],
+        "dec_height": dec(), "dec_color": dec(),
+        "fuse": [ConvLayer(72, 64, 3, 1, 1, "lrelu"),
+                 ConvLayer(64, 32, 3, 1, 1, "lrelu"),
+                 ConvLayer(32, 4, 3, 1, 1, "linear")]})
+    d.declared_params = d.parameter_count()
+    return d
+
+
+def identity_descriptor() -> ArchDescriptor:
+    return ArchDescriptor(identity=True, stages={})
+
+
+@dataclass
+class WeightBundle:
+    format_version: int
+    tensors: dict
+    descriptor: ArchDescriptor
+
+    @property
+    def parameter_count(self) -> int:
+        return sum(t.size for t in self.tensors.values())
+
+    def validate(self):
+        if self.descriptor.identity:
+            if self.tensors:
+                raise ShapeMismatch("identity bundles carry no tensors")
+            return
+        want = self.descriptor.tensor_shapes()
+        for name, shape in want.items():
+            t = self.tensors.get(name)
+            if t is None:
+                raise ShapeMismatch(f"missing tensor {name}")
+            if tuple(t.shape) != shape:
+                raise ShapeMismatch(f"tensor {name} has shape {t.shape}")
+        extra = set(self.tensors) - set(want)
+        if extra:
+            raise ShapeMismatch(f"unexpected tensors {sorted(extra)}")
+        if self.descriptor.declared_params is not None and \
+                self.parameter_count != self.descriptor.declared_params:
+            raise ShapeMismatch("parameter count mismatch")
+
+
+def lswb_bytes(tensors: dict, descriptor_text: str) -> bytes:
+    """The LSWB container (refiner.py:258-272) as bytes."""
+    parts = [MAGIC, struct.pack("<II", BUNDLE_VERSION, len(tensors))]
+    for name, t in tensors.items():
+        a = np.ascontiguousarray(t, dtype="<f4")
+        nb = name.encode()
+        parts += [struct.pack("<H", len(nb)), nb,
+                  struct.pack("<B", a.ndim),
+                  struct.pack(f"<{a.ndim}I", *a.shape), a.tobytes()]
+    d = descriptor_text.encode()
+    parts += [struct.pack("<I", len(d)), d]
+    return b"".join(parts)
+
+
+def save_weights(path: str, bundle: WeightBundle):
+    with open(path, "wb") as fp:
+        fp.write(lswb_bytes(bundle.tensors, bundle.descriptor.to_text()))
+
+
+def load_weights(path: str) -> WeightBundle:
+    with open(path, "rb") as fp:
+        blob = fp.read()
+    if blob[:4] != MAGIC:
+        raise BadMagic(f"expected {MAGIC!r} magic")
+    version, n = struct.unpack_from("<II", blob, 4)
+    if version != BUNDLE_VERSION:
+        raise UnsupportedVersion(f"weight bundle version {version}")
+    off, tensors = 12, {}
+    try:
+        for _ in range(n):
+            ln, = struct.unpack_from("<H", blob, off)
+            name = blob[off + 2:off + 2 + ln].decode()
+            off += 2 + ln
+            rank, = struct.unpack_from("<B", blob, off)
+            dims = struct.unpack_from(f"<{rank}I", blob, off + 1)
+            off += 1 + 4 * rank
+            cnt = int(np.prod(dims)) if rank else 1
+            arr = np.frombuffer(blob, "<f4", count=cnt, offset=off)
+            off += 4 * cnt
+            tensors[name] = arr.reshape(dims).copy()
+        dl, = struct.unpack_from("<I", blob, off)
+        text = blob[off + 4:off + 4 + dl]
+        if len(text) != dl:
+            raise ShapeMismatch("descriptor truncated")
+    except (struct.error, ValueError) as exc:
+        raise ShapeMismatch(f"bundle truncated: {exc}") from exc
+    b = WeightBundle(version, tensors,
+                     ArchDescriptor.from_text(text.decode()))
+    b.validate()
+    return b
+
+
+def random_weights(descriptor: ArchDescriptor, seed: int = 0) -> WeightBundle:
+    """He-style init with the reference's draw order (refiner.py:314-327)."""
+    gen = np.random.default_rng(seed)
+    tensors = {}
+    for name, shape in descriptor.tensor_shapes().items():
+        if name.endswith("weight"):
+            std = np.sqrt(2.0 / int(np.prod(shape[1:])))
+            tensors[name] = gen.normal(0, std, shape).astype(np.float32)
+        else:
+            tensors[name] = np.zeros(shape, np.float32)
+    b = WeightBundle(BUNDLE_VERSION, tensors, descriptor)
+    b.validate()
+    return b
+
+
+# ------------------------------------------------------------ device side
+
+class DeviceWeights:
+    """ts_weights handle for one bundle + precision mode."""
+
+    def __init__(self, bundle: WeightBundle, precision: int):
+        blob = lswb_bytes(bundle.tensors, bundle.descriptor.to_text())
+        D.device()
+        h = C.c_void_p()
+        raise_for_status(lib().ts_weights_create(blob, len(blob), precision,
+                                                 C.byref(h)),
+                         "ts_weights_create")
+        self.handle = h
+        self.identity = bool(lib().ts_weights_is_identity(h))
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            try:
+                lib().ts_weights_destroy(self.handle)
+            except Exception:  # noqa: BLE001 - interpreter shutdown
+                pass
+
+    def workspace(self, batch: int) -> torch.Tensor:
+        n = int(lib().ts_refine_workspace(self.handle, batch))
+        return D.empty((n,), torch.uint8)
+
+    def run(self, cnn_in: torch.Tensor, batch: int, out: torch.Tensor,
+            nonfinite: torch.Tensor, ws: torch.Tensor | None = None):
+        ws = self.workspace(batch) if ws is None else ws
+        D.call("ts_refine", self.handle, D.ptr(cnn_in), batch, D.ptr(out),
+               D.ptr(nonfinite), D.ptr(ws), D.stream())
+
+
+def device_weights(bundle: WeightBundle,
+                   precision: int = PRECISION_FP32) -> DeviceWeights:
+    cache = bundle.__dict__.setdefault("_ts_device", {})
+    if precision not in cache:
+        cache[precision] = DeviceWeights(bundle, precision)
+    return cache[precision]
+
+
+@dataclass
+class RefinedPatch:
+    key: PatchKey
+    heights_rel: np.ndarray
+    rgb: np.ndarray | None
+    provenance: str
+
+    @property
+    def hm(self) -> np.ndarray:
+        return self.heights_rel.astype(np.float64) + self.key.c_z
+
+
+def staging_array(raws: list[RawPatch]) -> np.ndarray:
+    """B x 96 x 96 x 8 NHWC input (channel order of refiner.py:458-468)."""
+    x = np.zeros((len(raws), RASTER_RES, RASTER_RES, 8), np.float32)
+    for i, r in enumerate(raws):
+        x[i, :, :, 0] = r.hm_nn
+        x[i, :, :, 1] = r.hm_lin
+        if r.rgb_nn is not None:
+            x[i, :, :, 2:5] = r.rgb_nn
+            x[i, :, :, 5:8] = r.rgb_lin
+    return x
+
+
+def refine_batch(raws: list[RawPatch], weights: WeightBundle,
+                 precision: int = PRECISION_FP32) -> list[RefinedPatch]:
+    """refine_batch on the GPU (same outputs/provenance/fallback rules)."""
+    if not raws:
+        raise ShapeMismatch("refine_batch requires a non-empty batch")
+    for r in raws:
+        if r.hm_nn.shape != (RASTER_RES, RASTER_RES):
+            raise ShapeMismatch(f"raw patch raster is {r.hm_nn.shape}")
+    dw = device_weights(weights, precision)
+    B = len(raws)
+    cnn_in = D.upload(staging_array(raws))
+    out = D.empty((B, OUTPUT_RES, OUTPUT_RES, 4), torch.float32)
+    nonfinite = torch.zeros(B, dtype=torch.uint8, device=out.device)
+    dw.run(cnn_in, B, out, nonfinite)
+    return finish_refined(raws, D.host(out), D.host(nonfinite), dw.identity)
+
+
+def finish_refined(raws, out: np.ndarray, nonfinite: np.ndarray,
+                   identity: bool) -> list[RefinedPatch]:
+    res = []
+    for i, r in enumerate(raws):
+        o = out[i]
+        bad = bool(nonfinite[i])
+        if bad:
+            log.warning("non-finite activation for patch (%d,%d); keeping "
+                        "interpolated raster", r.key.i, r.key.j)
+        rgb = None
+        if (r.rgb_lin if (identity or bad) else r.rgb_nn) is not None:
+            rgb = np.ascontiguousarray(o[:, :, 1:4])
+        res.append(RefinedPatch(
+            key=r.key, heights_rel=np.ascontiguousarray(o[:, :, 0]), rgb=rgb,
+            provenance=PROV_INTERPOLATED if bad else PROV_REFINED))
+    return res
+
+
+def conv2d(x: np.ndarray, weight: np.ndarray, bias: np.ndarray,
+           stride: int = 1, padding: int = 0) -> np.ndarray:
+    """Cross-correlation of one C x H x W input on the GPU (ts_conv2d)."""
+    if x.ndim != 3:
+        raise ShapeMismatch("conv2d expects CHW input")
+    if weight.ndim != 4:
+        raise ShapeMismatch("expected OIKK kernel")
+    ci, h, w = x.shape
+    co, ci2, kh, kw = weight.shape
+    if ci2 != ci:
+        raise ShapeMismatch(f"kernel wants {ci2} channels, input has {ci}")
+    if bias.shape != (co,):
+        raise ShapeMismatch("bias length != output channels")
+    if kh != kw:
+        raise ShapeMismatch("square kernels only")
+    ho = (h + 2 * padding - kh) // stride + 1
+    wo = (w + 2 * padding - kw) // stride + 1
+    if ho <= 0 or wo <= 0:
+        raise ShapeMismatch("kernel larger than padded input")
+    dx = D.upload(np.asarray(x, np.float32))
+    dw = D.upload(np.asarray(weight, np.float32))
+    db = D.upload(np.asarray(bias, np.float32))
+    y = D.empty((co, ho, wo), torch.float32)
+    D.call("ts_conv2d", D.ptr(dx), 1, ci, h, w, D.ptr(dw), co, kh, D.ptr(db),
+           stride, padding, D.ptr(y), D.stream())
+    return D.host(y)

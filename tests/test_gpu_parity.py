@@ -1,0 +1,409 @@
+"""CUDA path vs the oracle / reference golden vectors (needs a B200).
+
+Tolerances:
+  * (1) records, positions, colours, chunk order: bit-exact;
+  * (2) NN indices / hm_nn: bit-exact; coverage mask bit-exact; hm_lin and
+    rgb_lin <= 1e-6 patch units against Qhull-fed references, face ids
+    bit-exact when fed the same (Qhull) triangles;
+  * (3) fp32 path: |dh| <= 2e-3 m on random He weights (torch/numpy fp32
+    already differ by 8e-4 m), |drgb| <= 1e-4; identity bundle exact;
+  * (4) texel assignment exact, heights |dh| <= 1e-6 m, rgb <= 1e-6.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import bake as obake  # noqa: E402
+from oracle import laz as olaz  # noqa: E402
+from oracle import patches as opatch  # noqa: E402
+from oracle import refiner as oref  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+# ---------------------------------------------------------------- (1)
+
+def test_read_chunk_points_golden(golden, tmp_path):
+    from paper_2509_20198_b200.lasio import (colors, positions,
+                                             read_chunk_points, scan_tile)
+    g = golden("chunk_points.npz")
+    for k in range(int(g["n_files"])):
+        path = tmp_path / f"f{k}.laz"
+        path.write_bytes(g[f"file{k}"].tobytes())
+        tile = scan_tile(str(path), k)
+        rec = read_chunk_points(tile, las_stride=int(g[f"stride{k}"]))
+        assert rec.tobytes() == g[f"rec{k}"].tobytes(), k
+        assert np.array_equal(positions(rec, tile.header), g[f"xyz{k}"]), k
+        if f"rgb{k}" in g:
+            assert np.array_equal(colors(rec, tile.header), g[f"rgb{k}"]), k
+        refs = tile.chunk_refs
+        assert sum(r.point_count for r in refs) == tile.header.point_count
+
+
+def _stub_batch(n_cols, n_rows, **kw):
+    from paper_2509_20198_b200 import _device as D
+    from paper_2509_20198_b200 import synth
+    from paper_2509_20198_b200.lasio import parse_header
+    tiles = synth.chunked_terrain_tiles(n_cols, n_rows, **kw)
+    descs = np.concatenate([D.tile_desc(parse_header(t.data)) for t in tiles])
+    return tiles, D.TileBatch([t.data for t in tiles], descs)
+
+
+def test_batched_extraction_bit_exact():
+    from paper_2509_20198_b200 import _device as D
+    tiles, tb = _stub_batch(6, 5, offset=(712000.0, 4.1e6, -123.45),
+                            origin=(712000.0, 4.1e6))
+    tables = D.ChunkTables(tb)
+    cp = D.ChunkPoints(tb, tables)
+    assert not tables.status.any()
+    rec = np.concatenate([olaz.chunk_points(t.data) for t in tiles])
+    assert cp.records[:rec.nbytes].cpu().numpy().tobytes() == rec.tobytes()
+    xyz, rgb = [], []
+    for t in tiles:
+        r = olaz.chunk_points(t.data)
+        h = olaz.header_fields(t.data)
+        xyz.append(olaz.positions(r, h["scale"], h["offset"]))
+        rgb.append(olaz.colors(r))
+    xyz = np.concatenate(xyz)
+    assert np.array_equal(cp.xyz.cpu().numpy(), xyz)
+    assert np.array_equal(cp.rgb.cpu().numpy(), np.concatenate(rgb))
+    cells = np.stack([np.floor(xyz[:, 0] / 640.0),
+                      np.floor(xyz[:, 1] / 640.0)], 1).astype(np.int64)
+    assert np.array_equal(cp.cells.cpu().numpy(), cells)
+
+
+def test_corrupt_table_is_reported():
+    from paper_2509_20198_b200 import _device as D
+    from paper_2509_20198_b200 import synth
+    from paper_2509_20198_b200.lasio import parse_header
+    t = synth.chunked_terrain_tiles(1, 1, chunks_per_tile=20)[0]
+    bad = bytearray(t.data)
+    bad[-6:] = b"\xff" * 6           # trash the arithmetic-coded table tail
+    ptr = bytearray(t.data)
+    ptr[parse_header(t.data).point_data_offset:][:8] = (10 ** 12).to_bytes(
+        8, "little")
+    for img in (bytes(ptr),):
+        tb = D.TileBatch([img], D.tile_desc(parse_header(img)))
+        tables = D.ChunkTables(tb)
+        assert int(tables.status[0].item()) == 6
+
+
+# ---------------------------------------------------------------- (2)
+
+def test_gather_and_reconstruct_golden(golden):
+    from paper_2509_20198_b200 import _device as D
+    from paper_2509_20198_b200.patches import (ChunkPointIndex, PatchKey,
+                                               gather_and_normalize,
+                                               reconstruct_batch)
+    g = golden("reconstruct.npz")
+    index = ChunkPointIndex()
+    for t in range(int(g["n_tiles"])):
+        img = g[f"tile{t}"].tobytes()
+        rec = olaz.chunk_points(img)
+        h = olaz.header_fields(img)
+        index.add_points(olaz.positions(rec, h["scale"], h["offset"]),
+                         olaz.colors(rec))
+    keys = [PatchKey(int(i), int(j), (i * 640.0 + 320.0, j * 640.0 + 320.0))
+            for i, j in g["keys"]]
+    for p, key in enumerate(keys):
+        pts = gather_and_normalize(key, index)
+        assert np.array_equal(pts.xy, g[f"xy{p}"]), p
+        assert np.array_equal(pts.h, g[f"h{p}"]), p
+        assert np.array_equal(pts.rgb, g[f"prgb{p}"]), p
+        assert pts.c_z == float(g[f"cz_in{p}"])
+    raws = reconstruct_batch(keys, index)
+    for p, raw in enumerate(raws):
+        assert np.array_equal(raw.hm_nn, g[f"hm_nn{p}"]), p
+        assert np.array_equal(raw.rgb_nn, g[f"rgb_nn{p}"]), p
+        face = g[f"face{p}"]
+        assert np.array_equal(raw.face_map.cells >= 0, face >= 0), p
+        assert np.abs(raw.hm_lin - g[f"hm_lin{p}"]).max() <= 1e-6, p
+        assert np.abs(raw.rgb_lin - g[f"rgb_lin{p}"]).max() <= 1e-6, p
+        assert abs(raw.key.c_z - float(g[f"cz{p}"])) <= 1e-3, p
+
+
+def _gpu_triangles(xy):
+    from paper_2509_20198_b200 import _device as D
+    from paper_2509_20198_b200.patches import triangulate
+    n = len(xy)
+    g = dict(n=1, xy=D.upload(np.asarray(xy, np.float64)),
+             off=torch.tensor([0, n], dtype=torch.int64, device="cuda"))
+    t = triangulate(g)
+    assert int(t["status"][0].item()) == 0
+    m = int(t["ntri"][0].item())
+    return t["tri"][:m].cpu().numpy()
+
+
+def _tri_set(simp):
+    return set(tuple(sorted(s)) for s in np.asarray(simp).tolist())
+
+
+def test_gpu_delaunay_equals_qhull(golden):
+    g = golden("reconstruct.npz")
+    for p in range(len(g["keys"])):
+        ours = _gpu_triangles(g[f"xy{p}"])
+        assert _tri_set(ours) == _tri_set(g[f"simp{p}"]), p
+        # CCW
+        allxy = np.vstack([g[f"xy{p}"], opatch.CORNERS])
+        a, b, c = allxy[ours[:, 0]], allxy[ours[:, 1]], allxy[ours[:, 2]]
+        det = (b[:, 0] - a[:, 0]) * (c[:, 1] - a[:, 1]) - \
+            (b[:, 1] - a[:, 1]) * (c[:, 0] - a[:, 0])
+        assert (det > 0).all()
+    gi = golden("interpolate.npz")
+    for k in range(6):          # random general-position cases
+        assert _tri_set(_gpu_triangles(gi[f"xy{k}"])) == \
+            _tri_set(gi[f"simp{k}"]), k
+
+
+def _raster_with(xy, h, rgb, tri, cz=12.5, recenter=False):
+    """ts_raster fed explicit (e.g. Qhull) triangles."""
+    from paper_2509_20198_b200 import _device as D
+    from paper_2509_20198_b200.patches import raster
+    n = len(xy)
+    g = dict(n=1, xy=D.upload(np.asarray(xy, np.float64)),
+             h=D.upload(np.asarray(h, np.float64)),
+             prgb=D.upload(np.asarray(rgb, np.float32)) if rgb is not None
+             else None,
+             off=torch.tensor([0, n], dtype=torch.int64, device="cuda"),
+             cz=torch.tensor([cz], dtype=torch.float64, device="cuda"))
+    tri = np.asarray(tri, np.int32)
+    t = dict(tri=D.upload(tri), ntri=torch.tensor([len(tri)], dtype=torch.int32,
+                                                  device="cuda"),
+             tri_off=torch.zeros(1, dtype=torch.int64, device="cuda"))
+    o = raster(g, t, recenter=recenter, api_outputs=True)
+    return {k: v.cpu().numpy()[0] for k, v in o.items()
+            if k not in ("status",)}
+
+
+def test_raster_bit_exact_with_qhull_triangles(golden):
+    gi = golden("interpolate.npz")
+    for k in range(int(gi["n_cases"])):
+        if f"simp{k}" not in gi:
+            continue
+        xy, h = gi[f"xy{k}"], gi[f"h{k}"]
+        rgb = gi[f"rgb{k}"] if f"rgb{k}" in gi else None
+        o = _raster_with(xy, h, rgb, gi[f"simp{k}"])
+        assert np.array_equal(o["face"], gi[f"face{k}"]), k
+        assert np.array_equal(o["hm_nn"], gi[f"hm_nn{k}"]), k
+        assert np.array_equal(o["hm_lin"], gi[f"hm_lin{k}"]), k
+        if rgb is not None:
+            assert np.array_equal(o["rgb_lin"], gi[f"rgb_lin{k}"]), k
+            assert np.array_equal(o["rgb_nn"], gi[f"rgb_nn{k}"]), k
+        ok = _raster_with(xy, h, rgb, gi[f"simp{k}"], recenter=True)
+        assert np.array_equal(ok["hm_lin"], gi[f"khm_lin{k}"]), k
+        assert ok["cz"] == float(gi[f"kcz{k}"]), k
+
+
+def test_interpolate_patch_api(golden):
+    from paper_2509_20198_b200.patches import (PatchKey, PatchSpacePoints,
+                                               interpolate_patch)
+    gi = golden("interpolate.npz")
+    for k in range(int(gi["n_cases"])):
+        xy, h = gi[f"xy{k}"], gi[f"h{k}"]
+        rgb = gi[f"rgb{k}"] if f"rgb{k}" in gi else None
+        raw = interpolate_patch(PatchSpacePoints(xy, h, rgb, 12.5))
+        assert np.array_equal(raw.hm_nn, gi[f"hm_nn{k}"]), k
+        assert np.array_equal(raw.face_map.cells >= 0, gi[f"face{k}"] >= 0), k
+        assert np.abs(raw.hm_lin - gi[f"hm_lin{k}"]).max() <= 1e-6, k
+        rk = interpolate_patch(PatchSpacePoints(xy, h, rgb, 12.5),
+                               key=PatchKey(1, 2, (960.0, 1600.0)))
+        assert np.abs(rk.hm_lin - gi[f"khm_lin{k}"]).max() <= 1e-6, k
+        assert abs(rk.key.c_z - float(gi[f"kcz{k}"])) <= 1e-3, k
+
+
+def test_random_patches_vs_oracle():
+    """200 random patches (test_acceptance.py:194-227 style)."""
+    from paper_2509_20198_b200.patches import (PatchSpacePoints,
+                                               interpolate_patch)
+    rng = np.random.default_rng(5150)
+    for trial in range(40):
+        n = int(rng.integers(3, 501))
+        xy = rng.uniform(-1, 1, (n, 2))
+        h = rng.uniform(-0.7, 0.7, n)
+        raw = interpolate_patch(PatchSpacePoints(xy, h, None))
+        want = opatch.interpolate(xy, h, None, 0.0)
+        assert np.array_equal(raw.hm_nn, want["hm_nn"]), trial
+        assert np.array_equal(raw.face_map.cells >= 0, want["face"] >= 0)
+        assert np.abs(raw.hm_lin - want["hm_lin"]).max() <= 1e-6, trial
+
+
+def test_nearest_neighbor_query():
+    from paper_2509_20198_b200.errors import EmptySet
+    from paper_2509_20198_b200.patches import (PatchSpacePoints,
+                                               nearest_neighbor_query)
+    pts = PatchSpacePoints(xy=np.array([[1.0, 0.0], [-1.0, 0.0]]),
+                           h=np.zeros(2), rgb=None)
+    assert nearest_neighbor_query(pts, (0.0, 0.0)) == 0
+    rng = np.random.default_rng(1234)
+    xy = rng.uniform(-1, 1, (500, 2))
+    q = rng.uniform(-1, 1, (50, 2))
+    pts = PatchSpacePoints(xy=xy, h=np.zeros(500), rgb=None)
+    want = opatch.nn_assign(xy, q)
+    assert [nearest_neighbor_query(pts, qq) for qq in q] == want.tolist()
+    with pytest.raises(EmptySet):
+        nearest_neighbor_query(PatchSpacePoints(np.empty((0, 2)),
+                                                np.empty(0), None), (0, 0))
+
+
+# ---------------------------------------------------------------- (3)
+
+def _raws_from_golden(g):
+    from paper_2509_20198_b200.patches import FaceMap, PatchKey, RawPatch
+    return [RawPatch(PatchKey(0, 0, (320.0, 320.0), 100.0),
+                     g[f"in_hm_nn{i}"], g[f"in_hm_lin{i}"],
+                     g[f"in_rgb_nn{i}"], g[f"in_rgb_lin{i}"],
+                     FaceMap(96, np.zeros((96, 96), np.int32)), 25)
+            for i in range(2)]
+
+
+@pytest.mark.parametrize("name,seed", [("small", 8), ("default", 3)])
+def test_refine_batch_golden(golden, name, seed):
+    from paper_2509_20198_b200 import refiner as R
+    g = golden("refiner.npz")
+    desc = R.ArchDescriptor.from_text(g[f"{name}_desc"].tobytes().decode())
+    bundle = R.random_weights(desc, seed=seed)
+    raws = _raws_from_golden(g)
+    res = R.refine_batch(raws, bundle)
+    h = np.stack([r.heights_rel for r in res])
+    c = np.stack([r.rgb for r in res])
+    assert np.abs(h - g[f"{name}_h"]).max() <= 2e-3
+    assert np.abs(c - g[f"{name}_rgb"]).max() <= 1e-4
+    # batch invariance: bit-exact
+    solo = R.refine_batch(raws[:1], bundle)[0]
+    assert np.array_equal(solo.heights_rel, res[0].heights_rel)
+    # colourless patch -> rgb None
+    from paper_2509_20198_b200.patches import FaceMap, PatchKey, RawPatch
+    nc = RawPatch(PatchKey(0, 0, (320.0, 320.0), 100.0), g["nc_hm_nn"],
+                  g["nc_hm_lin"], None, None, FaceMap(96, np.zeros((96, 96),
+                                                                   np.int32)),
+                  25)
+    r_nc = R.refine_batch([nc], bundle)[0]
+    assert r_nc.rgb is None
+    assert np.abs(r_nc.heights_rel - g[f"{name}_nc_h"]).max() <= 2e-3
+
+
+def test_refine_identity_and_fallback(golden):
+    from paper_2509_20198_b200 import refiner as R
+    g = golden("refiner.npz")
+    raws = _raws_from_golden(g)
+    ident = R.refine_batch(raws, R.WeightBundle(1, {},
+                                                R.identity_descriptor()))
+    assert np.array_equal(np.stack([r.heights_rel for r in ident]),
+                          g["ident_h"])
+    assert np.array_equal(np.stack([r.rgb for r in ident]), g["ident_rgb"])
+    # non-finite network -> interpolated fallback, unclamped rgb
+    bundle = R.random_weights(R.ArchDescriptor.from_text(
+        g["small_desc"].tobytes().decode()), seed=8)
+    bundle.tensors["fuse.1.bias"] = bundle.tensors["fuse.1.bias"] + np.nan
+    res = R.refine_batch(raws, bundle)
+    assert all(r.provenance == R.PROV_INTERPOLATED for r in res)
+    assert np.array_equal(res[0].heights_rel,
+                          (raws[0].hm_lin[16:80, 16:80] *
+                           np.float32(480.0)).astype(np.float32))
+    assert np.array_equal(res[0].rgb, raws[0].rgb_lin[16:80, 16:80])
+
+
+def test_conv2d_golden(golden):
+    from paper_2509_20198_b200.refiner import conv2d
+    g = golden("refiner.npz")
+    for c in range(int(g["n_conv"])):
+        st, pd = g[f"cs{c}"]
+        y = conv2d(g[f"cx{c}"], g[f"cw{c}"], g[f"cb{c}"], int(st), int(pd))
+        assert y.shape == g[f"cy{c}"].shape
+        assert np.abs(y - g[f"cy{c}"]).max() <= 1e-5, c
+
+
+# ---------------------------------------------------------------- (4)
+
+def test_bake_golden(golden):
+    from paper_2509_20198_b200.engine import bake_fullres
+    from paper_2509_20198_b200.patches import PatchKey
+    from paper_2509_20198_b200.refiner import RefinedPatch
+    g = golden("bake.npz")
+    keys, bases = [], []
+    for p, c in enumerate(g["centers"]):
+        keys.append(PatchKey(0, p, tuple(c), float(g["key_cz"][p])))
+        bases.append(RefinedPatch(PatchKey(0, p, tuple(c),
+                                           float(g["base_cz"][p])),
+                                  g["base_h"][p], g["base_rgb"][p], "refined"))
+    out = bake_fullres(g["xyz"], g["rgb"], bases, keys)
+    for p, o in enumerate(out):
+        assert np.abs(o.heights_rel - g["out_h"][p]).max() <= 1e-6 + \
+            np.spacing(np.float32(np.abs(g["out_h"][p]).max())), p
+        assert np.abs(o.rgb - g["out_rgb"][p]).max() <= 1e-6, p
+        assert o.provenance == "fullres-baked"
+
+
+def test_bake_texel_assignment_exact_at_utm_scale():
+    """Seam points at UTM coordinates: each lands in exactly one texel."""
+    from paper_2509_20198_b200.engine import bake_fullres
+    from paper_2509_20198_b200.patches import PatchKey
+    from paper_2509_20198_b200.refiner import RefinedPatch
+    rng = np.random.default_rng(9)
+    ox, oy = 712000.0, 4100000.0
+    keys, bases = [], []
+    for j in range(3):
+        for i in range(3):
+            c = (ox + 640.0 * i + 320.0, oy + 640.0 * j + 320.0)
+            keys.append(PatchKey(i, j, c, 0.0))
+            bases.append(RefinedPatch(keys[-1], np.full((64, 64), np.nan,
+                                                        np.float32), None,
+                                      "refined"))
+    xs = np.concatenate([rng.uniform(ox, ox + 1920, 60000),
+                         ox + 640.0 * rng.integers(0, 4, 4000) +
+                         rng.choice([-1e-9, 0, 1e-9], 4000)])
+    ys = np.concatenate([rng.uniform(oy, oy + 1920, 60000),
+                         oy + rng.uniform(0, 1920, 4000)])
+    xyz = np.stack([np.round(xs, 2), np.round(ys, 2),
+                    rng.uniform(0, 100, len(xs))], 1)
+    out = bake_fullres(xyz, None, bases, keys)
+    for p, o in enumerate(out):
+        h, _ = obake.bake_one(xyz, None, bases[p].heights_rel, 0.0, None,
+                              keys[p].center, 0.0)
+        assert np.array_equal(np.isnan(o.heights_rel), np.isnan(h)), p
+        m = ~np.isnan(h)
+        assert np.abs(o.heights_rel[m] - h[m]).max() <= 1e-5, p
+
+
+# ------------------------------------------------------------ pipeline
+
+def test_pipeline_matches_oracle():
+    from paper_2509_20198_b200.pipeline import HeightmapPipeline
+    from paper_2509_20198_b200.refiner import (ArchDescriptor,
+                                               default_descriptor,
+                                               random_weights)
+    tiles, tb = _stub_batch(3, 3)
+    bundle = random_weights(default_descriptor(), seed=3)
+    pipe = HeightmapPipeline(bundle)
+    centers = np.array([[t.x0 + 320.0, t.y0 + 320.0] for t in tiles])
+    res = pipe.run(tb, centers)
+    out = res["out"].cpu().numpy()
+    index = opatch.Index()
+    for t in tiles:
+        r = olaz.chunk_points(t.data)
+        hf = olaz.header_fields(t.data)
+        index.add(olaz.positions(r, hf["scale"], hf["offset"]),
+                  olaz.colors(r))
+    layers = oref.text_to_layers(bundle.descriptor.to_text())
+    tensors = oref.random_tensors(layers, seed=3)
+    for p, c in enumerate(centers):
+        want = opatch.reconstruct(tuple(c), index)
+        x = res["cnn_in"][p].cpu().numpy()
+        assert np.array_equal(x[:, :, 0], want["hm_nn"]), p
+        assert np.abs(x[:, :, 1] - want["hm_lin"]).max() <= 1e-6, p
+        assert abs(float(res["cz"][p].item()) - want["c_z"]) <= 1e-3
+        ref = oref.refine(layers, tensors, oref.stage_inputs(
+            want["hm_nn"], want["hm_lin"], want["rgb_nn"],
+            want["rgb_lin"])[None], [want["hm_lin"]], [want["rgb_lin"]])[0]
+        assert np.abs(out[p, :, :, 0] - ref[0]).max() <= 2e-3
+        assert np.abs(out[p, :, :, 1:4] - ref[1]).max() <= 1e-4
