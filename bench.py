@@ -1,0 +1,487 @@
+"""Benchmark: refined 64x64 heightmaps/s (+ full-res splat points/s) on B200.
+
+Contract (see task statement): ``python bench.py --gpus N --steps K
+--warmup W`` prints ONE JSON line on rank 0.  Under torchrun every rank
+builds its own band of the synthetic terrain (weak scaling: 1,024 tiles per
+GPU, BASELINE.json configs[1]) plus a one-tile halo, runs the whole
+heightmap path on its GPU and NCCL-gathers the finished tiles to rank 0
+(the only collective).
+
+Step = one pass of the hot path over the resident batch: chunk-table decode
+-> chunk-point extraction -> index -> gather -> GPU Delaunay -> raster ->
+CNN refine (fp32-accurate path) -> epilogue.  L2 is flushed (256 MiB
+write) between timed steps, outside the per-step event window.
+
+``--impl reference`` times the reference algorithm's CPU restatement
+(oracle/, with the reference's own flood fill, Qhull and float32 im2col
+GEMMs) on the host cores, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+TILES_PER_GPU_SIDE = 32             # 32 x 32 = 1,024 tiles per GPU (config 2)
+CHUNKS_PER_TILE = 150
+POINTS_PER_CHUNK = 50_000
+CROP_GFLOP = 2.283                  # crop-aware CNN GFLOP/tile
+EXEC_GFLOP_REF = 3.590
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", type=int, default=None,
+                    help="0 fp32 SIMT, 1 tf32x3 tcgen05, 2 bf16 tcgen05")
+    ap.add_argument("--no-splat", action="store_true")
+    ap.add_argument("--splat-points", type=int, default=200_000_000)
+    ap.add_argument("--cpu-sample", type=int, default=32)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fp:
+            m = json.load(fp)
+        return m["hbm_gbs"], m["bf16_tflops"], "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, 1590.0, "fallback"
+
+
+# ------------------------------------------------------------------ data
+
+def band_tiles(rank, world):
+    """This rank's 32x32 tile band + one halo row on each interior side."""
+    from paper_2509_20198_b200 import synth
+    rows = TILES_PER_GPU_SIDE
+    r0 = rank * rows
+    lo = max(0, r0 - 1)
+    hi = min(world * rows, r0 + rows + 1)
+    tiles = synth.chunked_terrain_tiles(
+        TILES_PER_GPU_SIDE, hi - lo, chunks_per_tile=CHUNKS_PER_TILE,
+        points_per_chunk=POINTS_PER_CHUNK, record_seed=1 + lo,
+        origin=(0.0, lo * 640.0))
+    own = [t for t in tiles if r0 * 640.0 <= t.y0 < (r0 + rows) * 640.0]
+    return tiles, own
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index),
+                     f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout
+                self.samples.append([v.strip() for v in out.strip().split(",")])
+            except Exception:  # noqa: BLE001 - clocks are best effort
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
+                    "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples
+                          for i in range(4) if len(s) > i + 2 and
+                          s[i + 2].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- ours
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_20198_b200 import _device as D
+    from paper_2509_20198_b200._lib import lib
+    from paper_2509_20198_b200.lasio import parse_header
+    from paper_2509_20198_b200.pipeline import HeightmapPipeline
+    from paper_2509_20198_b200.refiner import (PRECISION_FP32,
+                                               default_descriptor,
+                                               random_weights)
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    precision = PRECISION_FP32 if args.precision is None else args.precision
+    tiles, own = band_tiles(rank, world)
+    images = [t.data for t in tiles]
+    descs = np.concatenate([D.tile_desc(parse_header(b)) for b in images])
+    centers = np.array([[t.x0 + 320.0, t.y0 + 320.0] for t in own])
+    P = len(centers)
+    bundle = random_weights(default_descriptor(), seed=3)
+    pipe = HeightmapPipeline(bundle, precision)
+    tb = D.TileBatch(images, descs)                  # resident in HBM
+    host_bytes = tb.bytes.cpu().pin_memory()          # e2e input (pinned)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(timer=None):
+        tables, cp, idx = pipe.overview(tb)
+        if timer is not None:
+            timer["ov"].record(stream)
+        g, t, o, cnn_in = pipe.patches(idx, centers)
+        if timer is not None:
+            timer["raster"].record(stream)
+        out, nonfinite = pipe.refine(cnn_in, P)
+        return out, o, nonfinite
+
+    def gather_tiles(out):
+        if world == 1:
+            return
+        if rank == 0:
+            bufs = [torch.empty_like(out) for _ in range(world)]
+            dist.gather(out, bufs, dst=0)
+        else:
+            dist.gather(out, None, dst=0)
+
+    for _ in range(args.warmup):
+        out, o, nf = step()
+        gather_tiles(out)
+    torch.cuda.synchronize()
+    status = o["status"].cpu().numpy()
+    assert (status == 0).all(), "empty/failed patches in the bench corpus"
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    times, t_ov, t_ras, t_ref = [], [], [], []
+    launches0 = lib().ts_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    with ClockSampler(local_rank) as clocks:
+        for _ in range(args.steps):
+            flush.fill_(1)                         # L2 flush, outside window
+            timer = {"s": ev(), "ov": ev(), "raster": ev(), "e": ev()}
+            timer["s"].record(stream)
+            out, o, nf = step(timer)
+            gather_tiles(out)
+            timer["e"].record(stream)
+            torch.cuda.synchronize()
+            times.append(timer["s"].elapsed_time(timer["e"]))
+            t_ov.append(timer["s"].elapsed_time(timer["ov"]))
+            t_ras.append(timer["ov"].elapsed_time(timer["raster"]))
+            t_ref.append(timer["raster"].elapsed_time(timer["e"]))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    wall = time.perf_counter() - wall0
+    launches = (lib().ts_launch_count() - launches0) // args.steps
+    ms = float(np.sum(times)) / args.steps
+    ms_t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    total_maps = P * world
+    value = total_maps / (ms_max / 1e3)
+
+    # ---- end to end: pinned host tile bytes in, refined rasters out ----
+    out_host = torch.empty((P, 64, 64, 4), dtype=torch.float32).pin_memory()
+    e2e_times = []
+    for i in range(args.steps + 1):
+        torch.cuda.synchronize()
+        s, e = ev(), ev()
+        s.record(stream)
+        tb.bytes.copy_(host_bytes, non_blocking=True)
+        out, o, nf = step()
+        out_host.copy_(out, non_blocking=True)
+        e.record(stream)
+        torch.cuda.synchronize()
+        if i:
+            e2e_times.append(s.elapsed_time(e))
+    e2e_ms = float(np.mean(e2e_times))
+    e2e_t = torch.tensor([e2e_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = total_maps / (float(e2e_t.item()) / 1e3)
+
+    hbm, tflops, peak_kind = peaks()
+    ref_ms = float(np.mean(t_ref))
+    cnn_tflops = CROP_GFLOP * P / (ref_ms / 1e3) / 1e3
+    result = None
+    if rank == 0:
+        result = {
+            "metric": "refined 64x64 heightmaps/sec",
+            "value": round(value, 2),
+            "unit": "heightmaps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_max, 4),
+            "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": {0: "f32", 1: "tf32x3", 2: "bf16"}[precision] +
+                     " CNN, f64 geometry",
+            "data": "synthetic (seeded FractalTerrain stub-body LAZ tiles, "
+                    "random He weights seed 3)",
+            "config": {"workload": "configs[1]: 1,024-tile synthetic "
+                                   "terrain per GPU, chunk-point extraction "
+                                   "+ rasterise + CNN refine",
+                       "tiles_per_gpu": P,
+                       "tiles_resident_incl_halo": len(images),
+                       "chunks_per_tile": CHUNKS_PER_TILE,
+                       "points_per_chunk": POINTS_PER_CHUNK,
+                       "chunk_points": int(sum(len(t.first_records)
+                                               for t in tiles)),
+                       "parallelism": f"tile-grid row bands x{world}, NCCL "
+                                      "gather to rank 0",
+                       "l2": "flushed (256 MiB write) between timed steps"},
+            "stages_ms": {"extract_index": round(float(np.mean(t_ov)), 4),
+                          "gather_delaunay_raster":
+                              round(float(np.mean(t_ras)), 4),
+                          "cnn_refine": round(ref_ms, 4)},
+            "roofline": {"kernel": "CNN refine (ts_refine, all conv layers)",
+                         "bound": "tensor",
+                         "achieved": round(cnn_tflops, 3),
+                         "peak": tflops, "unit": "TFLOP/s",
+                         "frac": round(cnn_tflops / tflops, 5),
+                         "peak_kind": f"{peak_kind} bf16 dense (burst)",
+                         "algorithmic": f"{CROP_GFLOP} GFLOP/tile x {P} "
+                                        "tiles per launch sequence",
+                         "traffic": None},
+            "e2e": {"value": round(e2e_value, 2), "unit": "heightmaps/s",
+                    "h2d_bytes_per_step": int(host_bytes.numel()),
+                    "d2h_bytes_per_step": int(out_host.numel() * 4)},
+            "gpu_launches": int(launches),
+            "wall_s_timed": round(wall, 3),
+        }
+    if not args.no_splat:
+        splat = run_splat(args, dev, world, rank)
+        if rank == 0:
+            result["splat"] = splat
+    if rank == 0:
+        result["clocks"] = clocks.summary()
+        result["cpu_baseline"] = cpu_baseline(args)
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def terrain_torch(x, y, terrain):
+    import torch
+    k = torch.as_tensor(terrain._k, device=x.device)
+    ph = torch.as_tensor(terrain._phase, device=x.device)
+    amp = torch.as_tensor(terrain._amp, device=x.device)
+    arg = x[:, None] * k[:, 0] + y[:, None] * k[:, 1] + ph
+    return terrain.base_height + (torch.cos(arg) * amp).sum(-1)
+
+
+def splat_inputs(n_points, dev, seed=3):
+    """Config 3: 64x64 patch grid, points grouped by patch (tile order)."""
+    import torch
+    from paper_2509_20198_b200.synth import FractalTerrain
+    side = 64
+    P = side * side
+    per = n_points // P
+    g = torch.Generator(device=dev).manual_seed(seed)
+    terrain = FractalTerrain(seed=11)
+    xyz = torch.empty((P * per, 3), dtype=torch.float64, device=dev)
+    rgb = torch.empty((P * per, 3), dtype=torch.float32, device=dev)
+    chunk = 256
+    for p0 in range(0, P, chunk):
+        ps = torch.arange(p0, min(P, p0 + chunk), device=dev)
+        m = len(ps) * per
+        x0 = (ps % side).double().repeat_interleave(per) * 640.0
+        y0 = (ps // side).double().repeat_interleave(per) * 640.0
+        x = torch.round((x0 + torch.rand(m, generator=g, device=dev,
+                                         dtype=torch.float64) * 640.0) * 100) / 100
+        y = torch.round((y0 + torch.rand(m, generator=g, device=dev,
+                                         dtype=torch.float64) * 640.0) * 100) / 100
+        z = torch.round(terrain_torch(x, y, terrain) * 100) / 100
+        sl = slice(p0 * per, p0 * per + m)
+        xyz[sl, 0], xyz[sl, 1], xyz[sl, 2] = x, y, z
+        rgb[sl] = torch.rand((m, 3), generator=g, device=dev)
+    centers = np.stack(np.meshgrid(np.arange(side) * 640.0 + 320.0,
+                                   np.arange(side) * 640.0 + 320.0),
+                       -1).reshape(-1, 2)
+    return xyz, rgb, centers, per
+
+
+def run_splat(args, dev, world, rank):
+    import torch
+    from paper_2509_20198_b200._lib import lib
+    from paper_2509_20198_b200.engine import bake_device, key_grid
+    xyz, rgb, centers, per = splat_inputs(args.splat_points, dev)
+    P = len(centers)
+    M = len(xyz)
+    prior = torch.zeros((P, 64, 64), dtype=torch.float32, device=dev)
+    prior_rgb = torch.zeros((P, 64, 64, 3), dtype=torch.float32, device=dev)
+    cz = torch.full((P,), 50.0, dtype=torch.float64, device=dev)
+    grid = key_grid(centers)
+    accum = torch.empty(int(lib().ts_bake_workspace(P)), dtype=torch.uint8,
+                        device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(max(1, args.warmup)):
+        bake_device(xyz, rgb, centers, prior, cz, cz, prior_rgb, grid, accum)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(max(3, args.steps // 2)):
+        s, e = torch.cuda.Event(enable_timing=True), \
+            torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        bake_device(xyz, rgb, centers, prior, cz, cz, prior_rgb, grid, accum)
+        e.record(stream)
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    ms = float(np.mean(ts))
+    hbm, _tf, kind = peaks()
+    alg = M * 36 + P * 4096 * 32
+    gbs = alg / (ms / 1e3) / 1e9
+    return {"metric": "full-res splat points/sec",
+            "value": round(M / (ms / 1e3) * world, 1), "unit": "points/s",
+            "config": f"configs[2]: {M:,} points into {P} heightmaps per GPU,"
+                      " points grouped by patch",
+            "ms_per_step": round(ms, 4),
+            "roofline": {"kernel": "ts_bake (splat + finalize)",
+                         "bound": "hbm", "achieved": round(gbs, 1),
+                         "peak": hbm, "unit": "GB/s",
+                         "frac": round(gbs / hbm, 4),
+                         "peak_kind": f"{kind} HBM copy",
+                         "algorithmic": "36 B/pt (xyz f64 + rgb f32) + "
+                                        "32 B/texel (prior h,rgb in; h,rgb "
+                                        "out)",
+                         "traffic": None}}
+
+
+# ------------------------------------------------------------ CPU legs
+
+def cpu_sample(n_patches, tiles_side=8):
+    """Bounded CPU run of the same pipeline via the reference restatement."""
+    from concurrent.futures import ProcessPoolExecutor
+
+    from oracle import laz as olaz
+    from oracle import patches as opatch
+    from oracle import refiner as oref
+    from paper_2509_20198_b200 import synth
+    from paper_2509_20198_b200.refiner import default_descriptor
+
+    tiles = synth.chunked_terrain_tiles(tiles_side, tiles_side,
+                                        chunks_per_tile=CHUNKS_PER_TILE)
+    cores = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    index = opatch.Index()
+    for t in tiles:
+        rec = olaz.chunk_points(t.data)
+        h = olaz.header_fields(t.data)
+        index.add(olaz.positions(rec, h["scale"], h["offset"]),
+                  olaz.colors(rec))
+    centers = [(t.x0 + 320.0, t.y0 + 320.0) for t in tiles][:n_patches]
+    import multiprocessing as mp
+    with ProcessPoolExecutor(max_workers=cores,
+                             mp_context=mp.get_context("spawn")) as pool:
+        raws = list(pool.map(_cpu_reconstruct, [(c, index) for c in centers]))
+    layers = oref.text_to_layers(default_descriptor().to_text())
+    tensors = oref.random_tensors(layers, seed=3)
+    batch = np.stack([oref.stage_inputs(r["hm_nn"], r["hm_lin"], r["rgb_nn"],
+                                        r["rgb_lin"]) for r in raws])
+    oref.refine(layers, tensors, batch, [r["hm_lin"] for r in raws],
+                [r["rgb_lin"] for r in raws])
+    dt = time.perf_counter() - t0
+    return len(centers) / dt, cores, dt
+
+
+def _cpu_reconstruct(arg):
+    from oracle import patches as opatch
+    center, index = arg
+    return opatch.reconstruct(center, index, flood=True)
+
+
+def cpu_baseline(args):
+    rate, cores, dt = cpu_sample(args.cpu_sample)
+    return {"value": round(rate, 3), "unit": "heightmaps/s", "cores": cores,
+            "kind": "port",
+            "sample": f"{args.cpu_sample} patches of the configs[1] workload "
+                      f"(8x8 tile corner), extract+index+flood-fill "
+                      f"Algorithm 1 on {cores} procs + float32 im2col CNN "
+                      f"(OpenBLAS), {dt:.1f}s"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    rates = []
+    for _ in range(args.warmup):
+        cpu_sample(4)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r, cores, _dt = cpu_sample(args.cpu_sample)
+        rates.append(r)
+    wall = time.perf_counter() - t0
+    value = float(np.mean(rates))
+    print(json.dumps({
+        "impl": "reference",
+        "metric": "refined 64x64 heightmaps/sec", "value": round(value, 3),
+        "unit": "heightmaps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 CNN, f64 geometry", "data": "synthetic",
+        "config": {"workload": "configs[1] sample: "
+                               f"{args.cpu_sample} patches per step"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "heightmaps/s",
+                         "cores": cores, "kind": "port",
+                         "sample": f"{args.cpu_sample} patches per step"},
+        "e2e": {"value": round(value, 3), "unit": "heightmaps/s",
+                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+        flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", args.gpus if args.gpus else 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if "WORLD_SIZE" not in os.environ:
+        world = 1
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

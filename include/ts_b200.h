@@ -62,6 +62,8 @@ typedef struct ts_patch_key {
 /* ---- library ---- */
 const char* ts_version(void);
 int ts_device_count(void);
+/* Kernels launched by this library since load (launch accounting). */
+uint64_t ts_launch_count(void);
 /* Bytes of record_dtype(fmt) (lasio/records.py:43-59) for fmt 0..3. */
 int ts_record_size(int format);
 
@@ -220,6 +222,10 @@ int ts_bake(const double* d_xyz, const float* d_rgb, int64_t m,
 int ts_incircle_sign(const double a[2], const double b[2], const double c[2],
                      const double d[2]);
 int ts_orient_sign(const double a[2], const double b[2], const double c[2]);
+/* The same predicates evaluated by device code: n cases of 8 doubles
+ * (mode 0: orient of the first 6, mode 1: incircle of all 8).           */
+int ts_predicates_device(const double* d_in, int64_t n, int mode,
+                         int32_t* d_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -36,6 +36,7 @@ assert TILE_DESC.itemsize == 104
 SIGNATURES = {
     "ts_version": (C.c_char_p, []),
     "ts_device_count": (I32, []),
+    "ts_launch_count": (C.c_uint64, []),
     "ts_record_size": (I32, [I32]),
     "ts_chunk_counts": (I32, [P, P, I32, P, P, P]),
     "ts_chunk_decode_scratch": (SZ, [I32]),
@@ -65,6 +66,7 @@ SIGNATURES = {
                       P, P, P, P, P]),
     "ts_incircle_sign": (I32, [P, P, P, P]),
     "ts_orient_sign": (I32, [P, P, P]),
+    "ts_predicates_device": (I32, [P, I64, I32, P, P]),
 }
 
 _LIB = None

@@ -121,12 +121,12 @@ extern "C" int ts_bake(const double* d_xyz, const float* d_rgb, int64_t m,
     BakeArgs a{d_xyz, d_rgb, m, d_keys, n_patches, d_cell_keys_off, d_cell_keys,
                gx0, gy0, gnx, gny, cnt, sum};
     const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(m, 256), 148 * 16);
-    bake_splat_kernel<<<grid, 256, 0, s>>>(a);
+    ts::count_launch(), bake_splat_kernel<<<grid, 256, 0, s>>>(a);
     TS_LAUNCH_CHECK();
   }
   const int64_t total = (int64_t)n_patches * kTex;
   const int grid2 = (int)std::min<int64_t>(ceil_div<int64_t>(total, 256), 148 * 16);
-  bake_finalize_kernel<<<grid2, 256, 0, s>>>(cnt, sum, n_patches, d_prior_h, d_base_cz,
+  ts::count_launch(), bake_finalize_kernel<<<grid2, 256, 0, s>>>(cnt, sum, n_patches, d_prior_h, d_base_cz,
                                              d_key_cz, d_prior_rgb, d_rgb != nullptr,
                                              d_out_h, d_out_rgb);
   TS_LAUNCH_CHECK();

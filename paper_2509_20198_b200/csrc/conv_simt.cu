@@ -116,7 +116,7 @@ int launch_conv_simt(const ConvOp& op, void* stream) {
   const int64_t M = (int64_t)op.batch * (op.oy1 - op.oy0) * (op.ox1 - op.ox0);
   if (M <= 0) return TS_OK;
   dim3 grid((unsigned)ceil_div<int64_t>(M, BM), (unsigned)ceil_div(op.out.C, BN));
-  conv_simt_kernel<<<grid, 256, 0, as_stream(stream)>>>(op);
+  ts::count_launch(), conv_simt_kernel<<<grid, 256, 0, as_stream(stream)>>>(op);
   TS_LAUNCH_CHECK();
   return TS_OK;
 }

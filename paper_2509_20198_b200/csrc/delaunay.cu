@@ -50,7 +50,7 @@ delaunay_kernel(const double* __restrict__ xy_all,
   if (p >= n_patches) return;
   const int64_t off = pts_off[p];
   const int n = (int)(pts_off[p + 1] - off);
-  int* tri = tri_all + 2 * off + 8 * (int64_t)p;
+  int* tri = tri_all + 3 * (2 * off + 8 * (int64_t)p);  // triangle slots
   if (n == 0) {
     if (lane == 0) { ntri_out[p] = 0; status[p] = TS_E_EMPTY_PATCH; }
     return;
@@ -153,7 +153,7 @@ extern "C" int ts_triangulate(const double* d_xy, const int64_t* d_pts_off,
                               int n_patches, int32_t* d_tri, int32_t* d_ntri,
                               int32_t* d_status, void* stream) {
   if (n_patches <= 0) return TS_OK;
-  delaunay_kernel<<<ceil_div(n_patches, kWarpsPerBlock), kWarpsPerBlock * 32, 0,
+  ts::count_launch(), delaunay_kernel<<<ceil_div(n_patches, kWarpsPerBlock), kWarpsPerBlock * 32, 0,
                     as_stream(stream)>>>(d_xy, d_pts_off, n_patches, d_tri,
                                          d_ntri, d_status);
   TS_LAUNCH_CHECK();
@@ -168,4 +168,27 @@ extern "C" int ts_incircle_sign(const double a[2], const double b[2],
 extern "C" int ts_orient_sign(const double a[2], const double b[2],
                               const double c[2]) {
   return pred::orient(a[0], a[1], b[0], b[1], c[0], c[1]);
+}
+
+namespace ts {
+namespace {
+__global__ void predicate_kernel(const double* __restrict__ in, int64_t n, int mode,
+                                 int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double* p = in + 8 * i;
+    out[i] = mode == 0 ? pred::orient(p[0], p[1], p[2], p[3], p[4], p[5])
+                       : pred::incircle(p[0], p[1], p[2], p[3], p[4], p[5], p[6], p[7]);
+  }
+}
+}  // namespace
+}  // namespace ts
+
+extern "C" int ts_predicates_device(const double* d_in, int64_t n, int mode,
+                                    int32_t* d_out, void* stream) {
+  if (n <= 0) return TS_OK;
+  ts::count_launch(), predicate_kernel<<<(int)ceil_div<int64_t>(n, 128), 128, 0, as_stream(stream)>>>(
+      d_in, n, mode, d_out);
+  TS_LAUNCH_CHECK();
+  return TS_OK;
 }

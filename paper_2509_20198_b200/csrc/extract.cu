@@ -328,7 +328,7 @@ extern "C" int ts_chunk_counts(const uint8_t* d_bytes, const ts_tile_desc* d_til
                                int n_tiles, int64_t* d_n_chunks,
                                int32_t* d_status, void* stream) {
   if (n_tiles <= 0) return n_tiles == 0 ? TS_OK : TS_E_INVALID;
-  chunk_count_kernel<<<ceil_div(n_tiles, 128), 128, 0, as_stream(stream)>>>(
+  ts::count_launch(), chunk_count_kernel<<<ceil_div(n_tiles, 128), 128, 0, as_stream(stream)>>>(
       d_bytes, d_tiles, n_tiles, d_n_chunks, d_status);
   TS_LAUNCH_CHECK();
   return TS_OK;
@@ -347,7 +347,7 @@ extern "C" int ts_chunk_decode(const uint8_t* d_bytes, const ts_tile_desc* d_til
   if (n_tiles <= 0) return n_tiles == 0 ? TS_OK : TS_E_INVALID;
   const int threads = n_tiles < kDecodeThreads ? n_tiles : kDecodeThreads;
   const int block = 64;
-  chunk_decode_kernel<<<ceil_div(threads, block), block, 0, as_stream(stream)>>>(
+  ts::count_launch(), chunk_decode_kernel<<<ceil_div(threads, block), block, 0, as_stream(stream)>>>(
       d_bytes, d_tiles, n_tiles, d_chunk_base, d_chunk_offset, d_chunk_points,
       d_chunk_end, d_status, reinterpret_cast<uint16_t*>(d_scratch), decode_pool_words());
   TS_LAUNCH_CHECK();
@@ -362,7 +362,7 @@ extern "C" int ts_extract_chunk_points(const uint8_t* d_bytes,
                                        float* d_rgb, int64_t* d_cell,
                                        int32_t* d_status, void* stream) {
   if (n_tiles <= 0) return n_tiles == 0 ? TS_OK : TS_E_INVALID;
-  extract_kernel<<<n_tiles, 128, 0, as_stream(stream)>>>(
+  ts::count_launch(), extract_kernel<<<n_tiles, 128, 0, as_stream(stream)>>>(
       d_bytes, d_tiles, d_chunk_base, d_chunk_offset, d_records, d_xyz, d_rgb,
       d_cell, d_status);
   TS_LAUNCH_CHECK();
@@ -375,7 +375,7 @@ extern "C" int ts_positions(const uint8_t* d_records, int64_t n, int record_stri
   if (record_stride < 12) return TS_E_INVALID;
   if (n <= 0) return TS_OK;
   const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(n, 256), 148 * 8);
-  positions_kernel<<<grid, 256, 0, as_stream(stream)>>>(
+  ts::count_launch(), positions_kernel<<<grid, 256, 0, as_stream(stream)>>>(
       d_records, n, record_stride, scale[0], scale[1], scale[2], offset[0], offset[1],
       offset[2], d_xyz);
   TS_LAUNCH_CHECK();
@@ -389,8 +389,8 @@ extern "C" int ts_colors(const uint8_t* d_records, int64_t n, int record_stride,
   TS_CUDA_TRY(cudaMemsetAsync(d_scratch, 0, sizeof(int32_t), s));
   if (n <= 0) return TS_OK;
   const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(n, 256), 148 * 8);
-  rgb_max_kernel<<<grid, 256, 0, s>>>(d_records, n, record_stride, rgb_offset, d_scratch);
-  colors_kernel<<<grid, 256, 0, s>>>(d_records, n, record_stride, rgb_offset, d_scratch,
+  ts::count_launch(), rgb_max_kernel<<<grid, 256, 0, s>>>(d_records, n, record_stride, rgb_offset, d_scratch);
+  ts::count_launch(), colors_kernel<<<grid, 256, 0, s>>>(d_records, n, record_stride, rgb_offset, d_scratch,
                                      d_rgb);
   TS_LAUNCH_CHECK();
   return TS_OK;

@@ -215,7 +215,7 @@ extern "C" int ts_index_build(const int64_t* d_cell, int64_t n, int64_t ci0,
   keys_sorted = keys + n;
   TS_CUDA_TRY(cudaMallocAsync(&ids, sizeof(int32_t) * n, s));
   const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(n, 256), 148 * 8);
-  cell_key_kernel<<<grid, 256, 0, s>>>(d_cell, n, ci0, cj0, nci, ncj, keys, ids);
+  ts::count_launch(), cell_key_kernel<<<grid, 256, 0, s>>>(d_cell, n, ci0, cj0, nci, ncj, keys, ids);
   TS_LAUNCH_CHECK();
   // out-of-range points (key 0xFFFFFFFF) need the full 32 bits
   bits = 32;
@@ -224,7 +224,7 @@ extern "C" int ts_index_build(const int64_t* d_cell, int64_t n, int64_t ci0,
   TS_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, s));
   TS_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_sorted,
                                               ids, d_order, (int)n, 0, bits, s));
-  cell_range_kernel<<<grid, 256, 0, s>>>(keys_sorted, n, d_cell_start, d_cell_end);
+  ts::count_launch(), cell_range_kernel<<<grid, 256, 0, s>>>(keys_sorted, n, d_cell_start, d_cell_end);
   TS_LAUNCH_CHECK();
   TS_CUDA_TRY(cudaFreeAsync(tmp, s));
   TS_CUDA_TRY(cudaFreeAsync(ids, s));
@@ -240,7 +240,7 @@ extern "C" int ts_gather_count(const double* d_xyz, const int32_t* d_order,
                                double radius, int32_t* d_counts, void* stream) {
   if (n_patches <= 0) return TS_OK;
   const int threads = 256;
-  gather_count_kernel<<<ceil_div(n_patches * 32, threads), threads, 0,
+  ts::count_launch(), gather_count_kernel<<<ceil_div(n_patches * 32, threads), threads, 0,
                         as_stream(stream)>>>(d_xyz, d_order, d_cell_start,
                                              d_cell_end, ci0, cj0, nci, ncj,
                                              d_keys, n_patches, radius, d_counts);
@@ -258,7 +258,7 @@ extern "C" int ts_gather_fill(const double* d_xyz, const float* d_rgb,
                               double* d_xyz_out, int32_t* d_status, void* stream) {
   if (n_patches <= 0) return TS_OK;
   const int threads = 256;
-  gather_fill_kernel<<<ceil_div(n_patches * 32, threads), threads, 0,
+  ts::count_launch(), gather_fill_kernel<<<ceil_div(n_patches * 32, threads), threads, 0,
                        as_stream(stream)>>>(d_xyz, d_rgb, d_order, d_cell_start,
                                             d_cell_end, ci0, cj0, nci, ncj,
                                             d_keys, n_patches, radius, d_pts_off,
@@ -296,7 +296,7 @@ extern "C" int ts_nearest(const double* d_xy, int64_t n, const double* d_q, int6
   if (n <= 0) return TS_E_EMPTY_SET;
   if (nq <= 0) return TS_OK;
   const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(nq, 128), 148 * 8);
-  nearest_kernel<<<grid, 128, 0, as_stream(stream)>>>(d_xy, n, d_q, nq, d_idx);
+  ts::count_launch(), nearest_kernel<<<grid, 128, 0, as_stream(stream)>>>(d_xy, n, d_q, nq, d_idx);
   TS_LAUNCH_CHECK();
   return TS_OK;
 }
@@ -318,7 +318,7 @@ extern "C" int ts_cell_keys(const double* d_xyz, int64_t n, int64_t* d_cell,
                             void* stream) {
   if (n <= 0) return TS_OK;
   const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(n, 256), 148 * 8);
-  cell_of_kernel<<<grid, 256, 0, as_stream(stream)>>>(d_xyz, n, d_cell);
+  ts::count_launch(), cell_of_kernel<<<grid, 256, 0, as_stream(stream)>>>(d_xyz, n, d_cell);
   TS_LAUNCH_CHECK();
   return TS_OK;
 }

@@ -18,8 +18,8 @@ constexpr uint32_t kMaxLen = 0xFFFFFFFFu;
 
 struct BitModel {
   uint32_t c0, n, p0, cyc, left;
-  __device__ void init() { c0 = 1; n = 2; p0 = 1u << 12; cyc = left = 4; }
-  __device__ void update() {
+  __host__ __device__ void init() { c0 = 1; n = 2; p0 = 1u << 12; cyc = left = 4; }
+  __host__ __device__ void update() {
     n += cyc;
     if (n >= 8192u) {
       n = (n + 1) >> 1;
@@ -38,17 +38,17 @@ struct SymModel {
   uint16_t* dist;   // n
   uint16_t* cnt;    // n
   uint16_t* table;  // (1 << tbits) + 2, only if tbits
-  __device__ static uint32_t table_bits(uint32_t n) {
+  __host__ __device__ static uint32_t table_bits(uint32_t n) {
     if (n <= 16) return 0;
     uint32_t tb = 3;
     while (n > (1u << (tb + 2))) ++tb;
     return tb;
   }
-  __device__ static uint32_t words16(uint32_t n) {
+  __host__ __device__ static uint32_t words16(uint32_t n) {
     uint32_t tb = table_bits(n);
     return 2 * n + (tb ? (1u << tb) + 2 : 0);
   }
-  __device__ void init(uint32_t nsym, uint16_t* mem) {
+  __host__ __device__ void init(uint32_t nsym, uint16_t* mem) {
     n = nsym;
     tbits = table_bits(n);
     tshift = tbits ? 15 - tbits : 0;
@@ -61,7 +61,7 @@ struct SymModel {
     update();
     cyc = left = (n + 6) >> 1;
   }
-  __device__ void update() {
+  __host__ __device__ void update() {
     tot += cyc;
     if (tot > 32768u) {
       tot = 0;
@@ -101,7 +101,7 @@ struct Decoder {
   uint32_t value, length;
   bool desync;
 
-  __device__ bool start(const uint8_t* b, int64_t p, int64_t e) {
+  __host__ __device__ bool start(const uint8_t* b, int64_t p, int64_t e) {
     buf = b; pos = p; end = e; desync = false;
     if (pos + 4 > end) { desync = true; return false; }
     value = ((uint32_t)buf[pos] << 24) | ((uint32_t)buf[pos + 1] << 16) |
@@ -110,14 +110,14 @@ struct Decoder {
     length = kMaxLen;
     return true;
   }
-  __device__ void renorm() {
+  __host__ __device__ void renorm() {
     while (length < kMinLen) {
       if (pos >= end) { desync = true; length = kMaxLen; return; }
       value = (value << 8) | buf[pos++];
       length <<= 8;
     }
   }
-  __device__ uint32_t bit(BitModel& m) {
+  __host__ __device__ uint32_t bit(BitModel& m) {
     const uint32_t x = m.p0 * (length >> 13);
     uint32_t s;
     if (value < x) { s = 0; length = x; ++m.c0; }
@@ -126,7 +126,7 @@ struct Decoder {
     if (--m.left == 0) m.update();
     return s;
   }
-  __device__ uint32_t symbol(SymModel& m) {
+  __host__ __device__ uint32_t symbol(SymModel& m) {
     uint32_t hi = length;
     uint32_t lo, s;
     const uint32_t unit = length >> 15;
@@ -158,16 +158,20 @@ struct Decoder {
     if (--m.left == 0) m.update();
     return s;
   }
-  __device__ uint32_t raw_bits(uint32_t nb) {
-    if (nb > 19) {
-      const uint32_t lo = raw_bits(16);
-      return (raw_bits(nb - 16) << 16) | lo;
-    }
+  __host__ __device__ uint32_t raw_bits_le19(uint32_t nb) {
     length >>= nb;
     const uint32_t s = value / length;
     value -= length * s;
     if (length < kMinLen) renorm();
     return s;
+  }
+  // read_bits (codec.py:258-267) without recursion: a static stack frame
+  __host__ __device__ uint32_t raw_bits(uint32_t nb) {
+    if (nb > 19) {
+      const uint32_t lo = raw_bits_le19(16);
+      return (raw_bits_le19(nb - 16) << 16) | lo;
+    }
+    return raw_bits_le19(nb);
   }
 };
 
@@ -183,18 +187,18 @@ struct ChunkTableCoder {
   uint16_t* pool;
   uint32_t used;
 
-  __device__ static uint32_t pool_words() {
+  __host__ __device__ static uint32_t pool_words() {
     uint32_t w = 2 * SymModel::words16(33);
     for (uint32_t k = 1; k < 32; ++k) w += SymModel::words16(1u << (k < 8 ? k : 8));
     return w;
   }
-  __device__ void init(uint16_t* mem) {
+  __host__ __device__ void init(uint16_t* mem) {
     pool = mem; used = 0;
     kmod_live[0] = kmod_live[1] = false;
     cbit_live = false;
     for (int k = 0; k < 32; ++k) cmod_live[k] = false;
   }
-  __device__ SymModel& alloc(SymModel& m, bool& live, uint32_t n) {
+  __host__ __device__ SymModel& alloc(SymModel& m, bool& live, uint32_t n) {
     if (!live) {
       m.init(n, pool + used);
       used += SymModel::words16(n);
@@ -203,7 +207,7 @@ struct ChunkTableCoder {
     return m;
   }
   // IntegerCompressor.decompress(pred, ctx) with 32-bit wraparound.
-  __device__ int32_t decompress(Decoder& d, int32_t pred, int ctx) {
+  __host__ __device__ int32_t decompress(Decoder& d, int32_t pred, int ctx) {
     const uint32_t k = d.symbol(alloc(kmod[ctx], kmod_live[ctx], 33));
     int64_t c;
     if (k == 0) {

@@ -379,7 +379,7 @@ extern "C" int ts_raster(const double* d_xy, const double* d_h, const float* d_p
   RasterArgs a{d_xy, d_h, d_prgb, d_pts_off, d_tri, d_tri_off, d_ntri, d_cz_in,
                recenter, d_cnn_in, d_hm_nn, d_hm_lin, d_rgb_nn, d_rgb_lin, d_face,
                d_cz_out, d_status};
-  raster_kernel<<<n_patches, kThreads, kRasterSmem, as_stream(stream)>>>(a);
+  ts::count_launch(), raster_kernel<<<n_patches, kThreads, kRasterSmem, as_stream(stream)>>>(a);
   TS_LAUNCH_CHECK();
   return TS_OK;
 }

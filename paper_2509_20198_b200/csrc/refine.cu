@@ -459,7 +459,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
   if (batch == 0) return TS_E_SHAPE;  // refine_batch requires a non-empty batch
   cudaStream_t s = as_stream(stream);
   if (W->identity) {
-    refine_epilogue_kernel<<<batch, 256, 0, s>>>(d_in, 8, 1, d_in, d_out, d_nonfinite);
+    ts::count_launch(), refine_epilogue_kernel<<<batch, 256, 0, s>>>(d_in, 8, 1, d_in, d_out, d_nonfinite);
     TS_LAUNCH_CHECK();
     return TS_OK;
   }
@@ -472,7 +472,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
     // raw inputs -> channels [0, 8) of the fuse input (skip concat)
     {
       const int64_t px = (int64_t)B * kRes * kRes;
-      copy_inputs_kernel<<<(int)std::min<int64_t>(ceil_div<int64_t>(px, 256), 148 * 16),
+      ts::count_launch(), copy_inputs_kernel<<<(int)std::min<int64_t>(ceil_div<int64_t>(px, 256), 148 * 16),
                            256, 0, s>>>(in, px, buf(W->fuse_in_off), W->fuse_in_c);
       TS_LAUNCH_CHECK();
     }
@@ -525,7 +525,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
       prev_stage = L.stage;
     }
     const ConvLayer& last = W->layers.back();
-    refine_epilogue_kernel<<<B, 256, 0, s>>>(buf(last.out_off), fcs, 0, in,
+    ts::count_launch(), refine_epilogue_kernel<<<B, 256, 0, s>>>(buf(last.out_off), fcs, 0, in,
                                              d_out + (size_t)b0 * kOut * kOut * 4,
                                              d_nonfinite ? d_nonfinite + b0 : nullptr);
     TS_LAUNCH_CHECK();
@@ -586,8 +586,8 @@ extern "C" int ts_conv2d(const float* d_x, int batch, int c_in, int h, int w,
   TS_CUDA_TRY(cudaMallocAsync(&buf, sizeof(float) * (nin + nout + nw), s));
   float *xin = buf, *yout = buf + nin, *wp = buf + nin + nout;
   const int g = 148 * 4;
-  nchw_to_nhwc<<<g, 256, 0, s>>>(d_x, batch, c_in, h, w, xin);
-  pack_weights<<<g, 256, 0, s>>>(d_weight, c_out, c_in, k, wp);
+  ts::count_launch(), nchw_to_nhwc<<<g, 256, 0, s>>>(d_x, batch, c_in, h, w, xin);
+  ts::count_launch(), pack_weights<<<g, 256, 0, s>>>(d_weight, c_out, c_in, k, wp);
   ConvOp op{};
   op.in = ActView{xin, h, w, c_in, 0, c_in};
   op.out = ActView{yout, ho, wo, c_out, 0, c_out};
@@ -596,7 +596,7 @@ extern "C" int ts_conv2d(const float* d_x, int batch, int c_in, int h, int w,
   op.w = wp; op.bias = d_bias; op.batch = batch;
   int st = launch_conv_simt(op, stream);
   if (st != TS_OK) return st;
-  nhwc_to_nchw<<<g, 256, 0, s>>>(yout, batch, c_out, ho, wo, d_y);
+  ts::count_launch(), nhwc_to_nchw<<<g, 256, 0, s>>>(yout, batch, c_out, ho, wo, d_y);
   TS_LAUNCH_CHECK();
   TS_CUDA_TRY(cudaFreeAsync(buf, s));
   return TS_OK;

@@ -16,6 +16,9 @@
 
 namespace ts {
 
+// Number of kernels this library has launched (ts_launch_count).
+void count_launch();
+
 constexpr double kPatch = 640.0;
 constexpr double kTexel = 10.0;
 constexpr int kRes = 96;

@@ -87,12 +87,13 @@ def test_corrupt_table_is_reported():
     from paper_2509_20198_b200 import synth
     from paper_2509_20198_b200.lasio import parse_header
     t = synth.chunked_terrain_tiles(1, 1, chunks_per_tile=20)[0]
-    bad = bytearray(t.data)
-    bad[-6:] = b"\xff" * 6           # trash the arithmetic-coded table tail
+    pdo = parse_header(t.data).point_data_offset
     ptr = bytearray(t.data)
-    ptr[parse_header(t.data).point_data_offset:][:8] = (10 ** 12).to_bytes(
-        8, "little")
-    for img in (bytes(ptr),):
+    ptr[pdo:pdo + 8] = (10 ** 12).to_bytes(8, "little")   # pointer past EOF
+    ver = bytearray(t.data)
+    tpos = int.from_bytes(t.data[pdo:pdo + 8], "little")
+    ver[tpos:tpos + 4] = (3).to_bytes(4, "little")        # table version 3
+    for img in (bytes(ptr), bytes(ver)):
         tb = D.TileBatch([img], D.tile_desc(parse_header(img)))
         tables = D.ChunkTables(tb)
         assert int(tables.status[0].item()) == 6
@@ -137,11 +138,42 @@ def _gpu_triangles(xy):
     from paper_2509_20198_b200.patches import triangulate
     n = len(xy)
     g = dict(n=1, xy=D.upload(np.asarray(xy, np.float64)),
+             h=D.upload(np.zeros(n)),
              off=torch.tensor([0, n], dtype=torch.int64, device="cuda"))
     t = triangulate(g)
     assert int(t["status"][0].item()) == 0
     m = int(t["ntri"][0].item())
     return t["tri"][:m].cpu().numpy()
+
+
+def test_device_predicates_match_host():
+    import ctypes as C
+    from paper_2509_20198_b200 import _device as D
+    from paper_2509_20198_b200._lib import lib
+    rng = np.random.default_rng(11)
+    cases = [rng.integers(-4, 5, 8) / 4.0 for _ in range(2000)]
+    for _ in range(2000):
+        t = rng.uniform(0, 2 * np.pi, 4)
+        p = (np.stack([np.cos(t), np.sin(t)], 1) * 0.7 + 0.1).ravel()
+        p[6:] = np.nextafter(p[6:], p[6:] + rng.choice([-1, 1], 2))
+        cases.append(p)
+    cases += [(rng.uniform(-1, 1, 8) * 10.0 ** rng.integers(-12, 0, 8))
+              for _ in range(2000)]
+    arr = np.stack(cases).astype(np.float64)
+    d_in = D.upload(arr)
+    out = D.empty((len(arr),), torch.int32)
+    for mode in (0, 1):
+        D.call("ts_predicates_device", D.ptr(d_in), len(arr), mode,
+               D.ptr(out), D.stream())
+        got = out.cpu().numpy()
+        c2 = lambda v: (C.c_double * 2)(*v)  # noqa: E731
+        for i, p in enumerate(arr):
+            if mode == 0:
+                want = lib().ts_orient_sign(c2(p[0:2]), c2(p[2:4]), c2(p[4:6]))
+            else:
+                want = lib().ts_incircle_sign(c2(p[0:2]), c2(p[2:4]),
+                                              c2(p[4:6]), c2(p[6:8]))
+            assert got[i] == want, (mode, i, p)
 
 
 def _tri_set(simp):
@@ -204,6 +236,24 @@ def test_raster_bit_exact_with_qhull_triangles(golden):
         assert ok["cz"] == float(gi[f"kcz{k}"]), k
 
 
+def _tie_cells(xy, simp):
+    """Cells inside (1e-9 tolerance) both a real and a padding triangle."""
+    allxy = np.vstack([xy, opatch.CORNERS])
+    tri = opatch.ccw(np.asarray(simp, np.int64), allxy)
+    geom = opatch.TriGeom(allxy, tri)
+    centers = opatch.cell_centers()
+    pad = (tri >= len(xy)).any(axis=1)
+    in_real = np.zeros(len(centers), bool)
+    in_pad = np.zeros(len(centers), bool)
+    for t in range(len(tri)):
+        ins = geom.inside(t, centers)
+        if pad[t]:
+            in_pad |= ins
+        else:
+            in_real |= ins
+    return (in_real & in_pad).reshape(96, 96)
+
+
 def test_interpolate_patch_api(golden):
     from paper_2509_20198_b200.patches import (PatchKey, PatchSpacePoints,
                                                interpolate_patch)
@@ -213,11 +263,17 @@ def test_interpolate_patch_api(golden):
         rgb = gi[f"rgb{k}"] if f"rgb{k}" in gi else None
         raw = interpolate_patch(PatchSpacePoints(xy, h, rgb, 12.5))
         assert np.array_equal(raw.hm_nn, gi[f"hm_nn{k}"]), k
-        assert np.array_equal(raw.face_map.cells >= 0, gi[f"face{k}"] >= 0), k
-        assert np.abs(raw.hm_lin - gi[f"hm_lin{k}"]).max() <= 1e-6, k
+        cov = raw.face_map.cells >= 0
+        ties = _tie_cells(xy, gi[f"simp{k}"]) if f"simp{k}" in gi else \
+            np.zeros_like(cov)
+        # Only cells whose centre lies on an edge shared by a real and a
+        # padding triangle may differ: there "lowest id wins" depends on
+        # Qhull's triangle numbering (case 10 puts a vertex on a centre).
+        assert not (cov != (gi[f"face{k}"] >= 0))[~ties].any(), k
+        assert np.abs(raw.hm_lin - gi[f"hm_lin{k}"])[~ties].max() <= 1e-6, k
         rk = interpolate_patch(PatchSpacePoints(xy, h, rgb, 12.5),
                                key=PatchKey(1, 2, (960.0, 1600.0)))
-        assert np.abs(rk.hm_lin - gi[f"khm_lin{k}"]).max() <= 1e-6, k
+        assert np.abs(rk.hm_lin - gi[f"khm_lin{k}"])[~ties].max() <= 1e-6, k
         assert abs(rk.key.c_z - float(gi[f"kcz{k}"])) <= 1e-3, k
 
 
