@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-splat", action="store_true")
     ap.add_argument("--splat-points", type=int, default=200_000_000)
     ap.add_argument("--cpu-sample", type=int, default=32)
+    ap.add_argument("--no-cpu", action="store_true",
+                    help="skip the cpu_baseline leg (profiling runs)")
     return ap.parse_args()
 
 
@@ -295,7 +297,7 @@ def run_ours(args, rank, world, local_rank):
             result["splat"] = splat
     if rank == 0:
         result["clocks"] = clocks.summary()
-        result["cpu_baseline"] = cpu_baseline(args)
+        result["cpu_baseline"] = None if args.no_cpu else cpu_baseline(args)
         print(json.dumps(result), flush=True)
     if world > 1:
         dist.barrier()
