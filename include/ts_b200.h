@@ -192,10 +192,13 @@ size_t ts_refine_workspace(const ts_weights* w, int batch);
 int ts_refine(const ts_weights* w, const float* d_in, int batch,
               float* d_out, uint8_t* d_nonfinite, void* d_workspace,
               void* stream);
-/* conv2d (refiner.py:330-388): NCHW float32 cross-correlation + bias.    */
+/* conv2d (refiner.py:330-388): NCHW float32 cross-correlation + bias.
+ * precision: 0 CUDA-core fp32, 1 tcgen05 3xTF32, 2 tcgen05 bf16 (shapes
+ * the tensor-core kernel cannot take run on the fp32 kernel).            */
 int ts_conv2d(const float* d_x, int batch, int c_in, int h, int w,
               const float* d_weight, int c_out, int k, const float* d_bias,
-              int stride, int padding, float* d_y, void* stream);
+              int stride, int padding, int precision, float* d_y,
+              void* stream);
 
 /* ---- (4) full-resolution texel update ---------------------------------
  * bake_fullres (engine.py:416-456) for P patches at once.  Points (M,3)

@@ -59,7 +59,7 @@ SIGNATURES = {
     "ts_weights_is_identity": (I32, [P]),
     "ts_refine_workspace": (SZ, [P, I32]),
     "ts_refine": (I32, [P, P, I32, P, P, P, P]),
-    "ts_conv2d": (I32, [P, I32, I32, I32, I32, P, I32, I32, P, I32, I32, P,
+    "ts_conv2d": (I32, [P, I32, I32, I32, I32, P, I32, I32, P, I32, I32, I32, P,
                         P]),
     "ts_bake_workspace": (SZ, [I32]),
     "ts_bake": (I32, [P, P, I64, P, I32, P, P, F64, F64, I32, I32, P, P, P,

@@ -3,6 +3,8 @@
 
 #include <stdint.h>
 
+#include <vector>
+
 namespace ts {
 
 // One NHWC activation view: element (b, y, x, c) lives at
@@ -25,8 +27,14 @@ struct ConvOp {
   const float* w;   // [K][C_out], K = (ky * k + kx) * C_in + ci
   const float* bias;
   int batch;
+  const uint8_t* w_tc;  // tensor-core packed weights (conv_tc.cu), or null
 };
 
 int launch_conv_simt(const ConvOp& op, void* stream);
+bool conv_tc_supported(const ConvOp& op, int precision);
+int launch_conv_tc(const ConvOp& op, int precision, void* stream);
+// Swizzled per-(n-tile, k-stage) shared-memory images of OIKK weights.
+std::vector<uint8_t> pack_tc_weights(const float* w_oikk, int co, int ci, int k,
+                                     int precision, const ConvOp& shape_op);
 
 }  // namespace ts

@@ -27,8 +27,8 @@
 
 namespace ts {
 
-int launch_conv_tc(const ConvOp& op, int precision, void* stream);
-bool conv_tc_supported(const ConvOp& op, int precision);
+
+
 
 namespace {
 
@@ -54,6 +54,7 @@ struct ConvLayer {
   Win out_win;
   float* w = nullptr;   // device [K][Cout]
   float* b = nullptr;   // device [Cout]
+  const uint8_t* w_tc = nullptr;  // tensor-core packed weights (or null)
   size_t out_off = 0;   // workspace offset (floats) of the output buffer
   int out_cstride = 0, out_coff = 0;
   int in_src = -1;      // -1: external/concat buffers handled by the planner
@@ -370,6 +371,17 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
                            cudaMemcpyHostToDevice));
     TS_CUDA_TRY(cudaMemcpy(L.b, bi->second.second.data(), Co * sizeof(float),
                            cudaMemcpyHostToDevice));
+    if (W->precision != 0 && L.d.ci % 4 == 0 && Co >= 8) {
+      ConvOp shape{};
+      shape.k = L.d.k;
+      const std::vector<uint8_t> pk =
+          pack_tc_weights(src.data(), Co, L.d.ci, L.d.k, W->precision, shape);
+      void* d = nullptr;
+      TS_CUDA_TRY(cudaMalloc(&d, pk.size()));
+      W->device_allocs.push_back(d);
+      TS_CUDA_TRY(cudaMemcpy(d, pk.data(), pk.size(), cudaMemcpyHostToDevice));
+      L.w_tc = reinterpret_cast<const uint8_t*>(d);
+    }
   }
   (void)params;
   if (tensors.size() != (size_t)nL * 2) return TS_E_SHAPE;  // unexpected tensors
@@ -514,8 +526,9 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
       op.ox0 = L.out_win.x0; op.ox1 = L.out_win.x1;
       op.w = L.w; op.bias = L.b;
       op.batch = B;
+      op.w_tc = L.w_tc;
       int st;
-      if (W->precision != 0 && conv_tc_supported(op, W->precision))
+      if (L.w_tc && conv_tc_supported(op, W->precision))
         st = launch_conv_tc(op, W->precision, stream);
       else
         st = launch_conv_simt(op, stream);
@@ -573,7 +586,8 @@ __global__ void pack_weights(const float* __restrict__ w, int Co, int Ci, int k,
 
 extern "C" int ts_conv2d(const float* d_x, int batch, int c_in, int h, int w,
                          const float* d_weight, int c_out, int k, const float* d_bias,
-                         int stride, int padding, float* d_y, void* stream) {
+                         int stride, int padding, int precision, float* d_y,
+                         void* stream) {
   if (batch <= 0 || c_in <= 0 || c_out <= 0 || k <= 0 || stride <= 0 || padding < 0)
     return TS_E_SHAPE;
   const int ho = (h + 2 * padding - k) / stride + 1;
@@ -594,7 +608,24 @@ extern "C" int ts_conv2d(const float* d_x, int batch, int c_in, int h, int w,
   op.up2 = 0; op.k = k; op.stride = stride; op.pad = padding; op.lrelu = 0;
   op.oy0 = 0; op.oy1 = ho; op.ox0 = 0; op.ox1 = wo;
   op.w = wp; op.bias = d_bias; op.batch = batch;
-  int st = launch_conv_simt(op, stream);
+  int st;
+  void* dpk = nullptr;
+  if (precision != 0 && k * k * c_in > 0 && c_in % 4 == 0 && c_out >= 8) {
+    // tensor-core path: pack the swizzled weight images on the host
+    std::vector<float> hw(nw);
+    TS_CUDA_TRY(cudaMemcpyAsync(hw.data(), d_weight, nw * sizeof(float),
+                                cudaMemcpyDeviceToHost, s));
+    TS_CUDA_TRY(cudaStreamSynchronize(s));
+    const std::vector<uint8_t> pk = pack_tc_weights(hw.data(), c_out, c_in, k, precision, op);
+    TS_CUDA_TRY(cudaMallocAsync(&dpk, pk.size(), s));
+    TS_CUDA_TRY(cudaMemcpyAsync(dpk, pk.data(), pk.size(), cudaMemcpyHostToDevice, s));
+    op.w_tc = reinterpret_cast<const uint8_t*>(dpk);
+    st = launch_conv_tc(op, precision, stream);
+    TS_CUDA_TRY(cudaStreamSynchronize(s));  // pk (host) must outlive the copy
+  } else {
+    st = launch_conv_simt(op, stream);
+  }
+  if (dpk) TS_CUDA_TRY(cudaFreeAsync(dpk, s));
   if (st != TS_OK) return st;
   ts::count_launch(), nhwc_to_nchw<<<g, 256, 0, s>>>(yout, batch, c_out, ho, wo, d_y);
   TS_LAUNCH_CHECK();

@@ -389,7 +389,8 @@ def finish_refined(raws, out: np.ndarray, nonfinite: np.ndarray,
 
 
 def conv2d(x: np.ndarray, weight: np.ndarray, bias: np.ndarray,
-           stride: int = 1, padding: int = 0) -> np.ndarray:
+           stride: int = 1, padding: int = 0,
+           precision: int = PRECISION_FP32) -> np.ndarray:
     """Cross-correlation of one C x H x W input on the GPU (ts_conv2d)."""
     if x.ndim != 3:
         raise ShapeMismatch("conv2d expects CHW input")
@@ -412,5 +413,5 @@ def conv2d(x: np.ndarray, weight: np.ndarray, bias: np.ndarray,
     db = D.upload(np.asarray(bias, np.float32))
     y = D.empty((co, ho, wo), torch.float32)
     D.call("ts_conv2d", D.ptr(dx), 1, ci, h, w, D.ptr(dw), co, kh, D.ptr(db),
-           stride, padding, D.ptr(y), D.stream())
+           stride, padding, precision, D.ptr(y), D.stream())
     return D.host(y)
