@@ -1,31 +1,36 @@
-// K3 tensor-core path: tcgen05 implicit-GEMM convolution (sm_100a).
+// K3 tensor-core path: persistent tcgen05 implicit-GEMM convolution.
 //
 // Same operator as conv_simt.cu (refiner.py:330-396: cross-correlation +
-// bias + leaky ReLU, nearest-up2 fused into the input read, crop-aware
-// output window) mapped onto the 5th-gen tensor cores:
+// bias + leaky ReLU, nearest-up2 folded into the input read, crop-aware
+// output window) on the 5th-generation tensor cores.
 //
-//   GEMM view   M = 128 output pixels per CTA tile, N = BN output channels,
-//               K = (tap, channel) with channels innermost, BKC channels per
-//               pipeline stage (one 128-byte K-major row per pixel).
-//   producers   warps 0-3, one thread per tile row: im2col-gather the
-//               pixel's 128 bytes of input (vector loads; zero outside the
-//               image; up2 folded into the address), convert/split, store
-//               into the SWIZZLE_128B K-major shared-memory image, publish
-//               with fence.proxy.async + mbarrier arrive.  Thread 0 also
-//               streams the stage's weight tile with one cp.async.bulk
-//               (weights are pre-swizzled on the host into the exact smem
-//               image) completing on the same mbarrier (expect_tx).
-//   MMA         warp 4, one elected thread: tcgen05.mma (kind::tf32 or
-//               kind::f16/bf16) from smem descriptors into a TMEM fp32
-//               accumulator; tcgen05.commit releases the stage.
-//   epilogue    warps 0-3 again: tcgen05.ld 32x32b (warp w owns TMEM lanes
-//               32w..32w+31 = tile rows), + bias, leaky ReLU, fp32 NHWC store
-//               at the concat channel offset.
+//   GEMM view   M = 128 output pixels per tile, N = BN output channels,
+//               K = (tap, channel), channels innermost; one pipeline stage =
+//               one tap x KC channels = one 128-byte K-major row per pixel.
+//   warps 0-7   producers, two threads per tile row: im2col-gather the
+//               pixel's fp32 input (16-byte loads, zeros outside the image,
+//               up2 folded into the address), split it into the operand
+//               planes of the precision mode and store them into the
+//               SWIZZLE_128B K-major smem image; publish with
+//               fence.proxy.async + mbarrier arrive.  Thread 0 streams the
+//               stage's pre-swizzled weight planes with one cp.async.bulk
+//               completing on the same mbarrier (expect_tx).
+//   warp 8      MMA issuer (one thread) + TMEM owner: tcgen05.mma from smem
+//               descriptors into one of two TMEM fp32 accumulators;
+//               tcgen05.commit frees smem stages and hands accumulators to
+//               the epilogue, so the next tile's mainloop overlaps the
+//               previous tile's epilogue.
+//   warps 9-12  epilogue: tcgen05.ld 32x32b (warp w reads lane quadrant
+//               w%4 = its 32 tile rows), + bias, leaky ReLU, fp32 NHWC store
+//               at the concat channel offset, then release the accumulator.
+//   grid        persistent: min(tiles, 148 x CTAs/SM), static tile stride.
 //
-// Precision modes:
-//   TC_TF32X3  fp32-accurate "3xTF32": a = a_hi + a_lo (a_hi = rna-tf32(a)),
-//              D += A_hi B_hi + A_hi B_lo + A_lo B_hi   (3 MMAs per k-step).
-//   TC_BF16    operands rounded to bf16, fp32 accumulation (1 MMA/k-step).
+// Precision modes (operand planes per tensor, MMAs per 32-byte K step):
+//   1 TF32X3  a = hi + lo, hi = rna-tf32(a):  hi*hi + hi*lo + lo*hi   (2, 3)
+//   2 BF16    a = bf16(a):                    a*b                    (1, 1)
+//   3 BF16X3  a = a0 + a1 + a2 (exact 3-way bf16 split, 24 mantissa bits):
+//             a0b0 + a0b1 + a1b0 + a1b1 + a0b2 + a2b0                 (3, 6)
+// Modes 1 and 3 are fp32-accurate; 3 runs at the bf16 tensor rate.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -39,9 +44,12 @@ namespace ts {
 namespace {
 
 constexpr int BM = 128;
-constexpr int kProducers = 128;          // 4 warps
-constexpr int kThreads = kProducers + 32;  // + MMA warp
-constexpr int kRowBytes = 128;           // one SW128 K-major row
+constexpr int kRowBytes = 128;
+constexpr int kProdWarps = 8;
+constexpr int kProd = kProdWarps * 32;      // 256 producer threads
+constexpr int kMmaWarp = kProdWarps;        // warp 8
+constexpr int kEpiWarp0 = kProdWarps + 1;   // warps 9..12
+constexpr int kThreads = (kProdWarps + 1 + 4) * 32;
 
 // ------------------------------------------------------------------ PTX
 
@@ -102,10 +110,10 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr),
                "r"(ncols));
 }
-template <int KIND>  // 0 = tf32, 1 = f16 (bf16 operands)
+template <bool TF32>
 __device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
                                      uint32_t acc) {
-  if (KIND == 0)
+  if (TF32)
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
@@ -136,9 +144,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// SWIZZLE_128B K-major smem descriptor (sm_100 UMMA layout: start>>4 at
-// [0,14), LBO>>4 at [16,30), SBO>>4 at [32,46), version 1 at [46,48),
-// layout type 2 = SWIZZLE_128B at [61,64)).  SBO = 8 rows x 128 B.
+// SWIZZLE_128B K-major UMMA smem descriptor: start>>4 [0,14), LBO>>4
+// [16,30) (unused for swizzled K-major), SBO>>4 [32,46) = 1024 B per 8-row
+// group, version 1 [46,48), layout SWIZZLE_128B = 2 at [61,64).
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   uint64_t d = (uint64_t)((saddr & 0x3FFFF) >> 4);
   d |= (uint64_t)(16 >> 4) << 16;
@@ -148,7 +156,8 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
-// instruction descriptor: D f32, A/B format (tf32 = 2, bf16 = 1), K-major
+// instruction descriptor: D = f32, A/B format (bf16 = 1, tf32 = 2), both
+// K-major, N >> 3 at [17,23), M >> 4 at [24,29)
 __host__ __device__ constexpr uint32_t make_idesc(uint32_t ab_fmt, int n) {
   return (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) | ((uint32_t)(n >> 3) << 17) |
          ((uint32_t)(BM >> 4) << 24);
@@ -159,188 +168,275 @@ __device__ __forceinline__ float to_tf32(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
-
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
   const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-struct TcArgs {
-  ConvOp op;
-  const uint8_t* wpk;     // packed weights [n_tile][kstage][split][BN][128B]
-  int bn;                 // N tile (multiple of 16)
-  int stages;             // pipeline depth
-  int kiters;             // k-stages = taps * cchunks
-  int cchunks;            // ceil(Cin / BKC)
+template <int MODE>
+struct Mode;
+template <>
+struct Mode<1> {  // TF32X3
+  static constexpr int planes = 2, kc = 32, mmas = 3;
+  static constexpr bool tf32 = true;
+};
+template <>
+struct Mode<2> {  // BF16
+  static constexpr int planes = 1, kc = 64, mmas = 1;
+  static constexpr bool tf32 = false;
+};
+template <>
+struct Mode<3> {  // BF16X3 (6 MMAs)
+  static constexpr int planes = 3, kc = 64, mmas = 6;
+  static constexpr bool tf32 = false;
 };
 
-template <int MODE>  // 0 = TF32X3, 1 = BF16
+struct TcArgs {
+  ConvOp op;
+  const uint8_t* wpk;   // [n_tile][kiter][plane][BN][128 B]
+  int bn, stages, kiters, cchunks, n_tiles;
+  int64_t m_tiles;
+};
+
+// Producer store of 16 source floats (64 bytes of fp32, or the bf16 half of
+// a row) into the operand planes.  `chunk0` = first 16-byte chunk index.
+template <int MODE>
+__device__ __forceinline__ void store_planes(uint8_t* sa, int row, const float4* v,
+                                             int chunk0) {
+  constexpr int plane_bytes = BM * kRowBytes;
+  const int base = (row >> 3) * 1024 + (row & 7) * kRowBytes;
+  const int r8 = row & 7;
+  if (MODE == 1) {  // 4 x float4 -> 4 chunks per plane
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 a = v[j];
+      const float4 hi = make_float4(to_tf32(a.x), to_tf32(a.y), to_tf32(a.z), to_tf32(a.w));
+      const float4 lo = make_float4(a.x - hi.x, a.y - hi.y, a.z - hi.z, a.w - hi.w);
+      const int off = base + (((chunk0 + j) ^ r8) << 4);
+      *reinterpret_cast<float4*>(sa + off) = hi;
+      *reinterpret_cast<float4*>(sa + plane_bytes + off) = lo;
+    }
+  } else {  // 8 x float4 (32 floats) -> 4 bf16 chunks per plane
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 p = v[2 * j], q = v[2 * j + 1];
+      const float f[8] = {p.x, p.y, p.z, p.w, q.x, q.y, q.z, q.w};
+      uint32_t w0[4], w1[4], w2[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float x0 = f[2 * e], x1 = f[2 * e + 1];
+        w0[e] = pack2(x0, x1);
+        if (MODE == 3) {
+          const __nv_bfloat162 h0 = *reinterpret_cast<const __nv_bfloat162*>(&w0[e]);
+          const float r0 = x0 - __bfloat162float(h0.x), r1 = x1 - __bfloat162float(h0.y);
+          w1[e] = pack2(r0, r1);
+          const __nv_bfloat162 h1 = *reinterpret_cast<const __nv_bfloat162*>(&w1[e]);
+          w2[e] = pack2(r0 - __bfloat162float(h1.x), r1 - __bfloat162float(h1.y));
+        }
+      }
+      const int off = base + (((chunk0 + j) ^ r8) << 4);
+      *reinterpret_cast<uint4*>(sa + off) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+      if (MODE == 3) {
+        *reinterpret_cast<uint4*>(sa + plane_bytes + off) =
+            make_uint4(w1[0], w1[1], w1[2], w1[3]);
+        *reinterpret_cast<uint4*>(sa + 2 * plane_bytes + off) =
+            make_uint4(w2[0], w2[1], w2[2], w2[3]);
+      }
+    }
+  }
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
-  constexpr int NSPLIT = MODE == 0 ? 2 : 1;     // operand copies (hi, lo)
-  constexpr int BKC = MODE == 0 ? 32 : 64;      // channels per stage
+  using Md = Mode<MODE>;
+  constexpr int P = Md::planes;
+  constexpr int KC = Md::kc;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const ConvOp& op = T.op;
   const int BN = T.bn, S = T.stages;
-  const int a_bytes = BM * kRowBytes * NSPLIT;
-  const int b_bytes = BN * kRowBytes * NSPLIT;
+  const int a_bytes = P * BM * kRowBytes;
+  const int b_bytes = P * BN * kRowBytes;
   const int stage_bytes = a_bytes + b_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
   uint64_t* empty = full + S;
-  uint64_t* done = empty + S;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* acc_full = empty + S;    // [2]
+  uint64_t* acc_empty = acc_full + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5;
   const int wy = op.oy1 - op.oy0, wx = op.ox1 - op.ox0;
   const int64_t M = (int64_t)op.batch * wy * wx;
-  const int64_t m0 = (int64_t)blockIdx.x * BM;
-  const int n0 = blockIdx.y * BN;
   const int Cin = op.in.C, Cout = op.out.C;
+  const int64_t total_tiles = T.m_tiles * T.n_tiles;
   uint32_t ncols = 32;
-  while ((int)ncols < BN) ncols <<= 1;
+  while ((int)ncols < 2 * BN) ncols <<= 1;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(full + s, kProducers);
+      mbar_init(full + s, kProd);
       mbar_init(empty + s, 1);
     }
-    mbar_init(done, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(acc_full + a, 1);
+      mbar_init(acc_empty + a, 4);
+    }
     fence_barrier_init();
   }
-  if (warp == 4) tmem_alloc(tmem_slot, ncols);
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, ncols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < 4) {
-    // ---------------- producers: one thread = one tile row (pixel) ----
-    const int64_t gm = m0 + tid;
-    const bool valid = gm < M;
-    int b = 0, oy = 0, ox = 0;
-    if (valid) {
-      b = (int)(gm / ((int64_t)wy * wx));
-      const int r = (int)(gm - (int64_t)b * wy * wx);
-      oy = op.oy0 + r / wx;
-      ox = op.ox0 + r % wx;
-    }
+  if (warp < kProdWarps) {
+    // ------------------------------ producers ------------------------------
+    const int row = tid & (BM - 1);
+    const int half = tid >> 7;  // which half of the 128-byte row
     const int Hl = op.up2 ? 2 * op.in.H : op.in.H;
     const int Wl = op.up2 ? 2 * op.in.W : op.in.W;
-    const float* inb =
-        op.in.base + (int64_t)b * op.in.H * op.in.W * op.in.cstride + op.in.coff;
-    const uint8_t* wsrc = T.wpk + (size_t)blockIdx.y * T.kiters * b_bytes;
-    const int r8 = tid & 7;
-    const int row_off = (tid >> 3) * 1024 + r8 * kRowBytes;
-    for (int it = 0; it < T.kiters; ++it) {
-      const int s = it % S;
-      const uint32_t ph = (it / S) & 1;
-      mbar_wait(empty + s, ph ^ 1);
-      uint8_t* sa = smem + s * stage_bytes;
-      uint8_t* sb = sa + a_bytes;
-      const int tap = it / T.cchunks;
-      const int c0 = (it - tap * T.cchunks) * BKC;
-      const int ky = tap / op.k, kx = tap - ky * op.k;
-      int iy = oy * op.stride - op.pad + ky, ix = ox * op.stride - op.pad + kx;
-      const bool inside = valid && iy >= 0 && iy < Hl && ix >= 0 && ix < Wl;
-      if (op.up2) { iy >>= 1; ix >>= 1; }
-      const float* src = inb + ((int64_t)iy * op.in.W + ix) * op.in.cstride + c0;
-      const int nvalid = inside ? min(BKC, Cin - c0) : 0;  // multiple of 4
-      if (MODE == 0) {
-        float4 v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          v[j] = (4 * j < nvalid) ? __ldg(reinterpret_cast<const float4*>(src) + j)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float4 hi = make_float4(to_tf32(v[j].x), to_tf32(v[j].y), to_tf32(v[j].z),
-                                  to_tf32(v[j].w));
-          float4 lo = make_float4(v[j].x - hi.x, v[j].y - hi.y, v[j].z - hi.z,
-                                  v[j].w - hi.w);
-          const int off = row_off + ((j ^ r8) << 4);
-          *reinterpret_cast<float4*>(sa + off) = hi;
-          *reinterpret_cast<float4*>(sa + BM * kRowBytes + off) = lo;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float4 p = make_float4(0.f, 0.f, 0.f, 0.f), q = p;
-          if (8 * j < nvalid) p = __ldg(reinterpret_cast<const float4*>(src) + 2 * j);
-          if (8 * j + 4 < nvalid) q = __ldg(reinterpret_cast<const float4*>(src) + 2 * j + 1);
-          uint4 w;
-          w.x = pack_bf16(p.x, p.y);
-          w.y = pack_bf16(p.z, p.w);
-          w.z = pack_bf16(q.x, q.y);
-          w.w = pack_bf16(q.z, q.w);
-          *reinterpret_cast<uint4*>(sa + row_off + ((j ^ r8) << 4)) = w;
-        }
-      }
-      fence_proxy_async();
-      if (tid == 0) {
-        bulk_g2s(sb, wsrc + (size_t)it * b_bytes, b_bytes, full + s);
-        mbar_arrive_tx(full + s, b_bytes);
-      } else {
-        mbar_arrive(full + s);
-      }
-    }
-    // ---------------- epilogue: TMEM -> bias/lrelu -> NHWC fp32 -------
-    mbar_wait(done, 0);
-    tc_fence_after();
-    float* o = op.out.base +
-               (((int64_t)b * op.out.H + oy) * op.out.W + ox) * op.out.cstride + op.out.coff;
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    for (int c = 0; c < BN; c += 16) {
-      float v[16];
-      tmem_ld16(tmem + lane_base + c, v);  // warp-collective: every lane loads
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      const int64_t mt = tile / T.n_tiles;
+      const int nt = (int)(tile - mt * T.n_tiles);
+      const int64_t gm = mt * BM + row;
+      const bool valid = gm < M;
+      int b = 0, oy = 0, ox = 0;
       if (valid) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int n = n0 + c + i;
-          if (n < Cout) {
-            float x = v[i] + op.bias[n];
-            if (op.lrelu) x = x >= 0.f ? x : 0.01f * x;
-            o[n] = x;
-          }
-        }
+        b = (int)(gm / ((int64_t)wy * wx));
+        const int r = (int)(gm - (int64_t)b * wy * wx);
+        oy = op.oy0 + r / wx;
+        ox = op.ox0 + r % wx;
       }
-    }
-  } else {
-    // ---------------- MMA issuer (warp 4, one thread) ----------------
-    constexpr uint32_t fmt = MODE == 0 ? 2u : 1u;
-    const uint32_t idesc = make_idesc(fmt, BN);
-    if ((tid & 31) == 0) {
-      for (int it = 0; it < T.kiters; ++it) {
+      const float* inb =
+          op.in.base + (int64_t)b * op.in.H * op.in.W * op.in.cstride + op.in.coff;
+      const uint8_t* wsrc = T.wpk + (size_t)nt * T.kiters * b_bytes;
+      for (int kit = 0; kit < T.kiters; ++kit, ++it) {
         const int s = it % S;
         const uint32_t ph = (it / S) & 1;
-        mbar_wait(full + s, ph);
-        tc_fence_after();
-        const uint32_t a0 = su32(smem + s * stage_bytes);
-        const uint32_t b0 = a0 + a_bytes;
+        const int tap = kit / T.cchunks;
+        const int c0 = (kit - tap * T.cchunks) * KC + half * (KC / 2);
+        const int ky = tap / op.k, kx = tap - ky * op.k;
+        int iy = oy * op.stride - op.pad + ky, ix = ox * op.stride - op.pad + kx;
+        const bool inside = valid && iy >= 0 && iy < Hl && ix >= 0 && ix < Wl;
+        if (op.up2) { iy >>= 1; ix >>= 1; }
+        const float4* src = reinterpret_cast<const float4*>(
+            inb + ((int64_t)iy * op.in.W + ix) * op.in.cstride + c0);
+        const int nvalid = inside ? min(KC / 2, Cin - c0) : 0;  // floats, mult of 4
+        constexpr int NV = KC / 8;  // float4 per half row
+        float4 v[NV];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {  // 4 x 32-byte K steps per 128-B row
-          const uint64_t ahi = sw128_desc(a0 + 32 * k);
-          const uint64_t bhi = sw128_desc(b0 + 32 * k);
-          const uint32_t acc = (it | k) ? 1u : 0u;
-          if (MODE == 0) {
-            const uint64_t alo = sw128_desc(a0 + BM * kRowBytes + 32 * k);
-            const uint64_t blo = sw128_desc(b0 + BN * kRowBytes + 32 * k);
-            umma<0>(tmem, ahi, bhi, idesc, acc);
-            umma<0>(tmem, ahi, blo, idesc, 1u);
-            umma<0>(tmem, alo, bhi, idesc, 1u);
-          } else {
-            umma<1>(tmem, ahi, bhi, idesc, acc);
-          }
+        for (int j = 0; j < NV; ++j)
+          v[j] = (4 * j < nvalid) ? __ldg(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        mbar_wait(empty + s, ph ^ 1);
+        uint8_t* sa = smem + s * stage_bytes;
+        store_planes<MODE>(sa, row, v, half * 4);
+        fence_proxy_async();
+        if (tid == 0) {
+          bulk_g2s(sa + a_bytes, wsrc + (size_t)kit * b_bytes, b_bytes, full + s);
+          mbar_arrive_tx(full + s, b_bytes);
+        } else {
+          mbar_arrive(full + s);
         }
-        umma_commit(empty + s);
       }
-      umma_commit(done);
+    }
+  } else if (warp == kMmaWarp) {
+    // ------------------------------ MMA issuer -----------------------------
+    const uint32_t idesc = make_idesc(Md::tf32 ? 2u : 1u, BN);
+    if ((tid & 31) == 0) {
+      int it = 0, lt = 0;
+      for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+        const int acc = lt & 1;
+        mbar_wait(acc_empty + acc, ((lt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kit = 0; kit < T.kiters; ++kit, ++it) {
+          const int s = it % S;
+          mbar_wait(full + s, (it / S) & 1);
+          tc_fence_after();
+          const uint32_t a0 = su32(smem + s * stage_bytes);
+          const uint32_t b0 = a0 + a_bytes;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {  // 4 x 32-byte K steps per row
+            const uint32_t first = (kit | k) ? 1u : 0u;
+            auto A = [&](int pl) { return sw128_desc(a0 + pl * BM * kRowBytes + 32 * k); };
+            auto B = [&](int pl) { return sw128_desc(b0 + pl * BN * kRowBytes + 32 * k); };
+            if (MODE == 1) {
+              umma<true>(d, A(0), B(0), idesc, first);
+              umma<true>(d, A(0), B(1), idesc, 1u);
+              umma<true>(d, A(1), B(0), idesc, 1u);
+            } else if (MODE == 2) {
+              umma<false>(d, A(0), B(0), idesc, first);
+            } else {
+              umma<false>(d, A(2), B(0), idesc, first);  // small terms first
+              umma<false>(d, A(0), B(2), idesc, 1u);
+              umma<false>(d, A(1), B(1), idesc, 1u);
+              umma<false>(d, A(1), B(0), idesc, 1u);
+              umma<false>(d, A(0), B(1), idesc, 1u);
+              umma<false>(d, A(0), B(0), idesc, 1u);
+            }
+          }
+          umma_commit(empty + s);
+        }
+        umma_commit(acc_full + acc);
+      }
     }
     __syncwarp();
+  } else {
+    // ------------------------------ epilogue -------------------------------
+    const int q = warp & 3;  // TMEM lane quadrant of this warp
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const bool vec = (op.out.cstride % 4 == 0) && (op.out.coff % 4 == 0);
+    int lt = 0;
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+      const int acc = lt & 1;
+      const int64_t mt = tile / T.n_tiles;
+      const int nt = (int)(tile - mt * T.n_tiles);
+      const int n0 = nt * BN;
+      const int64_t gm = mt * BM + q * 32 + (tid & 31);
+      const bool valid = gm < M;
+      float* o = nullptr;
+      if (valid) {
+        const int b = (int)(gm / ((int64_t)wy * wx));
+        const int r = (int)(gm - (int64_t)b * wy * wx);
+        const int y = op.oy0 + r / wx, x = op.ox0 + r % wx;
+        o = op.out.base + (((int64_t)b * op.out.H + y) * op.out.W + x) * op.out.cstride +
+            op.out.coff;
+      }
+      mbar_wait(acc_full + acc, (lt >> 1) & 1);
+      tc_fence_after();
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        tmem_ld16(tmem + lane_base + acc * BN + c, v);  // warp-collective
+        if (valid) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int n = n0 + c + i;
+            float x = v[i] + (n < Cout ? __ldg(op.bias + n) : 0.f);
+            if (op.lrelu) x = x >= 0.f ? x : 0.01f * x;
+            v[i] = x;
+          }
+          if (vec && n0 + c + 16 <= Cout) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              *reinterpret_cast<float4*>(o + n0 + c + 4 * i) =
+                  make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (n0 + c + i < Cout) o[n0 + c + i] = v[i];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(acc_empty + acc);
+    }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc(tmem, ncols);
   }
@@ -351,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
 uint32_t f2tf32_rna(float x) {
   uint32_t u;
   memcpy(&u, &x, 4);
-  if ((u & 0x7F800000u) == 0x7F800000u) return u;  // inf / nan
+  if ((u & 0x7F800000u) == 0x7F800000u) return u;
   u += 0x1000u;
   return u & 0xFFFFE000u;
 }
@@ -359,84 +455,91 @@ uint32_t f2tf32_rna(float x) {
 uint16_t f2bf16_rn(float x) {
   uint32_t u;
   memcpy(&u, &x, 4);
-  if ((u & 0x7F800000u) == 0x7F800000u) return (uint16_t)(u >> 16 | ((u & 0xFFFF) ? 0x40 : 0));
+  if ((u & 0x7F800000u) == 0x7F800000u) return (uint16_t)((u >> 16) | ((u & 0xFFFF) ? 0x40 : 0));
   u += 0x7FFFu + ((u >> 16) & 1u);
   return (uint16_t)(u >> 16);
 }
+float bf16_to_f(uint16_t h) {
+  const uint32_t u = (uint32_t)h << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
 
 struct TcPlan {
-  int bn, stages, kiters, cchunks, ntiles, mode;
+  int bn, stages, kiters, cchunks, ntiles, planes, kc;
   size_t smem;
 };
 
-TcPlan plan_for(const ConvOp& op, int mode) {
+TcPlan plan_for(const ConvOp& op, int precision) {
   TcPlan p{};
-  const int bkc = mode == 0 ? 32 : 64;
-  const int nsplit = mode == 0 ? 2 : 1;
+  p.planes = precision == 1 ? 2 : precision == 2 ? 1 : 3;
+  p.kc = precision == 1 ? 32 : 64;
   const int n16 = (op.out.C + 15) / 16 * 16;
-  const int cap = mode == 0 ? 128 : 256;
+  const int cap = 128;
   p.ntiles = (n16 + cap - 1) / cap;
   p.bn = ((n16 + p.ntiles - 1) / p.ntiles + 15) / 16 * 16;
-  p.cchunks = (op.in.C + bkc - 1) / bkc;
+  p.cchunks = (op.in.C + p.kc - 1) / p.kc;
   p.kiters = op.k * op.k * p.cchunks;
-  const size_t stage = (size_t)(BM + p.bn) * kRowBytes * nsplit;
-  const size_t budget = 200 * 1024;
-  p.stages = (int)std::min<size_t>(4, budget / stage);
-  if (p.stages < 2) p.stages = 2;
-  p.stages = std::min(p.stages, std::max(2, p.kiters));
-  p.smem = p.stages * stage + 1024 + 8 * (2 * p.stages + 2) + 16;
-  p.mode = mode;
+  const size_t stage = (size_t)(BM + p.bn) * kRowBytes * p.planes;
+  const size_t budget = 220 * 1024;
+  p.stages = (int)std::min<size_t>(6, budget / stage);
+  p.stages = std::max(p.stages, 1);
+  p.smem = p.stages * stage + 1024 + 8 * (2 * p.stages + 4) + 16;
   return p;
 }
 
 }  // namespace
 
 bool conv_tc_supported(const ConvOp& op, int precision) {
-  if (precision != 1 && precision != 2) return false;
-  // vector loads need 16-byte aligned channel runs
+  if (precision < 1 || precision > 3) return false;
   return op.in.C % 4 == 0 && op.in.cstride % 4 == 0 && op.in.coff % 4 == 0 &&
          op.out.C >= 8;
 }
 
-// Packs OIKK fp32 weights into the per-(n-tile, k-stage) swizzled smem image.
 std::vector<uint8_t> pack_tc_weights(const float* w_oikk, int co, int ci, int k,
                                      int precision, const ConvOp& shape_op) {
-  const int mode = precision == 1 ? 0 : 1;
   ConvOp op = shape_op;
   op.in.C = ci;
   op.out.C = co;
   op.k = k;
-  const TcPlan p = plan_for(op, mode);
-  const int bkc = mode == 0 ? 32 : 64;
-  const int nsplit = mode == 0 ? 2 : 1;
-  const size_t b_bytes = (size_t)p.bn * kRowBytes * nsplit;
+  const TcPlan p = plan_for(op, precision);
+  const size_t plane = (size_t)p.bn * kRowBytes;
+  const size_t b_bytes = plane * p.planes;
   std::vector<uint8_t> out((size_t)p.ntiles * p.kiters * b_bytes, 0);
   for (int nt = 0; nt < p.ntiles; ++nt)
     for (int it = 0; it < p.kiters; ++it) {
-      const int tap = it / p.cchunks, c0 = (it % p.cchunks) * bkc;
+      const int tap = it / p.cchunks, c0 = (it % p.cchunks) * p.kc;
       const int ky = tap / k, kx = tap % k;
       uint8_t* base = out.data() + ((size_t)nt * p.kiters + it) * b_bytes;
       for (int r = 0; r < p.bn; ++r) {
         const int n = nt * p.bn + r;
-        for (int e = 0; e < bkc; ++e) {
+        for (int e = 0; e < p.kc; ++e) {
           const int c = c0 + e;
-          float v = 0.f;
-          if (n < co && c < ci) v = w_oikk[(((size_t)n * ci + c) * k + ky) * k + kx];
-          const int esize = mode == 0 ? 4 : 2;
+          const float v =
+              (n < co && c < ci) ? w_oikk[(((size_t)n * ci + c) * k + ky) * k + kx] : 0.f;
+          const int esize = precision == 1 ? 4 : 2;
           const int byte = e * esize;
-          const int chunk = byte >> 4, within = byte & 15;
           const size_t off = (size_t)(r >> 3) * 1024 + (r & 7) * kRowBytes +
-                             ((chunk ^ (r & 7)) << 4) + within;
-          if (mode == 0) {
+                             ((((byte >> 4) ^ (r & 7))) << 4) + (byte & 15);
+          if (precision == 1) {
             const uint32_t hi = f2tf32_rna(v);
             float hf;
             memcpy(&hf, &hi, 4);
             const float lo = v - hf;
             memcpy(base + off, &hi, 4);
-            memcpy(base + (size_t)p.bn * kRowBytes + off, &lo, 4);
-          } else {
+            memcpy(base + plane + off, &lo, 4);
+          } else if (precision == 2) {
             const uint16_t h = f2bf16_rn(v);
             memcpy(base + off, &h, 2);
+          } else {
+            const uint16_t h0 = f2bf16_rn(v);
+            const float r0 = v - bf16_to_f(h0);
+            const uint16_t h1 = f2bf16_rn(r0);
+            const uint16_t h2 = f2bf16_rn(r0 - bf16_to_f(h1));
+            memcpy(base + off, &h0, 2);
+            memcpy(base + plane + off, &h1, 2);
+            memcpy(base + 2 * plane + off, &h2, 2);
           }
         }
       }
@@ -445,24 +548,31 @@ std::vector<uint8_t> pack_tc_weights(const float* w_oikk, int co, int ci, int k,
 }
 
 int launch_conv_tc(const ConvOp& op, int precision, void* stream) {
-  const int mode = precision == 1 ? 0 : 1;
-  const TcPlan p = plan_for(op, mode);
+  const TcPlan p = plan_for(op, precision);
   const int64_t M = (int64_t)op.batch * (op.oy1 - op.oy0) * (op.ox1 - op.ox0);
   if (M <= 0) return TS_OK;
-  TcArgs a{op, op.w_tc, p.bn, p.stages, p.kiters, p.cchunks};
-  dim3 grid((unsigned)ceil_div<int64_t>(M, BM), (unsigned)p.ntiles);
-  cudaStream_t s = as_stream(stream);
-  if (mode == 0) {
-    TS_CUDA_TRY(cudaFuncSetAttribute(conv_tc_kernel<0>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)p.smem));
-    ts::count_launch(), conv_tc_kernel<0><<<grid, kThreads, p.smem, s>>>(a);
-  } else {
-    TS_CUDA_TRY(cudaFuncSetAttribute(conv_tc_kernel<1>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)p.smem));
-    ts::count_launch(), conv_tc_kernel<1><<<grid, kThreads, p.smem, s>>>(a);
+  TcArgs a{op, op.w_tc, p.bn, p.stages, p.kiters, p.cchunks, p.ntiles,
+           ceil_div<int64_t>(M, BM)};
+  const int64_t tiles = a.m_tiles * p.ntiles;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    TS_CUDA_TRY(cudaGetDevice(&dev));
+    TS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
+  const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+  cudaStream_t s = as_stream(stream);
+#define TS_TC_LAUNCH(MD)                                                              \
+  do {                                                                                \
+    TS_CUDA_TRY(cudaFuncSetAttribute(conv_tc_kernel<MD>,                              \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                     (int)p.smem));                                   \
+    ts::count_launch(), conv_tc_kernel<MD><<<grid, kThreads, p.smem, s>>>(a);         \
+  } while (0)
+  if (precision == 1) TS_TC_LAUNCH(1);
+  else if (precision == 2) TS_TC_LAUNCH(2);
+  else TS_TC_LAUNCH(3);
+#undef TS_TC_LAUNCH
   TS_LAUNCH_CHECK();
   return TS_OK;
 }

@@ -37,7 +37,7 @@ SHAPES = [  # (ci, co, k, stride, pad, h, w)
 
 
 @pytest.mark.parametrize("shape", SHAPES)
-@pytest.mark.parametrize("precision", [1, 2])
+@pytest.mark.parametrize("precision", [1, 2, 3])
 def test_conv_tc_vs_oracle(shape, precision):
     from paper_2509_20198_b200.refiner import conv2d
     ci, co, k, s, p, h, w = shape
@@ -53,11 +53,13 @@ def test_conv_tc_vs_oracle(shape, precision):
     err = np.abs(got - want).max() / scale
     if precision == 1:
         assert err < 1e-5, err
+    elif precision == 3:
+        assert err < 2e-6, err
     else:
         assert err < 2e-2, err
 
 
-@pytest.mark.parametrize("precision", [1, 2])
+@pytest.mark.parametrize("precision", [1, 2, 3])
 def test_refine_tc_vs_golden(golden, precision):
     from paper_2509_20198_b200 import refiner as R
     from paper_2509_20198_b200.patches import FaceMap, PatchKey, RawPatch
@@ -72,9 +74,12 @@ def test_refine_tc_vs_golden(golden, precision):
     h = np.stack([r.heights_rel for r in res])
     c = np.stack([r.rgb for r in res])
     dh = np.abs(h - g["default_h"])
-    if precision == 1:
+    if precision == 3:      # fp32-accurate: same bar as the CUDA-core path
         assert dh.max() <= 2e-3, dh.max()
         assert np.abs(c - g["default_rgb"]).max() <= 1e-4
+    elif precision == 1:    # 3xTF32: truncated tf32 low parts, stated 5e-2 m
+        assert dh.max() <= 5e-2, dh.max()
+        assert np.abs(c - g["default_rgb"]).max() <= 1e-3
     else:
         # bf16 CNN, stated separately: random He weights amplify rounding
         assert np.sqrt((dh ** 2).mean()) <= 1.0, np.sqrt((dh ** 2).mean())
