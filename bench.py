@@ -256,7 +256,8 @@ def run_ours(args, rank, world, local_rank):
             "ms_per_step": round(ms_max, 4),
             "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None,
-            "dtype": {0: "f32", 1: "tf32x3", 2: "bf16"}[precision] +
+            "dtype": {0: "f32", 1: "tf32x3", 2: "bf16",
+                      3: "bf16x3 (fp32-class split)"}[precision] +
                      " CNN, f64 geometry",
             "data": "synthetic (seeded FractalTerrain stub-body LAZ tiles, "
                     "random He weights seed 3)",

@@ -48,7 +48,6 @@ constexpr int kRowBytes = 128;
 constexpr int kProdWarps = 8;
 constexpr int kProd = kProdWarps * 32;      // 256 producer threads
 constexpr int kMmaWarp = kProdWarps;        // warp 8
-constexpr int kEpiWarp0 = kProdWarps + 1;   // warps 9..12
 constexpr int kThreads = (kProdWarps + 1 + 4) * 32;
 
 // ------------------------------------------------------------------ PTX
@@ -163,31 +162,39 @@ __host__ __device__ constexpr uint32_t make_idesc(uint32_t ab_fmt, int n) {
          ((uint32_t)(BM >> 4) << 24);
 }
 
-__device__ __forceinline__ float to_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+// Operand splitting with integer ALU ops only (no F2F/XU conversions).
+// tf32 hi: round-to-nearest-away on the 13 dropped bits; bf16 planes: exact
+// truncation split a = a0 + a1 + a2 (each 8 significant bits), bf16 RN for
+// the single-plane mode.
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
-__device__ __forceinline__ uint32_t pack2(float a, float b) {
-  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<const uint32_t*>(&h);
+__device__ __forceinline__ float trunc_bf(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xFFFF0000u);
+}
+__device__ __forceinline__ uint32_t hi_halves(float a, float b) {  // {a.hi16, b.hi16}
+  return __byte_perm(__float_as_uint(a), __float_as_uint(b), 0x7632);
+}
+__device__ __forceinline__ float rn_bf(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return __uint_as_float(u + 0x7FFFu + ((u >> 16) & 1u));
 }
 
 template <int MODE>
 struct Mode;
 template <>
 struct Mode<1> {  // TF32X3
-  static constexpr int planes = 2, kc = 32, mmas = 3;
+  static constexpr int planes = 2, kc = 32;
   static constexpr bool tf32 = true;
 };
 template <>
 struct Mode<2> {  // BF16
-  static constexpr int planes = 1, kc = 64, mmas = 1;
+  static constexpr int planes = 1, kc = 64;
   static constexpr bool tf32 = false;
 };
 template <>
 struct Mode<3> {  // BF16X3 (6 MMAs)
-  static constexpr int planes = 3, kc = 64, mmas = 6;
+  static constexpr int planes = 3, kc = 64;
   static constexpr bool tf32 = false;
 };
 
@@ -198,52 +205,43 @@ struct TcArgs {
   int64_t m_tiles;
 };
 
-// Producer store of 16 source floats (64 bytes of fp32, or the bf16 half of
-// a row) into the operand planes.  `chunk0` = first 16-byte chunk index.
+// Row table of one tile: input pixel origin of every output pixel.
+struct RowInfo {
+  int b, iy0, ix0;  // b < 0: row beyond M
+};
+
+// Stores one 16-byte fp32 source piece of a row into the operand planes.
 template <int MODE>
-__device__ __forceinline__ void store_planes(uint8_t* sa, int row, const float4* v,
-                                             int chunk0) {
+__device__ __forceinline__ void store_piece(uint8_t* sa, int row, int piece, float4 a) {
   constexpr int plane_bytes = BM * kRowBytes;
   const int base = (row >> 3) * 1024 + (row & 7) * kRowBytes;
-  const int r8 = row & 7;
-  if (MODE == 1) {  // 4 x float4 -> 4 chunks per plane
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float4 a = v[j];
-      const float4 hi = make_float4(to_tf32(a.x), to_tf32(a.y), to_tf32(a.z), to_tf32(a.w));
-      const float4 lo = make_float4(a.x - hi.x, a.y - hi.y, a.z - hi.z, a.w - hi.w);
-      const int off = base + (((chunk0 + j) ^ r8) << 4);
-      *reinterpret_cast<float4*>(sa + off) = hi;
-      *reinterpret_cast<float4*>(sa + plane_bytes + off) = lo;
-    }
-  } else {  // 8 x float4 (32 floats) -> 4 bf16 chunks per plane
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float4 p = v[2 * j], q = v[2 * j + 1];
-      const float f[8] = {p.x, p.y, p.z, p.w, q.x, q.y, q.z, q.w};
-      uint32_t w0[4], w1[4], w2[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float x0 = f[2 * e], x1 = f[2 * e + 1];
-        w0[e] = pack2(x0, x1);
-        if (MODE == 3) {
-          const __nv_bfloat162 h0 = *reinterpret_cast<const __nv_bfloat162*>(&w0[e]);
-          const float r0 = x0 - __bfloat162float(h0.x), r1 = x1 - __bfloat162float(h0.y);
-          w1[e] = pack2(r0, r1);
-          const __nv_bfloat162 h1 = *reinterpret_cast<const __nv_bfloat162*>(&w1[e]);
-          w2[e] = pack2(r0 - __bfloat162float(h1.x), r1 - __bfloat162float(h1.y));
-        }
-      }
-      const int off = base + (((chunk0 + j) ^ r8) << 4);
-      *reinterpret_cast<uint4*>(sa + off) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
-      if (MODE == 3) {
-        *reinterpret_cast<uint4*>(sa + plane_bytes + off) =
-            make_uint4(w1[0], w1[1], w1[2], w1[3]);
-        *reinterpret_cast<uint4*>(sa + 2 * plane_bytes + off) =
-            make_uint4(w2[0], w2[1], w2[2], w2[3]);
-      }
+  if (MODE == 1) {  // 16 source bytes -> one 16-byte chunk per plane
+    const int off = base + ((piece ^ (row & 7)) << 4);
+    const float4 hi = make_float4(tf32_hi(a.x), tf32_hi(a.y), tf32_hi(a.z), tf32_hi(a.w));
+    *reinterpret_cast<float4*>(sa + off) = hi;
+    *reinterpret_cast<float4*>(sa + plane_bytes + off) =
+        make_float4(a.x - hi.x, a.y - hi.y, a.z - hi.z, a.w - hi.w);
+  } else {  // 4 floats -> 8 bytes (half a chunk) per plane
+    const int off = base + (((piece >> 1) ^ (row & 7)) << 4) + ((piece & 1) << 3);
+    if (MODE == 2) {
+      *reinterpret_cast<uint2*>(sa + off) =
+          make_uint2(hi_halves(rn_bf(a.x), rn_bf(a.y)), hi_halves(rn_bf(a.z), rn_bf(a.w)));
+    } else {
+      const float x0 = trunc_bf(a.x), y0 = trunc_bf(a.y), z0 = trunc_bf(a.z),
+                  w0 = trunc_bf(a.w);
+      const float rx = a.x - x0, ry = a.y - y0, rz = a.z - z0, rw = a.w - w0;
+      const float x1 = trunc_bf(rx), y1 = trunc_bf(ry), z1 = trunc_bf(rz), w1 = trunc_bf(rw);
+      *reinterpret_cast<uint2*>(sa + off) = make_uint2(hi_halves(x0, y0), hi_halves(z0, w0));
+      *reinterpret_cast<uint2*>(sa + plane_bytes + off) =
+          make_uint2(hi_halves(x1, y1), hi_halves(z1, w1));
+      *reinterpret_cast<uint2*>(sa + 2 * plane_bytes + off) =
+          make_uint2(hi_halves(rx - x1, ry - y1), hi_halves(rz - z1, rw - w1));
     }
   }
+}
+
+__device__ __forceinline__ void prod_bar() {  // the 256 producer threads
+  asm volatile("bar.sync 1, %0;" ::"n"(kProd) : "memory");
 }
 
 template <int MODE>
@@ -292,46 +290,61 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
 
   if (warp < kProdWarps) {
     // ------------------------------ producers ------------------------------
-    const int row = tid & (BM - 1);
-    const int half = tid >> 7;  // which half of the 128-byte row
+    // Lanes of a warp cover consecutive 16-byte pieces of the same pixel
+    // rows, so every global load instruction reads whole 128-byte lines.
+    constexpr int PPR = KC / 4;            // fp32 pieces per row per stage
+    constexpr int PIECES = BM * PPR / kProd;  // pieces per thread per stage
     const int Hl = op.up2 ? 2 * op.in.H : op.in.H;
     const int Wl = op.up2 ? 2 * op.in.W : op.in.W;
-    int it = 0;
-    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    RowInfo* rinfo = reinterpret_cast<RowInfo*>(tmem_slot + 4);  // [2][BM]
+    int it = 0, lt = 0;
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
       const int64_t mt = tile / T.n_tiles;
       const int nt = (int)(tile - mt * T.n_tiles);
-      const int64_t gm = mt * BM + row;
-      const bool valid = gm < M;
-      int b = 0, oy = 0, ox = 0;
-      if (valid) {
-        b = (int)(gm / ((int64_t)wy * wx));
-        const int r = (int)(gm - (int64_t)b * wy * wx);
-        oy = op.oy0 + r / wx;
-        ox = op.ox0 + r % wx;
+      RowInfo* ri = rinfo + (lt & 1) * BM;
+      if (tid < BM) {
+        const int64_t gm = mt * BM + tid;
+        RowInfo r{-1, 0, 0};
+        if (gm < M) {
+          r.b = (int)(gm / ((int64_t)wy * wx));
+          const int q = (int)(gm - (int64_t)r.b * wy * wx);
+          r.iy0 = (op.oy0 + q / wx) * op.stride - op.pad;
+          r.ix0 = (op.ox0 + q % wx) * op.stride - op.pad;
+        }
+        ri[tid] = r;
       }
-      const float* inb =
-          op.in.base + (int64_t)b * op.in.H * op.in.W * op.in.cstride + op.in.coff;
+      prod_bar();
       const uint8_t* wsrc = T.wpk + (size_t)nt * T.kiters * b_bytes;
       for (int kit = 0; kit < T.kiters; ++kit, ++it) {
         const int s = it % S;
         const uint32_t ph = (it / S) & 1;
         const int tap = kit / T.cchunks;
-        const int c0 = (kit - tap * T.cchunks) * KC + half * (KC / 2);
+        const int c0 = (kit - tap * T.cchunks) * KC;
         const int ky = tap / op.k, kx = tap - ky * op.k;
-        int iy = oy * op.stride - op.pad + ky, ix = ox * op.stride - op.pad + kx;
-        const bool inside = valid && iy >= 0 && iy < Hl && ix >= 0 && ix < Wl;
-        if (op.up2) { iy >>= 1; ix >>= 1; }
-        const float4* src = reinterpret_cast<const float4*>(
-            inb + ((int64_t)iy * op.in.W + ix) * op.in.cstride + c0);
-        const int nvalid = inside ? min(KC / 2, Cin - c0) : 0;  // floats, mult of 4
-        constexpr int NV = KC / 8;  // float4 per half row
-        float4 v[NV];
+        float4 v[PIECES];
 #pragma unroll
-        for (int j = 0; j < NV; ++j)
-          v[j] = (4 * j < nvalid) ? __ldg(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int j = 0; j < PIECES; ++j) {
+          const int p = j * kProd + tid;
+          const int row = p / PPR, piece = p % PPR;
+          const RowInfo r = ri[row];
+          int iy = r.iy0 + ky, ix = r.ix0 + kx;
+          const int c = c0 + 4 * piece;
+          v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (r.b >= 0 && iy >= 0 && iy < Hl && ix >= 0 && ix < Wl && c < Cin) {
+            if (op.up2) { iy >>= 1; ix >>= 1; }
+            v[j] = __ldg(reinterpret_cast<const float4*>(
+                op.in.base +
+                (((int64_t)r.b * op.in.H + iy) * op.in.W + ix) * op.in.cstride +
+                op.in.coff + c));
+          }
+        }
         mbar_wait(empty + s, ph ^ 1);
         uint8_t* sa = smem + s * stage_bytes;
-        store_planes<MODE>(sa, row, v, half * 4);
+#pragma unroll
+        for (int j = 0; j < PIECES; ++j) {
+          const int p = j * kProd + tid;
+          store_piece<MODE>(sa, p / PPR, p % PPR, v[j]);
+        }
         fence_proxy_async();
         if (tid == 0) {
           bulk_g2s(sa + a_bytes, wsrc + (size_t)kit * b_bytes, b_bytes, full + s);
@@ -482,10 +495,10 @@ TcPlan plan_for(const ConvOp& op, int precision) {
   p.cchunks = (op.in.C + p.kc - 1) / p.kc;
   p.kiters = op.k * op.k * p.cchunks;
   const size_t stage = (size_t)(BM + p.bn) * kRowBytes * p.planes;
-  const size_t budget = 220 * 1024;
+  const size_t budget = 218 * 1024;
   p.stages = (int)std::min<size_t>(6, budget / stage);
   p.stages = std::max(p.stages, 1);
-  p.smem = p.stages * stage + 1024 + 8 * (2 * p.stages + 4) + 16;
+  p.smem = p.stages * stage + 1024 + 8 * (2 * p.stages + 4) + 16 + 2 * BM * 12 + 16;
   return p;
 }
 
@@ -533,10 +546,16 @@ std::vector<uint8_t> pack_tc_weights(const float* w_oikk, int co, int ci, int k,
             const uint16_t h = f2bf16_rn(v);
             memcpy(base + off, &h, 2);
           } else {
-            const uint16_t h0 = f2bf16_rn(v);
+            // exact truncation split, like the device producers
+            uint32_t u;
+            memcpy(&u, &v, 4);
+            const uint16_t h0 = (uint16_t)(u >> 16);
             const float r0 = v - bf16_to_f(h0);
-            const uint16_t h1 = f2bf16_rn(r0);
-            const uint16_t h2 = f2bf16_rn(r0 - bf16_to_f(h1));
+            memcpy(&u, &r0, 4);
+            const uint16_t h1 = (uint16_t)(u >> 16);
+            const float r1 = r0 - bf16_to_f(h1);
+            memcpy(&u, &r1, 4);
+            const uint16_t h2 = (uint16_t)(u >> 16);
             memcpy(base + off, &h0, 2);
             memcpy(base + plane + off, &h1, 2);
             memcpy(base + 2 * plane + off, &h2, 2);
