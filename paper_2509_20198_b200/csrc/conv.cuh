@@ -31,6 +31,8 @@ struct ConvOp {
 };
 
 int launch_conv_simt(const ConvOp& op, void* stream);
+bool conv_direct_supported(const ConvOp& op);
+int launch_conv_direct(const ConvOp& op, void* stream);
 bool conv_tc_supported(const ConvOp& op, int precision);
 int launch_conv_tc(const ConvOp& op, int precision, void* stream);
 // Swizzled per-(n-tile, k-stage) shared-memory images of OIKK weights.

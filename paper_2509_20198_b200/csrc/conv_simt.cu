@@ -9,6 +9,8 @@
 // [K][C_out].  Used for layers the tensor-core path does not take and as
 // the reference implementation of ts_conv2d.
 #include "conv.cuh"
+#include <algorithm>
+
 #include "ts_common.cuh"
 
 namespace ts {
@@ -117,6 +119,99 @@ int launch_conv_simt(const ConvOp& op, void* stream) {
   if (M <= 0) return TS_OK;
   dim3 grid((unsigned)ceil_div<int64_t>(M, BM), (unsigned)ceil_div(op.out.C, BN));
   ts::count_launch(), conv_simt_kernel<<<grid, 256, 0, as_stream(stream)>>>(op);
+  TS_LAUNCH_CHECK();
+  return TS_OK;
+}
+
+}  // namespace ts
+
+// ---------------------------------------------------------------------------
+// Direct convolution for thin layers (C_in <= 4 or C_out <= 16): one thread
+// per output pixel keeps every output channel in registers, weights sit in
+// shared memory (broadcast reads).  GEMM tiling would waste up to 16x of its
+// 64-wide N tile on these (enc*.0: 1/3 -> 48, fuse.2: 32 -> 4).
+namespace ts {
+namespace {
+
+template <int CO>
+__global__ void __launch_bounds__(128) conv_direct_kernel(ConvOp op) {
+  extern __shared__ float sw[];
+  const int Cin = op.in.C, Cout = op.out.C;
+  const int K = op.k * op.k * Cin;
+  for (int i = threadIdx.x; i < K * Cout; i += blockDim.x) sw[i] = op.w[i];
+  float* sb = sw + K * Cout;
+  for (int i = threadIdx.x; i < Cout; i += blockDim.x) sb[i] = op.bias[i];
+  __syncthreads();
+  const int wy = op.oy1 - op.oy0, wx = op.ox1 - op.ox0;
+  const int64_t M = (int64_t)op.batch * wy * wx;
+  const int Hl = op.up2 ? 2 * op.in.H : op.in.H;
+  const int Wl = op.up2 ? 2 * op.in.W : op.in.W;
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < M;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(m / ((int64_t)wy * wx));
+    const int r = (int)(m - (int64_t)b * wy * wx);
+    const int oy = op.oy0 + r / wx, ox = op.ox0 + r % wx;
+    float acc[CO];
+#pragma unroll
+    for (int c = 0; c < CO; ++c) acc[c] = 0.f;
+    const float* inb = op.in.base + (int64_t)b * op.in.H * op.in.W * op.in.cstride + op.in.coff;
+    for (int ky = 0; ky < op.k; ++ky) {
+      int iy = oy * op.stride - op.pad + ky;
+      if (iy < 0 || iy >= Hl) continue;
+      if (op.up2) iy >>= 1;
+      for (int kx = 0; kx < op.k; ++kx) {
+        int ix = ox * op.stride - op.pad + kx;
+        if (ix < 0 || ix >= Wl) continue;
+        if (op.up2) ix >>= 1;
+        const float* src = inb + ((int64_t)iy * op.in.W + ix) * op.in.cstride;
+        const float* wt = sw + (ky * op.k + kx) * Cin * Cout;
+        for (int ci = 0; ci < Cin; ++ci) {
+          const float x = __ldg(src + ci);
+#pragma unroll
+          for (int c = 0; c < CO; ++c)
+            if (c < Cout) acc[c] = fmaf(x, wt[ci * Cout + c], acc[c]);
+        }
+      }
+    }
+    float* o = op.out.base + (((int64_t)b * op.out.H + oy) * op.out.W + ox) * op.out.cstride +
+               op.out.coff;
+#pragma unroll
+    for (int c = 0; c < CO; ++c) {
+      if (c < Cout) {
+        float v = acc[c] + sb[c];
+        if (op.lrelu) v = v >= 0.f ? v : 0.01f * v;
+        o[c] = v;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+bool conv_direct_supported(const ConvOp& op) {
+  const int K = op.k * op.k * op.in.C;
+  return (op.in.C <= 4 || op.out.C <= 16) && op.out.C <= 64 &&
+         (size_t)(K + 1) * op.out.C * sizeof(float) <= 96 * 1024;
+}
+
+int launch_conv_direct(const ConvOp& op, void* stream) {
+  const int64_t M = (int64_t)op.batch * (op.oy1 - op.oy0) * (op.ox1 - op.ox0);
+  if (M <= 0) return TS_OK;
+  const size_t smem = (size_t)(op.k * op.k * op.in.C + 1) * op.out.C * sizeof(float);
+  const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(M, 128), 148 * 16);
+  cudaStream_t s = as_stream(stream);
+#define TS_DIRECT(CO)                                                                  \
+  do {                                                                                 \
+    TS_CUDA_TRY(cudaFuncSetAttribute(conv_direct_kernel<CO>,                           \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                                     (int)smem));                                      \
+    ts::count_launch(), conv_direct_kernel<CO><<<grid, 128, smem, s>>>(op);            \
+  } while (0)
+  if (op.out.C <= 4) TS_DIRECT(4);
+  else if (op.out.C <= 16) TS_DIRECT(16);
+  else if (op.out.C <= 32) TS_DIRECT(32);
+  else TS_DIRECT(64);
+#undef TS_DIRECT
   TS_LAUNCH_CHECK();
   return TS_OK;
 }

@@ -250,8 +250,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
   constexpr int P = Md::planes;
   constexpr int KC = Md::kc;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // pointer arithmetic on the __shared__ array keeps the shared address
+  // space (STS/LDS instead of generic ST/LD)
+  uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   const ConvOp& op = T.op;
   const int BN = T.bn, S = T.stages;
   const int a_bytes = P * BM * kRowBytes;
@@ -297,7 +298,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
     const int Hl = op.up2 ? 2 * op.in.H : op.in.H;
     const int Wl = op.up2 ? 2 * op.in.W : op.in.W;
     RowInfo* rinfo = reinterpret_cast<RowInfo*>(tmem_slot + 4);  // [2][BM]
-    int it = 0, lt = 0;
+    int s = 0, lt = 0;
+    uint32_t ph = 0;
     for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
       const int64_t mt = tile / T.n_tiles;
       const int nt = (int)(tile - mt * T.n_tiles);
@@ -315,12 +317,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
       }
       prod_bar();
       const uint8_t* wsrc = T.wpk + (size_t)nt * T.kiters * b_bytes;
-      for (int kit = 0; kit < T.kiters; ++kit, ++it) {
-        const int s = it % S;
-        const uint32_t ph = (it / S) & 1;
-        const int tap = kit / T.cchunks;
-        const int c0 = (kit - tap * T.cchunks) * KC;
-        const int ky = tap / op.k, kx = tap - ky * op.k;
+      // (tap, channel chunk) walk without integer division
+      int c0 = 0, ky = 0, kx = 0;
+      for (int kit = 0; kit < T.kiters; ++kit) {
         float4 v[PIECES];
 #pragma unroll
         for (int j = 0; j < PIECES; ++j) {
@@ -352,21 +351,27 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
         } else {
           mbar_arrive(full + s);
         }
+        if (++s == S) { s = 0; ph ^= 1; }
+        c0 += KC;
+        if (c0 >= T.cchunks * KC) {
+          c0 = 0;
+          if (++kx == op.k) { kx = 0; ++ky; }
+        }
       }
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------ MMA issuer -----------------------------
     const uint32_t idesc = make_idesc(Md::tf32 ? 2u : 1u, BN);
     if ((tid & 31) == 0) {
-      int it = 0, lt = 0;
+      int s = 0, lt = 0;
+      uint32_t ph = 0;
       for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
         const int acc = lt & 1;
         mbar_wait(acc_empty + acc, ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
-        for (int kit = 0; kit < T.kiters; ++kit, ++it) {
-          const int s = it % S;
-          mbar_wait(full + s, (it / S) & 1);
+        for (int kit = 0; kit < T.kiters; ++kit) {
+          mbar_wait(full + s, ph);
           tc_fence_after();
           const uint32_t a0 = su32(smem + s * stage_bytes);
           const uint32_t b0 = a0 + a_bytes;
@@ -391,6 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
             }
           }
           umma_commit(empty + s);
+          if (++s == S) { s = 0; ph ^= 1; }
         }
         umma_commit(acc_full + acc);
       }
