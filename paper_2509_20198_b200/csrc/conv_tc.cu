@@ -293,56 +293,65 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
     // ------------------------------ producers ------------------------------
     // Lanes of a warp cover consecutive 16-byte pieces of the same pixel
     // rows, so every global load instruction reads whole 128-byte lines.
-    constexpr int PPR = KC / 4;            // fp32 pieces per row per stage
+    // Software-pipelined: stage k+1's loads are in flight while stage k is
+    // split and stored.
+    constexpr int PPR = KC / 4;               // fp32 pieces per row per stage
     constexpr int PIECES = BM * PPR / kProd;  // pieces per thread per stage
     const int Hl = op.up2 ? 2 * op.in.H : op.in.H;
     const int Wl = op.up2 ? 2 * op.in.W : op.in.W;
-    RowInfo* rinfo = reinterpret_cast<RowInfo*>(tmem_slot + 4);  // [2][BM]
-    int s = 0, lt = 0;
+    const int sh = op.up2 ? 1 : 0;
+    int s = 0;
     uint32_t ph = 0;
-    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
       const int64_t mt = tile / T.n_tiles;
       const int nt = (int)(tile - mt * T.n_tiles);
-      RowInfo* ri = rinfo + (lt & 1) * BM;
-      if (tid < BM) {
-        const int64_t gm = mt * BM + tid;
-        RowInfo r{-1, 0, 0};
+      // per-piece pixel origin (registers): image base, iy0, ix0
+      const float* pbase[PIECES];
+      int py0[PIECES], px0[PIECES];
+#pragma unroll
+      for (int j = 0; j < PIECES; ++j) {
+        const int p = j * kProd + tid;
+        const int64_t gm = mt * BM + p / PPR;
+        py0[j] = -(1 << 28);  // rows beyond M: always outside
+        px0[j] = 0;
+        pbase[j] = op.in.base;
         if (gm < M) {
-          r.b = (int)(gm / ((int64_t)wy * wx));
-          const int q = (int)(gm - (int64_t)r.b * wy * wx);
-          r.iy0 = (op.oy0 + q / wx) * op.stride - op.pad;
-          r.ix0 = (op.ox0 + q % wx) * op.stride - op.pad;
+          const int b = (int)(gm / ((int64_t)wy * wx));
+          const int q = (int)(gm - (int64_t)b * wy * wx);
+          py0[j] = (op.oy0 + q / wx) * op.stride - op.pad;
+          px0[j] = (op.ox0 + q % wx) * op.stride - op.pad;
+          pbase[j] = op.in.base + (int64_t)b * op.in.H * op.in.W * op.in.cstride +
+                     op.in.coff + 4 * (p % PPR);
         }
-        ri[tid] = r;
       }
-      prod_bar();
       const uint8_t* wsrc = T.wpk + (size_t)nt * T.kiters * b_bytes;
-      // (tap, channel chunk) walk without integer division
-      int c0 = 0, ky = 0, kx = 0;
-      for (int kit = 0; kit < T.kiters; ++kit) {
-        float4 v[PIECES];
+      auto load_stage = [&](int c0, int ky, int kx, float4* v) {
 #pragma unroll
         for (int j = 0; j < PIECES; ++j) {
-          const int p = j * kProd + tid;
-          const int row = p / PPR, piece = p % PPR;
-          const RowInfo r = ri[row];
-          int iy = r.iy0 + ky, ix = r.ix0 + kx;
-          const int c = c0 + 4 * piece;
+          const int iy = py0[j] + ky, ix = px0[j] + kx;
+          const int c = c0 + 4 * ((j * kProd + tid) % PPR);
           v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (r.b >= 0 && iy >= 0 && iy < Hl && ix >= 0 && ix < Wl && c < Cin) {
-            if (op.up2) { iy >>= 1; ix >>= 1; }
+          if (iy >= 0 && iy < Hl && ix >= 0 && ix < Wl && c < Cin)
             v[j] = __ldg(reinterpret_cast<const float4*>(
-                op.in.base +
-                (((int64_t)r.b * op.in.H + iy) * op.in.W + ix) * op.in.cstride +
-                op.in.coff + c));
-          }
+                pbase[j] + ((int64_t)(iy >> sh) * op.in.W + (ix >> sh)) * op.in.cstride + c0));
         }
+      };
+      int c0 = 0, ky = 0, kx = 0;  // (tap, channel chunk) walk, no division
+      float4 cur[PIECES], nxt[PIECES];
+      load_stage(0, 0, 0, cur);
+      for (int kit = 0; kit < T.kiters; ++kit) {
+        c0 += KC;
+        if (c0 >= T.cchunks * KC) {
+          c0 = 0;
+          if (++kx == op.k) { kx = 0; ++ky; }
+        }
+        if (kit + 1 < T.kiters) load_stage(c0, ky, kx, nxt);
         mbar_wait(empty + s, ph ^ 1);
         uint8_t* sa = smem + s * stage_bytes;
 #pragma unroll
         for (int j = 0; j < PIECES; ++j) {
           const int p = j * kProd + tid;
-          store_piece<MODE>(sa, p / PPR, p % PPR, v[j]);
+          store_piece<MODE>(sa, p / PPR, p % PPR, cur[j]);
         }
         fence_proxy_async();
         if (tid == 0) {
@@ -352,11 +361,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
           mbar_arrive(full + s);
         }
         if (++s == S) { s = 0; ph ^= 1; }
-        c0 += KC;
-        if (c0 >= T.cchunks * KC) {
-          c0 = 0;
-          if (++kx == op.k) { kx = 0; ++ky; }
-        }
+#pragma unroll
+        for (int j = 0; j < PIECES; ++j) cur[j] = nxt[j];
       }
     }
   } else if (warp == kMmaWarp) {
@@ -512,8 +518,7 @@ TcPlan plan_for(const ConvOp& op, int precision) {
 
 bool conv_tc_supported(const ConvOp& op, int precision) {
   if (precision < 1 || precision > 3) return false;
-  return op.in.C % 4 == 0 && op.in.cstride % 4 == 0 && op.in.coff % 4 == 0 &&
-         op.out.C >= 8;
+  return op.in.C % 4 == 0 && op.in.cstride % 4 == 0 && op.in.coff % 4 == 0;
 }
 
 std::vector<uint8_t> pack_tc_weights(const float* w_oikk, int co, int ci, int k,

@@ -371,7 +371,7 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
                            cudaMemcpyHostToDevice));
     TS_CUDA_TRY(cudaMemcpy(L.b, bi->second.second.data(), Co * sizeof(float),
                            cudaMemcpyHostToDevice));
-    if (W->precision != 0 && L.d.ci % 4 == 0 && Co >= 8) {
+    if (W->precision != 0 && L.d.ci % 4 == 0) {
       ConvOp shape{};
       shape.k = L.d.k;
       const std::vector<uint8_t> pk =
@@ -530,7 +530,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
       int st;
       // thin layers -> direct kernel; the rest -> tensor cores (or the
       // fp32 CUDA-core GEMM in precision mode 0)
-      if (conv_direct_supported(op) && (W->precision != 0 || op.out.C <= 16))
+      if (conv_direct_supported(op) && (op.in.C <= 4 || W->precision == 0))
         st = launch_conv_direct(op, stream);
       else if (L.w_tc && conv_tc_supported(op, W->precision))
         st = launch_conv_tc(op, W->precision, stream);
@@ -614,7 +614,7 @@ extern "C" int ts_conv2d(const float* d_x, int batch, int c_in, int h, int w,
   op.w = wp; op.bias = d_bias; op.batch = batch;
   int st;
   void* dpk = nullptr;
-  if (precision != 0 && k * k * c_in > 0 && c_in % 4 == 0 && c_out >= 8) {
+  if (precision != 0 && k * k * c_in > 0 && c_in % 4 == 0) {
     // tensor-core path: pack the swizzled weight images on the host
     std::vector<float> hw(nw);
     TS_CUDA_TRY(cudaMemcpyAsync(hw.data(), d_weight, nw * sizeof(float),
