@@ -69,15 +69,13 @@ def peaks():
 def band_tiles(rank, world):
     """This rank's 32x32 tile band + one halo row on each interior side."""
     from paper_2509_20198_b200 import synth
-    rows = TILES_PER_GPU_SIDE
-    r0 = rank * rows
-    lo = max(0, r0 - 1)
-    hi = min(world * rows, r0 + rows + 1)
+    from paper_2509_20198_b200.parallel import band_for
+    b = band_for(rank, world, world * TILES_PER_GPU_SIDE)
     tiles = synth.chunked_terrain_tiles(
-        TILES_PER_GPU_SIDE, hi - lo, chunks_per_tile=CHUNKS_PER_TILE,
-        points_per_chunk=POINTS_PER_CHUNK, record_seed=1 + lo,
-        origin=(0.0, lo * 640.0))
-    own = [t for t in tiles if r0 * 640.0 <= t.y0 < (r0 + rows) * 640.0]
+        TILES_PER_GPU_SIDE, b.halo1 - b.halo0, chunks_per_tile=CHUNKS_PER_TILE,
+        points_per_chunk=POINTS_PER_CHUNK, record_seed=1 + b.halo0,
+        origin=(0.0, b.halo0 * 640.0))
+    own = [t for t in tiles if b.owns(int(round(t.y0 / 640.0)))]
     return tiles, own
 
 
@@ -143,7 +141,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2509_20198_b200._lib import lib
     from paper_2509_20198_b200.lasio import parse_header
     from paper_2509_20198_b200.pipeline import HeightmapPipeline
-    from paper_2509_20198_b200.refiner import (PRECISION_FP32,
+    from paper_2509_20198_b200.refiner import (PRECISION_BF16X3,
                                                default_descriptor,
                                                random_weights)
 
@@ -151,7 +149,7 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    precision = PRECISION_FP32 if args.precision is None else args.precision
+    precision = PRECISION_BF16X3 if args.precision is None else args.precision
     tiles, own = band_tiles(rank, world)
     images = [t.data for t in tiles]
     descs = np.concatenate([D.tile_desc(parse_header(b)) for b in images])
@@ -175,13 +173,9 @@ def run_ours(args, rank, world, local_rank):
         return out, o, nonfinite
 
     def gather_tiles(out):
-        if world == 1:
-            return
-        if rank == 0:
-            bufs = [torch.empty_like(out) for _ in range(world)]
-            dist.gather(out, bufs, dst=0)
-        else:
-            dist.gather(out, None, dst=0)
+        if world > 1:
+            from paper_2509_20198_b200.parallel import gather_tiles as gt
+            gt(out, dst=0)
 
     for _ in range(args.warmup):
         out, o, nf = step()

@@ -44,6 +44,7 @@ PROV_BAKED = "fullres-baked"
 PRECISION_FP32 = 0      # CUDA-core fp32 implicit GEMM
 PRECISION_TF32X3 = 1    # tcgen05 kind::tf32, 3-pass split (fp32-accurate)
 PRECISION_BF16 = 2      # tcgen05 kind::f16 (bf16 operands, fp32 accumulate)
+PRECISION_BF16X3 = 3    # tcgen05 kind::f16, exact 3-way bf16 split (6 MMAs)
 
 
 @dataclass
