@@ -36,7 +36,11 @@ int launch_conv_direct(const ConvOp& op, void* stream);
 bool conv_tc_supported(const ConvOp& op, int precision);
 int launch_conv_tc(const ConvOp& op, int precision, void* stream);
 // Swizzled per-(n-tile, k-stage) shared-memory images of OIKK weights.
+// chunk_major: K stages ordered (channel chunk, tap) for the halo kernel,
+// else (tap, channel chunk).
 std::vector<uint8_t> pack_tc_weights(const float* w_oikk, int co, int ci, int k,
-                                     int precision, const ConvOp& shape_op);
+                                     int precision, const ConvOp& shape_op,
+                                     bool chunk_major);
+bool conv_tc_halo_eligible(const ConvOp& op, int precision);
 
 }  // namespace ts

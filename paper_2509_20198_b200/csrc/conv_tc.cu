@@ -34,6 +34,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -467,6 +468,298 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
   }
 }
 
+// ===========================================================================
+// Halo-reuse variant for stride-1 k x k convolutions (no up2).
+//
+// Output positions are linearised with a padded pitch Wp = wx + k - 1 and
+// (wy + k - 1) rows per image, so the input of tap (ky, kx) for the 128
+// consecutive positions of a tile is the contiguous run of "halo" rows
+// starting at ky*Wp + kx.  Producers load each channel chunk's halo run
+// (128 + (k-1)(Wp+1) rows) ONCE per tile into one SWIZZLE_128B image; the
+// MMA issuer walks the k*k taps by sliding the A descriptor start address
+// over that image (the swizzle is a function of absolute smem address
+// bits), so every input element is gathered, split and stored once per
+// tile instead of k*k times.  A dedicated warp streams the per-tap weight
+// tiles through a small ring with cp.async.bulk.
+// ===========================================================================
+
+constexpr int kHThreads = (kProdWarps + 1 + 4 + 1) * 32;  // + B-loader warp 13
+
+struct HaloArgs {
+  ConvOp op;
+  const uint8_t* wpk;   // [n_tile][chunk][tap][plane][BN][128 B]
+  int bn, bstages, cchunks, taps, wp, lrows, n_tiles, bofs;
+  int64_t m_tiles, positions;
+};
+
+__device__ __forceinline__ uint64_t sw128_desc_at(uint32_t saddr, int bofs) {
+  uint64_t d = sw128_desc(saddr);
+  if (bofs) d |= (uint64_t)((saddr >> 7) & 7) << 49;
+  return d;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) {
+  using Md = Mode<MODE>;
+  constexpr int P = Md::planes;
+  constexpr int KC = Md::kc;
+  constexpr int PPR = KC / 4;  // fp32 pieces per halo row
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  const ConvOp& op = T.op;
+  const int BN = T.bn, SB = T.bstages, L = T.lrows;
+  const int plane_a = L * kRowBytes;
+  const int halo_bytes = P * plane_a;
+  const int b_bytes = P * BN * kRowBytes;
+  uint8_t* halo = smem;
+  uint8_t* bring = smem + halo_bytes;
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(bring + SB * b_bytes);
+  uint64_t* bempty = bfull + SB;
+  uint64_t* hfull = bempty + SB;
+  uint64_t* hempty = hfull + 1;
+  uint64_t* acc_full = hempty + 1;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  int64_t* rowoff = reinterpret_cast<int64_t*>(tmem_slot + 4);  // [L]
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int wy = op.oy1 - op.oy0, wx = op.ox1 - op.ox0;
+  const int kk1 = op.k - 1;
+  const int Wp = T.wp;
+  const int64_t img_pos = (int64_t)(wy + kk1) * Wp;
+  const int Cin = op.in.C, Cout = op.out.C;
+  const int64_t total_tiles = T.m_tiles * T.n_tiles;
+  uint32_t ncols = 32;
+  while ((int)ncols < 2 * BN) ncols <<= 1;
+
+  if (tid == 0) {
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(bfull + s, 1);
+      mbar_init(bempty + s, 1);
+    }
+    mbar_init(hfull, kProd);
+    mbar_init(hempty, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(acc_full + a, 1);
+      mbar_init(acc_empty + a, 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, ncols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < kProdWarps) {
+    // ------------------------- halo producers -------------------------
+    uint32_t hph = 0;
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      const int64_t mt = tile / T.n_tiles;
+      const int64_t j0 = mt * BM;
+      // previous tile's chunks are done with rowoff once hempty flipped
+      mbar_wait(hempty, hph ^ 1);
+      for (int j = tid; j < L; j += kProd) {
+        const int64_t pos = j0 + j;
+        int64_t off = -1;
+        const int64_t b = pos / img_pos;
+        if (b < op.batch) {
+          const int r = (int)(pos - b * img_pos);
+          const int iy = op.oy0 - op.pad + r / Wp, ix = op.ox0 - op.pad + r % Wp;
+          if (iy >= 0 && iy < op.in.H && ix >= 0 && ix < op.in.W)
+            off = ((b * op.in.H + iy) * op.in.W + ix) * op.in.cstride + op.in.coff;
+        }
+        rowoff[j] = off;
+      }
+      prod_bar();
+      for (int c = 0; c < T.cchunks; ++c) {
+        if (c > 0) mbar_wait(hempty, hph ^ 1);
+        const int c0 = c * KC;
+        for (int pc = tid; pc < L * PPR; pc += kProd * 8) {
+          float4 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int q = pc + u * kProd;
+            v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (q < L * PPR) {
+              const int row = q / PPR, piece = q % PPR;
+              const int64_t off = rowoff[row];
+              const int ch = c0 + 4 * piece;
+              if (off >= 0 && ch < Cin)
+                v[u] = __ldg(reinterpret_cast<const float4*>(op.in.base + off + ch));
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int q = pc + u * kProd;
+            if (q < L * PPR) {
+              // store_piece's layout with a plane pitch of L rows
+              const int row = q / PPR, piece = q % PPR;
+              uint8_t* sa = halo;
+              const int base = (row >> 3) * 1024 + (row & 7) * kRowBytes;
+              const float4 a = v[u];
+              if (MODE == 1) {
+                const int o = base + ((piece ^ (row & 7)) << 4);
+                const float4 hi =
+                    make_float4(tf32_hi(a.x), tf32_hi(a.y), tf32_hi(a.z), tf32_hi(a.w));
+                *reinterpret_cast<float4*>(sa + o) = hi;
+                *reinterpret_cast<float4*>(sa + plane_a + o) =
+                    make_float4(a.x - hi.x, a.y - hi.y, a.z - hi.z, a.w - hi.w);
+              } else {
+                const int o = base + (((piece >> 1) ^ (row & 7)) << 4) + ((piece & 1) << 3);
+                if (MODE == 2) {
+                  *reinterpret_cast<uint2*>(sa + o) = make_uint2(
+                      hi_halves(rn_bf(a.x), rn_bf(a.y)), hi_halves(rn_bf(a.z), rn_bf(a.w)));
+                } else {
+                  const float x0 = trunc_bf(a.x), y0 = trunc_bf(a.y), z0 = trunc_bf(a.z),
+                              w0 = trunc_bf(a.w);
+                  const float rx = a.x - x0, ry = a.y - y0, rz = a.z - z0, rw = a.w - w0;
+                  const float x1 = trunc_bf(rx), y1 = trunc_bf(ry), z1 = trunc_bf(rz),
+                              w1 = trunc_bf(rw);
+                  *reinterpret_cast<uint2*>(sa + o) =
+                      make_uint2(hi_halves(x0, y0), hi_halves(z0, w0));
+                  *reinterpret_cast<uint2*>(sa + plane_a + o) =
+                      make_uint2(hi_halves(x1, y1), hi_halves(z1, w1));
+                  *reinterpret_cast<uint2*>(sa + 2 * plane_a + o) =
+                      make_uint2(hi_halves(rx - x1, ry - y1), hi_halves(rz - z1, rw - w1));
+                }
+              }
+            }
+          }
+        }
+        fence_proxy_async();
+        mbar_arrive(hfull);
+        hph ^= 1;
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ------------------------- MMA issuer -------------------------
+    const uint32_t idesc = make_idesc(Md::tf32 ? 2u : 1u, BN);
+    if ((tid & 31) == 0) {
+      int s = 0, lt = 0;
+      uint32_t bph = 0, hph = 0;
+      for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+        const int acc = lt & 1;
+        mbar_wait(acc_empty + acc, ((lt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        const uint32_t h0 = su32(halo);
+        for (int c = 0; c < T.cchunks; ++c) {
+          mbar_wait(hfull, hph);
+          hph ^= 1;
+          tc_fence_after();
+          for (int t = 0; t < T.taps; ++t) {
+            const int ky = t / op.k, kx = t - ky * op.k;
+            mbar_wait(bfull + s, bph);
+            tc_fence_after();
+            const uint32_t a0 = h0 + (uint32_t)(ky * Wp + kx) * kRowBytes;
+            const uint32_t b0 = su32(bring + s * b_bytes);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t first = (c | t | k) ? 1u : 0u;
+              auto A = [&](int pl) { return sw128_desc_at(a0 + pl * plane_a + 32 * k, T.bofs); };
+              auto B = [&](int pl) { return sw128_desc(b0 + pl * BN * kRowBytes + 32 * k); };
+              if (MODE == 1) {
+                umma<true>(d, A(0), B(0), idesc, first);
+                umma<true>(d, A(0), B(1), idesc, 1u);
+                umma<true>(d, A(1), B(0), idesc, 1u);
+              } else if (MODE == 2) {
+                umma<false>(d, A(0), B(0), idesc, first);
+              } else {
+                umma<false>(d, A(2), B(0), idesc, first);
+                umma<false>(d, A(0), B(2), idesc, 1u);
+                umma<false>(d, A(1), B(1), idesc, 1u);
+                umma<false>(d, A(1), B(0), idesc, 1u);
+                umma<false>(d, A(0), B(1), idesc, 1u);
+                umma<false>(d, A(0), B(0), idesc, 1u);
+              }
+            }
+            umma_commit(bempty + s);
+            if (++s == SB) { s = 0; bph ^= 1; }
+          }
+          umma_commit(hempty);
+        }
+        umma_commit(acc_full + acc);
+      }
+    }
+    __syncwarp();
+  } else if (warp == kHThreads / 32 - 1) {
+    // ------------------------- weight loader -------------------------
+    if ((tid & 31) == 0) {
+      int s = 0;
+      uint32_t bph = 0;
+      for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const int nt = (int)(tile % T.n_tiles);
+        const uint8_t* wsrc = T.wpk + (size_t)nt * T.cchunks * T.taps * b_bytes;
+        for (int kt = 0; kt < T.cchunks * T.taps; ++kt) {
+          mbar_wait(bempty + s, bph ^ 1);
+          bulk_g2s(bring + s * b_bytes, wsrc + (size_t)kt * b_bytes, b_bytes, bfull + s);
+          mbar_arrive_tx(bfull + s, b_bytes);
+          if (++s == SB) { s = 0; bph ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------- epilogue -------------------------
+    const int q = warp & 3;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const bool vec = (op.out.cstride % 4 == 0) && (op.out.coff % 4 == 0);
+    int lt = 0;
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+      const int acc = lt & 1;
+      const int64_t mt = tile / T.n_tiles;
+      const int nt = (int)(tile - mt * T.n_tiles);
+      const int n0 = nt * BN;
+      const int64_t pos = mt * BM + q * 32 + (tid & 31);
+      float* o = nullptr;
+      if (pos < T.positions) {
+        const int64_t b = pos / img_pos;
+        const int r = (int)(pos - b * img_pos);
+        const int y = r / Wp, x = r % Wp;
+        if (y < wy && x < wx)
+          o = op.out.base +
+              ((b * op.out.H + op.oy0 + y) * op.out.W + op.ox0 + x) * op.out.cstride +
+              op.out.coff;
+      }
+      mbar_wait(acc_full + acc, (lt >> 1) & 1);
+      tc_fence_after();
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        tmem_ld16(tmem + lane_base + acc * BN + c, v);
+        if (o) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int n = n0 + c + i;
+            float x = v[i] + (n < Cout ? __ldg(op.bias + n) : 0.f);
+            if (op.lrelu) x = x >= 0.f ? x : 0.01f * x;
+            v[i] = x;
+          }
+          if (vec && n0 + c + 16 <= Cout) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              *reinterpret_cast<float4*>(o + n0 + c + 4 * i) =
+                  make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (n0 + c + i < Cout) o[n0 + c + i] = v[i];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(acc_empty + acc);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    tmem_dealloc(tmem, ncols);
+  }
+}
+
 // ---------------------------------------------------------------- host
 
 uint32_t f2tf32_rna(float x) {
@@ -514,7 +807,41 @@ TcPlan plan_for(const ConvOp& op, int precision) {
   return p;
 }
 
+struct HaloPlan {
+  TcPlan base;
+  int wp, lrows, bstages;
+  size_t smem;
+  int64_t positions;
+};
+
+bool halo_plan(const ConvOp& op, int precision, HaloPlan* hp) {
+  if (op.stride != 1 || op.up2 || op.k < 2 || op.pad * 2 + 1 != op.k) return false;
+  HaloPlan h{};
+  h.base = plan_for(op, precision);
+  const int wx = op.ox1 - op.ox0, wy = op.oy1 - op.oy0;
+  h.wp = wx + op.k - 1;
+  const int L = BM + (op.k - 1) * h.wp + (op.k - 1);
+  h.lrows = (L + 7) / 8 * 8;
+  const size_t halo = (size_t)h.base.planes * h.lrows * kRowBytes;
+  const size_t bst = (size_t)h.base.planes * h.base.bn * kRowBytes;
+  const size_t fixed = 1024 + 8 * 16 + 16 + 8 * (size_t)h.lrows + 64;
+  const size_t cap = 225 * 1024;
+  if (halo + 2 * bst + fixed > cap) return false;
+  h.bstages = (int)std::min<size_t>(6, (cap - halo - fixed) / bst);
+  h.smem = halo + h.bstages * bst + fixed;
+  h.positions = (int64_t)op.batch * (wy + op.k - 1) * h.wp;
+  *hp = h;
+  return true;
+}
+
+int g_halo_bofs = -1;
+
 }  // namespace
+
+bool conv_tc_halo_eligible(const ConvOp& op, int precision) {
+  HaloPlan h;
+  return conv_tc_supported(op, precision) && halo_plan(op, precision, &h);
+}
 
 bool conv_tc_supported(const ConvOp& op, int precision) {
   if (precision < 1 || precision > 3) return false;
@@ -522,7 +849,7 @@ bool conv_tc_supported(const ConvOp& op, int precision) {
 }
 
 std::vector<uint8_t> pack_tc_weights(const float* w_oikk, int co, int ci, int k,
-                                     int precision, const ConvOp& shape_op) {
+                                     int precision, const ConvOp& shape_op, bool chunk_major) {
   ConvOp op = shape_op;
   op.in.C = ci;
   op.out.C = co;
@@ -533,7 +860,9 @@ std::vector<uint8_t> pack_tc_weights(const float* w_oikk, int co, int ci, int k,
   std::vector<uint8_t> out((size_t)p.ntiles * p.kiters * b_bytes, 0);
   for (int nt = 0; nt < p.ntiles; ++nt)
     for (int it = 0; it < p.kiters; ++it) {
-      const int tap = it / p.cchunks, c0 = (it % p.cchunks) * p.kc;
+      const int taps = k * k;
+      const int tap = chunk_major ? it % taps : it / p.cchunks;
+      const int c0 = (chunk_major ? it / taps : it % p.cchunks) * p.kc;
       const int ky = tap / k, kx = tap % k;
       uint8_t* base = out.data() + ((size_t)nt * p.kiters + it) * b_bytes;
       for (int r = 0; r < p.bn; ++r) {
@@ -577,7 +906,43 @@ std::vector<uint8_t> pack_tc_weights(const float* w_oikk, int co, int ci, int k,
   return out;
 }
 
+int launch_conv_tc_halo(const ConvOp& op, int precision, void* stream) {
+  HaloPlan h;
+  if (!halo_plan(op, precision, &h)) return TS_E_INVALID;
+  if (g_halo_bofs < 0) {
+    const char* e = getenv("TS_HALO_BOFS");
+    g_halo_bofs = (e && e[0] == '1') ? 1 : 0;
+  }
+  HaloArgs a{op, op.w_tc, h.base.bn, h.bstages, h.base.cchunks, op.k * op.k, h.wp,
+             h.lrows, h.base.ntiles, g_halo_bofs,
+             ceil_div<int64_t>(h.positions, BM), h.positions};
+  const int64_t tiles = a.m_tiles * h.base.ntiles;
+  if (tiles <= 0) return TS_OK;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    TS_CUDA_TRY(cudaGetDevice(&dev));
+    TS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+  cudaStream_t s = as_stream(stream);
+#define TS_TCH_LAUNCH(MD)                                                             \
+  do {                                                                                \
+    TS_CUDA_TRY(cudaFuncSetAttribute(conv_tc_halo_kernel<MD>,                         \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                     (int)h.smem));                                   \
+    ts::count_launch(), conv_tc_halo_kernel<MD><<<grid, kHThreads, h.smem, s>>>(a);   \
+  } while (0)
+  if (precision == 1) TS_TCH_LAUNCH(1);
+  else if (precision == 2) TS_TCH_LAUNCH(2);
+  else TS_TCH_LAUNCH(3);
+#undef TS_TCH_LAUNCH
+  TS_LAUNCH_CHECK();
+  return TS_OK;
+}
+
 int launch_conv_tc(const ConvOp& op, int precision, void* stream) {
+  if (conv_tc_halo_eligible(op, precision)) return launch_conv_tc_halo(op, precision, stream);
   const TcPlan p = plan_for(op, precision);
   const int64_t M = (int64_t)op.batch * (op.oy1 - op.oy0) * (op.ox1 - op.ox0);
   if (M <= 0) return TS_OK;

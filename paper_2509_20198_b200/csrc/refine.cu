@@ -374,8 +374,16 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
     if (W->precision != 0 && L.d.ci % 4 == 0) {
       ConvOp shape{};
       shape.k = L.d.k;
+      shape.stride = L.d.s;
+      shape.pad = L.d.p;
+      shape.up2 = L.up2;
+      shape.oy0 = L.out_win.y0; shape.oy1 = L.out_win.y1;
+      shape.ox0 = L.out_win.x0; shape.ox1 = L.out_win.x1;
+      shape.in.C = L.d.ci; shape.in.cstride = L.d.ci; shape.out.C = Co;
+      shape.batch = 1;
       const std::vector<uint8_t> pk =
-          pack_tc_weights(src.data(), Co, L.d.ci, L.d.k, W->precision, shape);
+          pack_tc_weights(src.data(), Co, L.d.ci, L.d.k, W->precision, shape,
+                          conv_tc_halo_eligible(shape, W->precision));
       void* d = nullptr;
       TS_CUDA_TRY(cudaMalloc(&d, pk.size()));
       W->device_allocs.push_back(d);
@@ -620,7 +628,8 @@ extern "C" int ts_conv2d(const float* d_x, int batch, int c_in, int h, int w,
     TS_CUDA_TRY(cudaMemcpyAsync(hw.data(), d_weight, nw * sizeof(float),
                                 cudaMemcpyDeviceToHost, s));
     TS_CUDA_TRY(cudaStreamSynchronize(s));
-    const std::vector<uint8_t> pk = pack_tc_weights(hw.data(), c_out, c_in, k, precision, op);
+    const std::vector<uint8_t> pk = pack_tc_weights(hw.data(), c_out, c_in, k, precision, op,
+                                                    conv_tc_halo_eligible(op, precision));
     TS_CUDA_TRY(cudaMallocAsync(&dpk, pk.size(), s));
     TS_CUDA_TRY(cudaMemcpyAsync(dpk, pk.data(), pk.size(), cudaMemcpyHostToDevice, s));
     op.w_tc = reinterpret_cast<const uint8_t*>(dpk);
