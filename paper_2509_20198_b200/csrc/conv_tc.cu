@@ -144,6 +144,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.b32 %0, 1, 0, P;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // SWIZZLE_128B K-major UMMA smem descriptor: start>>4 [0,14), LBO>>4
 // [16,30) (unused for swizzled K-major), SBO>>4 [32,46) = 1024 B per 8-row
 // group, version 1 [46,48), layout SWIZZLE_128B = 2 at [61,64).
@@ -368,47 +376,51 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------ MMA issuer -----------------------------
+    // The whole warp walks the loop (uniform registers), one elected lane
+    // issues; descriptors are integer offsets from precomputed bases.
     const uint32_t idesc = make_idesc(Md::tf32 ? 2u : 1u, BN);
-    if ((tid & 31) == 0) {
-      int s = 0, lt = 0;
-      uint32_t ph = 0;
-      for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
-        const int acc = lt & 1;
-        mbar_wait(acc_empty + acc, ((lt >> 1) & 1) ^ 1);
+    const uint64_t d_smem = sw128_desc(su32(smem));
+    const uint32_t pa = (BM * kRowBytes) >> 4, pb = (BN * kRowBytes) >> 4;
+    int s = 0, lt = 0;
+    uint32_t ph = 0;
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+      const int acc = lt & 1;
+      mbar_wait(acc_empty + acc, ((lt >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem + acc * BN;
+      for (int kit = 0; kit < T.kiters; ++kit) {
+        mbar_wait(full + s, ph);
         tc_fence_after();
-        const uint32_t d = tmem + acc * BN;
-        for (int kit = 0; kit < T.kiters; ++kit) {
-          mbar_wait(full + s, ph);
-          tc_fence_after();
-          const uint32_t a0 = su32(smem + s * stage_bytes);
-          const uint32_t b0 = a0 + a_bytes;
+        if (elect_one()) {
+          const uint64_t a0 = d_smem + (uint64_t)((s * stage_bytes) >> 4);
+          const uint64_t b0 = a0 + (uint64_t)(a_bytes >> 4);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {  // 4 x 32-byte K steps per row
             const uint32_t first = (kit | k) ? 1u : 0u;
-            auto A = [&](int pl) { return sw128_desc(a0 + pl * BM * kRowBytes + 32 * k); };
-            auto B = [&](int pl) { return sw128_desc(b0 + pl * BN * kRowBytes + 32 * k); };
+            const uint64_t ak = a0 + 2 * k, bk = b0 + 2 * k;
             if (MODE == 1) {
-              umma<true>(d, A(0), B(0), idesc, first);
-              umma<true>(d, A(0), B(1), idesc, 1u);
-              umma<true>(d, A(1), B(0), idesc, 1u);
+              umma<true>(d, ak, bk, idesc, first);
+              umma<true>(d, ak, bk + pb, idesc, 1u);
+              umma<true>(d, ak + pa, bk, idesc, 1u);
             } else if (MODE == 2) {
-              umma<false>(d, A(0), B(0), idesc, first);
+              umma<false>(d, ak, bk, idesc, first);
             } else {
-              umma<false>(d, A(2), B(0), idesc, first);  // small terms first
-              umma<false>(d, A(0), B(2), idesc, 1u);
-              umma<false>(d, A(1), B(1), idesc, 1u);
-              umma<false>(d, A(1), B(0), idesc, 1u);
-              umma<false>(d, A(0), B(1), idesc, 1u);
-              umma<false>(d, A(0), B(0), idesc, 1u);
+              umma<false>(d, ak + 2 * pa, bk, idesc, first);  // small terms first
+              umma<false>(d, ak, bk + 2 * pb, idesc, 1u);
+              umma<false>(d, ak + pa, bk + pb, idesc, 1u);
+              umma<false>(d, ak + pa, bk, idesc, 1u);
+              umma<false>(d, ak, bk + pb, idesc, 1u);
+              umma<false>(d, ak, bk, idesc, 1u);
             }
           }
           umma_commit(empty + s);
-          if (++s == S) { s = 0; ph ^= 1; }
         }
-        umma_commit(acc_full + acc);
+        __syncwarp();
+        if (++s == S) { s = 0; ph ^= 1; }
       }
+      if (elect_one()) umma_commit(acc_full + acc);
+      __syncwarp();
     }
-    __syncwarp();
   } else {
     // ------------------------------ epilogue -------------------------------
     const int q = warp & 3;  // TMEM lane quadrant of this warp
@@ -491,12 +503,6 @@ struct HaloArgs {
   int bn, bstages, cchunks, taps, wp, lrows, n_tiles, bofs;
   int64_t m_tiles, positions;
 };
-
-__device__ __forceinline__ uint64_t sw128_desc_at(uint32_t saddr, int bofs) {
-  uint64_t d = sw128_desc(saddr);
-  if (bofs) d |= (uint64_t)((saddr >> 7) & 7) << 49;
-  return d;
-}
 
 template <int MODE>
 __global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) {
@@ -635,54 +641,58 @@ __global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) 
   } else if (warp == kMmaWarp) {
     // ------------------------- MMA issuer -------------------------
     const uint32_t idesc = make_idesc(Md::tf32 ? 2u : 1u, BN);
-    if ((tid & 31) == 0) {
-      int s = 0, lt = 0;
-      uint32_t bph = 0, hph = 0;
-      for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
-        const int acc = lt & 1;
-        mbar_wait(acc_empty + acc, ((lt >> 1) & 1) ^ 1);
+    const uint64_t d_halo = sw128_desc(su32(halo));
+    const uint64_t d_ring = sw128_desc(su32(bring));
+    const uint32_t pa = (uint32_t)plane_a >> 4, pb = (BN * kRowBytes) >> 4;
+    int s = 0, lt = 0;
+    uint32_t bph = 0, hph = 0;
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+      const int acc = lt & 1;
+      mbar_wait(acc_empty + acc, ((lt >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem + acc * BN;
+      for (int c = 0; c < T.cchunks; ++c) {
+        mbar_wait(hfull, hph);
+        hph ^= 1;
         tc_fence_after();
-        const uint32_t d = tmem + acc * BN;
-        const uint32_t h0 = su32(halo);
-        for (int c = 0; c < T.cchunks; ++c) {
-          mbar_wait(hfull, hph);
-          hph ^= 1;
+        int ky = 0, kx = 0;
+        for (int t = 0; t < T.taps; ++t) {
+          mbar_wait(bfull + s, bph);
           tc_fence_after();
-          for (int t = 0; t < T.taps; ++t) {
-            const int ky = t / op.k, kx = t - ky * op.k;
-            mbar_wait(bfull + s, bph);
-            tc_fence_after();
-            const uint32_t a0 = h0 + (uint32_t)(ky * Wp + kx) * kRowBytes;
-            const uint32_t b0 = su32(bring + s * b_bytes);
+          if (elect_one()) {
+            const uint64_t a0 = d_halo + (uint64_t)((ky * Wp + kx) * (kRowBytes >> 4));
+            const uint64_t b0 = d_ring + (uint64_t)((s * b_bytes) >> 4);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint32_t first = (c | t | k) ? 1u : 0u;
-              auto A = [&](int pl) { return sw128_desc_at(a0 + pl * plane_a + 32 * k, T.bofs); };
-              auto B = [&](int pl) { return sw128_desc(b0 + pl * BN * kRowBytes + 32 * k); };
+              const uint64_t ak = a0 + 2 * k, bk = b0 + 2 * k;
               if (MODE == 1) {
-                umma<true>(d, A(0), B(0), idesc, first);
-                umma<true>(d, A(0), B(1), idesc, 1u);
-                umma<true>(d, A(1), B(0), idesc, 1u);
+                umma<true>(d, ak, bk, idesc, first);
+                umma<true>(d, ak, bk + pb, idesc, 1u);
+                umma<true>(d, ak + pa, bk, idesc, 1u);
               } else if (MODE == 2) {
-                umma<false>(d, A(0), B(0), idesc, first);
+                umma<false>(d, ak, bk, idesc, first);
               } else {
-                umma<false>(d, A(2), B(0), idesc, first);
-                umma<false>(d, A(0), B(2), idesc, 1u);
-                umma<false>(d, A(1), B(1), idesc, 1u);
-                umma<false>(d, A(1), B(0), idesc, 1u);
-                umma<false>(d, A(0), B(1), idesc, 1u);
-                umma<false>(d, A(0), B(0), idesc, 1u);
+                umma<false>(d, ak + 2 * pa, bk, idesc, first);
+                umma<false>(d, ak, bk + 2 * pb, idesc, 1u);
+                umma<false>(d, ak + pa, bk + pb, idesc, 1u);
+                umma<false>(d, ak + pa, bk, idesc, 1u);
+                umma<false>(d, ak, bk + pb, idesc, 1u);
+                umma<false>(d, ak, bk, idesc, 1u);
               }
             }
             umma_commit(bempty + s);
-            if (++s == SB) { s = 0; bph ^= 1; }
           }
-          umma_commit(hempty);
+          __syncwarp();
+          if (++s == SB) { s = 0; bph ^= 1; }
+          if (++kx == op.k) { kx = 0; ++ky; }
         }
-        umma_commit(acc_full + acc);
+        if (elect_one()) umma_commit(hempty);
+        __syncwarp();
       }
+      if (elect_one()) umma_commit(acc_full + acc);
+      __syncwarp();
     }
-    __syncwarp();
   } else if (warp == kHThreads / 32 - 1) {
     // ------------------------- weight loader -------------------------
     if ((tid & 31) == 0) {
