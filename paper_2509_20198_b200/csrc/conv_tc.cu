@@ -184,26 +184,42 @@ __device__ __forceinline__ float trunc_bf(float x) {
 __device__ __forceinline__ uint32_t hi_halves(float a, float b) {  // {a.hi16, b.hi16}
   return __byte_perm(__float_as_uint(a), __float_as_uint(b), 0x7632);
 }
+// bf16 round-to-nearest-even; the result's high 16 bits are the bf16 value
+// (low bits are garbage until bf_keep clears them)
 __device__ __forceinline__ float rn_bf(float x) {
   const uint32_t u = __float_as_uint(x);
   return __uint_as_float(u + 0x7FFFu + ((u >> 16) & 1u));
+}
+__device__ __forceinline__ float bf_keep(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xFFFF0000u);
+}
+
+// a = a0 + a1 + e, a0 = bf16_rn(a), a1 = bf16_rn(a - a0), |e| <= 2^-18 |a|
+__device__ __forceinline__ void store_split2(uint8_t* dst, int plane_bytes, float4 a) {
+  const float x0 = bf_keep(rn_bf(a.x)), y0 = bf_keep(rn_bf(a.y)), z0 = bf_keep(rn_bf(a.z)),
+              w0 = bf_keep(rn_bf(a.w));
+  const float x1 = rn_bf(a.x - x0), y1 = rn_bf(a.y - y0), z1 = rn_bf(a.z - z0),
+              w1 = rn_bf(a.w - w0);
+  *reinterpret_cast<uint2*>(dst) = make_uint2(hi_halves(x0, y0), hi_halves(z0, w0));
+  *reinterpret_cast<uint2*>(dst + plane_bytes) =
+      make_uint2(hi_halves(x1, y1), hi_halves(z1, w1));
 }
 
 template <int MODE>
 struct Mode;
 template <>
-struct Mode<1> {  // TF32X3
-  static constexpr int planes = 2, kc = 32;
+struct Mode<1> {  // TF32X3: A hi/lo, B hi/lo
+  static constexpr int pa = 2, pb = 2, kc = 32;
   static constexpr bool tf32 = true;
 };
 template <>
 struct Mode<2> {  // BF16
-  static constexpr int planes = 1, kc = 64;
+  static constexpr int pa = 1, pb = 1, kc = 64;
   static constexpr bool tf32 = false;
 };
 template <>
-struct Mode<3> {  // BF16X3 (6 MMAs)
-  static constexpr int planes = 3, kc = 64;
+struct Mode<3> {  // BF16X3: A = a0 + a1 (RN, residual <= 2^-18 |a|), B = b0+b1+b2
+  static constexpr int pa = 2, pb = 3, kc = 64;
   static constexpr bool tf32 = false;
 };
 
@@ -236,15 +252,7 @@ __device__ __forceinline__ void store_piece(uint8_t* sa, int row, int piece, flo
       *reinterpret_cast<uint2*>(sa + off) =
           make_uint2(hi_halves(rn_bf(a.x), rn_bf(a.y)), hi_halves(rn_bf(a.z), rn_bf(a.w)));
     } else {
-      const float x0 = trunc_bf(a.x), y0 = trunc_bf(a.y), z0 = trunc_bf(a.z),
-                  w0 = trunc_bf(a.w);
-      const float rx = a.x - x0, ry = a.y - y0, rz = a.z - z0, rw = a.w - w0;
-      const float x1 = trunc_bf(rx), y1 = trunc_bf(ry), z1 = trunc_bf(rz), w1 = trunc_bf(rw);
-      *reinterpret_cast<uint2*>(sa + off) = make_uint2(hi_halves(x0, y0), hi_halves(z0, w0));
-      *reinterpret_cast<uint2*>(sa + plane_bytes + off) =
-          make_uint2(hi_halves(x1, y1), hi_halves(z1, w1));
-      *reinterpret_cast<uint2*>(sa + 2 * plane_bytes + off) =
-          make_uint2(hi_halves(rx - x1, ry - y1), hi_halves(rz - z1, rw - w1));
+      store_split2(sa + off, plane_bytes, a);
     }
   }
 }
@@ -256,7 +264,7 @@ __device__ __forceinline__ void prod_bar() {  // the 256 producer threads
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
   using Md = Mode<MODE>;
-  constexpr int P = Md::planes;
+  constexpr int PA = Md::pa, PB = Md::pb;
   constexpr int KC = Md::kc;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // pointer arithmetic on the __shared__ array keeps the shared address
@@ -264,8 +272,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   const ConvOp& op = T.op;
   const int BN = T.bn, S = T.stages;
-  const int a_bytes = P * BM * kRowBytes;
-  const int b_bytes = P * BN * kRowBytes;
+  const int a_bytes = PA * BM * kRowBytes;
+  const int b_bytes = PB * BN * kRowBytes;
   const int stage_bytes = a_bytes + b_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
   uint64_t* empty = full + S;
@@ -405,9 +413,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
             } else if (MODE == 2) {
               umma<false>(d, ak, bk, idesc, first);
             } else {
-              umma<false>(d, ak + 2 * pa, bk, idesc, first);  // small terms first
+              umma<false>(d, ak + pa, bk + pb, idesc, first);  // small terms first
               umma<false>(d, ak, bk + 2 * pb, idesc, 1u);
-              umma<false>(d, ak + pa, bk + pb, idesc, 1u);
               umma<false>(d, ak + pa, bk, idesc, 1u);
               umma<false>(d, ak, bk + pb, idesc, 1u);
               umma<false>(d, ak, bk, idesc, 1u);
@@ -507,7 +514,7 @@ struct HaloArgs {
 template <int MODE>
 __global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) {
   using Md = Mode<MODE>;
-  constexpr int P = Md::planes;
+  constexpr int PA = Md::pa, PB = Md::pb;
   constexpr int KC = Md::kc;
   constexpr int PPR = KC / 4;  // fp32 pieces per halo row
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -515,18 +522,18 @@ __global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) 
   const ConvOp& op = T.op;
   const int BN = T.bn, SB = T.bstages, L = T.lrows;
   const int plane_a = L * kRowBytes;
-  const int halo_bytes = P * plane_a;
-  const int b_bytes = P * BN * kRowBytes;
+  const int halo_bytes = PA * plane_a;  // one halo buffer (2 are resident)
+  const int b_bytes = PB * BN * kRowBytes;
   uint8_t* halo = smem;
-  uint8_t* bring = smem + halo_bytes;
+  uint8_t* bring = smem + 2 * halo_bytes;
   uint64_t* bfull = reinterpret_cast<uint64_t*>(bring + SB * b_bytes);
   uint64_t* bempty = bfull + SB;
-  uint64_t* hfull = bempty + SB;
-  uint64_t* hempty = hfull + 1;
-  uint64_t* acc_full = hempty + 1;
+  uint64_t* hfull = bempty + SB;       // [2]
+  uint64_t* hempty = hfull + 2;        // [2]
+  uint64_t* acc_full = hempty + 2;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  int64_t* rowoff = reinterpret_cast<int64_t*>(tmem_slot + 4);  // [L]
+  int64_t* rowoff = reinterpret_cast<int64_t*>(tmem_slot + 4);  // [2][L]
 
   const int tid = threadIdx.x, warp = tid >> 5;
   const int wy = op.oy1 - op.oy0, wx = op.ox1 - op.ox0;
@@ -543,8 +550,10 @@ __global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) 
       mbar_init(bfull + s, 1);
       mbar_init(bempty + s, 1);
     }
-    mbar_init(hfull, kProd);
-    mbar_init(hempty, 1);
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(hfull + h, kProd);
+      mbar_init(hempty + h, 1);
+    }
     for (int a = 0; a < 2; ++a) {
       mbar_init(acc_full + a, 1);
       mbar_init(acc_empty + a, 4);
@@ -559,12 +568,16 @@ __global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) 
 
   if (warp < kProdWarps) {
     // ------------------------- halo producers -------------------------
-    uint32_t hph = 0;
-    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    // Halo buffers alternate per (tile, chunk); each producer thread walks
+    // the same sequence, so buffer hb and its phase are uniform.
+    int hb = 0, lt = 0;
+    uint32_t hmask = 0;  // bit hb = phase parity of halo buffer hb
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
       const int64_t mt = tile / T.n_tiles;
       const int64_t j0 = mt * BM;
-      // previous tile's chunks are done with rowoff once hempty flipped
-      mbar_wait(hempty, hph ^ 1);
+      int64_t* ro = rowoff + (lt & 1) * L;
+      // ro[] of tile lt-2 was last read by loads published before this
+      // thread passed prod_bar of tile lt-1
       for (int j = tid; j < L; j += kProd) {
         const int64_t pos = j0 + j;
         int64_t off = -1;
@@ -575,11 +588,12 @@ __global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) 
           if (iy >= 0 && iy < op.in.H && ix >= 0 && ix < op.in.W)
             off = ((b * op.in.H + iy) * op.in.W + ix) * op.in.cstride + op.in.coff;
         }
-        rowoff[j] = off;
+        ro[j] = off;
       }
       prod_bar();
       for (int c = 0; c < T.cchunks; ++c) {
-        if (c > 0) mbar_wait(hempty, hph ^ 1);
+        mbar_wait(hempty + hb, ((hmask >> hb) & 1u) ^ 1u);
+        uint8_t* sa = halo + hb * halo_bytes;
         const int c0 = c * KC;
         for (int pc = tid; pc < L * PPR; pc += kProd * 8) {
           float4 v[8];
@@ -589,7 +603,7 @@ __global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) 
             v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (q < L * PPR) {
               const int row = q / PPR, piece = q % PPR;
-              const int64_t off = rowoff[row];
+              const int64_t off = ro[row];
               const int ch = c0 + 4 * piece;
               if (off >= 0 && ch < Cin)
                 v[u] = __ldg(reinterpret_cast<const float4*>(op.in.base + off + ch));
@@ -599,9 +613,7 @@ __global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) 
           for (int u = 0; u < 8; ++u) {
             const int q = pc + u * kProd;
             if (q < L * PPR) {
-              // store_piece's layout with a plane pitch of L rows
               const int row = q / PPR, piece = q % PPR;
-              uint8_t* sa = halo;
               const int base = (row >> 3) * 1024 + (row & 7) * kRowBytes;
               const float4 a = v[u];
               if (MODE == 1) {
@@ -613,29 +625,19 @@ __global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) 
                     make_float4(a.x - hi.x, a.y - hi.y, a.z - hi.z, a.w - hi.w);
               } else {
                 const int o = base + (((piece >> 1) ^ (row & 7)) << 4) + ((piece & 1) << 3);
-                if (MODE == 2) {
+                if (MODE == 2)
                   *reinterpret_cast<uint2*>(sa + o) = make_uint2(
                       hi_halves(rn_bf(a.x), rn_bf(a.y)), hi_halves(rn_bf(a.z), rn_bf(a.w)));
-                } else {
-                  const float x0 = trunc_bf(a.x), y0 = trunc_bf(a.y), z0 = trunc_bf(a.z),
-                              w0 = trunc_bf(a.w);
-                  const float rx = a.x - x0, ry = a.y - y0, rz = a.z - z0, rw = a.w - w0;
-                  const float x1 = trunc_bf(rx), y1 = trunc_bf(ry), z1 = trunc_bf(rz),
-                              w1 = trunc_bf(rw);
-                  *reinterpret_cast<uint2*>(sa + o) =
-                      make_uint2(hi_halves(x0, y0), hi_halves(z0, w0));
-                  *reinterpret_cast<uint2*>(sa + plane_a + o) =
-                      make_uint2(hi_halves(x1, y1), hi_halves(z1, w1));
-                  *reinterpret_cast<uint2*>(sa + 2 * plane_a + o) =
-                      make_uint2(hi_halves(rx - x1, ry - y1), hi_halves(rz - z1, rw - w1));
-                }
+                else
+                  store_split2(sa + o, plane_a, a);
               }
             }
           }
         }
         fence_proxy_async();
-        mbar_arrive(hfull);
-        hph ^= 1;
+        mbar_arrive(hfull + hb);
+        hmask ^= 1u << hb;
+        hb ^= 1;
       }
     }
   } else if (warp == kMmaWarp) {
@@ -644,23 +646,25 @@ __global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) 
     const uint64_t d_halo = sw128_desc(su32(halo));
     const uint64_t d_ring = sw128_desc(su32(bring));
     const uint32_t pa = (uint32_t)plane_a >> 4, pb = (BN * kRowBytes) >> 4;
-    int s = 0, lt = 0;
-    uint32_t bph = 0, hph = 0;
+    int s = 0, lt = 0, hb = 0;
+    uint32_t bph = 0;
+    uint32_t hmask = 0;  // bit hb = phase parity of halo buffer hb
     for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
       const int acc = lt & 1;
       mbar_wait(acc_empty + acc, ((lt >> 1) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d = tmem + acc * BN;
       for (int c = 0; c < T.cchunks; ++c) {
-        mbar_wait(hfull, hph);
-        hph ^= 1;
+        mbar_wait(hfull + hb, (hmask >> hb) & 1u);
+        hmask ^= 1u << hb;
         tc_fence_after();
+        const uint64_t d_hb = d_halo + (uint64_t)((hb * halo_bytes) >> 4);
         int ky = 0, kx = 0;
         for (int t = 0; t < T.taps; ++t) {
           mbar_wait(bfull + s, bph);
           tc_fence_after();
           if (elect_one()) {
-            const uint64_t a0 = d_halo + (uint64_t)((ky * Wp + kx) * (kRowBytes >> 4));
+            const uint64_t a0 = d_hb + (uint64_t)((ky * Wp + kx) * (kRowBytes >> 4));
             const uint64_t b0 = d_ring + (uint64_t)((s * b_bytes) >> 4);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -673,9 +677,8 @@ __global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) 
               } else if (MODE == 2) {
                 umma<false>(d, ak, bk, idesc, first);
               } else {
-                umma<false>(d, ak + 2 * pa, bk, idesc, first);
+                umma<false>(d, ak + pa, bk + pb, idesc, first);
                 umma<false>(d, ak, bk + 2 * pb, idesc, 1u);
-                umma<false>(d, ak + pa, bk + pb, idesc, 1u);
                 umma<false>(d, ak + pa, bk, idesc, 1u);
                 umma<false>(d, ak, bk + pb, idesc, 1u);
                 umma<false>(d, ak, bk, idesc, 1u);
@@ -687,8 +690,9 @@ __global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) 
           if (++s == SB) { s = 0; bph ^= 1; }
           if (++kx == op.k) { kx = 0; ++ky; }
         }
-        if (elect_one()) umma_commit(hempty);
+        if (elect_one()) umma_commit(hempty + hb);
         __syncwarp();
+        hb ^= 1;
       }
       if (elect_one()) umma_commit(acc_full + acc);
       __syncwarp();
@@ -795,13 +799,14 @@ float bf16_to_f(uint16_t h) {
 }
 
 struct TcPlan {
-  int bn, stages, kiters, cchunks, ntiles, planes, kc;
+  int bn, stages, kiters, cchunks, ntiles, pa, pb, kc;
   size_t smem;
 };
 
 TcPlan plan_for(const ConvOp& op, int precision) {
   TcPlan p{};
-  p.planes = precision == 1 ? 2 : precision == 2 ? 1 : 3;
+  p.pa = precision == 2 ? 1 : 2;
+  p.pb = precision == 1 ? 2 : precision == 2 ? 1 : 3;
   p.kc = precision == 1 ? 32 : 64;
   const int n16 = (op.out.C + 15) / 16 * 16;
   const int cap = 128;
@@ -809,7 +814,7 @@ TcPlan plan_for(const ConvOp& op, int precision) {
   p.bn = ((n16 + p.ntiles - 1) / p.ntiles + 15) / 16 * 16;
   p.cchunks = (op.in.C + p.kc - 1) / p.kc;
   p.kiters = op.k * op.k * p.cchunks;
-  const size_t stage = (size_t)(BM + p.bn) * kRowBytes * p.planes;
+  const size_t stage = ((size_t)BM * p.pa + (size_t)p.bn * p.pb) * kRowBytes;
   const size_t budget = 218 * 1024;
   p.stages = (int)std::min<size_t>(6, budget / stage);
   p.stages = std::max(p.stages, 1);
@@ -832,9 +837,9 @@ bool halo_plan(const ConvOp& op, int precision, HaloPlan* hp) {
   h.wp = wx + op.k - 1;
   const int L = BM + (op.k - 1) * h.wp + (op.k - 1);
   h.lrows = (L + 7) / 8 * 8;
-  const size_t halo = (size_t)h.base.planes * h.lrows * kRowBytes;
-  const size_t bst = (size_t)h.base.planes * h.base.bn * kRowBytes;
-  const size_t fixed = 1024 + 8 * 16 + 16 + 8 * (size_t)h.lrows + 64;
+  const size_t halo = 2 * (size_t)h.base.pa * h.lrows * kRowBytes;  // double buffered
+  const size_t bst = (size_t)h.base.pb * h.base.bn * kRowBytes;
+  const size_t fixed = 1024 + 8 * 24 + 16 + 16 * (size_t)h.lrows + 64;
   const size_t cap = 225 * 1024;
   if (halo + 2 * bst + fixed > cap) return false;
   h.bstages = (int)std::min<size_t>(6, (cap - halo - fixed) / bst);
@@ -866,7 +871,7 @@ std::vector<uint8_t> pack_tc_weights(const float* w_oikk, int co, int ci, int k,
   op.k = k;
   const TcPlan p = plan_for(op, precision);
   const size_t plane = (size_t)p.bn * kRowBytes;
-  const size_t b_bytes = plane * p.planes;
+  const size_t b_bytes = plane * p.pb;
   std::vector<uint8_t> out((size_t)p.ntiles * p.kiters * b_bytes, 0);
   for (int nt = 0; nt < p.ntiles; ++nt)
     for (int it = 0; it < p.kiters; ++it) {
