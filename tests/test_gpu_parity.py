@@ -275,7 +275,7 @@ def test_interpolate_patch_api(golden):
                                key=PatchKey(1, 2, (960.0, 1600.0)))
         if not ties[48, 48]:        # a tie on the re-centring cell shifts all
             assert np.abs(rk.hm_lin - gi[f"khm_lin{k}"])[~ties].max() <= 1e-6, k
-        assert abs(rk.key.c_z - float(gi[f"kcz{k}"])) <= 1e-3, k
+            assert abs(rk.key.c_z - float(gi[f"kcz{k}"])) <= 1e-3, k
 
 
 def test_random_patches_vs_oracle():
