@@ -153,8 +153,13 @@ def run_ours(args, rank, world, local_rank):
     tiles, own = band_tiles(rank, world)
     images = [t.data for t in tiles]
     descs = np.concatenate([D.tile_desc(parse_header(b)) for b in images])
-    centers = np.array([[t.x0 + 320.0, t.y0 + 320.0] for t in own])
-    P = len(centers)
+    centers_h = np.array([[t.x0 + 320.0, t.y0 + 320.0] for t in own])
+    P = len(centers_h)
+    centers = D.upload(centers_h)                     # patch keys stay resident
+    x0s = [t.x0 for t in tiles]
+    y0s = [t.y0 for t in tiles]
+    cell_range = HeightmapPipeline.cell_range((min(x0s), min(y0s)),
+                                              (max(x0s) + 640.0, max(y0s) + 640.0))
     bundle = random_weights(default_descriptor(), seed=3)
     pipe = HeightmapPipeline(bundle, precision)
     tb = D.TileBatch(images, descs)                  # resident in HBM
@@ -163,7 +168,7 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
 
     def step(timer=None):
-        tables, cp, idx = pipe.overview(tb)
+        tables, cp, idx = pipe.overview(tb, cell_range)
         if timer is not None:
             timer["ov"].record(stream)
         g, t, o, cnn_in = pipe.patches(idx, centers)

@@ -195,11 +195,30 @@ __global__ void gather_fill_kernel(const double* __restrict__ xyz,
 
 using namespace ts;
 
+namespace ts {
+// The stream-ordered pool returns freed memory to the driver at every
+// synchronisation by default (release threshold 0); keep it instead so
+// per-step scratch allocations stay cheap.
+int keep_pool_memory() {
+  static int done = 0;
+  if (done) return TS_OK;
+  int dev = 0;
+  TS_CUDA_TRY(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  TS_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = ~0ull;
+  TS_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  done = 1;
+  return TS_OK;
+}
+}  // namespace ts
+
 extern "C" int ts_index_build(const int64_t* d_cell, int64_t n, int64_t ci0,
                               int64_t cj0, int64_t nci, int64_t ncj,
                               int32_t* d_order, int32_t* d_cell_start,
                               int32_t* d_cell_end, void* stream) {
   cudaStream_t s = as_stream(stream);
+  if (keep_pool_memory() != TS_OK) return TS_E_CUDA;
   if (nci <= 0 || ncj <= 0 || nci * ncj >= 0xFFFFFFFFLL) return TS_E_INVALID;
   TS_CUDA_TRY(cudaMemsetAsync(d_cell_start, 0, sizeof(int32_t) * nci * ncj, s));
   TS_CUDA_TRY(cudaMemsetAsync(d_cell_end, 0, sizeof(int32_t) * nci * ncj, s));

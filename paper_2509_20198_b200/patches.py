@@ -177,12 +177,19 @@ class ChunkPointIndex:
 class DeviceIndex:
     """xyz/rgb/cells on the device + the ts_index_build cell ranges."""
 
-    def __init__(self, xyz: torch.Tensor, rgb, cells: torch.Tensor):
+    def __init__(self, xyz: torch.Tensor, rgb, cells: torch.Tensor,
+                 cell_range=None):
+        """cell_range = (ci0, cj0, ci1, cj1) inclusive, e.g. from the LAS
+        header bboxes; without it the range is reduced on the device (one
+        host sync).  Points outside the range are not indexed."""
         self.xyz, self.rgb, self.cells = xyz, rgb, cells
         n = len(xyz)
-        lo = cells.min(dim=0).values
-        hi = cells.max(dim=0).values
-        lo_h, hi_h = lo.tolist(), hi.tolist()   # one sync: sizes the grid
+        if cell_range is not None:
+            lo_h, hi_h = list(cell_range[:2]), list(cell_range[2:])
+        else:
+            lo = cells.min(dim=0).values
+            hi = cells.max(dim=0).values
+            lo_h, hi_h = lo.tolist(), hi.tolist()   # sizes the grid
         self.ci0, self.cj0 = lo_h
         self.nci, self.ncj = hi_h[0] - lo_h[0] + 1, hi_h[1] - lo_h[1] + 1
         self.order = D.empty((max(n, 1),), torch.int32)

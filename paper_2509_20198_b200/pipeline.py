@@ -36,11 +36,19 @@ class HeightmapPipeline:
             self._ws_batch = batch
         return self._ws
 
-    def overview(self, tb: D.TileBatch):
+    @staticmethod
+    def cell_range(bbox_min, bbox_max):
+        """Inclusive 640 m cell range of a dataset bbox (plus one cell)."""
+        lo = np.floor(np.asarray(bbox_min[:2], np.float64) / 640.0) - 1
+        hi = np.floor(np.asarray(bbox_max[:2], np.float64) / 640.0) + 1
+        return (int(lo[0]), int(lo[1]), int(hi[0]), int(hi[1]))
+
+    def overview(self, tb: D.TileBatch, cell_range=None):
         """Chunk tables + chunk points + index (load_overview)."""
         tables = D.ChunkTables(tb)
         cp = D.ChunkPoints(tb, tables, records=False)
-        idx = DeviceIndex(cp.xyz[:max(cp.n, 1)], cp.rgb, cp.cells)
+        idx = DeviceIndex(cp.xyz[:max(cp.n, 1)], cp.rgb, cp.cells[:max(cp.n, 1)],
+                          cell_range)
         return tables, cp, idx
 
     def patches(self, idx: DeviceIndex, centers):
@@ -58,8 +66,10 @@ class HeightmapPipeline:
         self.weights.run(cnn_in, P, out, nonfinite, self._workspace(P))
         return out, nonfinite
 
-    def run(self, tb: D.TileBatch, centers: np.ndarray):
-        tables, cp, idx = self.overview(tb)
+    def run(self, tb: D.TileBatch, centers, cell_range=None):
+        """centers: (P, 2) patch centres (numpy, or a device tensor to keep
+        host->device copies out of the step)."""
+        tables, cp, idx = self.overview(tb, cell_range)
         g, t, o, cnn_in = self.patches(idx, centers)
         out, nonfinite = self.refine(cnn_in, g["n"])
         return dict(out=out, cz=o["cz"], status=o["status"],

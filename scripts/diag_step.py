@@ -18,7 +18,8 @@ torch.cuda.set_device(0)
 tiles, own = bench.band_tiles(0, 1)
 images = [t.data for t in tiles]
 descs = np.concatenate([D.tile_desc(parse_header(b)) for b in images])
-centers = np.array([[t.x0 + 320.0, t.y0 + 320.0] for t in own])
+centers = D.upload(np.array([[t.x0 + 320.0, t.y0 + 320.0] for t in own]))
+cell_range = HeightmapPipeline.cell_range((0.0, 0.0), (32 * 640.0, 32 * 640.0))
 pipe = HeightmapPipeline(random_weights(default_descriptor(), seed=3), 3)
 tb = D.TileBatch(images, descs)
 P = len(centers)
@@ -26,7 +27,7 @@ P = len(centers)
 
 def step():
     t0 = time.perf_counter()
-    tables, cp, idx = pipe.overview(tb)
+    tables, cp, idx = pipe.overview(tb, cell_range)
     t1 = time.perf_counter()
     g, t, o, cnn_in = pipe.patches(idx, centers)
     t2 = time.perf_counter()
