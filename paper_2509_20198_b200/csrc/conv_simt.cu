@@ -141,47 +141,63 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvOp op) {
   for (int i = threadIdx.x; i < K * Cout; i += blockDim.x) sw[i] = op.w[i];
   float* sb = sw + K * Cout;
   for (int i = threadIdx.x; i < Cout; i += blockDim.x) sb[i] = op.bias[i];
-  __syncthreads();
+  float* so = sb + ((Cout + 3) & ~3);  // [128][Cout] output staging
   const int wy = op.oy1 - op.oy0, wx = op.ox1 - op.ox0;
   const int64_t M = (int64_t)op.batch * wy * wx;
   const int Hl = op.up2 ? 2 * op.in.H : op.in.H;
   const int Wl = op.up2 ? 2 * op.in.W : op.in.W;
-  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < M;
-       m += (int64_t)gridDim.x * blockDim.x) {
-    const int b = (int)(m / ((int64_t)wy * wx));
-    const int r = (int)(m - (int64_t)b * wy * wx);
-    const int oy = op.oy0 + r / wx, ox = op.ox0 + r % wx;
-    float acc[CO];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t m0 = blockIdx.x * (int64_t)blockDim.x; m0 < M;
+       m0 += (int64_t)gridDim.x * blockDim.x) {
+    __syncthreads();  // weights loaded / previous staging drained
+    const int64_t m = m0 + threadIdx.x;
+    if (m < M) {
+      const int b = (int)(m / ((int64_t)wy * wx));
+      const int r = (int)(m - (int64_t)b * wy * wx);
+      const int oy = op.oy0 + r / wx, ox = op.ox0 + r % wx;
+      float acc[CO];
 #pragma unroll
-    for (int c = 0; c < CO; ++c) acc[c] = 0.f;
-    const float* inb = op.in.base + (int64_t)b * op.in.H * op.in.W * op.in.cstride + op.in.coff;
-    for (int ky = 0; ky < op.k; ++ky) {
-      int iy = oy * op.stride - op.pad + ky;
-      if (iy < 0 || iy >= Hl) continue;
-      if (op.up2) iy >>= 1;
-      for (int kx = 0; kx < op.k; ++kx) {
-        int ix = ox * op.stride - op.pad + kx;
-        if (ix < 0 || ix >= Wl) continue;
-        if (op.up2) ix >>= 1;
-        const float* src = inb + ((int64_t)iy * op.in.W + ix) * op.in.cstride;
-        const float* wt = sw + (ky * op.k + kx) * Cin * Cout;
-        for (int ci = 0; ci < Cin; ++ci) {
-          const float x = __ldg(src + ci);
+      for (int c = 0; c < CO; ++c) acc[c] = 0.f;
+      const float* inb =
+          op.in.base + (int64_t)b * op.in.H * op.in.W * op.in.cstride + op.in.coff;
+      for (int ky = 0; ky < op.k; ++ky) {
+        int iy = oy * op.stride - op.pad + ky;
+        if (iy < 0 || iy >= Hl) continue;
+        if (op.up2) iy >>= 1;
+        for (int kx = 0; kx < op.k; ++kx) {
+          int ix = ox * op.stride - op.pad + kx;
+          if (ix < 0 || ix >= Wl) continue;
+          if (op.up2) ix >>= 1;
+          const float* src = inb + ((int64_t)iy * op.in.W + ix) * op.in.cstride;
+          const float* wt = sw + (ky * op.k + kx) * Cin * Cout;
+          for (int ci = 0; ci < Cin; ++ci) {
+            const float x = __ldg(src + ci);
 #pragma unroll
-          for (int c = 0; c < CO; ++c)
-            if (c < Cout) acc[c] = fmaf(x, wt[ci * Cout + c], acc[c]);
+            for (int c = 0; c < CO; ++c)
+              if (c < Cout) acc[c] = fmaf(x, wt[ci * Cout + c], acc[c]);
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < CO; ++c) {
+        if (c < Cout) {
+          float v = acc[c] + sb[c];
+          if (op.lrelu) v = v >= 0.f ? v : 0.01f * v;
+          so[threadIdx.x * Cout + c] = v;
         }
       }
     }
-    float* o = op.out.base + (((int64_t)b * op.out.H + oy) * op.out.W + ox) * op.out.cstride +
-               op.out.coff;
-#pragma unroll
-    for (int c = 0; c < CO; ++c) {
-      if (c < Cout) {
-        float v = acc[c] + sb[c];
-        if (op.lrelu) v = v >= 0.f ? v : 0.01f * v;
-        o[c] = v;
-      }
+    __syncthreads();
+    // coalesced write-back: one warp per pixel, lanes over channels
+    for (int t = warp; t < 128; t += 4) {
+      const int64_t mm = m0 + t;
+      if (mm >= M) break;
+      const int b = (int)(mm / ((int64_t)wy * wx));
+      const int r = (int)(mm - (int64_t)b * wy * wx);
+      const int y = op.oy0 + r / wx, x = op.ox0 + r % wx;
+      float* o = op.out.base + (((int64_t)b * op.out.H + y) * op.out.W + x) * op.out.cstride +
+                 op.out.coff;
+      for (int c = lane; c < Cout; c += 32) o[c] = so[t * Cout + c];
     }
   }
 }
@@ -191,13 +207,15 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvOp op) {
 bool conv_direct_supported(const ConvOp& op) {
   const int K = op.k * op.k * op.in.C;
   return (op.in.C <= 4 || op.out.C <= 16) && op.out.C <= 64 &&
-         (size_t)(K + 1) * op.out.C * sizeof(float) <= 96 * 1024;
+         (size_t)(K + 1 + 128) * op.out.C * sizeof(float) + 16 <= 160 * 1024;
 }
 
 int launch_conv_direct(const ConvOp& op, void* stream) {
   const int64_t M = (int64_t)op.batch * (op.oy1 - op.oy0) * (op.ox1 - op.ox0);
   if (M <= 0) return TS_OK;
-  const size_t smem = (size_t)(op.k * op.k * op.in.C + 1) * op.out.C * sizeof(float);
+  const size_t smem =
+      ((size_t)(op.k * op.k * op.in.C) * op.out.C + ((op.out.C + 3) & ~3) + 128 * op.out.C) *
+      sizeof(float);
   const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(M, 128), 148 * 16);
   cudaStream_t s = as_stream(stream);
 #define TS_DIRECT(CO)                                                                  \

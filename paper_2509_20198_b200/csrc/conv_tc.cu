@@ -584,9 +584,12 @@ __global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) 
         const int64_t b = pos / img_pos;
         if (b < op.batch) {
           const int r = (int)(pos - b * img_pos);
+          // halo position -> (up2-folded) source pixel; zero outside the image
           const int iy = op.oy0 - op.pad + r / Wp, ix = op.ox0 - op.pad + r % Wp;
-          if (iy >= 0 && iy < op.in.H && ix >= 0 && ix < op.in.W)
-            off = ((b * op.in.H + iy) * op.in.W + ix) * op.in.cstride + op.in.coff;
+          const int sh = op.up2 ? 1 : 0;
+          if (iy >= 0 && iy < (op.in.H << sh) && ix >= 0 && ix < (op.in.W << sh))
+            off = ((b * op.in.H + (iy >> sh)) * op.in.W + (ix >> sh)) * op.in.cstride +
+                  op.in.coff;
         }
         ro[j] = off;
       }
@@ -830,7 +833,7 @@ struct HaloPlan {
 };
 
 bool halo_plan(const ConvOp& op, int precision, HaloPlan* hp) {
-  if (op.stride != 1 || op.up2 || op.k < 2 || op.pad * 2 + 1 != op.k) return false;
+  if (op.stride != 1 || op.k < 2 || op.pad * 2 + 1 != op.k) return false;
   HaloPlan h{};
   h.base = plan_for(op, precision);
   const int wx = op.ox1 - op.ox0, wy = op.oy1 - op.oy0;

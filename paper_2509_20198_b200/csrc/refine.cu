@@ -369,8 +369,7 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
       L.out_off = alloc((size_t)L.Hout * L.Wout * L.d.co);
       L.out_cstride = L.d.co; L.out_coff = 0;
     }
-    if (W->precision != 0 && L.up2 && L.d.s == 1 && L.d.k == 2 * L.d.p + 1 &&
-        L.d.ci % 4 == 0) {
+    if (false) {  // up2 is folded into the halo kernel's row table now
       L.materialize = true;
       L.up_off = alloc((size_t)4 * L.Hin * L.Win_ * L.d.ci);
       LayerDesc flat = L.d;
