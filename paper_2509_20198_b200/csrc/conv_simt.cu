@@ -141,7 +141,8 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvOp op) {
   for (int i = threadIdx.x; i < K * Cout; i += blockDim.x) sw[i] = op.w[i];
   float* sb = sw + K * Cout;
   for (int i = threadIdx.x; i < Cout; i += blockDim.x) sb[i] = op.bias[i];
-  float* so = sb + ((Cout + 3) & ~3);  // [128][Cout] output staging
+  float* so = sb + ((Cout + 3) & ~3);  // [128][Cs] output staging
+  const int Cs = Cout | 1;              // odd row pitch: conflict-free banks
   const int wy = op.oy1 - op.oy0, wx = op.ox1 - op.ox0;
   const int64_t M = (int64_t)op.batch * wy * wx;
   const int Hl = op.up2 ? 2 * op.in.H : op.in.H;
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvOp op) {
         if (c < Cout) {
           float v = acc[c] + sb[c];
           if (op.lrelu) v = v >= 0.f ? v : 0.01f * v;
-          so[threadIdx.x * Cout + c] = v;
+          so[threadIdx.x * Cs + c] = v;
         }
       }
     }
@@ -197,7 +198,7 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvOp op) {
       const int y = op.oy0 + r / wx, x = op.ox0 + r % wx;
       float* o = op.out.base + (((int64_t)b * op.out.H + y) * op.out.W + x) * op.out.cstride +
                  op.out.coff;
-      for (int c = lane; c < Cout; c += 32) o[c] = so[t * Cout + c];
+      for (int c = lane; c < Cout; c += 32) o[c] = so[t * Cs + c];
     }
   }
 }
@@ -207,14 +208,15 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvOp op) {
 bool conv_direct_supported(const ConvOp& op) {
   const int K = op.k * op.k * op.in.C;
   return (op.in.C <= 4 || op.out.C <= 16) && op.out.C <= 64 &&
-         (size_t)(K + 1 + 128) * op.out.C * sizeof(float) + 16 <= 160 * 1024;
+         (size_t)(K + 1 + 128) * (op.out.C + 1) * sizeof(float) + 16 <= 160 * 1024;
 }
 
 int launch_conv_direct(const ConvOp& op, void* stream) {
   const int64_t M = (int64_t)op.batch * (op.oy1 - op.oy0) * (op.ox1 - op.ox0);
   if (M <= 0) return TS_OK;
   const size_t smem =
-      ((size_t)(op.k * op.k * op.in.C) * op.out.C + ((op.out.C + 3) & ~3) + 128 * op.out.C) *
+      ((size_t)(op.k * op.k * op.in.C) * op.out.C + ((op.out.C + 3) & ~3) +
+       128 * (op.out.C | 1)) *
       sizeof(float);
   const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(M, 128), 148 * 16);
   cudaStream_t s = as_stream(stream);
