@@ -152,10 +152,13 @@ int ts_nearest(const double* d_xy, int64_t n, const double* d_q, int64_t nq,
  * (replaces scipy Delaunay/Qhull at patches.py:316-326).  Exact
  * orientation/incircle predicates; vertex ids 0..N-1 real, N..N+3 the
  * corners (-1,-1),(1,-1),(-1,1),(1,1).  Triangle slot p starts at
- * 2*pts_off[p] + 8*p; capacity 2N+8; d_ntri[p] gets the count.  CCW.   */
+ * 2*pts_off[p] + 8*p; capacity 2N+8; d_ntri[p] gets the count.  CCW.
+ * d_scratch: ts_triangulate_scratch(total points, patches) bytes (the
+ * per-triangle circumcircle cache).                                      */
+size_t ts_triangulate_scratch(int64_t total_points, int n_patches);
 int ts_triangulate(const double* d_xy, const int64_t* d_pts_off,
                    int n_patches, int32_t* d_tri, int32_t* d_ntri,
-                   int32_t* d_status, void* stream);
+                   int32_t* d_status, void* d_scratch, void* stream);
 /* Algorithm 1 rasterisation (patches.py:290-405) given triangles:
  * exact-d^2 NN (lowest index wins), lowest-id face map with the _TriGeom
  * 1e-9 barycentric test, padding-triangle blanking, barycentric hm/rgb,

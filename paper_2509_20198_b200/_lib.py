@@ -51,7 +51,8 @@ SIGNATURES = {
                              P, P, P, P, P, P, P, P]),
     "ts_nearest": (I32, [P, I64, P, I64, P, P]),
     "ts_cell_keys": (I32, [P, I64, P, P]),
-    "ts_triangulate": (I32, [P, P, I32, P, P, P, P]),
+    "ts_triangulate_scratch": (SZ, [I64, I32]),
+    "ts_triangulate": (I32, [P, P, I32, P, P, P, P, P]),
     "ts_raster": (I32, [P, P, P, P, P, P, P, P, I32, I32, P, P, P, P, P, P,
                         P, P, P]),
     "ts_weights_create": (I32, [P, SZ, I32, C.POINTER(P)]),

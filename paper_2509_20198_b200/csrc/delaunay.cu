@@ -34,6 +34,50 @@ struct PatchPts {
   }
 };
 
+// Circumcircle cache of one triangle: centre, r^2, and whether the fast
+// test may be trusted (well-conditioned triangles only).
+struct Circle {
+  double cx, cy, r2;
+  int ok;
+  int pad;
+};
+
+__device__ __forceinline__ Circle make_circle(const PatchPts& P, int a, int b, int c) {
+  double ax, ay, bx, by, cx, cy;
+  P.get(a, ax, ay);
+  P.get(b, bx, by);
+  P.get(c, cx, cy);
+  const double ux = bx - ax, uy = by - ay, vx = cx - ax, vy = cy - ay;
+  const double p1 = ux * vy, p2 = uy * vx;
+  const double D = 2.0 * (p1 - p2);
+  Circle o;
+  o.ok = fabs(D) > 1e-6 * (fabs(p1) + fabs(p2)) && fabs(D) > 1e-200;
+  const double l1 = ux * ux + uy * uy, l2 = vx * vx + vy * vy;
+  const double ox = (vy * l1 - uy * l2) / D, oy = (ux * l2 - vx * l1) / D;
+  o.cx = ax + ox;
+  o.cy = ay + oy;
+  o.r2 = ox * ox + oy * oy;
+  o.pad = 0;
+  return o;
+}
+
+// > 0 strictly inside, < 0 outside, == 0 on the circle (exact when unsure)
+__device__ __forceinline__ int in_circle(const Circle& C, const PatchPts& P, const int* t,
+                                         double px, double py) {
+  if (C.ok) {
+    const double dx = px - C.cx, dy = py - C.cy;
+    const double d2 = dx * dx + dy * dy;
+    const double m = 1e-6 * (d2 + C.r2);
+    if (d2 < C.r2 - m) return 1;
+    if (d2 > C.r2 + m) return -1;
+  }
+  double ax, ay, bx, by, cx, cy;
+  P.get(t[0], ax, ay);
+  P.get(t[1], bx, by);
+  P.get(t[2], cx, cy);
+  return pred::incircle(ax, ay, bx, by, cx, cy, px, py);
+}
+
 __device__ __forceinline__ bool has_edge(const int* t, int a, int b) {
   return (t[0] == a && t[1] == b) || (t[1] == a && t[2] == b) ||
          (t[2] == a && t[0] == b);
@@ -42,7 +86,8 @@ __device__ __forceinline__ bool has_edge(const int* t, int a, int b) {
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 delaunay_kernel(const double* __restrict__ xy_all,
                 const int64_t* __restrict__ pts_off, int n_patches,
-                int32_t* tri_all, int32_t* ntri_out, int32_t* status) {
+                int32_t* tri_all, int32_t* ntri_out, int32_t* status,
+                Circle* circ_all) {
   __shared__ int s_bad[kWarpsPerBlock][kMaxCavity];
   __shared__ int2 s_edge[kWarpsPerBlock][kMaxCavity + 8];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -51,6 +96,7 @@ delaunay_kernel(const double* __restrict__ xy_all,
   const int64_t off = pts_off[p];
   const int n = (int)(pts_off[p + 1] - off);
   int* tri = tri_all + 3 * (2 * off + 8 * (int64_t)p);  // triangle slots
+  Circle* circ = circ_all + (2 * off + 8 * (int64_t)p);
   if (n == 0) {
     if (lane == 0) { ntri_out[p] = 0; status[p] = TS_E_EMPTY_PATCH; }
     return;
@@ -62,6 +108,8 @@ delaunay_kernel(const double* __restrict__ xy_all,
   if (lane == 0) {
     tri[0] = n; tri[1] = n + 1; tri[2] = n + 3;
     tri[3] = n; tri[4] = n + 3; tri[5] = n + 2;
+    circ[0] = make_circle(P, n, n + 1, n + 3);
+    circ[1] = make_circle(P, n, n + 3, n + 2);
   }
   int ntri = 2;
   int st = TS_OK;
@@ -74,14 +122,7 @@ delaunay_kernel(const double* __restrict__ xy_all,
     for (int b0 = 0; b0 < ntri; b0 += 32) {
       const int t = b0 + lane;
       bool in = false;
-      if (t < ntri) {
-        const int a = tri[3 * t], b = tri[3 * t + 1], c = tri[3 * t + 2];
-        double ax, ay, bx, by, cx, cy;
-        P.get(a, ax, ay);
-        P.get(b, bx, by);
-        P.get(c, cx, cy);
-        in = pred::incircle(ax, ay, bx, by, cx, cy, px, py) > 0;
-      }
+      if (t < ntri) in = in_circle(circ[t], P, tri + 3 * t, px, py) > 0;
       const unsigned m = __ballot_sync(0xFFFFFFFFu, in);
       if (in) {
         const int slot = nb + __popc(m & ((1u << lane) - 1));
@@ -134,6 +175,7 @@ delaunay_kernel(const double* __restrict__ xy_all,
       tri[3 * slot] = ed.x;
       tri[3 * slot + 1] = ed.y;
       tri[3 * slot + 2] = v;
+      circ[slot] = make_circle(P, ed.x, ed.y, v);
     }
     ntri += ne - nb;
     __syncwarp();
@@ -149,13 +191,19 @@ delaunay_kernel(const double* __restrict__ xy_all,
 
 using namespace ts;
 
+extern "C" size_t ts_triangulate_scratch(int64_t total_points, int n_patches) {
+  return sizeof(Circle) * (size_t)(2 * total_points + 8 * (int64_t)n_patches + 8);
+}
+
 extern "C" int ts_triangulate(const double* d_xy, const int64_t* d_pts_off,
                               int n_patches, int32_t* d_tri, int32_t* d_ntri,
-                              int32_t* d_status, void* stream) {
+                              int32_t* d_status, void* d_scratch, void* stream) {
   if (n_patches <= 0) return TS_OK;
-  ts::count_launch(), delaunay_kernel<<<ceil_div(n_patches, kWarpsPerBlock), kWarpsPerBlock * 32, 0,
-                    as_stream(stream)>>>(d_xy, d_pts_off, n_patches, d_tri,
-                                         d_ntri, d_status);
+  if (!d_scratch) return TS_E_INVALID;
+  ts::count_launch(),
+      delaunay_kernel<<<ceil_div(n_patches, kWarpsPerBlock), kWarpsPerBlock * 32, 0,
+                        as_stream(stream)>>>(d_xy, d_pts_off, n_patches, d_tri, d_ntri,
+                                             d_status, reinterpret_cast<Circle*>(d_scratch));
   TS_LAUNCH_CHECK();
   return TS_OK;
 }

@@ -30,6 +30,7 @@ constexpr int kThreads = 256;
 constexpr int kCells = kRes * kRes;
 constexpr int kSmemPts = 512;          // points cached in shared memory
 constexpr int kSmemTri = 2 * kSmemPts + 8;
+constexpr int kBins = 16;              // NN bin grid over [-1,1]^2
 
 struct Tri {
   int v0, v1, v2;
@@ -126,6 +127,8 @@ raster_kernel(RasterArgs A) {
   double* s_h = s_xy + 2 * kSmemPts;                                // 512
   int* s_pref = reinterpret_cast<int*>(s_h + kSmemPts);             // 1033
   uint32_t* s_rng = reinterpret_cast<uint32_t*>(s_pref + kSmemTri + 1);  // 1032
+  int* s_bstart = reinterpret_cast<int*>(s_rng + kSmemTri);  // kBins^2 + 1
+  short* s_bid = reinterpret_cast<short*>(s_bstart + kBins * kBins + 2);  // kSmemPts
   __shared__ double s_shift;
   __shared__ int s_total;
   __shared__ int s_wsum[kThreads / 32];
@@ -268,16 +271,69 @@ raster_kernel(RasterArgs A) {
                      dmul(w2, (double)g_rgb[3 * tr.v2 + c]));
     }
   };
+  // Exact nearest neighbour (patches.py:180-199): the d^2 formula and the
+  // lowest-index tie rule of a linear scan; with points cached in shared
+  // memory they are binned on a 16x16 grid and searched ring by ring until
+  // the next ring's lower bound exceeds the best d^2 (with a 1e-12 relative
+  // safety margin, so ties on the bound are still visited).
+  auto bin_of = [](double v) {
+    int b = (int)floor((v + 1.0) * (kBins / 2));
+    return b < 0 ? 0 : (b >= kBins ? kBins - 1 : b);
+  };
   auto nn_of = [&](double qx, double qy) {
     double best = DBL_MAX;
     int bi = 0;
-    for (int i = 0; i < n; ++i) {
-      const double dx = dsub(qx, xy[2 * i]), dy = dsub(qy, xy[2 * i + 1]);
-      const double d2 = dadd(dmul(dx, dx), dmul(dy, dy));
-      if (d2 < best) { best = d2; bi = i; }
+    if (!cached) {
+      for (int i = 0; i < n; ++i) {
+        const double dx = dsub(qx, xy[2 * i]), dy = dsub(qy, xy[2 * i + 1]);
+        const double d2 = dadd(dmul(dx, dx), dmul(dy, dy));
+        if (d2 < best) { best = d2; bi = i; }
+      }
+      return bi;
+    }
+    const int bx = bin_of(qx), by = bin_of(qy);
+    const double hb = 2.0 / kBins;
+    for (int r = 0; r < kBins; ++r) {
+      const int x0 = max(bx - r, 0), x1 = min(bx + r, kBins - 1);
+      const int y0 = max(by - r, 0), y1 = min(by + r, kBins - 1);
+      for (int gy = y0; gy <= y1; ++gy) {
+        const bool edge_row = (gy == by - r) || (gy == by + r);
+        for (int gx = x0; gx <= x1; ++gx) {
+          if (!edge_row && gx != bx - r && gx != bx + r) continue;  // ring only
+          const int b = gy * kBins + gx;
+          for (int k = s_bstart[b]; k < s_bstart[b + 1]; ++k) {
+            const int i = s_bid[k];
+            const double dx = dsub(qx, xy[2 * i]), dy = dsub(qy, xy[2 * i + 1]);
+            const double d2 = dadd(dmul(dx, dx), dmul(dy, dy));
+            if (d2 < best || (d2 == best && i < bi)) { best = d2; bi = i; }
+          }
+        }
+      }
+      double mind = DBL_MAX;
+      if (bx - r > 0) mind = fmin(mind, qx - (-1.0 + (bx - r) * hb));
+      if (bx + r < kBins - 1) mind = fmin(mind, (-1.0 + (bx + r + 1) * hb) - qx);
+      if (by - r > 0) mind = fmin(mind, qy - (-1.0 + (by - r) * hb));
+      if (by + r < kBins - 1) mind = fmin(mind, (-1.0 + (by + r + 1) * hb) - qy);
+      if (mind == DBL_MAX) break;                      // every bin visited
+      if (best < DBL_MAX && mind * mind > best * (1.0 + 1e-12)) break;
     }
     return bi;
   };
+  if (cached) {  // counting sort of point ids into bins (ascending ids)
+    if (tid == 0) {
+      for (int b = 0; b <= kBins * kBins; ++b) s_bstart[b] = 0;
+      for (int i = 0; i < n; ++i)
+        ++s_bstart[bin_of(xy[2 * i + 1]) * kBins + bin_of(xy[2 * i]) + 1];
+      for (int b = 0; b < kBins * kBins; ++b) s_bstart[b + 1] += s_bstart[b];
+      for (int i = 0; i < n; ++i) {
+        const int b = bin_of(xy[2 * i + 1]) * kBins + bin_of(xy[2 * i]);
+        s_bid[s_bstart[b]++] = (short)i;
+      }
+      for (int b = kBins * kBins; b > 0; --b) s_bstart[b] = s_bstart[b - 1];
+      s_bstart[0] = 0;
+    }
+    __syncthreads();
+  }
 
   if (tid == 0) {
     double shift = 0.0;
@@ -298,24 +354,11 @@ raster_kernel(RasterArgs A) {
   const double shift = s_shift;
 
   for (int j0 = tid; j0 < kCells; j0 += 4 * kThreads) {
-    int jj[4], bi[4];
-    double qx[4], qy[4], best[4];
+    int bi[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      jj[u] = min(j0 + u * kThreads, kCells - 1);
-      qx[u] = cell_center(jj[u] % kRes, kRes);
-      qy[u] = cell_center(jj[u] / kRes, kRes);
-      best[u] = DBL_MAX;
-      bi[u] = 0;
-    }
-    for (int i = 0; i < n; ++i) {
-      const double px = xy[2 * i], py = xy[2 * i + 1];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double dx = dsub(qx[u], px), dy = dsub(qy[u], py);
-        const double d2 = dadd(dmul(dx, dx), dmul(dy, dy));
-        if (d2 < best[u]) { best[u] = d2; bi[u] = i; }
-      }
+      const int jj = min(j0 + u * kThreads, kCells - 1);
+      bi[u] = nn_of(cell_center(jj % kRes, kRes), cell_center(jj / kRes, kRes));
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -354,7 +397,8 @@ raster_kernel(RasterArgs A) {
 }
 
 constexpr size_t kRasterSmem = sizeof(int) * kCells + sizeof(double) * 3 * kSmemPts +
-                               sizeof(int) * (kSmemTri + 1) + sizeof(uint32_t) * kSmemTri;
+                               sizeof(int) * (kSmemTri + 1) + sizeof(uint32_t) * kSmemTri +
+                               sizeof(int) * (kBins * kBins + 2) + sizeof(short) * kSmemPts;
 
 }  // namespace
 }  // namespace ts

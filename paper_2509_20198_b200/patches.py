@@ -238,8 +238,10 @@ def triangulate(g) -> dict:
     tri = D.empty((2 * total + 8 * P + 8, 3), torch.int32)
     ntri = D.empty((P,), torch.int32)
     st = torch.zeros(P, dtype=torch.int32, device=tri.device)
+    from ._lib import lib
+    scratch = D.empty((int(lib().ts_triangulate_scratch(total, P)),), torch.uint8)
     D.call("ts_triangulate", D.ptr(g["xy"]), D.ptr(g["off"]), P, D.ptr(tri),
-           D.ptr(ntri), D.ptr(st), D.stream())
+           D.ptr(ntri), D.ptr(st), D.ptr(scratch), D.stream())
     tri_off = 3 * (2 * g["off"][:-1] + 8 * torch.arange(
         P, device=tri.device, dtype=torch.int64))
     return dict(tri=tri, ntri=ntri, tri_off=tri_off.contiguous(), status=st)
