@@ -161,38 +161,7 @@ __global__ void __launch_bounds__(128) conv_direct_kernel(ConvOp op) {
       for (int c = 0; c < CO; ++c) acc[c] = 0.f;
       const float* inb =
           op.in.base + (int64_t)b * op.in.H * op.in.W * op.in.cstride + op.in.coff;
-      if (Cin <= 4 && op.k <= 3) {
-        // thin input: issue every tap's loads first (independent, in flight
-        // together), then the FMAs
-        float xin[9][4];
-#pragma unroll
-        for (int ky = 0; ky < 3; ++ky)
-#pragma unroll
-          for (int kx = 0; kx < 3; ++kx) {
-            int iy = oy * op.stride - op.pad + ky, ix = ox * op.stride - op.pad + kx;
-            const bool ok = ky < op.k && kx < op.k && iy >= 0 && iy < Hl && ix >= 0 && ix < Wl;
-            if (op.up2) { iy >>= 1; ix >>= 1; }
-            const float* src = inb + ((int64_t)iy * op.in.W + ix) * op.in.cstride;
-#pragma unroll
-            for (int ci = 0; ci < 4; ++ci)
-              xin[ky * 3 + kx][ci] = (ok && ci < Cin) ? __ldg(src + ci) : 0.f;
-          }
-#pragma unroll
-        for (int ky = 0; ky < 3; ++ky)
-#pragma unroll
-          for (int kx = 0; kx < 3; ++kx) {
-            if (ky >= op.k || kx >= op.k) continue;
-            const float* wt = sw + (ky * op.k + kx) * Cin * Cout;
-#pragma unroll
-            for (int ci = 0; ci < 4; ++ci) {
-              if (ci >= Cin) break;
-              const float x = xin[ky * 3 + kx][ci];
-#pragma unroll
-              for (int c = 0; c < CO; ++c)
-                if (c < Cout) acc[c] = fmaf(x, wt[ci * Cout + c], acc[c]);
-            }
-          }
-      } else {
+      {
         for (int ky = 0; ky < op.k; ++ky) {
           int iy = oy * op.stride - op.pad + ky;
           if (iy < 0 || iy >= Hl) continue;

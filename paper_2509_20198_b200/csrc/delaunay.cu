@@ -18,8 +18,15 @@
 namespace ts {
 namespace {
 
-constexpr int kWarpsPerBlock = 4;
 constexpr int kMaxCavity = 512;
+// Patches up to kSmemPoints keep their whole mesh (triangles + circumcircle
+// cache, SoA) in shared memory: every insertion rewrites a few slots and the
+// next one re-reads them, so a global-memory mesh turns each step into a
+// chain of L1-miss latencies.  Larger patches spill to the caller's scratch.
+constexpr int kSmemPoints = 512;
+constexpr int kSmemSlots = 2 * kSmemPoints + 8;
+constexpr size_t kDelaunaySmem = (size_t)kSmemSlots * (3 * sizeof(int) + 3 * sizeof(double)) +
+                                 kMaxCavity * sizeof(int) + (kMaxCavity + 8) * sizeof(int2);
 
 struct PatchPts {
   const double* xy;
@@ -34,83 +41,84 @@ struct PatchPts {
   }
 };
 
-// Circumcircle cache of one triangle: centre, r^2, and whether the fast
-// test may be trusted (well-conditioned triangles only).
-struct Circle {
-  double cx, cy, r2;
-  int ok;
-  int pad;
-};
-
-__device__ __forceinline__ Circle make_circle(const PatchPts& P, int a, int b, int c) {
-  double ax, ay, bx, by, cx, cy;
-  P.get(a, ax, ay);
-  P.get(b, bx, by);
-  P.get(c, cx, cy);
-  const double ux = bx - ax, uy = by - ay, vx = cx - ax, vy = cy - ay;
-  const double p1 = ux * vy, p2 = uy * vx;
-  const double D = 2.0 * (p1 - p2);
-  Circle o;
-  o.ok = fabs(D) > 1e-6 * (fabs(p1) + fabs(p2)) && fabs(D) > 1e-200;
-  const double l1 = ux * ux + uy * uy, l2 = vx * vx + vy * vy;
-  const double ox = (vy * l1 - uy * l2) / D, oy = (ux * l2 - vx * l1) / D;
-  o.cx = ax + ox;
-  o.cy = ay + oy;
-  o.r2 = ox * ox + oy * oy;
-  o.pad = 0;
-  return o;
-}
-
-// > 0 strictly inside, < 0 outside, == 0 on the circle (exact when unsure)
-__device__ __forceinline__ int in_circle(const Circle& C, const PatchPts& P, const int* t,
-                                         double px, double py) {
-  if (C.ok) {
-    const double dx = px - C.cx, dy = py - C.cy;
-    const double d2 = dx * dx + dy * dy;
-    const double m = 1e-6 * (d2 + C.r2);
-    if (d2 < C.r2 - m) return 1;
-    if (d2 > C.r2 + m) return -1;
+// Circumcircle cache, structure of arrays.  An ill-conditioned triangle gets
+// r2 = NaN, which makes both fast comparisons false -> exact predicate.
+struct Mesh {
+  int* tri;
+  double *cx, *cy, *r2;
+  __device__ __forceinline__ void set(const PatchPts& P, int slot, int a, int b, int c) {
+    tri[3 * slot] = a;
+    tri[3 * slot + 1] = b;
+    tri[3 * slot + 2] = c;
+    double ax, ay, bx, by, qx, qy;
+    P.get(a, ax, ay);
+    P.get(b, bx, by);
+    P.get(c, qx, qy);
+    const double ux = bx - ax, uy = by - ay, vx = qx - ax, vy = qy - ay;
+    const double p1 = ux * vy, p2 = uy * vx;
+    const double D = 2.0 * (p1 - p2);
+    const bool ok = fabs(D) > 1e-6 * (fabs(p1) + fabs(p2)) && fabs(D) > 1e-200;
+    const double l1 = ux * ux + uy * uy, l2 = vx * vx + vy * vy;
+    const double ox = (vy * l1 - uy * l2) / D, oy = (ux * l2 - vx * l1) / D;
+    cx[slot] = ax + ox;
+    cy[slot] = ay + oy;
+    r2[slot] = ok ? ox * ox + oy * oy : __longlong_as_double(0x7ff8000000000000LL);
   }
-  double ax, ay, bx, by, cx, cy;
-  P.get(t[0], ax, ay);
-  P.get(t[1], bx, by);
-  P.get(t[2], cx, cy);
-  return pred::incircle(ax, ay, bx, by, cx, cy, px, py);
-}
+  // > 0 strictly inside, < 0 outside, == 0 on the circle (exact when unsure)
+  __device__ __forceinline__ int in_circle(const PatchPts& P, int t, double px,
+                                           double py) const {
+    const double dx = px - cx[t], dy = py - cy[t], rr = r2[t];
+    const double d2 = dx * dx + dy * dy;
+    const double m = 1e-6 * (d2 + rr);
+    if (d2 < rr - m) return 1;
+    if (d2 > rr + m) return -1;
+    double ax, ay, bx, by, qx, qy;
+    P.get(tri[3 * t], ax, ay);
+    P.get(tri[3 * t + 1], bx, by);
+    P.get(tri[3 * t + 2], qx, qy);
+    return pred::incircle(ax, ay, bx, by, qx, qy, px, py);
+  }
+};
 
 __device__ __forceinline__ bool has_edge(const int* t, int a, int b) {
   return (t[0] == a && t[1] == b) || (t[1] == a && t[2] == b) ||
          (t[2] == a && t[0] == b);
 }
 
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(32)
 delaunay_kernel(const double* __restrict__ xy_all,
                 const int64_t* __restrict__ pts_off, int n_patches,
                 int32_t* tri_all, int32_t* ntri_out, int32_t* status,
-                Circle* circ_all) {
-  __shared__ int s_bad[kWarpsPerBlock][kMaxCavity];
-  __shared__ int2 s_edge[kWarpsPerBlock][kMaxCavity + 8];
-  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int p = blockIdx.x * kWarpsPerBlock + wib;
-  if (p >= n_patches) return;
+                double* circ_all) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* s_cx = reinterpret_cast<double*>(smem);
+  double* s_cy = s_cx + kSmemSlots;
+  double* s_r2 = s_cy + kSmemSlots;
+  int* s_tri = reinterpret_cast<int*>(s_r2 + kSmemSlots);
+  int* bad = s_tri + 3 * kSmemSlots;
+  int2* edge = reinterpret_cast<int2*>(bad + kMaxCavity);
+  const int lane = threadIdx.x;
+  const int p = blockIdx.x;
   const int64_t off = pts_off[p];
   const int n = (int)(pts_off[p + 1] - off);
-  int* tri = tri_all + 3 * (2 * off + 8 * (int64_t)p);  // triangle slots
-  Circle* circ = circ_all + (2 * off + 8 * (int64_t)p);
+  const int64_t base = 2 * off + 8 * (int64_t)p;  // first triangle slot
+  int* tri_out = tri_all + 3 * base;
   if (n == 0) {
     if (lane == 0) { ntri_out[p] = 0; status[p] = TS_E_EMPTY_PATCH; }
     return;
   }
   const PatchPts P{xy_all + 2 * off, n};
-  int* bad = s_bad[wib];
-  int2* edge = s_edge[wib];
   const int cap = 2 * n + 8;
-  if (lane == 0) {
-    tri[0] = n; tri[1] = n + 1; tri[2] = n + 3;
-    tri[3] = n; tri[4] = n + 3; tri[5] = n + 2;
-    circ[0] = make_circle(P, n, n + 1, n + 3);
-    circ[1] = make_circle(P, n, n + 3, n + 2);
+  const bool in_smem = n <= kSmemPoints;
+  Mesh M;
+  if (in_smem) {
+    M = Mesh{s_tri, s_cx, s_cy, s_r2};
+  } else {
+    double* g = circ_all + 3 * base;
+    M = Mesh{tri_out, g, g + cap, g + 2 * cap};
   }
+  if (lane == 0) M.set(P, 0, n, n + 1, n + 3);
+  if (lane == 1) M.set(P, 1, n, n + 3, n + 2);
   int ntri = 2;
   int st = TS_OK;
   __syncwarp();
@@ -121,8 +129,7 @@ delaunay_kernel(const double* __restrict__ xy_all,
     int nb = 0;
     for (int b0 = 0; b0 < ntri; b0 += 32) {
       const int t = b0 + lane;
-      bool in = false;
-      if (t < ntri) in = in_circle(circ[t], P, tri + 3 * t, px, py) > 0;
+      const bool in = t < ntri && M.in_circle(P, t, px, py) > 0;
       const unsigned m = __ballot_sync(0xFFFFFFFFu, in);
       if (in) {
         const int slot = nb + __popc(m & ((1u << lane) - 1));
@@ -141,12 +148,12 @@ delaunay_kernel(const double* __restrict__ xy_all,
       int u = 0, w = 0;
       if (e < 3 * nb) {
         const int i = e / 3, j = e - 3 * i;
-        const int* t = tri + 3 * bad[i];
+        const int* t = M.tri + 3 * bad[i];
         u = t[j];
         w = t[j == 2 ? 0 : j + 1];
         keep = true;
         for (int k = 0; k < nb && keep; ++k)
-          if (k != i && has_edge(tri + 3 * bad[k], w, u)) keep = false;
+          if (k != i && has_edge(M.tri + 3 * bad[k], w, u)) keep = false;
         if (keep) {
           double ux, uy, wx, wy;
           P.get(u, ux, uy);
@@ -172,14 +179,13 @@ delaunay_kernel(const double* __restrict__ xy_all,
     for (int i = lane; i < ne; i += 32) {
       const int slot = i < nb ? bad[i] : ntri + (i - nb);
       const int2 ed = edge[i];
-      tri[3 * slot] = ed.x;
-      tri[3 * slot + 1] = ed.y;
-      tri[3 * slot + 2] = v;
-      circ[slot] = make_circle(P, ed.x, ed.y, v);
+      M.set(P, slot, ed.x, ed.y, v);
     }
     ntri += ne - nb;
     __syncwarp();
   }
+  if (in_smem && st == TS_OK)
+    for (int i = lane; i < 3 * ntri; i += 32) tri_out[i] = s_tri[i];
   if (lane == 0) {
     ntri_out[p] = st == TS_OK ? ntri : 0;
     status[p] = st;
@@ -192,7 +198,7 @@ delaunay_kernel(const double* __restrict__ xy_all,
 using namespace ts;
 
 extern "C" size_t ts_triangulate_scratch(int64_t total_points, int n_patches) {
-  return sizeof(Circle) * (size_t)(2 * total_points + 8 * (int64_t)n_patches + 8);
+  return 3 * sizeof(double) * (size_t)(2 * total_points + 8 * (int64_t)n_patches + 8);
 }
 
 extern "C" int ts_triangulate(const double* d_xy, const int64_t* d_pts_off,
@@ -200,10 +206,19 @@ extern "C" int ts_triangulate(const double* d_xy, const int64_t* d_pts_off,
                               int32_t* d_status, void* d_scratch, void* stream) {
   if (n_patches <= 0) return TS_OK;
   if (!d_scratch) return TS_E_INVALID;
+  static bool configured = false;
+  if (!configured) {
+    TS_CUDA_TRY(cudaFuncSetAttribute(delaunay_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kDelaunaySmem));
+    TS_CUDA_TRY(cudaFuncSetAttribute(delaunay_kernel,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    configured = true;
+  }
   ts::count_launch(),
-      delaunay_kernel<<<ceil_div(n_patches, kWarpsPerBlock), kWarpsPerBlock * 32, 0,
-                        as_stream(stream)>>>(d_xy, d_pts_off, n_patches, d_tri, d_ntri,
-                                             d_status, reinterpret_cast<Circle*>(d_scratch));
+      delaunay_kernel<<<n_patches, 32, kDelaunaySmem, as_stream(stream)>>>(
+          d_xy, d_pts_off, n_patches, d_tri, d_ntri, d_status,
+          reinterpret_cast<double*>(d_scratch));
   TS_LAUNCH_CHECK();
   return TS_OK;
 }

@@ -119,7 +119,7 @@ struct RasterArgs {
   int32_t* status;
 };
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 2)
 raster_kernel(RasterArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   int* s_face = reinterpret_cast<int*>(smem);                       // 9216
@@ -418,6 +418,8 @@ extern "C" int ts_raster(const double* d_xy, const double* d_h, const float* d_p
     TS_CUDA_TRY(cudaFuncSetAttribute(raster_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kRasterSmem));
+    TS_CUDA_TRY(cudaFuncSetAttribute(raster_kernel,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     configured = true;
   }
   RasterArgs a{d_xy, d_h, d_prgb, d_pts_off, d_tri, d_tri_off, d_ntri, d_cz_in,
