@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", type=int, default=None,
-                    help="0 fp32 SIMT, 1 tf32x3 tcgen05, 2 bf16 tcgen05")
+                    help="0 fp32 SIMT, 1 tf32x3, 2 bf16, 3 bf16 2x3 planes, "
+                         "4 bf16 2x2 planes (default; fp32-class)")
     ap.add_argument("--no-splat", action="store_true")
     ap.add_argument("--splat-points", type=int, default=200_000_000)
     ap.add_argument("--cpu-sample", type=int, default=32)
@@ -141,7 +142,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2509_20198_b200._lib import lib
     from paper_2509_20198_b200.lasio import parse_header
     from paper_2509_20198_b200.pipeline import HeightmapPipeline
-    from paper_2509_20198_b200.refiner import (PRECISION_BF16X3,
+    from paper_2509_20198_b200.refiner import (PRECISION_BF16X4,
                                                default_descriptor,
                                                random_weights)
 
@@ -149,7 +150,7 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    precision = PRECISION_BF16X3 if args.precision is None else args.precision
+    precision = PRECISION_BF16X4 if args.precision is None else args.precision
     tiles, own = band_tiles(rank, world)
     images = [t.data for t in tiles]
     descs = np.concatenate([D.tile_desc(parse_header(b)) for b in images])
@@ -256,7 +257,8 @@ def run_ours(args, rank, world, local_rank):
             "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None,
             "dtype": {0: "f32", 1: "tf32x3", 2: "bf16",
-                      3: "bf16x3 (fp32-class split)"}[precision] +
+                      3: "bf16 2x3-plane split (fp32-class)",
+                      4: "bf16 2x2-plane split (fp32-class)"}[precision] +
                      " CNN, f64 geometry",
             "data": "synthetic (seeded FractalTerrain stub-body LAZ tiles, "
                     "random He weights seed 3)",

@@ -178,9 +178,6 @@ __host__ __device__ constexpr uint32_t make_idesc(uint32_t ab_fmt, int n) {
 __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
-__device__ __forceinline__ float trunc_bf(float x) {
-  return __uint_as_float(__float_as_uint(x) & 0xFFFF0000u);
-}
 __device__ __forceinline__ uint32_t hi_halves(float a, float b) {  // {a.hi16, b.hi16}
   return __byte_perm(__float_as_uint(a), __float_as_uint(b), 0x7632);
 }
@@ -220,6 +217,11 @@ struct Mode<2> {  // BF16
 template <>
 struct Mode<3> {  // BF16X3: A = a0 + a1 (RN, residual <= 2^-18 |a|), B = b0+b1+b2
   static constexpr int pa = 2, pb = 3, kc = 64;
+  static constexpr bool tf32 = false;
+};
+template <>
+struct Mode<4> {  // BF16X4: A = a0 + a1, B = b0 + b1 (both RN, residual <= 2^-18)
+  static constexpr int pa = 2, pb = 2, kc = 64;
   static constexpr bool tf32 = false;
 };
 
@@ -412,6 +414,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
               umma<true>(d, ak + pa, bk, idesc, 1u);
             } else if (MODE == 2) {
               umma<false>(d, ak, bk, idesc, first);
+            } else if (MODE == 4) {
+              umma<false>(d, ak + pa, bk + pb, idesc, first);  // small terms first
+              umma<false>(d, ak + pa, bk, idesc, 1u);
+              umma<false>(d, ak, bk + pb, idesc, 1u);
+              umma<false>(d, ak, bk, idesc, 1u);
             } else {
               umma<false>(d, ak + pa, bk + pb, idesc, first);  // small terms first
               umma<false>(d, ak, bk + 2 * pb, idesc, 1u);
@@ -679,6 +686,11 @@ __global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) 
                 umma<true>(d, ak + pa, bk, idesc, 1u);
               } else if (MODE == 2) {
                 umma<false>(d, ak, bk, idesc, first);
+              } else if (MODE == 4) {
+                umma<false>(d, ak + pa, bk + pb, idesc, first);
+                umma<false>(d, ak + pa, bk, idesc, 1u);
+                umma<false>(d, ak, bk + pb, idesc, 1u);
+                umma<false>(d, ak, bk, idesc, 1u);
               } else {
                 umma<false>(d, ak + pa, bk + pb, idesc, first);
                 umma<false>(d, ak, bk + 2 * pb, idesc, 1u);
@@ -809,7 +821,7 @@ struct TcPlan {
 TcPlan plan_for(const ConvOp& op, int precision) {
   TcPlan p{};
   p.pa = precision == 2 ? 1 : 2;
-  p.pb = precision == 1 ? 2 : precision == 2 ? 1 : 3;
+  p.pb = precision == 1 ? 2 : precision == 2 ? 1 : precision == 4 ? 2 : 3;
   p.kc = precision == 1 ? 32 : 64;
   const int n16 = (op.out.C + 15) / 16 * 16;
   const int cap = 128;
@@ -862,7 +874,7 @@ bool conv_tc_halo_eligible(const ConvOp& op, int precision) {
 }
 
 bool conv_tc_supported(const ConvOp& op, int precision) {
-  if (precision < 1 || precision > 3) return false;
+  if (precision < 1 || precision > 4) return false;
   return op.in.C % 4 == 0 && op.in.cstride % 4 == 0 && op.in.coff % 4 == 0;
 }
 
@@ -903,6 +915,11 @@ std::vector<uint8_t> pack_tc_weights(const float* w_oikk, int co, int ci, int k,
           } else if (precision == 2) {
             const uint16_t h = f2bf16_rn(v);
             memcpy(base + off, &h, 2);
+          } else if (precision == 4) {  // RN split, like the device producers
+            const uint16_t h0 = f2bf16_rn(v);
+            const uint16_t h1 = f2bf16_rn(v - bf16_to_f(h0));
+            memcpy(base + off, &h0, 2);
+            memcpy(base + plane + off, &h1, 2);
           } else {
             // exact truncation split, like the device producers
             uint32_t u;
@@ -953,6 +970,7 @@ int launch_conv_tc_halo(const ConvOp& op, int precision, void* stream) {
   } while (0)
   if (precision == 1) TS_TCH_LAUNCH(1);
   else if (precision == 2) TS_TCH_LAUNCH(2);
+  else if (precision == 4) TS_TCH_LAUNCH(4);
   else TS_TCH_LAUNCH(3);
 #undef TS_TCH_LAUNCH
   TS_LAUNCH_CHECK();
@@ -984,6 +1002,7 @@ int launch_conv_tc(const ConvOp& op, int precision, void* stream) {
   } while (0)
   if (precision == 1) TS_TC_LAUNCH(1);
   else if (precision == 2) TS_TC_LAUNCH(2);
+  else if (precision == 4) TS_TC_LAUNCH(4);
   else TS_TC_LAUNCH(3);
 #undef TS_TC_LAUNCH
   TS_LAUNCH_CHECK();

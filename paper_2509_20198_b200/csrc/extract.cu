@@ -77,6 +77,9 @@ __global__ void chunk_count_kernel(const uint8_t* __restrict__ bytes,
   status[i] = st;
 }
 
+constexpr uint32_t kDecodeSmemWords = 12 * 1024;  // 24 KB of models per thread
+constexpr int kDecodeBlock = 8;                     // 192 KB shared per CTA
+
 __global__ void chunk_decode_kernel(const uint8_t* __restrict__ bytes,
                                     const ts_tile_desc* __restrict__ tiles,
                                     int n_tiles,
@@ -86,6 +89,7 @@ __global__ void chunk_decode_kernel(const uint8_t* __restrict__ bytes,
                                     int64_t* __restrict__ chunk_end,
                                     int32_t* status, uint16_t* scratch,
                                     uint32_t scratch_words) {
+  extern __shared__ __align__(16) uint16_t s_pool[];
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   laz::ChunkTableCoder coder;
   for (int i = gtid; i < n_tiles; i += gridDim.x * blockDim.x) {
@@ -110,7 +114,11 @@ __global__ void chunk_decode_kernel(const uint8_t* __restrict__ bytes,
     const bool variable = t.chunk_size == 0xFFFFFFFFu;
     if (st == TS_OK && n > 0) {
       laz::Decoder dec;
-      coder.init(scratch + (size_t)gtid * scratch_words);
+      // model tables live in shared memory (every symbol decode reads and
+      // adapts them; a global-memory pool made each step an L1/L2 round
+      // trip), overflowing to the per-thread global scratch
+      coder.init(s_pool + (size_t)threadIdx.x * kDecodeSmemWords, kDecodeSmemWords,
+                 scratch + (size_t)gtid * scratch_words);
       if (!dec.start(f, pos + 8, t.file_size)) st = TS_E_CORRUPT_TABLE;
       int32_t pc = 0, ps = 0;
       int64_t off = t.point_data_offset + 8, total = 0;
@@ -303,7 +311,7 @@ __global__ void colors_kernel(const uint8_t* __restrict__ rec, int64_t n, int rs
   }
 }
 
-constexpr int kDecodeThreads = 4096;
+constexpr int kDecodeThreads = 148 * kDecodeBlock;
 
 uint32_t decode_pool_words() {
   // mirror of ChunkTableCoder::pool_words() on the host
@@ -346,8 +354,15 @@ extern "C" int ts_chunk_decode(const uint8_t* d_bytes, const ts_tile_desc* d_til
                                void* stream) {
   if (n_tiles <= 0) return n_tiles == 0 ? TS_OK : TS_E_INVALID;
   const int threads = n_tiles < kDecodeThreads ? n_tiles : kDecodeThreads;
-  const int block = 64;
-  ts::count_launch(), chunk_decode_kernel<<<ceil_div(threads, block), block, 0, as_stream(stream)>>>(
+  const int block = kDecodeBlock;
+  const size_t smem = (size_t)block * kDecodeSmemWords * sizeof(uint16_t);
+  static bool configured = false;
+  if (!configured) {
+    TS_CUDA_TRY(cudaFuncSetAttribute(chunk_decode_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  ts::count_launch(), chunk_decode_kernel<<<ceil_div(threads, block), block, smem, as_stream(stream)>>>(
       d_bytes, d_tiles, n_tiles, d_chunk_base, d_chunk_offset, d_chunk_points,
       d_chunk_end, d_status, reinterpret_cast<uint16_t*>(d_scratch), decode_pool_words());
   TS_LAUNCH_CHECK();

@@ -184,24 +184,32 @@ struct ChunkTableCoder {
   bool cbit_live;
   SymModel cmod[32];
   bool cmod_live[32];
-  uint16_t* pool;
-  uint32_t used;
+  uint16_t* pool;      // fast pool (shared memory), `budget` words
+  uint16_t* overflow;  // global-memory pool for models beyond the budget
+  uint32_t used, budget, used_over;
 
   __host__ __device__ static uint32_t pool_words() {
     uint32_t w = 2 * SymModel::words16(33);
     for (uint32_t k = 1; k < 32; ++k) w += SymModel::words16(1u << (k < 8 ? k : 8));
     return w;
   }
-  __host__ __device__ void init(uint16_t* mem) {
-    pool = mem; used = 0;
+  __host__ __device__ void init(uint16_t* mem) { init(mem, 0xFFFFFFFFu, nullptr); }
+  __host__ __device__ void init(uint16_t* fast, uint32_t fast_words, uint16_t* over) {
+    pool = fast; budget = fast_words; overflow = over; used = 0; used_over = 0;
     kmod_live[0] = kmod_live[1] = false;
     cbit_live = false;
     for (int k = 0; k < 32; ++k) cmod_live[k] = false;
   }
   __host__ __device__ SymModel& alloc(SymModel& m, bool& live, uint32_t n) {
     if (!live) {
-      m.init(n, pool + used);
-      used += SymModel::words16(n);
+      const uint32_t w = SymModel::words16(n);
+      if (used + w <= budget) {
+        m.init(n, pool + used);
+        used += w;
+      } else {
+        m.init(n, overflow + used_over);
+        used_over += w;
+      }
       live = true;
     }
     return m;

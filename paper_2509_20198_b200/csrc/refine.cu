@@ -582,9 +582,11 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
       op.batch = B;
       op.w_tc = L.w_tc;
       int st;
-      // thin layers -> direct kernel; the rest -> tensor cores (or the
-      // fp32 CUDA-core GEMM in precision mode 0)
-      if (conv_direct_supported(op) && (op.in.C <= 4 || W->precision == 0))
+      // thin layers (few input or output channels: an MMA tile would be
+      // mostly padding) -> fp32 direct kernel; the rest -> tensor cores (or
+      // the fp32 CUDA-core GEMM in precision mode 0)
+      if (conv_direct_supported(op) &&
+          (op.in.C <= 4 || op.out.C <= 16 || W->precision == 0))
         st = launch_conv_direct(op, stream);
       else if (L.w_tc && conv_tc_supported(op, W->precision))
         st = launch_conv_tc(op, W->precision, stream);
