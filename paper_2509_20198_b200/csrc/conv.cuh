@@ -3,6 +3,7 @@
 
 #include <stdint.h>
 
+#include <cstring>
 #include <vector>
 
 namespace ts {
@@ -28,19 +29,40 @@ struct ConvOp {
   const float* bias;
   int batch;
   const uint8_t* w_tc;  // tensor-core packed weights (conv_tc.cu), or null
+  int w_layout;         // layout of w_tc: 0 regular, 1 halo (128 B rows), 2 halo2
 };
+
+inline uint16_t f2bf16_rn_host(float x) {
+  uint32_t u;
+  memcpy(&u, &x, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u) return (uint16_t)((u >> 16) | ((u & 0xFFFF) ? 0x40 : 0));
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+inline float bf16_to_f_host(uint16_t h) {
+  const uint32_t u = (uint32_t)h << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
 
 int launch_conv_simt(const ConvOp& op, void* stream);
 bool conv_direct_supported(const ConvOp& op);
 int launch_conv_direct(const ConvOp& op, void* stream);
 bool conv_tc_supported(const ConvOp& op, int precision);
 int launch_conv_tc(const ConvOp& op, int precision, void* stream);
-// Swizzled per-(n-tile, k-stage) shared-memory images of OIKK weights.
-// chunk_major: K stages ordered (channel chunk, tap) for the halo kernel,
-// else (tap, channel chunk).
+// Which tensor-core kernel (and so which packed weight layout) serves this
+// layer shape: 0 regular implicit GEMM, 1 halo kernel (conv_tc.cu), 2 wide-M
+// halo kernel (conv_tc2.cu).
+int tc_weight_layout(const ConvOp& shape, int precision);
+// Swizzled per-(n-tile, k-stage) shared-memory images of OIKK weights in the
+// given layout (launch_conv_tc dispatches on op.w_layout).
 std::vector<uint8_t> pack_tc_weights(const float* w_oikk, int co, int ci, int k,
-                                     int precision, const ConvOp& shape_op,
-                                     bool chunk_major);
+                                     int precision, const ConvOp& shape_op, int layout);
 bool conv_tc_halo_eligible(const ConvOp& op, int precision);
+bool conv_tc_halo2_eligible(const ConvOp& op, int precision);
+std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, int k,
+                                           int precision, const ConvOp& op);
+int launch_conv_tc_halo2(const ConvOp& op, int precision, void* stream);
 
 }  // namespace ts

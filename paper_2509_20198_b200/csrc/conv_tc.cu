@@ -39,6 +39,7 @@
 #include <vector>
 
 #include "conv.cuh"
+#include "tc_ptx.cuh"
 #include "ts_common.cuh"
 
 namespace ts {
@@ -51,179 +52,7 @@ constexpr int kProd = kProdWarps * 32;      // 256 producer threads
 constexpr int kMmaWarp = kProdWarps;        // warp 8
 constexpr int kThreads = (kProdWarps + 1 + 4) * 32;
 
-// ------------------------------------------------------------------ PTX
-
-__device__ __forceinline__ uint32_t su32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t tx) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)),
-               "r"(tx)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(su32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(su32(dst)),
-      "l"(src), "r"(bytes), "r"(su32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void fence_barrier_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                   su32(dst)),
-               "r"(ncols));
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-}
-__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr),
-               "r"(ncols));
-}
-template <bool TF32>
-__device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
-                                     uint32_t acc) {
-  if (TF32)
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc));
-  else
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          su32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ bool elect_one() {
-  uint32_t pred = 0;
-  asm volatile(
-      "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.b32 %0, 1, 0, P;\n}\n"
-      : "=r"(pred));
-  return pred != 0;
-}
-
-// SWIZZLE_128B K-major UMMA smem descriptor: start>>4 [0,14), LBO>>4
-// [16,30) (unused for swizzled K-major), SBO>>4 [32,46) = 1024 B per 8-row
-// group, version 1 [46,48), layout SWIZZLE_128B = 2 at [61,64).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  uint64_t d = (uint64_t)((saddr & 0x3FFFF) >> 4);
-  d |= (uint64_t)(16 >> 4) << 16;
-  d |= (uint64_t)(1024 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
-  return d;
-}
-
-// instruction descriptor: D = f32, A/B format (bf16 = 1, tf32 = 2), both
-// K-major, N >> 3 at [17,23), M >> 4 at [24,29)
-__host__ __device__ constexpr uint32_t make_idesc(uint32_t ab_fmt, int n) {
-  return (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) | ((uint32_t)(n >> 3) << 17) |
-         ((uint32_t)(BM >> 4) << 24);
-}
-
-// Operand splitting with integer ALU ops only (no F2F/XU conversions).
-// tf32 hi: round-to-nearest-away on the 13 dropped bits; bf16 planes: exact
-// truncation split a = a0 + a1 + a2 (each 8 significant bits), bf16 RN for
-// the single-plane mode.
-__device__ __forceinline__ float tf32_hi(float x) {
-  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
-}
-__device__ __forceinline__ uint32_t hi_halves(float a, float b) {  // {a.hi16, b.hi16}
-  return __byte_perm(__float_as_uint(a), __float_as_uint(b), 0x7632);
-}
-// bf16 round-to-nearest-even; the result's high 16 bits are the bf16 value
-// (low bits are garbage until bf_keep clears them)
-__device__ __forceinline__ float rn_bf(float x) {
-  const uint32_t u = __float_as_uint(x);
-  return __uint_as_float(u + 0x7FFFu + ((u >> 16) & 1u));
-}
-__device__ __forceinline__ float bf_keep(float x) {
-  return __uint_as_float(__float_as_uint(x) & 0xFFFF0000u);
-}
-
-// a = a0 + a1 + e, a0 = bf16_rn(a), a1 = bf16_rn(a - a0), |e| <= 2^-18 |a|
-__device__ __forceinline__ void store_split2(uint8_t* dst, int plane_bytes, float4 a) {
-  const float x0 = bf_keep(rn_bf(a.x)), y0 = bf_keep(rn_bf(a.y)), z0 = bf_keep(rn_bf(a.z)),
-              w0 = bf_keep(rn_bf(a.w));
-  const float x1 = rn_bf(a.x - x0), y1 = rn_bf(a.y - y0), z1 = rn_bf(a.z - z0),
-              w1 = rn_bf(a.w - w0);
-  *reinterpret_cast<uint2*>(dst) = make_uint2(hi_halves(x0, y0), hi_halves(z0, w0));
-  *reinterpret_cast<uint2*>(dst + plane_bytes) =
-      make_uint2(hi_halves(x1, y1), hi_halves(z1, w1));
-}
-
-template <int MODE>
-struct Mode;
-template <>
-struct Mode<1> {  // TF32X3: A hi/lo, B hi/lo
-  static constexpr int pa = 2, pb = 2, kc = 32;
-  static constexpr bool tf32 = true;
-};
-template <>
-struct Mode<2> {  // BF16
-  static constexpr int pa = 1, pb = 1, kc = 64;
-  static constexpr bool tf32 = false;
-};
-template <>
-struct Mode<3> {  // BF16X3: A = a0 + a1 (RN, residual <= 2^-18 |a|), B = b0+b1+b2
-  static constexpr int pa = 2, pb = 3, kc = 64;
-  static constexpr bool tf32 = false;
-};
-template <>
-struct Mode<4> {  // BF16X4: A = a0 + a1, B = b0 + b1 (both RN, residual <= 2^-18)
-  static constexpr int pa = 2, pb = 2, kc = 64;
-  static constexpr bool tf32 = false;
-};
+using namespace tcx;
 
 struct TcArgs {
   ConvOp op;
@@ -288,8 +117,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
   const int64_t M = (int64_t)op.batch * wy * wx;
   const int Cin = op.in.C, Cout = op.out.C;
   const int64_t total_tiles = T.m_tiles * T.n_tiles;
+  // MODE 4 stacks the two weight planes along N (one MMA per A plane,
+  // N = 2 BN; the epilogue adds the halves): half the A-operand shared
+  // memory reads of one MMA per plane pair
+  constexpr int NST = MODE == 4 ? 2 : 1;
   uint32_t ncols = 32;
-  while ((int)ncols < 2 * BN) ncols <<= 1;
+  while ((int)ncols < 2 * NST * BN) ncols <<= 1;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -388,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
     // ------------------------------ MMA issuer -----------------------------
     // The whole warp walks the loop (uniform registers), one elected lane
     // issues; descriptors are integer offsets from precomputed bases.
-    const uint32_t idesc = make_idesc(Md::tf32 ? 2u : 1u, BN);
+    const uint32_t idesc = make_idesc(Md::tf32 ? 2u : 1u, NST * BN);
     const uint64_t d_smem = sw128_desc(su32(smem));
     const uint32_t pa = (BM * kRowBytes) >> 4, pb = (BN * kRowBytes) >> 4;
     int s = 0, lt = 0;
@@ -397,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
       const int acc = lt & 1;
       mbar_wait(acc_empty + acc, ((lt >> 1) & 1) ^ 1);
       tc_fence_after();
-      const uint32_t d = tmem + acc * BN;
+      const uint32_t d = tmem + acc * NST * BN;
       for (int kit = 0; kit < T.kiters; ++kit) {
         mbar_wait(full + s, ph);
         tc_fence_after();
@@ -415,9 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
             } else if (MODE == 2) {
               umma<false>(d, ak, bk, idesc, first);
             } else if (MODE == 4) {
-              umma<false>(d, ak + pa, bk + pb, idesc, first);  // small terms first
-              umma<false>(d, ak + pa, bk, idesc, 1u);
-              umma<false>(d, ak, bk + pb, idesc, 1u);
+              umma<false>(d, ak + pa, bk, idesc, first);  // small plane first
               umma<false>(d, ak, bk, idesc, 1u);
             } else {
               umma<false>(d, ak + pa, bk + pb, idesc, first);  // small terms first
@@ -460,7 +291,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
       tc_fence_after();
       for (int c = 0; c < BN; c += 16) {
         float v[16];
-        tmem_ld16(tmem + lane_base + acc * BN + c, v);  // warp-collective
+        tmem_ld16(tmem + lane_base + acc * NST * BN + c, v);  // warp-collective
+        if (NST == 2) {
+          float w[16];
+          tmem_ld16(tmem + lane_base + acc * NST * BN + BN + c, w);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += w[i];
+        }
         if (valid) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -799,19 +636,8 @@ uint32_t f2tf32_rna(float x) {
   return u & 0xFFFFE000u;
 }
 
-uint16_t f2bf16_rn(float x) {
-  uint32_t u;
-  memcpy(&u, &x, 4);
-  if ((u & 0x7F800000u) == 0x7F800000u) return (uint16_t)((u >> 16) | ((u & 0xFFFF) ? 0x40 : 0));
-  u += 0x7FFFu + ((u >> 16) & 1u);
-  return (uint16_t)(u >> 16);
-}
-float bf16_to_f(uint16_t h) {
-  const uint32_t u = (uint32_t)h << 16;
-  float f;
-  memcpy(&f, &u, 4);
-  return f;
-}
+uint16_t f2bf16_rn(float x) { return f2bf16_rn_host(x); }
+float bf16_to_f(uint16_t h) { return bf16_to_f_host(h); }
 
 struct TcPlan {
   int bn, stages, kiters, cchunks, ntiles, pa, pb, kc;
@@ -879,7 +705,9 @@ bool conv_tc_supported(const ConvOp& op, int precision) {
 }
 
 std::vector<uint8_t> pack_tc_weights(const float* w_oikk, int co, int ci, int k,
-                                     int precision, const ConvOp& shape_op, bool chunk_major) {
+                                     int precision, const ConvOp& shape_op, int layout) {
+  if (layout == 2) return pack_tc_weights_halo2(w_oikk, co, ci, k, precision, shape_op);
+  const bool chunk_major = layout == 1;
   ConvOp op = shape_op;
   op.in.C = ci;
   op.out.C = co;
@@ -977,8 +805,23 @@ int launch_conv_tc_halo(const ConvOp& op, int precision, void* stream) {
   return TS_OK;
 }
 
+int tc_weight_layout(const ConvOp& shape, int precision) {
+  static int halo2 = -1;
+  if (halo2 < 0) {
+    const char* e = getenv("TS_HALO2");
+    halo2 = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (halo2 && conv_tc_halo2_eligible(shape, precision)) return 2;
+  if (conv_tc_halo_eligible(shape, precision)) return 1;
+  return 0;
+}
+
 int launch_conv_tc(const ConvOp& op, int precision, void* stream) {
-  if (conv_tc_halo_eligible(op, precision)) return launch_conv_tc_halo(op, precision, stream);
+  if (op.w_layout == 2) return launch_conv_tc_halo2(op, precision, stream);
+  if (op.w_layout == 1) {
+    if (!conv_tc_halo_eligible(op, precision)) return TS_E_INVALID;
+    return launch_conv_tc_halo(op, precision, stream);
+  }
   const TcPlan p = plan_for(op, precision);
   const int64_t M = (int64_t)op.batch * (op.oy1 - op.oy0) * (op.ox1 - op.ox0);
   if (M <= 0) return TS_OK;

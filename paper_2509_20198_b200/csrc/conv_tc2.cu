@@ -1,0 +1,460 @@
+// K3b: halo-reuse tcgen05 convolution, wide-M variant (bf16 operand modes).
+//
+// Same operator as conv_tc.cu's halo kernel (refiner.py:330-396: stride-1
+// k x k cross-correlation + bias + leaky ReLU, nearest-up2 folded into the
+// input read, crop-aware output window), re-tiled for L2 bandwidth:
+//
+//   * one CTA tile = SUB x 128 consecutive output positions (SUB = 2 or 4
+//     M=128 MMAs per K step), so every weight stage fetched from L2 feeds
+//     SUB times more MMAs, and the halo overhead ((k-1)(Wp+1) extra rows
+//     per tile) is amortised over 256-512 positions instead of 128;
+//   * K chunks of 32 channels = 64-byte K-major rows in the SWIZZLE_64B
+//     layout: channel padding is at most 28 (fuse.0's 72 channels run as
+//     96, not 128) and 2-3 halo buffers fit next to the weight ring.
+//
+// Output positions are linearised with the padded pitch Wp = wx + k - 1
+// and (wy + k - 1) rows per image, so tap (ky, kx) of a run of consecutive
+// positions reads the contiguous run of halo rows starting at ky*Wp + kx:
+// the MMA issuer slides the A descriptor over one staged halo image (the
+// swizzle is a function of absolute smem address bits).
+//
+//   warps 0-7   producers: per (tile, chunk) gather the halo rows' fp32
+//               channels (16-byte loads, zeros outside the image), split
+//               into the mode's bf16 planes, store the SW64 image, arrive.
+//   warp 8      MMA issuer + TMEM owner (2 x SUB x BN fp32 columns).
+//   warp 9      weight loader: cp.async.bulk of pre-swizzled weight stages.
+//   warps 10-13 epilogue: tcgen05.ld, + bias, leaky ReLU, fp32 NHWC store.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "conv.cuh"
+#include "tc_ptx.cuh"
+#include "ts_common.cuh"
+
+namespace ts {
+namespace {
+
+using namespace tcx;
+
+constexpr int kRow = 64;   // bytes per K-major row (32 bf16 channels)
+constexpr int kKC = 32;    // channels per K chunk
+constexpr int kProdW = 8;
+constexpr int kProdT = kProdW * 32;
+constexpr int kMmaW = 8;
+constexpr int kLoadW = 9;
+constexpr int kThreads = 14 * 32;
+constexpr int kInflight = 8;   // 16-byte loads in flight per producer thread
+
+struct Halo2Args {
+  ConvOp op;
+  const uint8_t* wpk;  // [n_tile][chunk][tap][plane][BN][64 B] SW64 images
+  int bn, sub, hbufs, bstages, cchunks, taps, wp, lrows, n_tiles, accbufs;
+  int64_t m_tiles, positions;
+  int exp;  // timing experiments only (TS_H2_EXP): 1 = weights once, 2 = no halo fill
+};
+
+__device__ __forceinline__ void prod_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kProdT) : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T) {
+  using Md = Mode<MODE>;
+  constexpr int PA = Md::pa, PB = Md::pb;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  const ConvOp& op = T.op;
+  const int BN = T.bn, SUB = T.sub, HB = T.hbufs, SB = T.bstages, L = T.lrows;
+  const int plane_a = L * kRow;          // multiple of 512 (L % 8 == 0)
+  const int halo_bytes = PA * plane_a;
+  const int b_bytes = PB * BN * kRow;
+  uint8_t* halo = smem;
+  uint8_t* bring = smem + HB * halo_bytes;
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(bring + SB * b_bytes);
+  uint64_t* bempty = bfull + SB;
+  uint64_t* hfull = bempty + SB;
+  uint64_t* hempty = hfull + HB;
+  uint64_t* acc_full = hempty + HB;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  int64_t* rowoff = reinterpret_cast<int64_t*>(tmem_slot + 4);  // [2][L]
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int wy = op.oy1 - op.oy0, wx = op.ox1 - op.ox0;
+  const int Wp = T.wp;
+  const int64_t img_pos = (int64_t)(wy + op.k - 1) * Wp;
+  const int Cin = op.in.C, Cout = op.out.C;
+  const int MT = SUB * 128;
+  const int64_t total_tiles = T.m_tiles * T.n_tiles;
+  const int AB = T.accbufs;
+  const int acc_cols = SUB * PB * BN;  // per accumulator buffer
+  uint32_t ncols = 32;
+  while ((int)ncols < AB * acc_cols) ncols <<= 1;
+
+  if (tid == 0) {
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(bfull + s, 1);
+      mbar_init(bempty + s, 1);
+    }
+    for (int h = 0; h < HB; ++h) {
+      mbar_init(hfull + h, kProdT);
+      mbar_init(hempty + h, 1);
+    }
+    for (int a = 0; a < AB; ++a) {
+      mbar_init(acc_full + a, 1);
+      mbar_init(acc_empty + a, 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == kMmaW) tmem_alloc(tmem_slot, ncols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < kProdW) {
+    // ------------------------- halo producers -------------------------
+    // buffers are used round-robin per (tile, chunk); hph bit h = phase of
+    // buffer h
+    int hb = 0, lt = 0;
+    uint32_t hph = 0;
+    constexpr int PPR = kKC / 4;  // float4 pieces per row
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+      const int64_t mt = tile / T.n_tiles;
+      const int64_t j0 = mt * MT;
+      int64_t* ro = rowoff + (lt & 1) * L;
+      for (int j = tid; j < L; j += kProdT) {
+        const int64_t pos = j0 + j;
+        int64_t off = -1;
+        const int64_t b = pos / img_pos;
+        if (b < op.batch) {
+          const int r = (int)(pos - b * img_pos);
+          const int iy = op.oy0 - op.pad + r / Wp, ix = op.ox0 - op.pad + r % Wp;
+          const int sh = op.up2 ? 1 : 0;
+          if (iy >= 0 && iy < (op.in.H << sh) && ix >= 0 && ix < (op.in.W << sh))
+            off = ((b * op.in.H + (iy >> sh)) * op.in.W + (ix >> sh)) * op.in.cstride +
+                  op.in.coff;
+        }
+        ro[j] = off;
+      }
+      prod_sync();
+      for (int c = 0; c < T.cchunks; ++c) {
+        mbar_wait(hempty + hb, ((hph >> hb) & 1u) ^ 1u);
+        uint8_t* sa = halo + hb * halo_bytes;
+        const int c0 = c * kKC;
+        for (int pc = tid; pc < ((T.exp & 2) && lt > 0 ? 0 : L * PPR);
+             pc += kProdT * kInflight) {
+          float4 v[kInflight];
+#pragma unroll
+          for (int u = 0; u < kInflight; ++u) {
+            const int q = pc + u * kProdT;
+            v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (q < L * PPR) {
+              const int64_t off = ro[q >> 3];
+              const int ch = c0 + 4 * (q & 7);
+              if (off >= 0 && ch < Cin)
+                v[u] = __ldg(reinterpret_cast<const float4*>(op.in.base + off + ch));
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kInflight; ++u) {
+            const int q = pc + u * kProdT;
+            if (q < L * PPR) {
+              const int row = q >> 3, piece = q & 7;
+              const int o = row * kRow + (((piece >> 1) ^ ((row >> 1) & 3)) << 4) +
+                            ((piece & 1) << 3);
+              const float4 a = v[u];
+              if (MODE == 2)
+                *reinterpret_cast<uint2*>(sa + o) = make_uint2(
+                    hi_halves(rn_bf(a.x), rn_bf(a.y)), hi_halves(rn_bf(a.z), rn_bf(a.w)));
+              else
+                store_split2(sa + o, plane_a, a);
+            }
+          }
+        }
+        fence_proxy_async();
+        mbar_arrive(hfull + hb);
+        hph ^= 1u << hb;
+        if (++hb == HB) hb = 0;
+      }
+    }
+  } else if (warp == kMmaW) {
+    // ------------------------- MMA issuer -------------------------
+    // one MMA per A plane against all PB weight planes stacked along N:
+    // D[:, p*BN + n] accumulates A . b_p, summed by the epilogue.  Same
+    // MACs as one MMA per (A plane, B plane) pair at N = BN, but every
+    // 4 KB A read from shared memory now feeds PB*BN columns.
+    const uint32_t idesc = make_idesc(1u, PB * BN);
+    const uint64_t d_halo = sw64_desc(su32(halo));
+    const uint64_t d_ring = sw64_desc(su32(bring));
+    const uint32_t pa = (uint32_t)plane_a >> 4;
+    int s = 0, lt = 0, hb = 0, nwait = 0;
+    uint32_t bph = 0, hph = 0;
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+      const int acc = lt % AB;
+      mbar_wait(acc_empty + acc, ((lt / AB) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem + acc * acc_cols;
+      for (int c = 0; c < T.cchunks; ++c) {
+        mbar_wait(hfull + hb, (hph >> hb) & 1u);
+        hph ^= 1u << hb;
+        tc_fence_after();
+        const uint64_t d_hb = d_halo + (uint64_t)((hb * halo_bytes) >> 4);
+        int ky = 0, kx = 0;
+        for (int t = 0; t < T.taps; ++t) {
+          if (!(T.exp & 1) || nwait < SB) mbar_wait(bfull + s, bph);
+          ++nwait;
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t a0 = d_hb + (uint64_t)((ky * Wp + kx) * (kRow >> 4));
+            const uint64_t b0 = d_ring + (uint64_t)((s * b_bytes) >> 4);
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {  // 2 x 32-byte K steps per row
+              const uint32_t first = (c | t | k) ? 1u : 0u;
+              const uint64_t bk = b0 + 2 * k;
+              for (int u = 0; u < SUB; ++u) {
+                const uint64_t ak = a0 + (uint64_t)(u * (128 * kRow >> 4)) + 2 * k;
+                const uint32_t du = d + u * PB * BN;
+                if (PA == 2) umma<false>(du, ak + pa, bk, idesc, first);  // small plane first
+                umma<false>(du, ak, bk, idesc, PA == 2 ? 1u : first);
+              }
+            }
+            if (!(T.exp & 1)) umma_commit(bempty + s);
+          }
+          __syncwarp();
+          if (++s == SB) { s = 0; bph ^= 1; }
+          if (++kx == op.k) { kx = 0; ++ky; }
+        }
+        if (elect_one()) umma_commit(hempty + hb);
+        __syncwarp();
+        if (++hb == HB) hb = 0;
+      }
+      if (elect_one()) umma_commit(acc_full + acc);
+      __syncwarp();
+    }
+  } else if (warp == kLoadW) {
+    // ------------------------- weight loader -------------------------
+    if ((tid & 31) == 0) {
+      int s = 0;
+      uint32_t bph = 0;
+      for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const int nt = (int)(tile % T.n_tiles);
+        const uint8_t* wsrc = T.wpk + (size_t)nt * T.cchunks * T.taps * b_bytes;
+        for (int kt = 0; kt < T.cchunks * T.taps; ++kt) {
+          if ((T.exp & 1) && (tile > blockIdx.x || kt >= SB)) break;
+          mbar_wait(bempty + s, bph ^ 1);
+          bulk_g2s(bring + s * b_bytes, wsrc + (size_t)kt * b_bytes, b_bytes, bfull + s);
+          mbar_arrive_tx(bfull + s, b_bytes);
+          if (++s == SB) { s = 0; bph ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------- epilogue -------------------------
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const bool vec = (op.out.cstride % 4 == 0) && (op.out.coff % 4 == 0);
+    int lt = 0;
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+      const int acc = lt % AB;
+      const int64_t mt = tile / T.n_tiles;
+      const int nt = (int)(tile - mt * T.n_tiles);
+      const int n0 = nt * BN;
+      mbar_wait(acc_full + acc, (lt / AB) & 1);
+      tc_fence_after();
+      for (int u = 0; u < SUB; ++u) {
+        const int64_t pos = mt * MT + u * 128 + q * 32 + (tid & 31);
+        float* o = nullptr;
+        if (pos < T.positions) {
+          const int64_t b = pos / img_pos;
+          const int r = (int)(pos - b * img_pos);
+          const int y = r / Wp, x = r % Wp;
+          if (y < wy && x < wx)
+            o = op.out.base +
+                ((b * op.out.H + op.oy0 + y) * op.out.W + op.ox0 + x) * op.out.cstride +
+                op.out.coff;
+        }
+        for (int c = 0; c < BN; c += 16) {
+          float v[16];
+          const uint32_t ta = tmem + lane_base + acc * acc_cols + u * PB * BN + c;
+          tmem_ld16(ta, v);
+#pragma unroll
+          for (int p = 1; p < PB; ++p) {
+            float w[16];
+            tmem_ld16(ta + p * BN, w);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += w[i];
+          }
+          if (o) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int n = n0 + c + i;
+              float x = v[i] + (n < Cout ? __ldg(op.bias + n) : 0.f);
+              if (op.lrelu) x = x >= 0.f ? x : 0.01f * x;
+              v[i] = x;
+            }
+            if (vec && n0 + c + 16 <= Cout) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                *reinterpret_cast<float4*>(o + n0 + c + 4 * i) =
+                    make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (n0 + c + i < Cout) o[n0 + c + i] = v[i];
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(acc_empty + acc);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaW) {
+    tc_fence_after();
+    tmem_dealloc(tmem, ncols);
+  }
+}
+
+struct Halo2Plan {
+  int bn, ntiles, pa, pb, sub, hbufs, bstages, cchunks, wp, lrows, accbufs;
+  size_t smem;
+  int64_t positions;
+};
+
+bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
+  if (precision != 2 && precision != 3 && precision != 4) return false;
+  if (op.stride != 1 || op.k < 2 || op.pad * 2 + 1 != op.k) return false;
+  if (op.in.C % 4 || op.in.cstride % 4 || op.in.coff % 4) return false;
+  Halo2Plan p{};
+  p.pa = precision == 2 ? 1 : 2;
+  p.pb = precision == 2 ? 1 : precision == 4 ? 2 : 3;
+  const int n16 = (op.out.C + 15) / 16 * 16;
+  p.ntiles = (n16 + 127) / 128;
+  p.bn = ((n16 + p.ntiles - 1) / p.ntiles + 15) / 16 * 16;
+  if (p.pb * p.bn > 256) return false;  // MMA N limit with stacked planes
+  p.cchunks = (op.in.C + kKC - 1) / kKC;
+  const int wx = op.ox1 - op.ox0, wy = op.oy1 - op.oy0;
+  p.wp = wx + op.k - 1;
+  p.positions = (int64_t)op.batch * (wy + op.k - 1) * p.wp;
+  const size_t cap = 225 * 1024;
+  const size_t bst = (size_t)p.pb * p.bn * kRow;
+  // (sub-tiles, accumulator buffers): prefer M >= 256 with the epilogue
+  // overlapped; fall back to a single accumulator buffer, then M = 128
+  const int cand[5][2] = {{4, 2}, {2, 2}, {4, 1}, {2, 1}, {1, 2}};
+  for (const auto& cb : cand) {
+    const int sub = cb[0], ab = cb[1];
+    if (ab * sub * p.pb * p.bn > 512) continue;
+    const int L = (128 * sub + (op.k - 1) * (p.wp + 1) + 7) / 8 * 8;
+    const size_t hbuf = (size_t)p.pa * L * kRow;
+    const size_t fixed = 1024 + 8 * 40 + 16 + 16 * (size_t)L + 64;
+    for (int hb : {3, 2}) {
+      if (hb * hbuf + 3 * bst + fixed > cap) continue;
+      p.sub = sub;
+      p.accbufs = ab;
+      p.hbufs = hb;
+      p.lrows = L;
+      p.bstages = (int)std::min<size_t>(8, (cap - hb * hbuf - fixed) / bst);
+      p.smem = hb * hbuf + p.bstages * bst + fixed;
+      *out = p;
+      return true;
+    }
+  }
+  return false;
+}
+
+}  // namespace
+
+bool conv_tc_halo2_eligible(const ConvOp& op, int precision) {
+  Halo2Plan p;
+  return plan2(op, precision, &p);
+}
+
+std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, int k,
+                                           int precision, const ConvOp& op) {
+  Halo2Plan p;
+  if (!plan2(op, precision, &p)) return {};
+  const size_t plane = (size_t)p.bn * kRow;
+  const size_t b_bytes = plane * p.pb;
+  const int taps = k * k;
+  std::vector<uint8_t> out((size_t)p.ntiles * p.cchunks * taps * b_bytes, 0);
+  for (int nt = 0; nt < p.ntiles; ++nt)
+    for (int c = 0; c < p.cchunks; ++c)
+      for (int t = 0; t < taps; ++t) {
+        const int ky = t / k, kx = t % k;
+        uint8_t* base = out.data() + (((size_t)nt * p.cchunks + c) * taps + t) * b_bytes;
+        for (int r = 0; r < p.bn; ++r) {
+          const int n = nt * p.bn + r;
+          for (int e = 0; e < kKC; ++e) {
+            const int ch = c * kKC + e;
+            const float v =
+                (n < co && ch < ci) ? w_oikk[(((size_t)n * ci + ch) * k + ky) * k + kx] : 0.f;
+            const int byte = 2 * e;
+            const size_t off =
+                (size_t)r * kRow + (size_t)((((byte >> 4) ^ ((r >> 1) & 3))) << 4) + (byte & 15);
+            uint16_t h[3] = {0, 0, 0};
+            if (precision == 2) {
+              h[0] = f2bf16_rn_host(v);
+            } else if (precision == 4) {  // RN split, like the device producers
+              h[0] = f2bf16_rn_host(v);
+              h[1] = f2bf16_rn_host(v - bf16_to_f_host(h[0]));
+            } else {  // exact truncation split
+              uint32_t u;
+              float rr = v;
+              for (int pl = 0; pl < 3; ++pl) {
+                memcpy(&u, &rr, 4);
+                h[pl] = (uint16_t)(u >> 16);
+                rr -= bf16_to_f_host(h[pl]);
+              }
+            }
+            for (int pl = 0; pl < p.pb; ++pl) memcpy(base + pl * plane + off, &h[pl], 2);
+          }
+        }
+      }
+  return out;
+}
+
+int launch_conv_tc_halo2(const ConvOp& op, int precision, void* stream) {
+  Halo2Plan p;
+  if (!plan2(op, precision, &p)) return TS_E_INVALID;
+  Halo2Args a{op, op.w_tc, p.bn, p.sub, p.hbufs, p.bstages, p.cchunks, op.k * op.k, p.wp,
+              p.lrows, p.ntiles, p.accbufs, ceil_div<int64_t>(p.positions, 128 * p.sub),
+              p.positions, 0};
+  static int exp = -1;
+  if (exp < 0) {
+    const char* e = getenv("TS_H2_EXP");
+    exp = e ? atoi(e) : 0;
+  }
+  a.exp = exp;
+  const int64_t tiles = a.m_tiles * p.ntiles;
+  if (tiles <= 0) return TS_OK;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    TS_CUDA_TRY(cudaGetDevice(&dev));
+    TS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+  cudaStream_t s = as_stream(stream);
+#define TS_TCH2_LAUNCH(MD)                                                            \
+  do {                                                                                \
+    TS_CUDA_TRY(cudaFuncSetAttribute(conv_tc_halo2_kernel<MD>,                        \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                     (int)p.smem));                                   \
+    ts::count_launch(), conv_tc_halo2_kernel<MD><<<grid, kThreads, p.smem, s>>>(a);   \
+  } while (0)
+  if (precision == 2) TS_TCH2_LAUNCH(2);
+  else if (precision == 4) TS_TCH2_LAUNCH(4);
+  else TS_TCH2_LAUNCH(3);
+#undef TS_TCH2_LAUNCH
+  TS_LAUNCH_CHECK();
+  return TS_OK;
+}
+
+}  // namespace ts

@@ -55,6 +55,7 @@ struct ConvLayer {
   float* w = nullptr;   // device [K][Cout]
   float* b = nullptr;   // device [Cout]
   const uint8_t* w_tc = nullptr;  // tensor-core packed weights (or null)
+  int w_layout = 0;               // which TC kernel the packed weights serve
   size_t out_off = 0;   // workspace offset (floats) of the output buffer
   bool materialize = false;  // tensor-core mode: up2 input copied once, then a
                              // stride-1 halo conv (conv_tc.cu)
@@ -413,9 +414,9 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
       shape.ox0 = L.out_win.x0; shape.ox1 = L.out_win.x1;
       shape.in.C = L.d.ci; shape.in.cstride = L.d.ci; shape.out.C = Co;
       shape.batch = 1;
+      L.w_layout = tc_weight_layout(shape, W->precision);
       const std::vector<uint8_t> pk =
-          pack_tc_weights(src.data(), Co, L.d.ci, L.d.k, W->precision, shape,
-                          conv_tc_halo_eligible(shape, W->precision));
+          pack_tc_weights(src.data(), Co, L.d.ci, L.d.k, W->precision, shape, L.w_layout);
       void* d = nullptr;
       TS_CUDA_TRY(cudaMalloc(&d, pk.size()));
       W->device_allocs.push_back(d);
@@ -581,6 +582,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
       op.w = L.w; op.bias = L.b;
       op.batch = B;
       op.w_tc = L.w_tc;
+      op.w_layout = L.w_layout;
       int st;
       // thin layers (few input or output channels: an MMA tile would be
       // mostly padding) -> fp32 direct kernel; the rest -> tensor cores (or
@@ -676,8 +678,9 @@ extern "C" int ts_conv2d(const float* d_x, int batch, int c_in, int h, int w,
     TS_CUDA_TRY(cudaMemcpyAsync(hw.data(), d_weight, nw * sizeof(float),
                                 cudaMemcpyDeviceToHost, s));
     TS_CUDA_TRY(cudaStreamSynchronize(s));
-    const std::vector<uint8_t> pk = pack_tc_weights(hw.data(), c_out, c_in, k, precision, op,
-                                                    conv_tc_halo_eligible(op, precision));
+    op.w_layout = tc_weight_layout(op, precision);
+    const std::vector<uint8_t> pk =
+        pack_tc_weights(hw.data(), c_out, c_in, k, precision, op, op.w_layout);
     TS_CUDA_TRY(cudaMallocAsync(&dpk, pk.size(), s));
     TS_CUDA_TRY(cudaMemcpyAsync(dpk, pk.data(), pk.size(), cudaMemcpyHostToDevice, s));
     op.w_tc = reinterpret_cast<const uint8_t*>(dpk);

@@ -1,0 +1,200 @@
+// tcgen05 / TMEM / mbarrier / bulk-copy PTX wrappers and the operand-split
+// helpers shared by the implicit-GEMM convolution kernels (conv_tc.cu,
+// conv_tc2.cu).  sm_100a only.
+#pragma once
+
+#include <stdint.h>
+
+namespace ts {
+namespace tcx {
+
+// ------------------------------------------------------------------ PTX
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)),
+               "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   su32(dst)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr),
+               "r"(ncols));
+}
+template <bool TF32>
+__device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                     uint32_t acc) {
+  if (TF32)
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  else
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.b32 %0, 1, 0, P;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+// SWIZZLE_128B K-major UMMA smem descriptor: start>>4 [0,14), LBO>>4
+// [16,30) (unused for swizzled K-major), SBO>>4 [32,46) = 1024 B per 8-row
+// group, version 1 [46,48), layout SWIZZLE_128B = 2 at [61,64).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)(16 >> 4) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// instruction descriptor: D = f32, A/B format (bf16 = 1, tf32 = 2), both
+// K-major, N >> 3 at [17,23), M >> 4 at [24,29)
+__host__ __device__ constexpr uint32_t make_idesc(uint32_t ab_fmt, int n, int m = 128) {
+  return (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(m >> 4) << 24);
+}
+
+// SWIZZLE_64B K-major descriptor: 64-byte rows, SBO = 512 B per 8-row group,
+// layout SWIZZLE_64B = 4 at [61,64).  The swizzle XORs address bits [4,6)
+// with bits [7,9), i.e. 16-byte chunk c of row r sits at chunk c ^ ((r>>1)&3)
+// for a 512-byte aligned image.
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
+
+// Operand splitting with integer ALU ops only (no F2F/XU conversions).
+// tf32 hi: round-to-nearest-away on the 13 dropped bits; bf16 planes: exact
+// truncation split a = a0 + a1 + a2 (each 8 significant bits), bf16 RN for
+// the single-plane mode.
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+__device__ __forceinline__ uint32_t hi_halves(float a, float b) {  // {a.hi16, b.hi16}
+  return __byte_perm(__float_as_uint(a), __float_as_uint(b), 0x7632);
+}
+// bf16 round-to-nearest-even; the result's high 16 bits are the bf16 value
+// (low bits are garbage until bf_keep clears them)
+__device__ __forceinline__ float rn_bf(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return __uint_as_float(u + 0x7FFFu + ((u >> 16) & 1u));
+}
+__device__ __forceinline__ float bf_keep(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xFFFF0000u);
+}
+
+// a = a0 + a1 + e, a0 = bf16_rn(a), a1 = bf16_rn(a - a0), |e| <= 2^-18 |a|
+__device__ __forceinline__ void store_split2(uint8_t* dst, int plane_bytes, float4 a) {
+  const float x0 = bf_keep(rn_bf(a.x)), y0 = bf_keep(rn_bf(a.y)), z0 = bf_keep(rn_bf(a.z)),
+              w0 = bf_keep(rn_bf(a.w));
+  const float x1 = rn_bf(a.x - x0), y1 = rn_bf(a.y - y0), z1 = rn_bf(a.z - z0),
+              w1 = rn_bf(a.w - w0);
+  *reinterpret_cast<uint2*>(dst) = make_uint2(hi_halves(x0, y0), hi_halves(z0, w0));
+  *reinterpret_cast<uint2*>(dst + plane_bytes) =
+      make_uint2(hi_halves(x1, y1), hi_halves(z1, w1));
+}
+
+template <int MODE>
+struct Mode;
+template <>
+struct Mode<1> {  // TF32X3: A hi/lo, B hi/lo
+  static constexpr int pa = 2, pb = 2, kc = 32;
+  static constexpr bool tf32 = true;
+};
+template <>
+struct Mode<2> {  // BF16
+  static constexpr int pa = 1, pb = 1, kc = 64;
+  static constexpr bool tf32 = false;
+};
+template <>
+struct Mode<3> {  // BF16X3: A = a0 + a1 (RN, residual <= 2^-18 |a|), B = b0+b1+b2
+  static constexpr int pa = 2, pb = 3, kc = 64;
+  static constexpr bool tf32 = false;
+};
+template <>
+struct Mode<4> {  // BF16X4: A = a0 + a1, B = b0 + b1 (both RN, residual <= 2^-18)
+  static constexpr int pa = 2, pb = 2, kc = 64;
+  static constexpr bool tf32 = false;
+};
+
+
+}  // namespace tcx
+}  // namespace ts
