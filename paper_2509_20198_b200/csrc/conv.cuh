@@ -10,10 +10,23 @@ namespace ts {
 
 // One NHWC activation view: element (b, y, x, c) lives at
 // base[((b * H + y) * W + x) * cstride + coff + c].
+//
+// s2d = 1: space-to-depth storage of an even-sized image (the input layout
+// of a stride-2 3x3 layer run as a stride-1 2x2 convolution): element
+// (b, y, x, c) of the logical H x W x C image lives at half-resolution pixel
+// (y/2, x/2), channel ((y&1)*2 + (x&1))*C + c; cstride is then the physical
+// pixel stride (>= 4C).
 struct ActView {
   float* base;
   int H, W, cstride, coff, C;
+  int s2d;
 };
+
+__host__ __device__ inline int64_t act_off(const ActView& v, int64_t b, int y, int x) {
+  if (!v.s2d) return ((b * v.H + y) * v.W + x) * v.cstride + v.coff;
+  return ((b * (v.H >> 1) + (y >> 1)) * (v.W >> 1) + (x >> 1)) * v.cstride + v.coff +
+         ((y & 1) * 2 + (x & 1)) * v.C;
+}
 
 // A convolution launch (cross-correlation, refiner.py:330-380) with fused
 // nearest x2 upsampling of the input (refiner.py:395), bias, optional

@@ -115,6 +115,7 @@ conv_simt_kernel(ConvOp op) {
 }  // namespace
 
 int launch_conv_simt(const ConvOp& op, void* stream) {
+  if (op.out.s2d) return TS_E_INVALID;  // s2d outputs: direct / halo2 kernels only
   const int64_t M = (int64_t)op.batch * (op.oy1 - op.oy0) * (op.ox1 - op.ox0);
   if (M <= 0) return TS_OK;
   dim3 grid((unsigned)ceil_div<int64_t>(M, BM), (unsigned)ceil_div(op.out.C, BN));
@@ -281,7 +282,28 @@ __global__ void __launch_bounds__(kDThreads) conv_direct_kernel(ConvOp op, Direc
     const int64_t orow = (int64_t)op.out.W * op.out.cstride;
     float* ob = op.out.base + ((int64_t)b * op.out.H + y0) * orow +
                 (int64_t)x0 * op.out.cstride + op.out.coff;
-    if (Cout == CO && op.out.cstride == CO) {
+    if (op.out.s2d && Cout == CO && op.out.cstride == 4 * CO && op.out.coff == 0 &&
+        ((y0 | x0) & 1) == 0) {
+      // the 8 x 16 tile is 4 runs of 8 consecutive s2d pixels (4*CO floats
+      // each): linear, coalesced stores
+      const int64_t s2row = (int64_t)(op.out.W >> 1) * 4 * CO;
+      float* sb0 = op.out.base + ((int64_t)b * (op.out.H >> 1) + (y0 >> 1)) * s2row +
+                   (int64_t)(x0 >> 1) * 4 * CO;
+      for (int e = threadIdx.x; e < kDThreads * CO; e += kDThreads) {
+        const int r = e / (32 * CO), w = e - r * (32 * CO);
+        const int j = w / (4 * CO), ph = (w / CO) & 3, c = w % CO;
+        const int py = 2 * r + (ph >> 1), px = 2 * j + (ph & 1);
+        if (y0 + py < op.oy1 && x0 + px < op.ox1)
+          sb0[r * s2row + w] = so[(py * kDTX + px) * Cs + c];
+      }
+    } else if (op.out.s2d) {
+      for (int t = warp; t < kDThreads; t += kDThreads / 32) {
+        const int py = t / kDTX, px = t % kDTX;
+        if (y0 + py >= op.oy1 || x0 + px >= op.ox1) continue;
+        float* o = op.out.base + act_off(op.out, b, y0 + py, x0 + px);
+        for (int c = lane; c < Cout; c += 32) o[c] = so[t * Cs + c];
+      }
+    } else if (Cout == CO && op.out.cstride == CO) {
       for (int e = threadIdx.x; e < kDThreads * CO; e += kDThreads) {
         const int t = e / CO, c = e - t * CO;
         const int py = t / kDTX, px = t % kDTX;

@@ -818,6 +818,7 @@ int tc_weight_layout(const ConvOp& shape, int precision) {
 
 int launch_conv_tc(const ConvOp& op, int precision, void* stream) {
   if (op.w_layout == 2) return launch_conv_tc_halo2(op, precision, stream);
+  if (op.out.s2d) return TS_E_INVALID;  // s2d outputs: direct / halo2 kernels only
   if (op.w_layout == 1) {
     if (!conv_tc_halo_eligible(op, precision)) return TS_E_INVALID;
     return launch_conv_tc_halo(op, precision, stream);

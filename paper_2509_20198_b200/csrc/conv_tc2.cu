@@ -45,11 +45,14 @@ constexpr int kProdT = kProdW * 32;
 constexpr int kMmaW = 8;
 constexpr int kLoadW = 9;
 constexpr int kThreads = 14 * 32;
-constexpr int kInflight = 8;   // 16-byte loads in flight per producer thread
+constexpr int kInflight = 8; 
+constexpr int kHdr = 1024;         // packed-weight header: u32 count, u32 0, u16 list
+constexpr int kMaxStages = (kHdr - 8) / 2 - 1;  // + sentinel  // 16-byte loads in flight per producer thread
 
 struct Halo2Args {
   ConvOp op;
-  const uint8_t* wpk;  // [n_tile][chunk][tap][plane][BN][64 B] SW64 images
+  const uint8_t* wpk;  // packed weights: kHdr-byte stage list, then
+                       // [n_tile][stage][plane][BN][64 B] SW64 images
   int bn, sub, hbufs, bstages, cchunks, taps, wp, lrows, n_tiles, accbufs;
   int64_t m_tiles, positions;
   int exp;  // timing experiments only (TS_H2_EXP): 1 = weights once, 2 = no halo fill
@@ -80,6 +83,22 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   int64_t* rowoff = reinterpret_cast<int64_t*>(tmem_slot + 4);  // [2][L]
+  // stage table: (chunk, tap) pairs with nonzero weights, chunk-major,
+  // decoded once into the chunk id and the A-descriptor row offset of the tap
+  uint32_t* s_aoff = reinterpret_cast<uint32_t*>(rowoff + 2 * L);  // [nst]
+  uint16_t* s_chunk = reinterpret_cast<uint16_t*>(s_aoff + kMaxStages);
+  const int nst = (int)reinterpret_cast<const uint32_t*>(T.wpk)[0];
+  {
+    const uint16_t* gl = reinterpret_cast<const uint16_t*>(T.wpk + 8);
+    for (int i = threadIdx.x; i < nst; i += blockDim.x) {
+      const int e = gl[i], c = e / T.taps, t = e - c * T.taps;
+      const int ky = t / op.k, kx = t - ky * op.k;
+      s_chunk[i] = (uint16_t)c;
+      s_aoff[i] = (uint32_t)((ky * T.wp + kx) * (kRow >> 4));
+    }
+    s_chunk[nst] = 0xFFFF;  // sentinel
+  }
+  const uint8_t* wdata = T.wpk + kHdr;
 
   const int tid = threadIdx.x, warp = tid >> 5;
   const int wy = op.oy1 - op.oy0, wx = op.ox1 - op.ox0;
@@ -192,27 +211,28 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     const uint32_t pa = (uint32_t)plane_a >> 4;
     int s = 0, lt = 0, hb = 0, nwait = 0;
     uint32_t bph = 0, hph = 0;
+    (void)nwait;
     for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
       const int acc = lt % AB;
       mbar_wait(acc_empty + acc, ((lt / AB) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d = tmem + acc * acc_cols;
+      int si = 0;
       for (int c = 0; c < T.cchunks; ++c) {
         mbar_wait(hfull + hb, (hph >> hb) & 1u);
         hph ^= 1u << hb;
         tc_fence_after();
         const uint64_t d_hb = d_halo + (uint64_t)((hb * halo_bytes) >> 4);
-        int ky = 0, kx = 0;
-        for (int t = 0; t < T.taps; ++t) {
+        for (; s_chunk[si] == c; ++si) {
           if (!(T.exp & 1) || nwait < SB) mbar_wait(bfull + s, bph);
           ++nwait;
           tc_fence_after();
           if (elect_one()) {
-            const uint64_t a0 = d_hb + (uint64_t)((ky * Wp + kx) * (kRow >> 4));
+            const uint64_t a0 = d_hb + (uint64_t)s_aoff[si];
             const uint64_t b0 = d_ring + (uint64_t)((s * b_bytes) >> 4);
 #pragma unroll
             for (int k = 0; k < 2; ++k) {  // 2 x 32-byte K steps per row
-              const uint32_t first = (c | t | k) ? 1u : 0u;
+              const uint32_t first = (si | k) ? 1u : 0u;
               const uint64_t bk = b0 + 2 * k;
               for (int u = 0; u < SUB; ++u) {
                 const uint64_t ak = a0 + (uint64_t)(u * (128 * kRow >> 4)) + 2 * k;
@@ -225,7 +245,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
           }
           __syncwarp();
           if (++s == SB) { s = 0; bph ^= 1; }
-          if (++kx == op.k) { kx = 0; ++ky; }
         }
         if (elect_one()) umma_commit(hempty + hb);
         __syncwarp();
@@ -241,8 +260,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
       uint32_t bph = 0;
       for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
         const int nt = (int)(tile % T.n_tiles);
-        const uint8_t* wsrc = T.wpk + (size_t)nt * T.cchunks * T.taps * b_bytes;
-        for (int kt = 0; kt < T.cchunks * T.taps; ++kt) {
+        const uint8_t* wsrc = wdata + (size_t)nt * nst * b_bytes;
+        for (int kt = 0; kt < nst; ++kt) {
           if ((T.exp & 1) && (tile > blockIdx.x || kt >= SB)) break;
           mbar_wait(bempty + s, bph ^ 1);
           bulk_g2s(bring + s * b_bytes, wsrc + (size_t)kt * b_bytes, b_bytes, bfull + s);
@@ -272,10 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
           const int64_t b = pos / img_pos;
           const int r = (int)(pos - b * img_pos);
           const int y = r / Wp, x = r % Wp;
-          if (y < wy && x < wx)
-            o = op.out.base +
-                ((b * op.out.H + op.oy0 + y) * op.out.W + op.ox0 + x) * op.out.cstride +
-                op.out.coff;
+          if (y < wy && x < wx) o = op.out.base + act_off(op.out, b, op.oy0 + y, op.ox0 + x);
         }
         for (int c = 0; c < BN; c += 16) {
           float v[16];
@@ -330,7 +346,10 @@ struct Halo2Plan {
 
 bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
   if (precision != 2 && precision != 3 && precision != 4) return false;
-  if (op.stride != 1 || op.k < 2 || op.pad * 2 + 1 != op.k) return false;
+  // stride-1 k >= 2 (incl. the 2x2 space-to-depth form of stride-2 layers);
+  // 1x1 layers stay on the regular kernel (no halo to reuse, and their
+  // multi-N-tile shapes re-read A per N tile here)
+  if (op.stride != 1 || op.k < 2 || op.pad < 0 || op.pad >= op.k) return false;
   if (op.in.C % 4 || op.in.cstride % 4 || op.in.coff % 4) return false;
   Halo2Plan p{};
   p.pa = precision == 2 ? 1 : 2;
@@ -353,7 +372,7 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
     if (ab * sub * p.pb * p.bn > 512) continue;
     const int L = (128 * sub + (op.k - 1) * (p.wp + 1) + 7) / 8 * 8;
     const size_t hbuf = (size_t)p.pa * L * kRow;
-    const size_t fixed = 1024 + 8 * 40 + 16 + 16 * (size_t)L + 64;
+    const size_t fixed = 1024 + 8 * 40 + 16 + 16 * (size_t)L + 6 * kMaxStages + 64;
     for (int hb : {3, 2}) {
       if (hb * hbuf + 3 * bst + fixed > cap) continue;
       p.sub = sub;
@@ -383,40 +402,61 @@ std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, 
   const size_t plane = (size_t)p.bn * kRow;
   const size_t b_bytes = plane * p.pb;
   const int taps = k * k;
-  std::vector<uint8_t> out((size_t)p.ntiles * p.cchunks * taps * b_bytes, 0);
+  // (chunk, tap) stages whose weights are all zero in every n-tile are
+  // skipped (the space-to-depth form of a stride-2 3x3 layer has 7 such
+  // taps of 16 per 4 channel groups)
+  std::vector<uint16_t> list;
+  for (int c = 0; c < p.cchunks; ++c)
+    for (int t = 0; t < taps; ++t) {
+      const int ky = t / k, kx = t % k;
+      bool nz = false;
+      for (int n = 0; n < co && !nz; ++n)
+        for (int e = 0; e < kKC && !nz; ++e) {
+          const int ch = c * kKC + e;
+          if (ch < ci && w_oikk[(((size_t)n * ci + ch) * k + ky) * k + kx] != 0.f) nz = true;
+        }
+      if (nz) list.push_back((uint16_t)(c * taps + t));
+    }
+  if (list.empty()) list.push_back(0);  // all-zero layer: keep one stage
+  if ((int)list.size() > kMaxStages) return {};
+  const int nst = (int)list.size();
+  std::vector<uint8_t> out(kHdr + (size_t)p.ntiles * nst * b_bytes, 0);
+  const uint32_t hdr[2] = {(uint32_t)nst, 0u};
+  memcpy(out.data(), hdr, 8);
+  memcpy(out.data() + 8, list.data(), 2 * list.size());
   for (int nt = 0; nt < p.ntiles; ++nt)
-    for (int c = 0; c < p.cchunks; ++c)
-      for (int t = 0; t < taps; ++t) {
-        const int ky = t / k, kx = t % k;
-        uint8_t* base = out.data() + (((size_t)nt * p.cchunks + c) * taps + t) * b_bytes;
-        for (int r = 0; r < p.bn; ++r) {
-          const int n = nt * p.bn + r;
-          for (int e = 0; e < kKC; ++e) {
-            const int ch = c * kKC + e;
-            const float v =
-                (n < co && ch < ci) ? w_oikk[(((size_t)n * ci + ch) * k + ky) * k + kx] : 0.f;
-            const int byte = 2 * e;
-            const size_t off =
-                (size_t)r * kRow + (size_t)((((byte >> 4) ^ ((r >> 1) & 3))) << 4) + (byte & 15);
-            uint16_t h[3] = {0, 0, 0};
-            if (precision == 2) {
-              h[0] = f2bf16_rn_host(v);
-            } else if (precision == 4) {  // RN split, like the device producers
-              h[0] = f2bf16_rn_host(v);
-              h[1] = f2bf16_rn_host(v - bf16_to_f_host(h[0]));
-            } else {  // exact truncation split
-              uint32_t u;
-              float rr = v;
-              for (int pl = 0; pl < 3; ++pl) {
-                memcpy(&u, &rr, 4);
-                h[pl] = (uint16_t)(u >> 16);
-                rr -= bf16_to_f_host(h[pl]);
-              }
+    for (int i = 0; i < nst; ++i) {
+      const int c = list[i] / taps, t = list[i] % taps;
+      const int ky = t / k, kx = t % k;
+      uint8_t* base = out.data() + kHdr + ((size_t)nt * nst + i) * b_bytes;
+      for (int r = 0; r < p.bn; ++r) {
+        const int n = nt * p.bn + r;
+        for (int e = 0; e < kKC; ++e) {
+          const int ch = c * kKC + e;
+          const float v =
+              (n < co && ch < ci) ? w_oikk[(((size_t)n * ci + ch) * k + ky) * k + kx] : 0.f;
+          const int byte = 2 * e;
+          const size_t off =
+              (size_t)r * kRow + (size_t)((((byte >> 4) ^ ((r >> 1) & 3))) << 4) + (byte & 15);
+          uint16_t h[3] = {0, 0, 0};
+          if (precision == 2) {
+            h[0] = f2bf16_rn_host(v);
+          } else if (precision == 4) {  // RN split, like the device producers
+            h[0] = f2bf16_rn_host(v);
+            h[1] = f2bf16_rn_host(v - bf16_to_f_host(h[0]));
+          } else {  // exact truncation split
+            uint32_t u;
+            float rr = v;
+            for (int pl = 0; pl < 3; ++pl) {
+              memcpy(&u, &rr, 4);
+              h[pl] = (uint16_t)(u >> 16);
+              rr -= bf16_to_f_host(h[pl]);
             }
-            for (int pl = 0; pl < p.pb; ++pl) memcpy(base + pl * plane + off, &h[pl], 2);
           }
+          for (int pl = 0; pl < p.pb; ++pl) memcpy(base + pl * plane + off, &h[pl], 2);
         }
       }
+    }
   return out;
 }
 

@@ -15,6 +15,7 @@
 // default descriptor); results on the crop are unchanged.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -63,6 +64,11 @@ struct ConvLayer {
   Win up_win{0, 0, 0, 0};    // upsampled-coordinate window that is copied
   int out_cstride = 0, out_coff = 0;
   int in_src = -1;      // -1: external/concat buffers handled by the planner
+  // space-to-depth execution of a stride-2 3x3 layer (conv.cuh ActView):
+  // s2d_in runs it as a stride-1 2x2 conv over 4*C_in channels (weights
+  // remapped, dexec); s2d_out = this layer writes its output in that layout
+  bool s2d_in = false, s2d_out = false;
+  LayerDesc dexec;      // executed shape (== d unless s2d_in)
 };
 
 }  // namespace
@@ -335,16 +341,68 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
   }
   auto back = [&](int s, Win w) {  // returns needed window of the stage input
     for (int i = stage_last[s]; i >= stage_first[s]; --i) {
+      if (layers[i].s2d_out) {  // s2d pixels are written whole (2x2 groups)
+        w.y0 &= ~1; w.x0 &= ~1;
+        w.y1 = std::min(layers[i].Hout, (w.y1 + 1) & ~1);
+        w.x1 = std::min(layers[i].Wout, (w.x1 + 1) & ~1);
+      }
       layers[i].out_win = w;
       w = need_in(w, layers[i].d, layers[i].Hin, layers[i].Win_);
     }
     return w;
   };
   Win crop{kCrop, kCrop + kOut, kCrop, kCrop + kOut};
-  const Win fuse_in_need = back(7, crop);
-  Win merge_need = unite(back(5, fuse_in_need), back(6, fuse_in_need));
-  Win enc_need = back(4, merge_need);
-  for (int s = 0; s < 4; ++s) back(s, enc_need);
+  auto propagate = [&]() {
+    const Win fuse_in_need = back(7, crop);
+    Win merge_need = unite(back(5, fuse_in_need), back(6, fuse_in_need));
+    Win enc_need = back(4, merge_need);
+    for (int s = 0; s < 4; ++s) back(s, enc_need);
+  };
+  for (auto& L : layers) L.dexec = L.d;
+  propagate();
+  // stride-2 3x3 encoder layers run as stride-1 2x2 convolutions over a
+  // space-to-depth input on the wide-M halo kernel (bf16 operand modes): a
+  // strided im2col gather re-reads the input 9x and cannot use the halo
+  // reuse.  The producing layer must be able to write s2d (direct kernel or
+  // halo2), else the layer keeps its plain form.
+  {
+    const char* e = getenv("TS_S2D");
+    const bool s2d_ok = (W->precision >= 2 && W->precision <= 4) && !(e && e[0] == '0');
+    auto exec_shape = [&](const ConvLayer& L, const LayerDesc& d) {
+      ConvOp o{};
+      o.k = d.k; o.stride = d.s; o.pad = d.p; o.up2 = L.up2;
+      o.oy0 = L.out_win.y0; o.oy1 = L.out_win.y1; o.ox0 = L.out_win.x0; o.ox1 = L.out_win.x1;
+      o.in.C = d.ci; o.in.cstride = d.ci; o.out.C = d.co; o.out.cstride = d.co;
+      o.in.H = L.s2d_in ? L.Hin / 2 : L.Hin; o.in.W = o.in.H;
+      o.batch = 1;
+      return o;
+    };
+    for (int s = 0; s < 4 && s2d_ok; ++s)
+      for (int i = stage_first[s] + 1; i <= stage_last[s]; ++i) {
+        ConvLayer& L = layers[i];
+        ConvLayer& P = layers[i - 1];
+        const LayerDesc& d = L.d;
+        if (d.s != 2 || d.k != 3 || d.p != 1 || L.up2 || L.Hin % 2 || L.Win_ % 2) continue;
+        LayerDesc x = d;
+        x.ci = 4 * d.ci; x.k = 2; x.s = 1; x.p = 1;
+        L.s2d_in = true;
+        const bool l_ok = conv_tc_halo2_eligible(exec_shape(L, x), W->precision);
+        const ConvOp ps = exec_shape(P, P.dexec);
+        const bool p_ok = P.s2d_in || (conv_direct_supported(ps) &&
+                                       (P.dexec.ci <= 4 || P.dexec.co <= 16));
+        if (!l_ok || !p_ok) { L.s2d_in = false; continue; }
+        L.dexec = x;
+        P.s2d_out = true;
+      }
+    propagate();
+    bool ok = true;
+    for (auto& L : layers)
+      if (L.s2d_in && !conv_tc_halo2_eligible(exec_shape(L, L.dexec), W->precision)) ok = false;
+    if (!ok) {
+      for (auto& L : layers) { L.s2d_in = L.s2d_out = false; L.dexec = L.d; }
+      propagate();
+    }
+  }
 
   // ---- weights upload + buffer offsets (floats per tile) ----
   size_t off = 0;
@@ -386,15 +444,33 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
         ws[3] != L.d.k)
       return TS_E_SHAPE;
     if (bi->second.first.size() != 1 || bi->second.first[0] != L.d.co) return TS_E_SHAPE;
-    const int K = L.d.k * L.d.k * L.d.ci, Co = L.d.co;
+    const LayerDesc& dx = L.dexec;
+    const int K = dx.k * dx.k * dx.ci, Co = dx.co;
     std::vector<float> packed((size_t)K * Co);
-    const std::vector<float>& src = wi->second.second;
+    std::vector<float> src = wi->second.second;  // OIKK of the executed shape
+    if (L.s2d_in) {
+      // W'[o][(a*2+b)*ci + c][ty][tx] = W[o][c][2ty+a-1][2tx+b-1] (0 outside)
+      const int ci0 = L.d.ci;
+      std::vector<float> t((size_t)Co * dx.ci * 4, 0.f);
+      for (int o = 0; o < Co; ++o)
+        for (int a = 0; a < 2; ++a)
+          for (int b = 0; b < 2; ++b)
+            for (int c = 0; c < ci0; ++c)
+              for (int ty = 0; ty < 2; ++ty)
+                for (int tx = 0; tx < 2; ++tx) {
+                  const int ky = 2 * ty + a - 1, kx = 2 * tx + b - 1;
+                  if (ky < 0 || ky > 2 || kx < 0 || kx > 2) continue;
+                  t[(((size_t)o * dx.ci + (a * 2 + b) * ci0 + c) * 2 + ty) * 2 + tx] =
+                      src[(((size_t)o * ci0 + c) * 3 + ky) * 3 + kx];
+                }
+      src.swap(t);
+    }
     for (int o = 0; o < Co; ++o)
-      for (int ci = 0; ci < L.d.ci; ++ci)
-        for (int ky = 0; ky < L.d.k; ++ky)
-          for (int kx = 0; kx < L.d.k; ++kx)
-            packed[(size_t)((ky * L.d.k + kx) * L.d.ci + ci) * Co + o] =
-                src[(((size_t)o * L.d.ci + ci) * L.d.k + ky) * L.d.k + kx];
+      for (int ci = 0; ci < dx.ci; ++ci)
+        for (int ky = 0; ky < dx.k; ++ky)
+          for (int kx = 0; kx < dx.k; ++kx)
+            packed[(size_t)((ky * dx.k + kx) * dx.ci + ci) * Co + o] =
+                src[(((size_t)o * dx.ci + ci) * dx.k + ky) * dx.k + kx];
     params += packed.size() + Co;
     TS_CUDA_TRY(cudaMalloc(&L.w, packed.size() * sizeof(float)));
     TS_CUDA_TRY(cudaMalloc(&L.b, Co * sizeof(float)));
@@ -404,19 +480,22 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
                            cudaMemcpyHostToDevice));
     TS_CUDA_TRY(cudaMemcpy(L.b, bi->second.second.data(), Co * sizeof(float),
                            cudaMemcpyHostToDevice));
-    if (W->precision != 0 && L.d.ci % 4 == 0) {
+    if (W->precision != 0 && dx.ci % 4 == 0) {
       ConvOp shape{};
-      shape.k = L.d.k;
-      shape.stride = L.d.s;
-      shape.pad = L.d.p;
+      shape.k = dx.k;
+      shape.stride = dx.s;
+      shape.pad = dx.p;
       shape.up2 = L.up2 && !L.materialize;
       shape.oy0 = L.out_win.y0; shape.oy1 = L.out_win.y1;
       shape.ox0 = L.out_win.x0; shape.ox1 = L.out_win.x1;
-      shape.in.C = L.d.ci; shape.in.cstride = L.d.ci; shape.out.C = Co;
+      shape.in.C = dx.ci; shape.in.cstride = dx.ci; shape.out.C = Co;
+      shape.out.cstride = Co;
+      shape.in.H = L.s2d_in ? L.Hin / 2 : L.Hin; shape.in.W = shape.in.H;
       shape.batch = 1;
       L.w_layout = tc_weight_layout(shape, W->precision);
       const std::vector<uint8_t> pk =
-          pack_tc_weights(src.data(), Co, L.d.ci, L.d.k, W->precision, shape, L.w_layout);
+          pack_tc_weights(src.data(), Co, dx.ci, dx.k, W->precision, shape, L.w_layout);
+      if (L.s2d_in && L.w_layout != 2) return TS_E_INVALID;  // planner invariant
       void* d = nullptr;
       TS_CUDA_TRY(cudaMalloc(&d, pk.size()));
       W->device_allocs.push_back(d);
@@ -559,7 +638,18 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
         op.in = ActView{const_cast<float*>(prev_base), prev_H, prev_H, prev_cs, prev_coff,
                         prev_C};
       }
+      if (L.s2d_in) {
+        // previous layer wrote s2d: half-resolution pixels of 4 C channels
+        if (prev_coff != 0 || prev_cs != prev_C) return TS_E_INVALID;
+        op.in = ActView{const_cast<float*>(prev_base), prev_H / 2, prev_H / 2, 4 * prev_C, 0,
+                        4 * prev_C};
+      }
       op.out = ActView{buf(L.out_off), L.Hout, L.Wout, L.out_cstride, L.out_coff, L.d.co};
+      if (L.s2d_out) {
+        if (L.out_coff != 0 || L.out_cstride != L.d.co) return TS_E_INVALID;
+        op.out.cstride = 4 * L.d.co;
+        op.out.s2d = 1;
+      }
       op.up2 = L.up2;
       if (L.materialize) {
         float* ub = buf(L.up_off);
@@ -575,7 +665,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
         op.in = ActView{ub, H2, W2, L.d.ci, 0, L.d.ci};
         op.up2 = 0;
       }
-      op.k = L.d.k; op.stride = L.d.s; op.pad = L.d.p;
+      op.k = L.dexec.k; op.stride = L.dexec.s; op.pad = L.dexec.p;
       op.lrelu = L.d.lrelu;
       op.oy0 = L.out_win.y0; op.oy1 = L.out_win.y1;
       op.ox0 = L.out_win.x0; op.ox1 = L.out_win.x1;
