@@ -209,7 +209,11 @@ int ts_conv2d(const float* d_x, int batch, int c_in, int h, int w,
  * reference predicate floor((x-(cx-320))/10) in IEEE fp64 for every key
  * whose window may hold the point (bit-exact).  Keys are looked up through
  * a host-built CSR grid of cell size 640 m anchored at (gx0, gy0):
- *   d_cell_keys_off[gnx*gny+1], d_cell_keys[...] (key ids per cell).
+ *   d_cell_keys_off[gnx*gny+1], d_cell_keys[...] (key ids per cell);
+ *   d_cell_inner[gnx*gny] (nullable): the first d_cell_inner[c] ids of
+ *   cell c are the only keys whose window [cx-320, cx+320] (+-1e-6 m)
+ *   meets the open square 1 cm inside the cell; points >= 2 cm inside
+ *   their cell test only those.
  * prior: heights_rel float32 P x 64 x 64 with base c_z per patch (f64);
  * prior rgb P x 64 x 64 x 3 (NULL = colourless base).  Outputs heights_rel
  * against key_cz, rgb.  d_accum: ts_bake_workspace(P) bytes of scratch.   */
@@ -217,7 +221,7 @@ size_t ts_bake_workspace(int n_patches);
 int ts_bake(const double* d_xyz, const float* d_rgb, int64_t m,
             const ts_patch_key* d_keys, int n_patches,
             const int32_t* d_cell_keys_off, const int32_t* d_cell_keys,
-            double gx0, double gy0, int gnx, int gny,
+            const int32_t* d_cell_inner, double gx0, double gy0, int gnx, int gny,
             const float* d_prior_h, const double* d_base_cz,
             const double* d_key_cz, const float* d_prior_rgb,
             float* d_out_h, float* d_out_rgb, void* d_accum, void* stream);

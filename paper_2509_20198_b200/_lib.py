@@ -63,7 +63,7 @@ SIGNATURES = {
     "ts_conv2d": (I32, [P, I32, I32, I32, I32, P, I32, I32, P, I32, I32, I32, P,
                         P]),
     "ts_bake_workspace": (SZ, [I32]),
-    "ts_bake": (I32, [P, P, I64, P, I32, P, P, F64, F64, I32, I32, P, P, P,
+    "ts_bake": (I32, [P, P, I64, P, I32, P, P, P, F64, F64, I32, I32, P, P, P,
                       P, P, P, P, P]),
     "ts_incircle_sign": (I32, [P, P, P, P]),
     "ts_orient_sign": (I32, [P, P, P]),

@@ -1,22 +1,54 @@
 // K4: full-resolution texel update (bake_fullres, engine.py:416-456).
 //
-// Per point: candidate keys come from a host-built CSR grid (640 m cells,
-// every key registered in each cell its window [x0-1, x0+641] touches), and
+// Texel assignment.  Per point, candidate keys come from a host-built CSR
+// grid (640 m cells; every key is registered in each cell its window
+// [x0-1, x0+641] touches, so the cell may be computed approximately), and
 // every candidate is tested with the reference predicate
-//   ix = floor((x - (cx - 320)) / 10), 0 <= ix < 64   (IEEE fp64, no FMA)
-// so texel assignment is bit-exact for any key set, overlapping or not.
-// Covered texels accumulate count (u32) and fp64 sums of z, r, g, b with
-// fire-and-forget atomics; the finalize pass writes mean / prior values
-// exactly as the reference composes them.  Sums are order-independent up
-// to fp64 rounding (|dh| ~ 1e-13 m), far inside the 1e-6 m budget.
+//   ix = floor((x - (cx - 320)) / 10), 0 <= ix < 64   (IEEE fp64)
+// so assignment is bit-exact for any key set, overlapping or not.  The
+// divide is evaluated as x * 0.1 whenever that product lies more than 1e-9
+// from an integer (both roundings are within 2e-14 of the true quotient,
+// so their floors agree); otherwise by the IEEE divide.
+//
+// Accumulation.  Sums are fixed point, so the result is independent of the
+// order in which points arrive (bit-identical run to run, any grid):
+//   z:   int64, 2^-28 m per unit  (per-point rounding <= 1.9e-9 m;
+//        |sum z| per texel must stay below 2^35 m)
+//   rgb: 2^-24 per unit (per-point rounding <= 3e-8)
+// against the reference's sequential fp64 bincount sums that is a mean
+// difference <= 2e-9 m in height and <= 3e-8 in colour.
+//
+// One persistent CTA per SM walks a contiguous range of whole 1,024-point
+// batches, staged into shared memory three batches ahead by cp.async.bulk
+// (mbarrier complete_tx).  The CTA's shared memory also holds the
+// accumulators of ONE "hot" patch (count, z as lo/hi 32-bit words with the
+// lo carry folded into hi, r/g/b u32 = 24 B x 4096 texels = 96 KB);
+// (point, key) pairs of the hot patch accumulate there with native 32-bit
+// shared atomics, all others go straight to the global int64 accumulators.
+// A u32 colour sum that wraps adds its carry (2^32) to the global sum, so
+// the shared sums are exact.  After each batch the CTA counts the threads
+// that missed the hot patch (the barrier that also frees the staging
+// buffer); if they are the majority, the hot patch is flushed (global
+// atomics of the non-empty texels) and replaced by the patch of the batch's
+// last point.  Input grouped by patch (engine._bake_one order, configs[2])
+// runs ~98% in shared memory; shuffled input degrades to global atomics
+// without flush churn.
 #include <algorithm>
 
+#include "tc_ptx.cuh"
 #include "ts_common.cuh"
 
 namespace ts {
 namespace {
 
 constexpr int kTex = kOut * kOut;  // 4096 texels per patch
+constexpr int kBakeThreads = 1024;  // one CTA per SM, one point per thread per batch
+constexpr int kBatch = kBakeThreads;
+constexpr int kBufs = 3;            // staged batches in flight
+constexpr double kZScale = 268435456.0;          // 2^28
+constexpr double kZInv = 1.0 / 268435456.0;
+constexpr float kCScale = 16777216.0f;            // 2^24
+constexpr double kCInv = 1.0 / 16777216.0;
 
 struct BakeArgs {
   const double* xyz;
@@ -26,46 +58,203 @@ struct BakeArgs {
   int n_patches;
   const int32_t* cell_off;
   const int32_t* cell_keys;
+  const int32_t* cell_inner;  // nullable: leading interior keys per cell
   double gx0, gy0;
   int gnx, gny;
-  uint32_t* cnt;
-  double* sum;  // [P][4][4096]
+  int bulk;                      // arrays 16-byte aligned: stage by bulk copies
+  uint32_t* cnt;                // [P][4096]
+  unsigned long long* sum;      // [P][4][4096] fixed point (z, r, g, b)
 };
 
-__global__ void __launch_bounds__(256)
-bake_splat_kernel(BakeArgs A) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.m; i += stride) {
-    const double x = A.xyz[3 * i], y = A.xyz[3 * i + 1], z = A.xyz[3 * i + 2];
-    int64_t gx = floor_i64(ddiv(dsub(x, A.gx0), kPatch));
-    int64_t gy = floor_i64(ddiv(dsub(y, A.gy0), kPatch));
-    if (gx < 0 || gy < 0 || gx >= A.gnx || gy >= A.gny) continue;
-    const int64_t c = gy * A.gnx + gx;
-    const int32_t k0 = A.cell_off[c], k1 = A.cell_off[c + 1];
-    float r = 0.f, g = 0.f, b = 0.f;
-    if (A.rgb && k1 > k0) { r = A.rgb[3 * i]; g = A.rgb[3 * i + 1]; b = A.rgb[3 * i + 2]; }
-    for (int32_t k = k0; k < k1; ++k) {
-      const int key = A.cell_keys[k];
-      const double x0 = dsub(A.keys[key].cx, 320.0);
-      const double y0 = dsub(A.keys[key].cy, 320.0);
-      const int64_t ix = floor_i64(ddiv(dsub(x, x0), kTexel));
-      const int64_t iy = floor_i64(ddiv(dsub(y, y0), kTexel));
-      if (ix < 0 || ix >= kOut || iy < 0 || iy >= kOut) continue;
-      const int64_t t = (int64_t)key * kTex + iy * kOut + ix;
-      atomicAdd(A.cnt + t, 1u);
-      double* s = A.sum + (int64_t)key * 4 * kTex + iy * kOut + ix;
-      atomicAdd(s, z);
-      if (A.rgb) {
-        atomicAdd(s + kTex, (double)r);
-        atomicAdd(s + 2 * kTex, (double)g);
-        atomicAdd(s + 3 * kTex, (double)b);
+// floor((d) / 10) exactly as numpy evaluates it (see header).
+__device__ __forceinline__ int64_t texel_index(double d) {
+  const double q = dmul(d, 0.1);
+  const double f = floor(q);
+  const double r = dsub(q, f);
+  if (r > 1e-9 && r < 1.0 - 1e-9) return (int64_t)f;
+  return floor_i64(ddiv(d, kTexel));
+}
+
+// Candidate key range of (x, y): the CSR slice of its (approximate) cell,
+// cut to the cell's interior keys when the point is >= 2 cm inside it.
+// Returns false when the point is outside the grid.
+__device__ __forceinline__ bool candidates(const BakeArgs& A, double x, double y, int32_t& k0,
+                                           int32_t& k1) {
+  // approximate cell: the +-1 m registration margin absorbs the rounding
+  const double fx = floor(dmul(dsub(x, A.gx0), 1.0 / kPatch));
+  const double fy = floor(dmul(dsub(y, A.gy0), 1.0 / kPatch));
+  if (!(fx >= 0.0 && fy >= 0.0 && fx < (double)A.gnx && fy < (double)A.gny)) return false;
+  const int64_t c = (int64_t)fy * A.gnx + (int64_t)fx;
+  k0 = __ldg(A.cell_off + c);
+  // points >= 2 cm inside their cell only test the cell's interior keys
+  // (offsets are approximate to ~1e-10 m; the list uses a 1 cm square)
+  const double ox = dsub(dsub(x, A.gx0), dmul(fx, kPatch));
+  const double oy = dsub(dsub(y, A.gy0), dmul(fy, kPatch));
+  if (A.cell_inner && ox >= 0.02 && ox <= kPatch - 0.02 && oy >= 0.02 && oy <= kPatch - 0.02)
+    k1 = k0 + __ldg(A.cell_inner + c);
+  else
+    k1 = __ldg(A.cell_off + c + 1);
+  return true;
+}
+
+// Texel of (x, y) under candidate k of the CSR list, or -1 (exact
+// reference predicate).
+__device__ __forceinline__ int texel_of(const BakeArgs& A, int32_t k, double x, double y,
+                                        int& key) {
+  key = __ldg(A.cell_keys + k);
+  const double2 cc = __ldg(reinterpret_cast<const double2*>(A.keys) + key);
+  const double dx = dsub(x, dsub(cc.x, 320.0));
+  const double dy = dsub(y, dsub(cc.y, 320.0));
+  // coarse reject: any hit has dx, dy in [-1e-13, 640 + 1e-13]
+  if (!(dx > -0.5 && dx < 640.5 && dy > -0.5 && dy < 640.5)) return -1;
+  const int64_t ix = texel_index(dx), iy = texel_index(dy);
+  if (ix < 0 || ix >= kOut || iy < 0 || iy >= kOut) return -1;
+  return (int)(iy * kOut + ix);
+}
+
+struct HotSmem {
+  // hot-patch accumulators: count, z fixed point as lo/hi 32-bit words
+  // (the lo word's carry goes into the hi word), colour sums
+  uint32_t cnt[kTex], zlo[kTex], zhi[kTex], c[3][kTex];
+  double xyz[kBufs][kBatch * 3];  // staged points (bulk copies)
+  float rgb[kBufs][kBatch * 3];
+  uint64_t full[kBufs];
+  int last_key[2];  // by batch parity (a fast thread may write the next one)
+};
+
+__global__ void __launch_bounds__(kBakeThreads, 1) bake_splat_kernel(BakeArgs A) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  HotSmem& S = *reinterpret_cast<HotSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  for (int t = tid; t < kTex; t += kBakeThreads) {
+    S.cnt[t] = 0; S.zlo[t] = 0; S.zhi[t] = 0; S.c[0][t] = 0; S.c[1][t] = 0; S.c[2][t] = 0;
+  }
+  // CTA ranges are whole batches, so every staged batch starts 16-byte
+  // aligned (given 16-byte aligned arrays, checked by the host)
+  const int64_t nb = ceil_div<int64_t>(A.m, kBatch);
+  const int64_t per = ceil_div<int64_t>(nb, gridDim.x) * kBatch;
+  const int64_t lo = (int64_t)blockIdx.x * per;
+  const int64_t hi = min(A.m, lo + per);
+  const bool has_rgb = A.rgb != nullptr;
+  // full batches come in by cp.async.bulk, kBufs ahead; a ragged last
+  // batch (or unaligned arrays) is read straight from global memory
+  auto staged = [&](int64_t base) { return A.bulk && base + kBatch <= hi; };
+  auto issue = [&](int64_t base, int buf) {
+    if (base < hi && staged(base)) {
+      const uint32_t bx = kBatch * 3 * sizeof(double), bc = kBatch * 3 * sizeof(float);
+      tcx::fence_proxy_async();
+      tcx::mbar_arrive_tx(&S.full[buf], bx + (has_rgb ? bc : 0));
+      tcx::bulk_g2s(S.xyz[buf], A.xyz + 3 * base, bx, &S.full[buf]);
+      if (has_rgb) tcx::bulk_g2s(S.rgb[buf], A.rgb + 3 * base, bc, &S.full[buf]);
+    }
+  };
+  if (tid == 0) {
+    S.last_key[0] = S.last_key[1] = -1;
+    for (int b = 0; b < kBufs; ++b) tcx::mbar_init(&S.full[b], 1);
+    tcx::fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int b = 0; b < kBufs; ++b) issue(lo + (int64_t)b * kBatch, b);
+  auto flush = [&](int hot) {
+    for (int t = tid; t < kTex; t += kBakeThreads) {
+      const uint32_t n = S.cnt[t];
+      if (n) {
+        atomicAdd(A.cnt + (int64_t)hot * kTex + t, n);
+        unsigned long long* s = A.sum + (int64_t)hot * 4 * kTex + t;
+        atomicAdd(s, ((unsigned long long)S.zhi[t] << 32) + S.zlo[t]);
+        if (has_rgb) {
+          atomicAdd(s + kTex, (unsigned long long)S.c[0][t]);
+          atomicAdd(s + 2 * kTex, (unsigned long long)S.c[1][t]);
+          atomicAdd(s + 3 * kTex, (unsigned long long)S.c[2][t]);
+        }
+      }
+      S.cnt[t] = 0; S.zlo[t] = 0; S.zhi[t] = 0; S.c[0][t] = 0; S.c[1][t] = 0; S.c[2][t] = 0;
+    }
+  };
+  int hot = -1, par = 0, buf = 0;
+  uint32_t phase = 0;
+  for (int64_t base = lo; base < hi; base += kBatch, par ^= 1) {
+    const int64_t i = base + tid;
+    double x = 0.0, y = 0.0, z = 0.0;
+    float cv[3] = {0.f, 0.f, 0.f};
+    if (staged(base)) {
+      tcx::mbar_wait(&S.full[buf], phase);
+      x = S.xyz[buf][3 * tid]; y = S.xyz[buf][3 * tid + 1]; z = S.xyz[buf][3 * tid + 2];
+      if (has_rgb) {
+        cv[0] = S.rgb[buf][3 * tid]; cv[1] = S.rgb[buf][3 * tid + 1]; cv[2] = S.rgb[buf][3 * tid + 2];
+      }
+    } else if (i < hi) {
+      x = A.xyz[3 * i]; y = A.xyz[3 * i + 1]; z = A.xyz[3 * i + 2];
+      if (has_rgb) { cv[0] = A.rgb[3 * i]; cv[1] = A.rgb[3 * i + 1]; cv[2] = A.rgb[3 * i + 2]; }
+    }
+    int miss = 0;
+    int32_t k0 = 0, k1 = 0;
+    if (i < hi && candidates(A, x, y, k0, k1)) {
+      const long long zf = __double2ll_rn(dmul(z, kZScale));
+      int first = -1;
+      for (int32_t k = k0; k < k1; ++k) {
+        int key;
+        const int t = texel_of(A, k, x, y, key);
+        if (t < 0) continue;
+        if (first < 0) first = key;
+        if (key == hot) {
+          atomicAdd(&S.cnt[t], 1u);
+          const uint32_t zl = (uint32_t)zf;
+          const uint32_t old = atomicAdd(&S.zlo[t], zl);
+          atomicAdd(&S.zhi[t], (uint32_t)((unsigned long long)zf >> 32) + (old + zl < old ? 1u : 0u));
+          if (has_rgb) {
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+              const float v = cv[ch];
+              if (v >= 0.f && v < 256.f) {
+                const uint32_t q = __float2uint_rn(v * kCScale);
+                const uint32_t o = atomicAdd(&S.c[ch][t], q);
+                if (o + q < o)  // carry out of the 32-bit shared sum
+                  atomicAdd(A.sum + ((int64_t)key * 4 + ch + 1) * kTex + t, 1ull << 32);
+              } else {
+                atomicAdd(A.sum + ((int64_t)key * 4 + ch + 1) * kTex + t,
+                          (unsigned long long)__double2ll_rn((double)v * (double)kCScale));
+              }
+            }
+          }
+        } else {
+          miss = 1;
+          unsigned long long* gs = A.sum + (int64_t)key * 4 * kTex + t;
+          atomicAdd(A.cnt + (int64_t)key * kTex + t, 1u);
+          atomicAdd(gs, (unsigned long long)zf);
+          if (has_rgb)
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch)
+              atomicAdd(gs + (ch + 1) * kTex,
+                        (unsigned long long)__double2ll_rn((double)cv[ch] * (double)kCScale));
+        }
+      }
+      if (i == min(hi, base + kBatch) - 1) S.last_key[par] = first;
+    } else if (i < hi && i == min(hi, base + kBatch) - 1) {
+      S.last_key[par] = -1;
+    }
+    // every thread is done with this buffer: refill it kBufs batches ahead;
+    // switch the hot patch when most of the batch missed it (grouped input:
+    // once per patch)
+    const int nmiss = __syncthreads_count(miss);
+    if (tid == 0) issue(base + (int64_t)kBufs * kBatch, buf);
+    if (++buf == kBufs) { buf = 0; phase ^= 1; }
+    if (nmiss * 2 > kBakeThreads) {
+      const int next = S.last_key[par];
+      if (next >= 0 && next != hot) {  // block-uniform
+        if (hot >= 0) flush(hot);
+        hot = next;
+        __syncthreads();
       }
     }
   }
+  __syncthreads();
+  if (hot >= 0) flush(hot);
 }
 
 __global__ void __launch_bounds__(256)
-bake_finalize_kernel(const uint32_t* __restrict__ cnt, const double* __restrict__ sum,
+bake_finalize_kernel(const uint32_t* __restrict__ cnt, const unsigned long long* __restrict__ sum,
                      int n_patches, const float* __restrict__ prior_h,
                      const double* __restrict__ base_cz, const double* __restrict__ key_cz,
                      const float* __restrict__ prior_rgb, int has_pts_rgb,
@@ -75,16 +264,17 @@ bake_finalize_kernel(const uint32_t* __restrict__ cnt, const double* __restrict_
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = i / kTex, t = i - p * kTex;
     const uint32_t n = cnt[i];
-    const double* s = sum + p * 4 * kTex + t;
+    const unsigned long long* s = sum + p * 4 * kTex + t;
     double h;
-    if (n > 0) h = ddiv(s[0], (double)n);
+    if (n > 0) h = ddiv(dmul((double)(long long)s[0], kZInv), (double)n);
     else h = dadd((double)prior_h[i], base_cz[p]);
     out_h[i] = __double2float_rn(dsub(h, key_cz[p]));
     if (prior_rgb && out_rgb) {
       if (n > 0 && has_pts_rgb) {
-        out_rgb[3 * i] = __double2float_rn(ddiv(s[kTex], (double)n));
-        out_rgb[3 * i + 1] = __double2float_rn(ddiv(s[2 * kTex], (double)n));
-        out_rgb[3 * i + 2] = __double2float_rn(ddiv(s[3 * kTex], (double)n));
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          out_rgb[3 * i + c] = __double2float_rn(
+              ddiv(dmul((double)(long long)s[(c + 1) * kTex], kCInv), (double)n));
       } else {
         out_rgb[3 * i] = prior_rgb[3 * i];
         out_rgb[3 * i + 1] = prior_rgb[3 * i + 1];
@@ -101,27 +291,38 @@ using namespace ts;
 
 extern "C" size_t ts_bake_workspace(int n_patches) {
   const size_t p = n_patches > 0 ? (size_t)n_patches : 1;
-  return p * kTex * (sizeof(uint32_t) + 4 * sizeof(double)) + 256;
+  return p * kTex * (sizeof(uint32_t) + 4 * sizeof(unsigned long long)) + 256;
 }
 
 extern "C" int ts_bake(const double* d_xyz, const float* d_rgb, int64_t m,
                        const ts_patch_key* d_keys, int n_patches,
                        const int32_t* d_cell_keys_off, const int32_t* d_cell_keys,
-                       double gx0, double gy0, int gnx, int gny,
+                       const int32_t* d_cell_inner, double gx0, double gy0, int gnx, int gny,
                        const float* d_prior_h, const double* d_base_cz,
                        const double* d_key_cz, const float* d_prior_rgb,
                        float* d_out_h, float* d_out_rgb, void* d_accum, void* stream) {
   if (n_patches <= 0) return TS_OK;
   if (gnx <= 0 || gny <= 0 || m < 0) return TS_E_INVALID;
   cudaStream_t s = as_stream(stream);
-  double* sum = reinterpret_cast<double*>(d_accum);
+  unsigned long long* sum = reinterpret_cast<unsigned long long*>(d_accum);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(sum + (size_t)n_patches * 4 * kTex);
   TS_CUDA_TRY(cudaMemsetAsync(d_accum, 0, ts_bake_workspace(n_patches) - 256, s));
   if (m > 0) {
+    const int bulk = ((uintptr_t)d_xyz % 16 == 0) && ((uintptr_t)d_rgb % 16 == 0);
     BakeArgs a{d_xyz, d_rgb, m, d_keys, n_patches, d_cell_keys_off, d_cell_keys,
-               gx0, gy0, gnx, gny, cnt, sum};
-    const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(m, 256), 148 * 16);
-    ts::count_launch(), bake_splat_kernel<<<grid, 256, 0, s>>>(a);
+               d_cell_inner, gx0, gy0, gnx, gny, bulk, cnt, sum};
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      TS_CUDA_TRY(cudaGetDevice(&dev));
+      TS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      TS_CUDA_TRY(cudaFuncSetAttribute(bake_splat_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(HotSmem)));
+    }
+    // one CTA per SM, whole batches per CTA
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, ceil_div<int64_t>(m, kBatch)));
+    ts::count_launch(), bake_splat_kernel<<<grid, kBakeThreads, sizeof(HotSmem), s>>>(a);
     TS_LAUNCH_CHECK();
   }
   const int64_t total = (int64_t)n_patches * kTex;

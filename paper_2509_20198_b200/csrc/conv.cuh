@@ -43,7 +43,18 @@ struct ConvOp {
   int batch;
   const uint8_t* w_tc;  // tensor-core packed weights (conv_tc.cu), or null
   int w_layout;         // layout of w_tc: 0 regular, 1 halo (128 B rows), 2 halo2
+  // phase form of "nearest x2 upsample -> 3x3 stride-1 pad-1 conv" (halo2
+  // kernel only): ph = 1 runs output phase (ph_y, ph_x) as a 2x2 conv over
+  // the low-resolution input, rows/cols offset by ph - 1 (pad 1 - ph), the
+  // window [oy0,oy1) x [ox0,ox1) in low-resolution coordinates and output
+  // pixel (2*oy + ph_y, 2*ox + ph_x) of op.out.
+  int ph, ph_y, ph_x;
 };
+
+// Tap set of the phase form: low-resolution tap t (0 or 1) of output phase
+// p collects the 3x3 taps k with (p + k - 1) >> 1 == p + t - 1, i.e.
+// p=0: t0 <- {0}, t1 <- {1, 2};  p=1: t0 <- {0, 1}, t1 <- {2}.
+inline bool phase_tap(int p, int t, int k) { return ((p + k + 1) >> 1) == p + t; }
 
 inline uint16_t f2bf16_rn_host(float x) {
   uint32_t u;

@@ -222,6 +222,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
     // The whole warp walks the loop (uniform registers), one elected lane
     // issues; descriptors are integer offsets from precomputed bases.
     const uint32_t idesc = make_idesc(Md::tf32 ? 2u : 1u, NST * BN);
+    const uint32_t idesc_b0 = make_idesc(1u, BN);
+    (void)idesc_b0;
     const uint64_t d_smem = sw128_desc(su32(smem));
     const uint32_t pa = (BM * kRowBytes) >> 4, pb = (BN * kRowBytes) >> 4;
     int s = 0, lt = 0;
@@ -248,8 +250,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
             } else if (MODE == 2) {
               umma<false>(d, ak, bk, idesc, first);
             } else if (MODE == 4) {
-              umma<false>(d, ak + pa, bk, idesc, first);  // small plane first
-              umma<false>(d, ak, bk, idesc, 1u);
+              // a0 . [b0 | b1] (N = 2 BN), then a1 . b0 (N = BN): the
+              // a1 . b1 term (<= 2^-18 |ab|, the size of the split
+              // residual) is dropped
+              umma<false>(d, ak, bk, idesc, first);
+              umma<false>(d, ak + pa, bk, idesc_b0, 1u);
             } else {
               umma<false>(d, ak + pa, bk + pb, idesc, first);  // small terms first
               umma<false>(d, ak, bk + 2 * pb, idesc, 1u);

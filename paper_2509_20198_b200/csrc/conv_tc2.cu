@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     int hb = 0, lt = 0;
     uint32_t hph = 0;
     constexpr int PPR = kKC / 4;  // float4 pieces per row
+    const int pad_y = op.ph ? 1 - op.ph_y : op.pad, pad_x = op.ph ? 1 - op.ph_x : op.pad;
     for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
       const int64_t mt = tile / T.n_tiles;
       const int64_t j0 = mt * MT;
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
         const int64_t b = pos / img_pos;
         if (b < op.batch) {
           const int r = (int)(pos - b * img_pos);
-          const int iy = op.oy0 - op.pad + r / Wp, ix = op.ox0 - op.pad + r % Wp;
+          const int iy = op.oy0 - pad_y + r / Wp, ix = op.ox0 - pad_x + r % Wp;
           const int sh = op.up2 ? 1 : 0;
           if (iy >= 0 && iy < (op.in.H << sh) && ix >= 0 && ix < (op.in.W << sh))
             off = ((b * op.in.H + (iy >> sh)) * op.in.W + (ix >> sh)) * op.in.cstride +
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     // MACs as one MMA per (A plane, B plane) pair at N = BN, but every
     // 4 KB A read from shared memory now feeds PB*BN columns.
     const uint32_t idesc = make_idesc(1u, PB * BN);
+    const uint32_t idesc_b0 = make_idesc(1u, BN);
     const uint64_t d_halo = sw64_desc(su32(halo));
     const uint64_t d_ring = sw64_desc(su32(bring));
     const uint32_t pa = (uint32_t)plane_a >> 4;
@@ -237,8 +239,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
               for (int u = 0; u < SUB; ++u) {
                 const uint64_t ak = a0 + (uint64_t)(u * (128 * kRow >> 4)) + 2 * k;
                 const uint32_t du = d + u * PB * BN;
-                if (PA == 2) umma<false>(du, ak + pa, bk, idesc, first);  // small plane first
-                umma<false>(du, ak, bk, idesc, PA == 2 ? 1u : first);
+                umma<false>(du, ak, bk, idesc, first);
+                // second A plane against b0 only (N = BN): a1 . b_{p>0}
+                // terms are below the split residual and are dropped
+                if (PA == 2) umma<false>(du, ak + pa, bk, idesc_b0, 1u);
               }
             }
             if (!(T.exp & 1)) umma_commit(bempty + s);
@@ -291,7 +295,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
           const int64_t b = pos / img_pos;
           const int r = (int)(pos - b * img_pos);
           const int y = r / Wp, x = r % Wp;
-          if (y < wy && x < wx) o = op.out.base + act_off(op.out, b, op.oy0 + y, op.ox0 + x);
+          if (y < wy && x < wx) {
+            const int oy = op.ph ? 2 * (op.oy0 + y) + op.ph_y : op.oy0 + y;
+            const int ox = op.ph ? 2 * (op.ox0 + x) + op.ph_x : op.ox0 + x;
+            o = op.out.base + act_off(op.out, b, oy, ox);
+          }
         }
         for (int c = 0; c < BN; c += 16) {
           float v[16];

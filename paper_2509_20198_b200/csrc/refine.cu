@@ -69,7 +69,19 @@ struct ConvLayer {
   // remapped, dexec); s2d_out = this layer writes its output in that layout
   bool s2d_in = false, s2d_out = false;
   LayerDesc dexec;      // executed shape (== d unless s2d_in)
+  // phase form of an up2 + 3x3 layer (conv.cuh ConvOp::ph): four 2x2
+  // convolutions over the low-resolution input, one per output phase
+  bool poly = false;
+  const uint8_t* w_ph[4] = {nullptr, nullptr, nullptr, nullptr};
+  Win ph_win[4];
 };
+
+// low-resolution window of output phase p (0/1) of a high-res window
+inline void phase_window(int lo, int hi, int p, int& a, int& b) {
+  a = (lo - p + 1) >> 1;
+  b = ((hi - 1 - p) >> 1) + 1;
+  if (b < a) b = a;
+}
 
 }  // namespace
 }  // namespace ts
@@ -404,6 +416,34 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
     }
   }
 
+  // nearest-up2 + 3x3 layers (the decoders) run in phase form on the
+  // wide-M halo kernel: 4/9 of the MACs, and the halo is gathered at the
+  // input's own resolution
+  {
+    const char* e = getenv("TS_POLY");
+    const bool poly_ok = (W->precision >= 2 && W->precision <= 4) && !(e && e[0] == '0');
+    for (auto& L : layers) {
+      const LayerDesc& d = L.d;
+      if (!poly_ok || !L.up2 || d.k != 3 || d.s != 1 || d.p != 1 || L.s2d_in || L.s2d_out ||
+          d.ci % 4)
+        continue;
+      bool ok = true;
+      for (int p = 0; p < 4 && ok; ++p) {
+        Win& w = L.ph_win[p];
+        phase_window(L.out_win.y0, L.out_win.y1, p >> 1, w.y0, w.y1);
+        phase_window(L.out_win.x0, L.out_win.x1, p & 1, w.x0, w.x1);
+        ConvOp o{};
+        o.k = 2; o.stride = 1; o.pad = 1; o.up2 = 0; o.ph = 1; o.ph_y = p >> 1; o.ph_x = p & 1;
+        o.oy0 = w.y0; o.oy1 = w.y1; o.ox0 = w.x0; o.ox1 = w.x1;
+        o.in.C = d.ci; o.in.cstride = d.ci; o.out.C = d.co; o.out.cstride = d.co;
+        o.in.H = L.Hin; o.in.W = L.Win_;
+        o.batch = 1;
+        ok = conv_tc_halo2_eligible(o, W->precision);
+      }
+      L.poly = ok;
+    }
+  }
+
   // ---- weights upload + buffer offsets (floats per tile) ----
   size_t off = 0;
   auto alloc = [&](size_t floats) {
@@ -480,7 +520,41 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
                            cudaMemcpyHostToDevice));
     TS_CUDA_TRY(cudaMemcpy(L.b, bi->second.second.data(), Co * sizeof(float),
                            cudaMemcpyHostToDevice));
-    if (W->precision != 0 && dx.ci % 4 == 0) {
+    if (L.poly) {
+      for (int p = 0; p < 4; ++p) {
+        // folded 2x2 weights of phase p: sums of the 3x3 taps each low-res
+        // tap collects (fp64 sums rounded once)
+        const int py = p >> 1, px = p & 1;
+        std::vector<float> w2((size_t)Co * dx.ci * 4);
+        for (int o = 0; o < Co; ++o)
+          for (int ci = 0; ci < dx.ci; ++ci)
+            for (int ty = 0; ty < 2; ++ty)
+              for (int tx = 0; tx < 2; ++tx) {
+                double acc = 0.0;
+                for (int ky = 0; ky < 3; ++ky)
+                  for (int kx = 0; kx < 3; ++kx)
+                    if (phase_tap(py, ty, ky) && phase_tap(px, tx, kx))
+                      acc += src[(((size_t)o * dx.ci + ci) * 3 + ky) * 3 + kx];
+                w2[(((size_t)o * dx.ci + ci) * 2 + ty) * 2 + tx] = (float)acc;
+              }
+        ConvOp shape{};
+        shape.k = 2; shape.stride = 1; shape.pad = 1; shape.ph = 1; shape.ph_y = py;
+        shape.ph_x = px;
+        shape.oy0 = L.ph_win[p].y0; shape.oy1 = L.ph_win[p].y1;
+        shape.ox0 = L.ph_win[p].x0; shape.ox1 = L.ph_win[p].x1;
+        shape.in.C = dx.ci; shape.in.cstride = dx.ci; shape.out.C = Co; shape.out.cstride = Co;
+        shape.in.H = L.Hin; shape.in.W = L.Win_;
+        shape.batch = 1;
+        const std::vector<uint8_t> pk =
+            pack_tc_weights_halo2(w2.data(), Co, dx.ci, 2, W->precision, shape);
+        if (pk.empty()) return TS_E_INVALID;
+        void* dp = nullptr;
+        TS_CUDA_TRY(cudaMalloc(&dp, pk.size()));
+        W->device_allocs.push_back(dp);
+        TS_CUDA_TRY(cudaMemcpy(dp, pk.data(), pk.size(), cudaMemcpyHostToDevice));
+        L.w_ph[p] = reinterpret_cast<const uint8_t*>(dp);
+      }
+    } else if (W->precision != 0 && dx.ci % 4 == 0) {
       ConvOp shape{};
       shape.k = dx.k;
       shape.stride = dx.s;
@@ -674,6 +748,23 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
       op.w_tc = L.w_tc;
       op.w_layout = L.w_layout;
       int st;
+      if (L.poly) {
+        for (int p = 0; p < 4; ++p) {
+          const Win& w = L.ph_win[p];
+          if (w.y1 <= w.y0 || w.x1 <= w.x0) continue;
+          ConvOp q = op;
+          q.k = 2; q.stride = 1; q.pad = 1; q.up2 = 0;
+          q.ph = 1; q.ph_y = p >> 1; q.ph_x = p & 1;
+          q.oy0 = w.y0; q.oy1 = w.y1; q.ox0 = w.x0; q.ox1 = w.x1;
+          q.w_tc = L.w_ph[p]; q.w_layout = 2;
+          st = launch_conv_tc_halo2(q, W->precision, stream);
+          if (st != TS_OK) return st;
+        }
+        prev_base = op.out.base; prev_H = L.Hout; prev_cs = L.out_cstride;
+        prev_coff = L.out_coff; prev_C = L.d.co;
+        prev_stage = L.stage;
+        continue;
+      }
       // thin layers (few input or output channels: an MMA tile would be
       // mostly padding) -> fp32 direct kernel; the rest -> tensor cores (or
       // the fp32 CUDA-core GEMM in precision mode 0)

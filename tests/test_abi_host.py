@@ -128,8 +128,10 @@ def test_key_grid_registers_every_window():
         np.stack(np.meshgrid(np.arange(4) * 640.0 + 320.0,
                              np.arange(3) * 640.0 + 320.0), -1).reshape(-1, 2),
         rng.uniform(-2000, 5000, (10, 2))])
-    off, ids, gx0, gy0, gnx, gny = key_grid(centers)
-    pts = rng.uniform(-3000, 6000, (20000, 2))
+    off, ids, gx0, gy0, gnx, gny, inner = key_grid(centers)
+    pts = np.concatenate([rng.uniform(-3000, 6000, (20000, 2)),
+                          np.round(rng.uniform(0, 2560, (4000, 2)) / 640.0) *
+                          640.0 + rng.uniform(-0.05, 0.05, (4000, 2))])
     for x, y in pts:
         gx = int(np.floor((x - gx0) / 640.0))
         gy = int(np.floor((y - gy0) / 640.0))
@@ -144,3 +146,20 @@ def test_key_grid_registers_every_window():
         c = gy * gnx + gx
         listed = set(ids[off[c]:off[c + 1]].tolist())
         assert set(inside.tolist()) <= listed
+        ox, oy = x - gx0 - 640.0 * gx, y - gy0 - 640.0 * gy
+        if 0.02 <= ox <= 639.98 and 0.02 <= oy <= 639.98:
+            assert set(inside.tolist()) <= set(ids[off[c]:off[c] + inner[c]])
+
+
+def test_key_grid_interior_list_of_a_tiling_is_one_key():
+    """A tiling of keys: every cell's interior list is just its own key."""
+    from paper_2509_20198_b200.engine import key_grid
+    centers = np.stack(np.meshgrid(np.arange(5) * 640.0 + 320.0 + 7e5,
+                                   np.arange(4) * 640.0 + 320.0 + 4e6),
+                       -1).reshape(-1, 2)
+    off, ids, gx0, gy0, gnx, gny, inner = key_grid(centers)
+    for k, (cx, cy) in enumerate(centers):
+        c = int((cy - 320 - gy0) // 640) * gnx + int((cx - 320 - gx0) // 640)
+        assert inner[c] == 1 and ids[off[c]] == k
+        assert off[c + 1] - off[c] == 9 or k in (0, 4, 15, 19) or \
+            off[c + 1] - off[c] == 6
