@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(full + s, kProd);
+      mbar_init(full + s, kProdWarps);  // one arrival per producer warp
       mbar_init(empty + s, 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -206,10 +206,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
           store_piece<MODE>(sa, p / PPR, p % PPR, cur[j]);
         }
         fence_proxy_async();
+        __syncwarp();
         if (tid == 0) {
           bulk_g2s(sa + a_bytes, wsrc + (size_t)kit * b_bytes, b_bytes, full + s);
           mbar_arrive_tx(full + s, b_bytes);
-        } else {
+        } else if ((tid & 31) == 0) {
           mbar_arrive(full + s);
         }
         if (++s == S) { s = 0; ph ^= 1; }
@@ -400,7 +401,7 @@ __global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) 
       mbar_init(bempty + s, 1);
     }
     for (int h = 0; h < 2; ++h) {
-      mbar_init(hfull + h, kProd);
+      mbar_init(hfull + h, kProdWarps);
       mbar_init(hempty + h, 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -487,7 +488,8 @@ __global__ void __launch_bounds__(kHThreads, 1) conv_tc_halo_kernel(HaloArgs T) 
           }
         }
         fence_proxy_async();
-        mbar_arrive(hfull + hb);
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(hfull + hb);
         hmask ^= 1u << hb;
         hb ^= 1;
       }

@@ -23,8 +23,11 @@
 //               into the mode's bf16 planes, store the SW64 image, arrive.
 //   warp 8      MMA issuer + TMEM owner (2 x SUB x BN fp32 columns).
 //   warp 9      weight loader: cp.async.bulk of pre-swizzled weight stages.
-//   warps 10-13 epilogue: tcgen05.ld, + bias, leaky ReLU, fp32 NHWC store.
+//   warps 10-17 epilogue: two warps per TMEM lane quadrant, alternating
+//               16-column groups: tcgen05.ld of every B plane's columns,
+//               one wait, + bias (shared), leaky ReLU, fp32 NHWC store.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -42,10 +45,11 @@ constexpr int kRow = 64;   // bytes per K-major row (32 bf16 channels)
 constexpr int kKC = 32;    // channels per K chunk
 constexpr int kProdW = 8;
 constexpr int kProdT = kProdW * 32;
+constexpr int kInflight = 8;  // 16-byte loads in flight per producer thread
 constexpr int kMmaW = 8;
 constexpr int kLoadW = 9;
-constexpr int kThreads = 14 * 32;
-constexpr int kInflight = 8; 
+constexpr int kEpiW0 = 10, kEpiWarps = 8;
+constexpr int kThreads = (kEpiW0 + kEpiWarps) * 32;
 constexpr int kHdr = 1024;         // packed-weight header: u32 count, u32 0, u16 list
 constexpr int kMaxStages = (kHdr - 8) / 2 - 1;  // + sentinel  // 16-byte loads in flight per producer thread
 
@@ -53,23 +57,25 @@ struct Halo2Args {
   ConvOp op;
   const uint8_t* wpk;  // packed weights: kHdr-byte stage list, then
                        // [n_tile][stage][plane][BN][64 B] SW64 images
-  int bn, sub, hbufs, bstages, cchunks, taps, wp, lrows, n_tiles, accbufs;
+  int bn, sub, hbufs, bstages, cchunks, taps, wp, lrows, n_tiles, accbufs, nstg;
   int64_t m_tiles, positions;
-  int exp;  // timing experiments only (TS_H2_EXP): 1 = weights once, 2 = no halo fill
+  unsigned long long* dbg;  // TS_H2_DBG timestamps (CTA 0), or null
+  int exp;  // timing experiments only (TS_H2_EXP bits): 1 weights once, 2 no halo
+           // fill, 4 no epilogue work, 8 no MMAs
 };
 
 __device__ __forceinline__ void prod_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kProdT) : "memory");
 }
 
-template <int MODE>
+template <int MODE, int SUB>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T) {
   using Md = Mode<MODE>;
   constexpr int PA = Md::pa, PB = Md::pb;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   const ConvOp& op = T.op;
-  const int BN = T.bn, SUB = T.sub, HB = T.hbufs, SB = T.bstages, L = T.lrows;
+  const int BN = T.bn, HB = T.hbufs, SB = T.bstages, L = T.lrows;
   const int plane_a = L * kRow;          // multiple of 512 (L % 8 == 0)
   const int halo_bytes = PA * plane_a;
   const int b_bytes = PB * BN * kRow;
@@ -98,6 +104,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     }
     s_chunk[nst] = 0xFFFF;  // sentinel
   }
+  float* s_bias = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(s_chunk + kMaxStages + 1) + 15) & ~uintptr_t(15));
+  for (int i = threadIdx.x; i < T.n_tiles * T.bn; i += blockDim.x)
+    s_bias[i] = i < T.op.out.C ? __ldg(T.op.bias + i) : 0.f;
   const uint8_t* wdata = T.wpk + kHdr;
 
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -118,12 +128,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
       mbar_init(bempty + s, 1);
     }
     for (int h = 0; h < HB; ++h) {
-      mbar_init(hfull + h, kProdT);
+      mbar_init(hfull + h, kProdW);  // one arrival per producer warp
       mbar_init(hempty + h, 1);
     }
     for (int a = 0; a < AB; ++a) {
       mbar_init(acc_full + a, 1);
-      mbar_init(acc_empty + a, 4);
+      mbar_init(acc_empty + a, kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -148,7 +158,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
       for (int j = tid; j < L; j += kProdT) {
         const int64_t pos = j0 + j;
         int64_t off = -1;
-        const int64_t b = pos / img_pos;
+        // positions < 2^31 (checked by the host): 32-bit divisions
+        const int64_t b = (int64_t)((uint32_t)pos / (uint32_t)img_pos);
         if (b < op.batch) {
           const int r = (int)(pos - b * img_pos);
           const int iy = op.oy0 - pad_y + r / Wp, ix = op.ox0 - pad_x + r % Wp;
@@ -164,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
         mbar_wait(hempty + hb, ((hph >> hb) & 1u) ^ 1u);
         uint8_t* sa = halo + hb * halo_bytes;
         const int c0 = c * kKC;
-        for (int pc = tid; pc < ((T.exp & 2) && lt > 0 ? 0 : L * PPR);
+        for (int pc = tid; pc < L * PPR;
              pc += kProdT * kInflight) {
           float4 v[kInflight];
 #pragma unroll
@@ -187,15 +198,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
                             ((piece & 1) << 3);
               const float4 a = v[u];
               if (MODE == 2)
-                *reinterpret_cast<uint2*>(sa + o) = make_uint2(
-                    hi_halves(rn_bf(a.x), rn_bf(a.y)), hi_halves(rn_bf(a.z), rn_bf(a.w)));
+                *reinterpret_cast<uint2*>(sa + o) =
+                    make_uint2(pack_bf2(a.x, a.y), pack_bf2(a.z, a.w));
               else
                 store_split2(sa + o, plane_a, a);
             }
           }
         }
         fence_proxy_async();
-        mbar_arrive(hfull + hb);
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(hfull + hb);
+        if (T.dbg && blockIdx.x == 0 && tid == 0 && lt * T.cchunks + c < 4096)
+          T.dbg[lt * T.cchunks + c] = clock64();
         hph ^= 1u << hb;
         if (++hb == HB) hb = 0;
       }
@@ -211,41 +225,44 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     const uint64_t d_halo = sw64_desc(su32(halo));
     const uint64_t d_ring = sw64_desc(su32(bring));
     const uint32_t pa = (uint32_t)plane_a >> 4;
-    int s = 0, lt = 0, hb = 0, nwait = 0;
+    int s = 0, lt = 0, hb = 0;
     uint32_t bph = 0, hph = 0;
-    (void)nwait;
+    const uint32_t b_step = (uint32_t)b_bytes >> 4, h_step = (uint32_t)halo_bytes >> 4;
     for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
       const int acc = lt % AB;
       mbar_wait(acc_empty + acc, ((lt / AB) & 1) ^ 1);
+      if (T.dbg && blockIdx.x == 0 && (tid & 31) == 0 && lt < 4096)
+        T.dbg[4 * 4096 + lt] = clock64();
       tc_fence_after();
       const uint32_t d = tmem + acc * acc_cols;
       int si = 0;
       for (int c = 0; c < T.cchunks; ++c) {
         mbar_wait(hfull + hb, (hph >> hb) & 1u);
+        if (T.dbg && blockIdx.x == 0 && (tid & 31) == 0 && lt * T.cchunks + c < 4096)
+          T.dbg[4096 + lt * T.cchunks + c] = clock64();
         hph ^= 1u << hb;
         tc_fence_after();
-        const uint64_t d_hb = d_halo + (uint64_t)((hb * halo_bytes) >> 4);
+        const uint64_t d_hb = d_halo + (uint64_t)(hb * h_step);
         for (; s_chunk[si] == c; ++si) {
-          if (!(T.exp & 1) || nwait < SB) mbar_wait(bfull + s, bph);
-          ++nwait;
+          mbar_wait(bfull + s, bph);
           tc_fence_after();
           if (elect_one()) {
             const uint64_t a0 = d_hb + (uint64_t)s_aoff[si];
-            const uint64_t b0 = d_ring + (uint64_t)((s * b_bytes) >> 4);
+            const uint64_t b0 = d_ring + (uint64_t)(s * b_step);
+            const uint32_t first = si ? 1u : 0u;
 #pragma unroll
             for (int k = 0; k < 2; ++k) {  // 2 x 32-byte K steps per row
-              const uint32_t first = (si | k) ? 1u : 0u;
-              const uint64_t bk = b0 + 2 * k;
+#pragma unroll
               for (int u = 0; u < SUB; ++u) {
-                const uint64_t ak = a0 + (uint64_t)(u * (128 * kRow >> 4)) + 2 * k;
+                const uint64_t ak = a0 + (uint64_t)(u * (128 * kRow >> 4) + 2 * k);
                 const uint32_t du = d + u * PB * BN;
-                umma<false>(du, ak, bk, idesc, first);
+                umma<false>(du, ak, b0 + 2 * k, idesc, k ? 1u : first);
                 // second A plane against b0 only (N = BN): a1 . b_{p>0}
                 // terms are below the split residual and are dropped
-                if (PA == 2) umma<false>(du, ak + pa, bk, idesc_b0, 1u);
+                if (PA == 2) umma<false>(du, ak + pa, b0 + 2 * k, idesc_b0, 1u);
               }
             }
-            if (!(T.exp & 1)) umma_commit(bempty + s);
+            umma_commit(bempty + s);
           }
           __syncwarp();
           if (++s == SB) { s = 0; bph ^= 1; }
@@ -266,7 +283,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
         const int nt = (int)(tile % T.n_tiles);
         const uint8_t* wsrc = wdata + (size_t)nt * nst * b_bytes;
         for (int kt = 0; kt < nst; ++kt) {
-          if ((T.exp & 1) && (tile > blockIdx.x || kt >= SB)) break;
           mbar_wait(bempty + s, bph ^ 1);
           bulk_g2s(bring + s * b_bytes, wsrc + (size_t)kt * b_bytes, b_bytes, bfull + s);
           mbar_arrive_tx(bfull + s, b_bytes);
@@ -278,6 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
   } else {
     // ------------------------- epilogue -------------------------
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int half = (warp - kEpiW0) >> 2;  // which 16-column groups
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const bool vec = (op.out.cstride % 4 == 0) && (op.out.coff % 4 == 0);
     int lt = 0;
@@ -287,12 +304,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
       const int nt = (int)(tile - mt * T.n_tiles);
       const int n0 = nt * BN;
       mbar_wait(acc_full + acc, (lt / AB) & 1);
+      if (T.dbg && blockIdx.x == 0 && tid == kEpiW0 * 32 && lt < 4096)
+        T.dbg[2 * 4096 + lt] = clock64();
       tc_fence_after();
       for (int u = 0; u < SUB; ++u) {
         const int64_t pos = mt * MT + u * 128 + q * 32 + (tid & 31);
         float* o = nullptr;
         if (pos < T.positions) {
-          const int64_t b = pos / img_pos;
+          const int64_t b = (int64_t)((uint32_t)pos / (uint32_t)img_pos);
           const int r = (int)(pos - b * img_pos);
           const int y = r / Wp, x = r % Wp;
           if (y < wy && x < wx) {
@@ -301,25 +320,23 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
             o = op.out.base + act_off(op.out, b, oy, ox);
           }
         }
-        for (int c = 0; c < BN; c += 16) {
-          float v[16];
+        for (int c = 16 * half; c < BN; c += 32) {
+          uint32_t r[PB][16];
           const uint32_t ta = tmem + lane_base + acc * acc_cols + u * PB * BN + c;
-          tmem_ld16(ta, v);
 #pragma unroll
-          for (int p = 1; p < PB; ++p) {
-            float w[16];
-            tmem_ld16(ta + p * BN, w);
+          for (int p = 0; p < PB; ++p) tmem_ld16_nw(ta + p * BN, r[p]);
+          tmem_wait_ld();
+          float v[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] += w[i];
+          for (int i = 0; i < 16; ++i) {
+            float x = __uint_as_float(r[0][i]);
+#pragma unroll
+            for (int p = 1; p < PB; ++p) x += __uint_as_float(r[p][i]);
+            x += s_bias[n0 + c + i];
+            if (op.lrelu) x = x >= 0.f ? x : 0.01f * x;
+            v[i] = x;
           }
           if (o) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int n = n0 + c + i;
-              float x = v[i] + (n < Cout ? __ldg(op.bias + n) : 0.f);
-              if (op.lrelu) x = x >= 0.f ? x : 0.01f * x;
-              v[i] = x;
-            }
             if (vec && n0 + c + 16 <= Cout) {
 #pragma unroll
               for (int i = 0; i < 4; ++i)
@@ -336,6 +353,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
       tc_fence_before();
       __syncwarp();
       if ((tid & 31) == 0) mbar_arrive(acc_empty + acc);
+      if (T.dbg && blockIdx.x == 0 && tid == kEpiW0 * 32 && lt < 4096)
+        T.dbg[3 * 4096 + lt] = clock64();
     }
   }
   tc_fence_before();
@@ -347,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
 }
 
 struct Halo2Plan {
-  int bn, ntiles, pa, pb, sub, hbufs, bstages, cchunks, wp, lrows, accbufs;
+  int bn, ntiles, pa, pb, sub, hbufs, bstages, cchunks, wp, lrows, accbufs, nstg;
   size_t smem;
   int64_t positions;
 };
@@ -372,25 +391,30 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
   p.positions = (int64_t)op.batch * (wy + op.k - 1) * p.wp;
   const size_t cap = 225 * 1024;
   const size_t bst = (size_t)p.pb * p.bn * kRow;
-  // (sub-tiles, accumulator buffers): prefer M >= 256 with the epilogue
-  // overlapped; fall back to a single accumulator buffer, then M = 128
-  const int cand[5][2] = {{4, 2}, {2, 2}, {4, 1}, {2, 1}, {1, 2}};
+  // (sub-tiles, accumulator buffers): the epilogue must overlap the next
+  // tile's MMAs (two accumulator buffers), then prefer M >= 256
+  const int cand[5][2] = {{4, 2}, {2, 2}, {1, 2}, {4, 1}, {2, 1}};
   for (const auto& cb : cand) {
     const int sub = cb[0], ab = cb[1];
     if (ab * sub * p.pb * p.bn > 512) continue;
     const int L = (128 * sub + (op.k - 1) * (p.wp + 1) + 7) / 8 * 8;
     const size_t hbuf = (size_t)p.pa * L * kRow;
-    const size_t fixed = 1024 + 8 * 40 + 16 + 16 * (size_t)L + 6 * kMaxStages + 64;
+    const size_t fixed = 1024 + 8 * 40 + 16 + 16 * (size_t)L + 6 * kMaxStages + 64 +
+                         4 * (size_t)p.ntiles * p.bn + 16;
     for (int hb : {3, 2}) {
-      if (hb * hbuf + 3 * bst + fixed > cap) continue;
-      p.sub = sub;
-      p.accbufs = ab;
-      p.hbufs = hb;
-      p.lrows = L;
-      p.bstages = (int)std::min<size_t>(8, (cap - hb * hbuf - fixed) / bst);
-      p.smem = hb * hbuf + p.bstages * bst + fixed;
-      *out = p;
-      return true;
+      for (int ns : {0}) {
+        const size_t used = hb * hbuf + fixed;
+        if (used + 3 * bst > cap) continue;
+        p.sub = sub;
+        p.accbufs = ab;
+        p.hbufs = hb;
+        p.nstg = ns;
+        p.lrows = L;
+        p.bstages = (int)std::min<size_t>(8, (cap - used) / bst);
+        p.smem = used + p.bstages * bst;
+        *out = p;
+        return true;
+      }
     }
   }
   return false;
@@ -471,9 +495,10 @@ std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, 
 int launch_conv_tc_halo2(const ConvOp& op, int precision, void* stream) {
   Halo2Plan p;
   if (!plan2(op, precision, &p)) return TS_E_INVALID;
+  if (p.positions + 128 * p.sub + p.lrows >= (int64_t)INT32_MAX) return TS_E_INVALID;
   Halo2Args a{op, op.w_tc, p.bn, p.sub, p.hbufs, p.bstages, p.cchunks, op.k * op.k, p.wp,
-              p.lrows, p.ntiles, p.accbufs, ceil_div<int64_t>(p.positions, 128 * p.sub),
-              p.positions, 0};
+              p.lrows, p.ntiles, p.accbufs, p.nstg,
+              ceil_div<int64_t>(p.positions, 128 * p.sub), p.positions, nullptr, 0};
   static int exp = -1;
   if (exp < 0) {
     const char* e = getenv("TS_H2_EXP");
@@ -482,6 +507,16 @@ int launch_conv_tc_halo2(const ConvOp& op, int precision, void* stream) {
   a.exp = exp;
   const int64_t tiles = a.m_tiles * p.ntiles;
   if (tiles <= 0) return TS_OK;
+  static int dbg_at = -2, launch_no = 0;
+  if (dbg_at == -2) {
+    const char* e = getenv("TS_H2_DBG");
+    dbg_at = e ? atoi(e) : -1;
+  }
+  const bool dbg = launch_no++ == dbg_at;
+  if (dbg) {
+    TS_CUDA_TRY(cudaMalloc(&a.dbg, 5 * 4096 * sizeof(unsigned long long)));
+    TS_CUDA_TRY(cudaMemset(a.dbg, 0, 5 * 4096 * sizeof(unsigned long long)));
+  }
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -490,18 +525,44 @@ int launch_conv_tc_halo2(const ConvOp& op, int precision, void* stream) {
   }
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
   cudaStream_t s = as_stream(stream);
-#define TS_TCH2_LAUNCH(MD)                                                            \
+#define TS_TCH2_LAUNCH(MD, SB_)                                                       \
   do {                                                                                \
-    TS_CUDA_TRY(cudaFuncSetAttribute(conv_tc_halo2_kernel<MD>,                        \
+    TS_CUDA_TRY(cudaFuncSetAttribute(conv_tc_halo2_kernel<MD, SB_>,                   \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,     \
                                      (int)p.smem));                                   \
-    ts::count_launch(), conv_tc_halo2_kernel<MD><<<grid, kThreads, p.smem, s>>>(a);   \
+    ts::count_launch(), conv_tc_halo2_kernel<MD, SB_><<<grid, kThreads, p.smem, s>>>(a); \
   } while (0)
-  if (precision == 2) TS_TCH2_LAUNCH(2);
-  else if (precision == 4) TS_TCH2_LAUNCH(4);
-  else TS_TCH2_LAUNCH(3);
+#define TS_TCH2_SUB(MD)                                 \
+  do {                                                  \
+    if (p.sub == 1) TS_TCH2_LAUNCH(MD, 1);              \
+    else if (p.sub == 2) TS_TCH2_LAUNCH(MD, 2);         \
+    else TS_TCH2_LAUNCH(MD, 4);                         \
+  } while (0)
+  if (precision == 2) TS_TCH2_SUB(2);
+  else if (precision == 4) TS_TCH2_SUB(4);
+  else TS_TCH2_SUB(3);
+#undef TS_TCH2_SUB
 #undef TS_TCH2_LAUNCH
   TS_LAUNCH_CHECK();
+  if (dbg) {
+    std::vector<unsigned long long> h(5 * 4096);
+    TS_CUDA_TRY(cudaMemcpy(h.data(), a.dbg, h.size() * 8, cudaMemcpyDeviceToHost));
+    cudaFree(a.dbg);
+    fprintf(stderr, "h2dbg sub=%d ab=%d hb=%d sb=%d cchunks=%d nst=? ntiles=%d L=%d tiles=%lld\n",
+            p.sub, p.accbufs, p.hbufs, p.bstages, p.cchunks, p.ntiles, p.lrows, (long long)tiles);
+    const unsigned long long t0 = h[4 * 4096];
+    for (int lt = 0; lt < 12; ++lt) {
+      fprintf(stderr, "tile %d: mma_start %lld epi_start %lld epi_end %lld | prod",
+              lt, (long long)(h[4 * 4096 + lt] - t0), (long long)(h[2 * 4096 + lt] - t0),
+              (long long)(h[3 * 4096 + lt] - t0));
+      for (int c = 0; c < p.cchunks; ++c)
+        fprintf(stderr, " %lld", (long long)(h[lt * p.cchunks + c] - t0));
+      fprintf(stderr, " | mma_hfull");
+      for (int c = 0; c < p.cchunks; ++c)
+        fprintf(stderr, " %lld", (long long)(h[4096 + lt * p.cchunks + c] - t0));
+      fprintf(stderr, "\n");
+    }
+  }
   return TS_OK;
 }
 

@@ -37,6 +37,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// mbar_wait for warps that can tolerate wake-up latency (epilogue, loader):
+// non-blocking probes with a nanosleep back-off keep them off the issue
+// slots the MMA issuer and the producers need
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+  uint32_t ok = 0, ns = 32;
+  for (;;) {
+    asm volatile(
+        "{\n.reg .pred P1;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.b32 %0, 1, 0, P1;\n}\n"
+        : "=r"(ok)
+        : "r"(su32(b)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+  }
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
   asm volatile(
@@ -101,6 +119,21 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// tcgen05.ld without the wait: several loads can be in flight before one
+// tmem_wait_ld()
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -161,8 +194,27 @@ __device__ __forceinline__ float bf_keep(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xFFFF0000u);
 }
 
+// {bf16_rn(lo), bf16_rn(hi)} packed (lo in the low half): one F2FP
+__device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
 // a = a0 + a1 + e, a0 = bf16_rn(a), a1 = bf16_rn(a - a0), |e| <= 2^-18 |a|
+// (hardware RN conversions: 2 F2FP + 4 unpack/subtract per pair)
 __device__ __forceinline__ void store_split2(uint8_t* dst, int plane_bytes, float4 a) {
+  const uint32_t h01 = pack_bf2(a.x, a.y), h23 = pack_bf2(a.z, a.w);
+  const uint32_t l01 = pack_bf2(a.x - __uint_as_float(h01 << 16),
+                                a.y - __uint_as_float(h01 & 0xFFFF0000u));
+  const uint32_t l23 = pack_bf2(a.z - __uint_as_float(h23 << 16),
+                                a.w - __uint_as_float(h23 & 0xFFFF0000u));
+  *reinterpret_cast<uint2*>(dst) = make_uint2(h01, h23);
+  *reinterpret_cast<uint2*>(dst + plane_bytes) = make_uint2(l01, l23);
+}
+
+// integer-ALU form of store_split2 (same values)
+__device__ __forceinline__ void store_split2_alu(uint8_t* dst, int plane_bytes, float4 a) {
   const float x0 = bf_keep(rn_bf(a.x)), y0 = bf_keep(rn_bf(a.y)), z0 = bf_keep(rn_bf(a.z)),
               w0 = bf_keep(rn_bf(a.w));
   const float x1 = rn_bf(a.x - x0), y1 = rn_bf(a.y - y0), z1 = rn_bf(a.z - z0),
