@@ -70,6 +70,20 @@ inline float bf16_to_f_host(uint16_t h) {
   return f;
 }
 
+// The four encoders' first layers (3x3 stride 2 pad 1 over 1/1/3/3 raw
+// input channels) in one launch; outputs in space-to-depth layout.
+struct Enc0Op {
+  const float* in;          // B x H x W x 8 fp32 CNN input
+  int H, W, batch;
+  int ch0[4], cin[4], lrelu[4];
+  const float* w[4];        // [9 * cin][C_out] packed like ConvOp::w
+  const float* bias[4];
+  ActView out[4];           // s2d views
+  int oy0, oy1, ox0, ox1;   // common output window
+};
+bool conv_enc0_supported(const Enc0Op& e, int co);
+int launch_conv_enc0(const Enc0Op& e, int co, void* stream);
+
 int launch_conv_simt(const ConvOp& op, void* stream);
 bool conv_direct_supported(const ConvOp& op);
 int launch_conv_direct(const ConvOp& op, void* stream);

@@ -1,0 +1,163 @@
+// K3c: the four encoders' first layers in one launch (refiner.py:399-441,
+// stages enc_hm_nn / enc_hm_lin / enc_rgb_nn / enc_rgb_lin, layer 0:
+// 3x3 stride-2 pad-1 convolutions of 1, 1, 3, 3 raw input channels).
+//
+// The four layers read disjoint channels of the same B x 96 x 96 x 8 CNN
+// input, so one CTA stages the input halo of a 4 x 16 output tile ONCE for
+// all of them (the per-layer direct kernel read it four times) and its 16
+// warps split as 4 encoders x 2 row pairs.  fp32 CUDA-core FMAs (thin K: 9
+// or 27 MACs per output channel), outputs written straight into the
+// space-to-depth layout the stride-2 tensor-core layers consume (a pixel's
+// C_out channels are one contiguous run there: float4 stores).  Two
+// 256-thread CTAs per SM so one CTA's halo load overlaps the other's FMAs.
+//
+// Shared memory: halo [8 ch][9 rows][2 column parities][20] (stride-2
+// reads become stride-1 per parity plane: bank-conflict free), weights
+// [K][C_out] per encoder.
+#include <algorithm>
+
+#include "conv.cuh"
+#include "ts_common.cuh"
+
+namespace ts {
+namespace {
+
+constexpr int kETY = 4, kETX = 16;          // output tile
+constexpr int kEHY = 2 * kETY + 1;          // 9 halo rows
+constexpr int kEPitch = 20;                 // floats per parity row (>= 17; 4*pitch = 16 mod 32)
+constexpr int kEPlane = kEHY * 2 * kEPitch; // floats per channel
+constexpr int kEThreads = 256;  // 4 encoders x 2 row pairs; 2 CTAs per SM
+
+__device__ __forceinline__ float lrelu(float v) { return v >= 0.f ? v : 0.01f * v; }
+
+template <int CIN, int CO>
+__device__ __forceinline__ void enc0_accumulate(const float* __restrict__ halo, int ch0,
+                                                const float* __restrict__ w, int ty, int tx,
+                                                float* acc) {
+#pragma unroll
+  for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+    for (int kx = 0; kx < 3; ++kx) {
+      // input column 2 tx + kx lives in parity plane kx & 1 at index tx + kx / 2
+      const float* hp = halo + (2 * ty + ky) * 2 * kEPitch + (kx & 1) * kEPitch + tx + (kx >> 1);
+#pragma unroll
+      for (int ci = 0; ci < CIN; ++ci) {
+        const float x = hp[(ch0 + ci) * kEPlane];
+        const float4* w4 = reinterpret_cast<const float4*>(w + ((ky * 3 + kx) * CIN + ci) * CO);
+#pragma unroll
+        for (int o = 0; o < CO / 4; ++o) {
+          const float4 q = w4[o];
+          acc[4 * o] = fmaf(x, q.x, acc[4 * o]);
+          acc[4 * o + 1] = fmaf(x, q.y, acc[4 * o + 1]);
+          acc[4 * o + 2] = fmaf(x, q.z, acc[4 * o + 2]);
+          acc[4 * o + 3] = fmaf(x, q.w, acc[4 * o + 3]);
+        }
+      }
+    }
+}
+
+template <int CO>
+__global__ void __launch_bounds__(kEThreads, 2) conv_enc0_kernel(Enc0Op E) {
+  extern __shared__ __align__(16) float sm[];
+  float* halo = sm;                                   // 8 * kEPlane
+  float* sw = halo + 8 * kEPlane;                     // weights, 4 encoders
+  int woff[4];
+  {
+    int o = 0;
+    for (int e = 0; e < 4; ++e) { woff[e] = o; o += 9 * E.cin[e] * CO; }
+    for (int e = 0; e < 4; ++e)
+      for (int i = threadIdx.x; i < 9 * E.cin[e] * CO; i += kEThreads) sw[woff[e] + i] = E.w[e][i];
+    o = (o + 3) & ~3;
+    for (int i = threadIdx.x; i < 4 * CO; i += kEThreads) sw[o + i] = E.bias[i / CO][i % CO];
+  }
+  const float* sbias = sw + ((woff[3] + 9 * E.cin[3] * CO + 3) & ~3);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int e = warp & 3;                             // encoder of this warp
+  const int ty = 2 * (warp >> 2) + (lane >> 4), tx = lane & 15;
+  const int wy = E.oy1 - E.oy0, wx = E.ox1 - E.ox0;
+  const int ntx = (wx + kETX - 1) / kETX, nty = (wy + kETY - 1) / kETY;
+  const int64_t tiles = (int64_t)E.batch * nty * ntx;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t b = tile / (nty * ntx);
+    const int r = (int)(tile - b * nty * ntx);
+    const int y0 = E.oy0 + (r / ntx) * kETY, x0 = E.ox0 + (r % ntx) * kETX;
+    __syncthreads();  // previous tile's halo reads done
+    // halo: input rows 2 y0 - 1 .. + 16, columns 2 x0 - 1 .. + 32, 8 channels
+    const float* inb = E.in + b * (int64_t)E.H * E.W * 8;
+    for (int i = threadIdx.x; i < kEHY * 33 * 2; i += kEThreads) {
+      const int hy = i / 66, rem = i - hy * 66, hx = rem >> 1, half = rem & 1;
+      const int iy = 2 * y0 - 1 + hy, ix = 2 * x0 - 1 + hx;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (iy >= 0 && iy < E.H && ix >= 0 && ix < E.W)
+        v = __ldg(reinterpret_cast<const float4*>(inb + ((int64_t)iy * E.W + ix) * 8) + half);
+      float* d = halo + hy * 2 * kEPitch + (hx & 1) * kEPitch + (hx >> 1) + 4 * half * kEPlane;
+      d[0] = v.x; d[kEPlane] = v.y; d[2 * kEPlane] = v.z; d[3 * kEPlane] = v.w;
+    }
+    __syncthreads();
+    float acc[CO];
+#pragma unroll
+    for (int o = 0; o < CO; ++o) acc[o] = sbias[e * CO + o];
+    if (E.cin[e] == 1) enc0_accumulate<1, CO>(halo, E.ch0[e], sw + woff[e], ty, tx, acc);
+    else enc0_accumulate<3, CO>(halo, E.ch0[e], sw + woff[e], ty, tx, acc);
+    // space-to-depth store: the pixel's C_out channels are contiguous
+    const int y = y0 + ty, x = x0 + tx;
+    if (y < E.oy1 && x < E.ox1) {
+      float4* o4 = reinterpret_cast<float4*>(E.out[e].base + act_off(E.out[e], b, y, x));
+#pragma unroll
+      for (int o = 0; o < CO / 4; ++o) {
+        float4 v = make_float4(acc[4 * o], acc[4 * o + 1], acc[4 * o + 2], acc[4 * o + 3]);
+        if (E.lrelu[e]) { v.x = lrelu(v.x); v.y = lrelu(v.y); v.z = lrelu(v.z); v.w = lrelu(v.w); }
+        o4[o] = v;
+      }
+    }
+  }
+}
+
+size_t enc0_smem(const Enc0Op& E, int co) {
+  int k = 0;
+  for (int e = 0; e < 4; ++e) k += 9 * E.cin[e] * co;
+  return sizeof(float) * ((size_t)8 * kEPlane + ((k + 3) & ~3) + 4 * co);
+}
+
+}  // namespace
+
+bool conv_enc0_supported(const Enc0Op& E, int co) {
+  if (co != 48 && co != 32 && co != 64) return false;
+  for (int e = 0; e < 4; ++e) {
+    if (E.cin[e] != 1 && E.cin[e] != 3) return false;
+    if (E.ch0[e] < 0 || E.ch0[e] + E.cin[e] > 8) return false;
+  }
+  if ((E.oy0 | E.ox0) & 1) return false;  // space-to-depth pairs
+  return enc0_smem(E, co) <= 220 * 1024;
+}
+
+int launch_conv_enc0(const Enc0Op& E, int co, void* stream) {
+  if (!conv_enc0_supported(E, co)) return TS_E_INVALID;
+  if (E.batch <= 0 || E.oy1 <= E.oy0 || E.ox1 <= E.ox0) return TS_OK;
+  const size_t smem = enc0_smem(E, co);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    TS_CUDA_TRY(cudaGetDevice(&dev));
+    TS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int64_t tiles = (int64_t)E.batch * ((E.oy1 - E.oy0 + kETY - 1) / kETY) *
+                        ((E.ox1 - E.ox0 + kETX - 1) / kETX);
+  const int grid = (int)std::min<int64_t>(tiles, 2 * sms);
+  cudaStream_t s = as_stream(stream);
+#define TS_ENC0(CO)                                                                    \
+  do {                                                                                 \
+    TS_CUDA_TRY(cudaFuncSetAttribute(conv_enc0_kernel<CO>,                             \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                                     (int)smem));                                      \
+    ts::count_launch(), conv_enc0_kernel<CO><<<grid, kEThreads, smem, s>>>(E);         \
+  } while (0)
+  if (co == 48) TS_ENC0(48);
+  else if (co == 32) TS_ENC0(32);
+  else TS_ENC0(64);
+#undef TS_ENC0
+  TS_LAUNCH_CHECK();
+  return TS_OK;
+}
+
+}  // namespace ts

@@ -95,6 +95,7 @@ struct ts_weights {
   int enc_out_c = 0, dec_h_c = 0, dec_c_c = 0, fuse_in_c = 0;
   int enc_hw = 0;
   size_t cat_off = 0, fuse_in_off = 0;
+  bool enc0_fused = false;  // the four encoders' first layers in one launch
   std::vector<void*> device_allocs;
 };
 
@@ -444,6 +445,29 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
     }
   }
 
+  // the four first encoder layers share one input read (conv_enc0.cu)
+  {
+    const char* e = getenv("TS_ENC0");
+    bool ok = !(e && e[0] == '0') && W->precision >= 2 && W->precision <= 4;
+    const ConvLayer* f[4];
+    for (int st = 0; st < 4 && ok; ++st) {
+      f[st] = &layers[stage_first[st]];
+      const ConvLayer& L = *f[st];
+      ok = L.d.k == 3 && L.d.s == 2 && L.d.p == 1 && !L.up2 && L.s2d_out && !L.s2d_in &&
+           L.Hin == kRes && L.d.co == f[0]->d.co && L.out_win.y0 == f[0]->out_win.y0 &&
+           L.out_win.y1 == f[0]->out_win.y1 && L.out_win.x0 == f[0]->out_win.x0 &&
+           L.out_win.x1 == f[0]->out_win.x1;
+    }
+    if (ok) {
+      Enc0Op probe{};
+      const int ch0[4] = {0, 1, 2, 5}, cin[4] = {1, 1, 3, 3};
+      for (int st = 0; st < 4; ++st) { probe.ch0[st] = ch0[st]; probe.cin[st] = cin[st]; }
+      probe.oy0 = f[0]->out_win.y0; probe.ox0 = f[0]->out_win.x0;
+      ok = conv_enc0_supported(probe, f[0]->d.co);
+    }
+    W->enc0_fused = ok;
+  }
+
   // ---- weights upload + buffer offsets (floats per tile) ----
   size_t off = 0;
   auto alloc = [&](size_t floats) {
@@ -748,6 +772,28 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
       op.w_tc = L.w_tc;
       op.w_layout = L.w_layout;
       int st;
+      if (W->enc0_fused && L.stage < 4 && L.index == 0) {
+        if (L.stage == 0) {
+          Enc0Op E{};
+          E.in = in; E.H = kRes; E.W = kRes; E.batch = B;
+          int e = 0;
+          for (size_t j = 0; j < W->layers.size() && e < 4; ++j) {
+            const ConvLayer& F = W->layers[j];
+            if (F.stage != e || F.index != 0) continue;
+            E.ch0[e] = enc_ch0[e]; E.cin[e] = enc_cin[e]; E.lrelu[e] = F.d.lrelu;
+            E.w[e] = F.w; E.bias[e] = F.b;
+            E.out[e] = ActView{buf(F.out_off), F.Hout, F.Wout, 4 * F.d.co, 0, F.d.co, 1};
+            ++e;
+          }
+          E.oy0 = L.out_win.y0; E.oy1 = L.out_win.y1; E.ox0 = L.out_win.x0; E.ox1 = L.out_win.x1;
+          st = launch_conv_enc0(E, L.d.co, stream);
+          if (st != TS_OK) return st;
+        }
+        prev_base = buf(L.out_off); prev_H = L.Hout; prev_cs = L.out_cstride;
+        prev_coff = L.out_coff; prev_C = L.d.co;
+        prev_stage = L.stage;
+        continue;
+      }
       if (L.poly) {
         for (int p = 0; p < 4; ++p) {
           const Win& w = L.ph_win[p];
@@ -768,7 +814,11 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
       // thin layers (few input or output channels: an MMA tile would be
       // mostly padding) -> fp32 direct kernel; the rest -> tensor cores (or
       // the fp32 CUDA-core GEMM in precision mode 0)
-      if (conv_direct_supported(op) &&
+      // (thin outputs with a wide input, e.g. fuse.2 32 -> 4, stay on the
+      // wide-M halo kernel: N = 16 columns per plane, K = 9 x 32)
+      const bool thin_tc = op.out.C <= 16 && op.in.C > 4 && L.w_tc && L.w_layout == 2 &&
+                           !op.out.s2d;
+      if (conv_direct_supported(op) && !thin_tc &&
           (op.in.C <= 4 || op.out.C <= 16 || W->precision == 0))
         st = launch_conv_direct(op, stream);
       else if (L.w_tc && conv_tc_supported(op, W->precision))
