@@ -53,7 +53,19 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=32)
     ap.add_argument("--no-cpu", action="store_true",
                     help="skip the cpu_baseline leg (profiling runs)")
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip the configs[4] CNN batch sweep")
     return ap.parse_args()
+
+
+def ncu_traffic():
+    """DRAM bytes per step of the CNN launches / per splat launch from the
+    committed ncu capture of this command (profiles/r01_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fp:
+            return json.load(fp)
+    except (OSError, ValueError):
+        return {}
 
 
 def peaks():
@@ -278,15 +290,27 @@ def run_ours(args, rank, world, local_rank):
                           "gather_delaunay_raster":
                               round(float(np.mean(t_ras)), 4),
                           "cnn_refine": round(ref_ms, 4)},
-            "roofline": {"kernel": "CNN refine (ts_refine, all conv layers)",
+            "roofline": {"kernel": "CNN refine (ts_refine: every conv "
+                                   "launch + epilogue of one step)",
                          "bound": "tensor",
                          "achieved": round(cnn_tflops, 3),
                          "peak": tflops, "unit": "TFLOP/s",
                          "frac": round(cnn_tflops / tflops, 5),
                          "peak_kind": f"{peak_kind} bf16 dense (burst)",
-                         "algorithmic": f"{CROP_GFLOP} GFLOP/tile x {P} "
-                                        "tiles per launch sequence",
-                         "traffic": None},
+                         "algorithmic": f"{CROP_GFLOP} GFLOP/tile (fp32 "
+                                        f"MACs x2, crop-aware) x {P} tiles",
+                         "note": "fp32-class mode issues 3 bf16 products "
+                                 "per MAC (a0.b0 + a0.b1 + a1.b0): its "
+                                 "tensor ceiling is peak/3; decoders run "
+                                 "in phase form (4/9 of the reference "
+                                 "MACs), counted at the reference's MACs",
+                         "frac_of_emulated_peak": round(
+                             3 * cnn_tflops / tflops, 5),
+                         "traffic": ncu_traffic().get(
+                             "cnn_dram_bytes_per_step"),
+                         "traffic_unit": "DRAM bytes per step (ncu "
+                                         "launch list, "
+                                         "profiles/r01_traffic.json)"},
             "e2e": {"value": round(e2e_value, 2), "unit": "heightmaps/s",
                     "h2d_bytes_per_step": int(host_bytes.numel()),
                     "d2h_bytes_per_step": int(out_host.numel() * 4)},
@@ -297,6 +321,9 @@ def run_ours(args, rank, world, local_rank):
         splat = run_splat(args, dev, world, rank)
         if rank == 0:
             result["splat"] = splat
+    if not args.no_sweep and rank == 0:
+        result["cnn_sweep"] = cnn_sweep(bundle, cnn_in_of(pipe, tb, centers,
+                                                          cell_range), dev)
     if rank == 0:
         result["clocks"] = clocks.summary()
         result["cpu_baseline"] = None if args.no_cpu else cpu_baseline(args)
@@ -304,6 +331,54 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def cnn_in_of(pipe, tb, centers, cell_range):
+    _t, _cp, idx = pipe.overview(tb, cell_range)
+    _g, _t2, _o, cnn_in = pipe.patches(idx, centers)
+    return cnn_in
+
+
+def cnn_sweep(bundle, cnn_in, dev, batches=(64, 1024, 16384)):
+    """configs[4]: CNN refine alone over batches of the configs[1] rasters
+    (repeated), fp32-class (bf16x3 products) vs plain bf16, CUDA events."""
+    import torch
+    from paper_2509_20198_b200.refiner import (PRECISION_BF16,
+                                               PRECISION_BF16X4,
+                                               device_weights)
+    hbm, tflops, _kind = peaks()
+    rows = []
+    src = cnn_in
+    for prec, name in ((PRECISION_BF16X4, "fp32-class (3 bf16 products)"),
+                       (PRECISION_BF16, "bf16")):
+        w = device_weights(bundle, prec)
+        for B in batches:
+            reps = (B + len(src) - 1) // len(src)
+            x = src.repeat(reps, 1, 1, 1)[:B].contiguous()
+            out = torch.empty((B, 64, 64, 4), dtype=torch.float32, device=dev)
+            nf = torch.zeros(B, dtype=torch.uint8, device=dev)
+            ws = w.workspace(B)
+            w.run(x, B, out, nf, ws)
+            torch.cuda.synchronize()
+            n = 3 if B >= 4096 else 5
+            s, e = torch.cuda.Event(enable_timing=True), \
+                torch.cuda.Event(enable_timing=True)
+            s.record()
+            for _ in range(n):
+                w.run(x, B, out, nf, ws)
+            e.record()
+            torch.cuda.synchronize()
+            ms = s.elapsed_time(e) / n
+            tf = CROP_GFLOP * B / (ms / 1e3) / 1e3
+            rows.append({"precision": name, "batch": B,
+                         "ms": round(ms, 3),
+                         "tiles_per_s": round(B / (ms / 1e3), 1),
+                         "tflops_alg": round(tf, 2),
+                         "frac_bf16_peak": round(tf / tflops, 4)})
+            del x, out, nf, ws
+    return {"config": "configs[4]: CNN refine batch sweep on configs[1] "
+                      "rasters (inputs resident, no L2 flush)",
+            "rows": rows}
 
 
 def terrain_torch(x, y, terrain):
@@ -381,7 +456,8 @@ def run_splat(args, dev, world, rank):
             "config": f"configs[2]: {M:,} points into {P} heightmaps per GPU,"
                       " points grouped by patch",
             "ms_per_step": round(ms, 4),
-            "roofline": {"kernel": "ts_bake (splat + finalize)",
+            "roofline": {"kernel": "ts_bake (accumulator clear + splat + "
+                                   "finalize)",
                          "bound": "hbm", "achieved": round(gbs, 1),
                          "peak": hbm, "unit": "GB/s",
                          "frac": round(gbs / hbm, 4),
@@ -389,7 +465,11 @@ def run_splat(args, dev, world, rank):
                          "algorithmic": "36 B/pt (xyz f64 + rgb f32) + "
                                         "32 B/texel (prior h,rgb in; h,rgb "
                                         "out)",
-                         "traffic": None}}
+                         "traffic": ncu_traffic().get(
+                             "bake_dram_bytes_per_launch"),
+                         "traffic_unit": "DRAM bytes, splat + finalize "
+                                         "launches (ncu, "
+                                         "profiles/r01_traffic.json)"}}
 
 
 # ------------------------------------------------------------ CPU legs
