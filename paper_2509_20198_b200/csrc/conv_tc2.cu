@@ -58,6 +58,8 @@ struct Halo2Args {
   const uint8_t* wpk;  // packed weights: kHdr-byte stage list, then
                        // [n_tile][stage][plane][BN][64 B] SW64 images
   int bn, sub, hbufs, bstages, cchunks, taps, wp, lrows, n_tiles, accbufs, nstg;
+  int stack;  // 1: B planes stacked along N (PB*BN columns per sub-tile);
+              // 0: every product accumulates into the same BN columns
   int64_t m_tiles, positions;
   unsigned long long* dbg;  // TS_H2_DBG timestamps (CTA 0), or null
   int exp;  // timing experiments only (TS_H2_EXP bits): 1 weights once, 2 no halo
@@ -118,7 +120,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
   const int MT = SUB * 128;
   const int64_t total_tiles = T.m_tiles * T.n_tiles;
   const int AB = T.accbufs;
-  const int acc_cols = SUB * PB * BN;  // per accumulator buffer
+  const int PBS = T.stack ? PB : 1;     // accumulator column blocks per sub
+  const int acc_cols = SUB * PBS * BN;  // per accumulator buffer
   uint32_t ncols = 32;
   while ((int)ncols < AB * acc_cols) ncols <<= 1;
 
@@ -228,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     int s = 0, lt = 0, hb = 0;
     uint32_t bph = 0, hph = 0;
     const uint32_t b_step = (uint32_t)b_bytes >> 4, h_step = (uint32_t)halo_bytes >> 4;
+    const uint32_t b_plane16 = (uint32_t)(BN * kRow) >> 4;  // one B plane
     for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
       const int acc = lt % AB;
       mbar_wait(acc_empty + acc, ((lt / AB) & 1) ^ 1);
@@ -255,8 +259,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
 #pragma unroll
               for (int u = 0; u < SUB; ++u) {
                 const uint64_t ak = a0 + (uint64_t)(u * (128 * kRow >> 4) + 2 * k);
-                const uint32_t du = d + u * PB * BN;
-                umma<false>(du, ak, b0 + 2 * k, idesc, k ? 1u : first);
+                const uint32_t du = d + u * PBS * BN;
+                if (T.stack) {
+                  umma<false>(du, ak, b0 + 2 * k, idesc, k ? 1u : first);
+                } else {  // a0 . b_p for every plane into the same columns
+                  umma<false>(du, ak, b0 + 2 * k, idesc_b0, k ? 1u : first);
+#pragma unroll
+                  for (int q = 1; q < PB; ++q)
+                    umma<false>(du, ak, b0 + (uint64_t)(q * b_plane16) + 2 * k, idesc_b0, 1u);
+                }
                 // second A plane against b0 only (N = BN): a1 . b_{p>0}
                 // terms are below the split residual and are dropped
                 if (PA == 2) umma<false>(du, ak + pa, b0 + 2 * k, idesc_b0, 1u);
@@ -322,16 +333,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
         }
         for (int c = 16 * half; c < BN; c += 32) {
           uint32_t r[PB][16];
-          const uint32_t ta = tmem + lane_base + acc * acc_cols + u * PB * BN + c;
+          const uint32_t ta = tmem + lane_base + acc * acc_cols + u * PBS * BN + c;
 #pragma unroll
-          for (int p = 0; p < PB; ++p) tmem_ld16_nw(ta + p * BN, r[p]);
+          for (int p = 0; p < PB; ++p)
+            if (p < PBS) tmem_ld16_nw(ta + p * BN, r[p]);
           tmem_wait_ld();
           float v[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             float x = __uint_as_float(r[0][i]);
 #pragma unroll
-            for (int p = 1; p < PB; ++p) x += __uint_as_float(r[p][i]);
+            for (int p = 1; p < PB; ++p)
+              if (p < PBS) x += __uint_as_float(r[p][i]);
             x += s_bias[n0 + c + i];
             if (op.lrelu) x = x >= 0.f ? x : 0.01f * x;
             v[i] = x;
@@ -366,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
 }
 
 struct Halo2Plan {
-  int bn, ntiles, pa, pb, sub, hbufs, bstages, cchunks, wp, lrows, accbufs, nstg;
+  int bn, ntiles, pa, pb, sub, hbufs, bstages, cchunks, wp, lrows, accbufs, nstg, stack;
   size_t smem;
   int64_t positions;
 };
@@ -376,7 +389,10 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
   // stride-1 k >= 2 (incl. the 2x2 space-to-depth form of stride-2 layers);
   // 1x1 layers stay on the regular kernel (no halo to reuse, and their
   // multi-N-tile shapes re-read A per N tile here)
-  if (op.stride != 1 || op.k < 2 || op.pad < 0 || op.pad >= op.k) return false;
+  if (op.stride != 1 || op.k < 1 || op.pad < 0 || op.pad >= op.k) return false;
+  // 1x1 layers: measured slower than the regular kernel (A re-read per N
+  // tile); opt in with TS_H2_1X1=1
+  if (op.k == 1 && !(getenv("TS_H2_1X1") && getenv("TS_H2_1X1")[0] == '1')) return false;
   if (op.in.C % 4 || op.in.cstride % 4 || op.in.coff % 4) return false;
   Halo2Plan p{};
   p.pa = precision == 2 ? 1 : 2;
@@ -384,7 +400,6 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
   const int n16 = (op.out.C + 15) / 16 * 16;
   p.ntiles = (n16 + 127) / 128;
   p.bn = ((n16 + p.ntiles - 1) / p.ntiles + 15) / 16 * 16;
-  if (p.pb * p.bn > 256) return false;  // MMA N limit with stacked planes
   p.cchunks = (op.in.C + kKC - 1) / kKC;
   const int wx = op.ox1 - op.ox0, wy = op.oy1 - op.oy0;
   p.wp = wx + op.k - 1;
@@ -393,10 +408,19 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
   const size_t bst = (size_t)p.pb * p.bn * kRow;
   // (sub-tiles, accumulator buffers): the epilogue must overlap the next
   // tile's MMAs (two accumulator buffers), then prefer M >= 256
+  // B planes stacked along N feed one MMA per A plane (fewer, wider MMAs)
+  // unless that forces single 128-row sub-tiles (BN > 64), where the MMA
+  // issue loop, not the tensor pipe, would set the pace
+  {
+    const char* e = getenv("TS_H2_STACK");
+    p.stack = e ? (e[0] == '1') : (p.pb * p.bn <= 128);
+    if (p.pb * p.bn > 256) p.stack = 0;  // MMA N limit
+  }
+  const int cols = p.stack ? p.pb * p.bn : p.bn;
   const int cand[5][2] = {{4, 2}, {2, 2}, {1, 2}, {4, 1}, {2, 1}};
   for (const auto& cb : cand) {
     const int sub = cb[0], ab = cb[1];
-    if (ab * sub * p.pb * p.bn > 512) continue;
+    if (ab * sub * cols > 512) continue;
     const int L = (128 * sub + (op.k - 1) * (p.wp + 1) + 7) / 8 * 8;
     const size_t hbuf = (size_t)p.pa * L * kRow;
     const size_t fixed = 1024 + 8 * 40 + 16 + 16 * (size_t)L + 6 * kMaxStages + 64 +
@@ -497,7 +521,7 @@ int launch_conv_tc_halo2(const ConvOp& op, int precision, void* stream) {
   if (!plan2(op, precision, &p)) return TS_E_INVALID;
   if (p.positions + 128 * p.sub + p.lrows >= (int64_t)INT32_MAX) return TS_E_INVALID;
   Halo2Args a{op, op.w_tc, p.bn, p.sub, p.hbufs, p.bstages, p.cchunks, op.k * op.k, p.wp,
-              p.lrows, p.ntiles, p.accbufs, p.nstg,
+              p.lrows, p.ntiles, p.accbufs, p.nstg, p.stack,
               ceil_div<int64_t>(p.positions, 128 * p.sub), p.positions, nullptr, 0};
   static int exp = -1;
   if (exp < 0) {

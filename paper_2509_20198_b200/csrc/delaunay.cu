@@ -18,12 +18,14 @@
 namespace ts {
 namespace {
 
-constexpr int kMaxCavity = 512;
+constexpr int kMaxCavity = 256;
 // Patches up to kSmemPoints keep their whole mesh (triangles + circumcircle
 // cache, SoA) in shared memory: every insertion rewrites a few slots and the
 // next one re-reads them, so a global-memory mesh turns each step into a
 // chain of L1-miss latencies.  Larger patches spill to the caller's scratch.
-constexpr int kSmemPoints = 512;
+// 384 points (~31 KB per warp) lets 7 patch-warps share an SM, so the
+// 1,024 patches of a configs[1] batch (N ~ 310-340) run in ONE wave.
+constexpr int kSmemPoints = 384;
 constexpr int kSmemSlots = 2 * kSmemPoints + 8;
 constexpr size_t kDelaunaySmem = (size_t)kSmemSlots * (3 * sizeof(int) + 3 * sizeof(double)) +
                                  kMaxCavity * sizeof(int) + (kMaxCavity + 8) * sizeof(int2);
