@@ -44,8 +44,8 @@ PROV_BAKED = "fullres-baked"
 PRECISION_FP32 = 0      # CUDA-core fp32 implicit GEMM
 PRECISION_TF32X3 = 1    # tcgen05 kind::tf32, 3-pass split (fp32-accurate)
 PRECISION_BF16 = 2      # tcgen05 kind::f16 (bf16 operands, fp32 accumulate)
-PRECISION_BF16X3 = 3    # tcgen05 kind::f16, A 2 RN planes x B 3 exact planes (5 MMAs)
-PRECISION_BF16X4 = 4    # tcgen05 kind::f16, A and B 2 RN planes each (4 MMAs)
+PRECISION_BF16X3 = 3    # tcgen05 kind::f16, A 2 RN planes, B 3 exact planes (a0.b* + a1.b0)
+PRECISION_BF16X4 = 4    # tcgen05 kind::f16, A, B 2 RN planes: a0.b0 + a0.b1 + a1.b0
 
 
 @dataclass
