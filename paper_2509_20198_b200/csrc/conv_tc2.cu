@@ -177,34 +177,39 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
       for (int c = 0; c < T.cchunks; ++c) {
         mbar_wait(hempty + hb, ((hph >> hb) & 1u) ^ 1u);
         uint8_t* sa = halo + hb * halo_bytes;
-        const int c0 = c * kKC;
-        for (int pc = tid; pc < L * PPR;
-             pc += kProdT * kInflight) {
+        // each thread owns one 16-byte piece column (kProdT % 8 == 0): its
+        // channel, validity and swizzled byte offset within a row are fixed,
+        // and rows advance by kProdT / 8 = 32 (the swizzle phase repeats)
+        const int piece = tid & 7;
+        const int ch = c * kKC + 4 * piece;
+        const bool ch_ok = ch < Cin;
+        const float* src = op.in.base + ch;
+        const int row0 = tid >> 3;
+        const int obase = row0 * kRow + (((piece >> 1) ^ ((row0 >> 1) & 3)) << 4) +
+                          ((piece & 1) << 3);
+        constexpr int kRowStep = kProdT / PPR;  // 32 rows per pass
+        for (int r0 = row0; r0 < L; r0 += kRowStep * kInflight) {
           float4 v[kInflight];
 #pragma unroll
           for (int u = 0; u < kInflight; ++u) {
-            const int q = pc + u * kProdT;
+            const int row = r0 + u * kRowStep;
             v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (q < L * PPR) {
-              const int64_t off = ro[q >> 3];
-              const int ch = c0 + 4 * (q & 7);
-              if (off >= 0 && ch < Cin)
-                v[u] = __ldg(reinterpret_cast<const float4*>(op.in.base + off + ch));
+            if (row < L) {
+              const int64_t off = ro[row];
+              if (off >= 0 && ch_ok) v[u] = __ldg(reinterpret_cast<const float4*>(src + off));
             }
           }
+          uint8_t* so = sa + obase + (r0 - row0) * kRow;
 #pragma unroll
           for (int u = 0; u < kInflight; ++u) {
-            const int q = pc + u * kProdT;
-            if (q < L * PPR) {
-              const int row = q >> 3, piece = q & 7;
-              const int o = row * kRow + (((piece >> 1) ^ ((row >> 1) & 3)) << 4) +
-                            ((piece & 1) << 3);
+            if (r0 + u * kRowStep < L) {
               const float4 a = v[u];
+              uint8_t* d = so + u * kRowStep * kRow;
               if (MODE == 2)
-                *reinterpret_cast<uint2*>(sa + o) =
+                *reinterpret_cast<uint2*>(d) =
                     make_uint2(pack_bf2(a.x, a.y), pack_bf2(a.z, a.w));
               else
-                store_split2(sa + o, plane_a, a);
+                store_split2(d, plane_a, a);
             }
           }
         }

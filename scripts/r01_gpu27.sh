@@ -1,0 +1,7 @@
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests27.log 2>&1; echo "pytest exit $?"
+tail -3 gpurun_out/gpu_tests27.log
+timeout 300 python scripts/precision_check.py 2>&1 | grep "mode [234]"
+timeout 600 python bench.py --no-cpu --no-splat --no-sweep --steps 5 > gpurun_out/bench27.json 2> gpurun_out/bench27.err; echo "bench exit $?"
+python -c "import json; d=json.load(open('gpurun_out/bench27.json')); print(d['value'], d['stages_ms'], d['gpu_launches'])"
+source <(sed -n '/^run()/,/^}/p' scripts/r01_gpu15.sh)
+run "0" x
