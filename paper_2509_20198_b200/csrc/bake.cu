@@ -18,9 +18,10 @@
 // against the reference's sequential fp64 bincount sums that is a mean
 // difference <= 2e-9 m in height and <= 3e-8 in colour.
 //
-// One persistent CTA per SM walks a contiguous range of whole 1,024-point
-// batches, staged into shared memory three batches ahead by cp.async.bulk
-// (mbarrier complete_tx).  The CTA's shared memory also holds the
+// One persistent CTA per SM walks a contiguous range of whole 2,048-point
+// batches (two points per thread); positions are staged into shared memory
+// one batch ahead by cp.async.bulk (mbarrier complete_tx), colours are read
+// directly (coalesced) before the wait.  The CTA's shared memory also holds the
 // accumulators of ONE "hot" patch (count, z as lo/hi 32-bit words with the
 // lo carry folded into hi, r/g/b u32 = 24 B x 4096 texels = 96 KB);
 // (point, key) pairs of the hot patch accumulate there with native 32-bit
@@ -42,9 +43,10 @@ namespace ts {
 namespace {
 
 constexpr int kTex = kOut * kOut;  // 4096 texels per patch
-constexpr int kBakeThreads = 1024;  // one CTA per SM, one point per thread per batch
-constexpr int kBatch = kBakeThreads;
-constexpr int kBufs = 3;            // staged batches in flight
+constexpr int kBakeThreads = 1024;  // one CTA per SM
+constexpr int kBakeU = 2;            // points per thread per batch
+constexpr int kBatch = kBakeU * kBakeThreads;
+constexpr int kBufs = 2;             // staged xyz batches (48 KB each)
 constexpr double kZScale = 268435456.0;          // 2^28
 constexpr double kZInv = 1.0 / 268435456.0;
 constexpr float kCScale = 16777216.0f;            // 2^24
@@ -116,8 +118,7 @@ struct HotSmem {
   // hot-patch accumulators: count, z fixed point as lo/hi 32-bit words
   // (the lo word's carry goes into the hi word), colour sums
   uint32_t cnt[kTex], zlo[kTex], zhi[kTex], c[3][kTex];
-  double xyz[kBufs][kBatch * 3];  // staged points (bulk copies)
-  float rgb[kBufs][kBatch * 3];
+  double xyz[kBufs][kBatch * 3];  // staged positions (bulk copies)
   uint64_t full[kBufs];
   int last_key[2];  // by batch parity (a fast thread may write the next one)
 };
@@ -141,11 +142,10 @@ __global__ void __launch_bounds__(kBakeThreads, 1) bake_splat_kernel(BakeArgs A)
   auto staged = [&](int64_t base) { return A.bulk && base + kBatch <= hi; };
   auto issue = [&](int64_t base, int buf) {
     if (base < hi && staged(base)) {
-      const uint32_t bx = kBatch * 3 * sizeof(double), bc = kBatch * 3 * sizeof(float);
+      const uint32_t bx = kBatch * 3 * sizeof(double);
       tcx::fence_proxy_async();
-      tcx::mbar_arrive_tx(&S.full[buf], bx + (has_rgb ? bc : 0));
+      tcx::mbar_arrive_tx(&S.full[buf], bx);
       tcx::bulk_g2s(S.xyz[buf], A.xyz + 3 * base, bx, &S.full[buf]);
-      if (has_rgb) tcx::bulk_g2s(S.rgb[buf], A.rgb + 3 * base, bc, &S.full[buf]);
     }
   };
   if (tid == 0) {
@@ -175,69 +175,78 @@ __global__ void __launch_bounds__(kBakeThreads, 1) bake_splat_kernel(BakeArgs A)
   int hot = -1, par = 0, buf = 0;
   uint32_t phase = 0;
   for (int64_t base = lo; base < hi; base += kBatch, par ^= 1) {
-    const int64_t i = base + tid;
-    double x = 0.0, y = 0.0, z = 0.0;
-    float cv[3] = {0.f, 0.f, 0.f};
-    if (staged(base)) {
-      tcx::mbar_wait(&S.full[buf], phase);
-      x = S.xyz[buf][3 * tid]; y = S.xyz[buf][3 * tid + 1]; z = S.xyz[buf][3 * tid + 2];
-      if (has_rgb) {
-        cv[0] = S.rgb[buf][3 * tid]; cv[1] = S.rgb[buf][3 * tid + 1]; cv[2] = S.rgb[buf][3 * tid + 2];
-      }
-    } else if (i < hi) {
-      x = A.xyz[3 * i]; y = A.xyz[3 * i + 1]; z = A.xyz[3 * i + 2];
-      if (has_rgb) { cv[0] = A.rgb[3 * i]; cv[1] = A.rgb[3 * i + 1]; cv[2] = A.rgb[3 * i + 2]; }
-    }
-    int miss = 0;
-    int32_t k0 = 0, k1 = 0;
-    if (i < hi && candidates(A, x, y, k0, k1)) {
-      const long long zf = __double2ll_rn(dmul(z, kZScale));
-      int first = -1;
-      for (int32_t k = k0; k < k1; ++k) {
-        int key;
-        const int t = texel_of(A, k, x, y, key);
-        if (t < 0) continue;
-        if (first < 0) first = key;
-        if (key == hot) {
-          atomicAdd(&S.cnt[t], 1u);
-          const uint32_t zl = (uint32_t)zf;
-          const uint32_t old = atomicAdd(&S.zlo[t], zl);
-          atomicAdd(&S.zhi[t], (uint32_t)((unsigned long long)zf >> 32) + (old + zl < old ? 1u : 0u));
-          if (has_rgb) {
+    const int64_t last = min(hi, base + kBatch) - 1;
+    // colours straight from global (coalesced 12-byte runs), issued before
+    // the staged positions are waited for
+    float cv[kBakeU][3];
 #pragma unroll
-            for (int ch = 0; ch < 3; ++ch) {
-              const float v = cv[ch];
-              if (v >= 0.f && v < 256.f) {
-                const uint32_t q = __float2uint_rn(v * kCScale);
-                const uint32_t o = atomicAdd(&S.c[ch][t], q);
-                if (o + q < o)  // carry out of the 32-bit shared sum
-                  atomicAdd(A.sum + ((int64_t)key * 4 + ch + 1) * kTex + t, 1ull << 32);
-              } else {
-                atomicAdd(A.sum + ((int64_t)key * 4 + ch + 1) * kTex + t,
-                          (unsigned long long)__double2ll_rn((double)v * (double)kCScale));
+    for (int u = 0; u < kBakeU; ++u) {
+      const int64_t i = base + u * kBakeThreads + tid;
+      cv[u][0] = cv[u][1] = cv[u][2] = 0.f;
+      if (has_rgb && i < hi) {
+        cv[u][0] = __ldg(A.rgb + 3 * i); cv[u][1] = __ldg(A.rgb + 3 * i + 1);
+        cv[u][2] = __ldg(A.rgb + 3 * i + 2);
+      }
+    }
+    const bool stg = staged(base);
+    if (stg) tcx::mbar_wait(&S.full[buf], phase);
+    int miss = 0;
+#pragma unroll
+    for (int u = 0; u < kBakeU; ++u) {
+      const int j = u * kBakeThreads + tid;
+      const int64_t i = base + j;
+      if (i >= hi) continue;
+      double x, y, z;
+      if (stg) { x = S.xyz[buf][3 * j]; y = S.xyz[buf][3 * j + 1]; z = S.xyz[buf][3 * j + 2]; }
+      else { x = A.xyz[3 * i]; y = A.xyz[3 * i + 1]; z = A.xyz[3 * i + 2]; }
+      int32_t k0 = 0, k1 = 0;
+      int first = -1;
+      if (candidates(A, x, y, k0, k1)) {
+        const long long zf = __double2ll_rn(dmul(z, kZScale));
+        for (int32_t k = k0; k < k1; ++k) {
+          int key;
+          const int t = texel_of(A, k, x, y, key);
+          if (t < 0) continue;
+          if (first < 0) first = key;
+          if (key == hot) {
+            atomicAdd(&S.cnt[t], 1u);
+            const uint32_t zl = (uint32_t)zf;
+            const uint32_t old = atomicAdd(&S.zlo[t], zl);
+            atomicAdd(&S.zhi[t], (uint32_t)((unsigned long long)zf >> 32) + (old + zl < old ? 1u : 0u));
+            if (has_rgb) {
+#pragma unroll
+              for (int ch = 0; ch < 3; ++ch) {
+                const float v = cv[u][ch];
+                if (v >= 0.f && v < 256.f) {
+                  const uint32_t q = __float2uint_rn(v * kCScale);
+                  const uint32_t o = atomicAdd(&S.c[ch][t], q);
+                  if (o + q < o)  // carry out of the 32-bit shared sum
+                    atomicAdd(A.sum + ((int64_t)key * 4 + ch + 1) * kTex + t, 1ull << 32);
+                } else {
+                  atomicAdd(A.sum + ((int64_t)key * 4 + ch + 1) * kTex + t,
+                            (unsigned long long)__double2ll_rn((double)v * (double)kCScale));
+                }
               }
             }
-          }
-        } else {
-          miss = 1;
-          unsigned long long* gs = A.sum + (int64_t)key * 4 * kTex + t;
-          atomicAdd(A.cnt + (int64_t)key * kTex + t, 1u);
-          atomicAdd(gs, (unsigned long long)zf);
-          if (has_rgb)
+          } else {
+            ++miss;
+            unsigned long long* gs = A.sum + (int64_t)key * 4 * kTex + t;
+            atomicAdd(A.cnt + (int64_t)key * kTex + t, 1u);
+            atomicAdd(gs, (unsigned long long)zf);
+            if (has_rgb)
 #pragma unroll
-            for (int ch = 0; ch < 3; ++ch)
-              atomicAdd(gs + (ch + 1) * kTex,
-                        (unsigned long long)__double2ll_rn((double)cv[ch] * (double)kCScale));
+              for (int ch = 0; ch < 3; ++ch)
+                atomicAdd(gs + (ch + 1) * kTex,
+                          (unsigned long long)__double2ll_rn((double)cv[u][ch] * (double)kCScale));
+          }
         }
       }
-      if (i == min(hi, base + kBatch) - 1) S.last_key[par] = first;
-    } else if (i < hi && i == min(hi, base + kBatch) - 1) {
-      S.last_key[par] = -1;
+      if (i == last) S.last_key[par] = first;
     }
     // every thread is done with this buffer: refill it kBufs batches ahead;
     // switch the hot patch when most of the batch missed it (grouped input:
     // once per patch)
-    const int nmiss = __syncthreads_count(miss);
+    const int nmiss = __syncthreads_count(2 * miss > kBakeU);
     if (tid == 0) issue(base + (int64_t)kBufs * kBatch, buf);
     if (++buf == kBufs) { buf = 0; phase ^= 1; }
     if (nmiss * 2 > kBakeThreads) {

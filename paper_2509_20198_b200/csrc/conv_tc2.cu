@@ -43,12 +43,16 @@ using namespace tcx;
 
 constexpr int kRow = 64;   // bytes per K-major row (32 bf16 channels)
 constexpr int kKC = 32;    // channels per K chunk
-constexpr int kProdW = 8;
+#ifndef TS_H2_PRODW
+#define TS_H2_PRODW 12
+#endif
+constexpr int kProdW = TS_H2_PRODW;
 constexpr int kProdT = kProdW * 32;
 constexpr int kInflight = 8;  // 16-byte loads in flight per producer thread
-constexpr int kMmaW = 8;
-constexpr int kLoadW = 9;
-constexpr int kEpiW0 = 10, kEpiWarps = 8;
+constexpr int kMmaW = kProdW;
+constexpr int kLoadW = kProdW + 1;
+constexpr int kEpiW0 = kProdW + 2, kEpiWarps = 8;
+static_assert(kProdW % 2 == 0, "row stride must keep the swizzle phase");
 constexpr int kThreads = (kEpiW0 + kEpiWarps) * 32;
 constexpr int kHdr = 1024;         // packed-weight header: u32 count, u32 0, u16 list
 constexpr int kMaxStages = (kHdr - 8) / 2 - 1;  // + sentinel  // 16-byte loads in flight per producer thread
@@ -187,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
         const int row0 = tid >> 3;
         const int obase = row0 * kRow + (((piece >> 1) ^ ((row0 >> 1) & 3)) << 4) +
                           ((piece & 1) << 3);
-        constexpr int kRowStep = kProdT / PPR;  // 32 rows per pass
+        constexpr int kRowStep = kProdT / PPR;  // rows per pass (multiple of 8)
         for (int r0 = row0; r0 < L; r0 += kRowStep * kInflight) {
           float4 v[kInflight];
 #pragma unroll
@@ -413,12 +417,13 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
   const size_t bst = (size_t)p.pb * p.bn * kRow;
   // (sub-tiles, accumulator buffers): the epilogue must overlap the next
   // tile's MMAs (two accumulator buffers), then prefer M >= 256
-  // B planes stacked along N feed one MMA per A plane (fewer, wider MMAs)
-  // unless that forces single 128-row sub-tiles (BN > 64), where the MMA
-  // issue loop, not the tensor pipe, would set the pace
+  // B planes stacked along N feed one MMA per A plane (fewer, wider MMAs);
+  // measured better only for thin N (BN <= 32).  Wider layers accumulate
+  // every product into the same BN columns, which doubles the sub-tiles
+  // per TMEM buffer and amortises the MMA issuer's per-stage overhead.
   {
     const char* e = getenv("TS_H2_STACK");
-    p.stack = e ? (e[0] == '1') : (p.pb * p.bn <= 128);
+    p.stack = e ? (e[0] == '1') : (p.pb * p.bn <= 64);
     if (p.pb * p.bn > 256) p.stack = 0;  // MMA N limit
   }
   const int cols = p.stack ? p.pb * p.bn : p.bn;
