@@ -16,16 +16,35 @@ namespace ts {
 // (b, y, x, c) of the logical H x W x C image lives at half-resolution pixel
 // (y/2, x/2), channel ((y&1)*2 + (x&1))*C + c; cstride is then the physical
 // pixel stride (>= 4C).
+//
+// planes = 1: pre-split storage for tensor-core consumers.  Same bytes per
+// element as fp32: in the pixel block of cstride fp32 slots, bytes
+// [2c, 2c+2) hold hi(c) = bf16_rn(v) and bytes [2 cstride + 2c, ...) hold
+// lo(c) = bf16_rn(v - hi), the split the tensor-core producers would
+// otherwise compute per halo row (so results are bit-identical).
 struct ActView {
   float* base;
   int H, W, cstride, coff, C;
   int s2d;
+  int planes;
 };
 
 __host__ __device__ inline int64_t act_off(const ActView& v, int64_t b, int y, int x) {
   if (!v.s2d) return ((b * v.H + y) * v.W + x) * v.cstride + v.coff;
   return ((b * (v.H >> 1) + (y >> 1)) * (v.W >> 1) + (x >> 1)) * v.cstride + v.coff +
          ((y & 1) * 2 + (x & 1)) * v.C;
+}
+
+// pixel block start (fp32 slots) and channel index of channel 0 within it
+__host__ __device__ inline void act_block(const ActView& v, int64_t b, int y, int x,
+                                          int64_t& block, int& chan) {
+  if (!v.s2d) {
+    block = ((b * v.H + y) * v.W + x) * v.cstride;
+    chan = v.coff;
+  } else {
+    block = ((b * (v.H >> 1) + (y >> 1)) * (v.W >> 1) + (x >> 1)) * v.cstride;
+    chan = v.coff + ((y & 1) * 2 + (x & 1)) * v.C;
+  }
 }
 
 // A convolution launch (cross-correlation, refiner.py:330-380) with fused

@@ -17,6 +17,7 @@
 #include <algorithm>
 
 #include "conv.cuh"
+#include "tc_ptx.cuh"
 #include "ts_common.cuh"
 
 namespace ts {
@@ -102,12 +103,22 @@ __global__ void __launch_bounds__(kEThreads, 2) conv_enc0_kernel(Enc0Op E) {
     // space-to-depth store: the pixel's C_out channels are contiguous
     const int y = y0 + ty, x = x0 + tx;
     if (y < E.oy1 && x < E.ox1) {
-      float4* o4 = reinterpret_cast<float4*>(E.out[e].base + act_off(E.out[e], b, y, x));
+      if (E.lrelu[e])
 #pragma unroll
-      for (int o = 0; o < CO / 4; ++o) {
-        float4 v = make_float4(acc[4 * o], acc[4 * o + 1], acc[4 * o + 2], acc[4 * o + 3]);
-        if (E.lrelu[e]) { v.x = lrelu(v.x); v.y = lrelu(v.y); v.z = lrelu(v.z); v.w = lrelu(v.w); }
-        o4[o] = v;
+        for (int o = 0; o < CO; ++o) acc[o] = lrelu(acc[o]);
+      const ActView& ov = E.out[e];
+      if (ov.planes) {  // pre-split for the tensor-core consumer
+        int64_t blk;
+        int chan;
+        act_block(ov, b, y, x, blk, chan);
+#pragma unroll
+        for (int o = 0; o < CO; o += 16)
+          tcx::store16_planes(ov.base + blk, ov.cstride, chan + o, acc + o);
+      } else {
+        float4* o4 = reinterpret_cast<float4*>(ov.base + act_off(ov, b, y, x));
+#pragma unroll
+        for (int o = 0; o < CO / 4; ++o)
+          o4[o] = make_float4(acc[4 * o], acc[4 * o + 1], acc[4 * o + 2], acc[4 * o + 3]);
       }
     }
   }

@@ -115,6 +115,7 @@ conv_simt_kernel(ConvOp op) {
 }  // namespace
 
 int launch_conv_simt(const ConvOp& op, void* stream) {
+  if (op.in.planes || op.out.planes) return TS_E_INVALID;  // fp32 activations only
   if (op.out.s2d) return TS_E_INVALID;  // s2d outputs: direct / halo2 kernels only
   const int64_t M = (int64_t)op.batch * (op.oy1 - op.oy0) * (op.ox1 - op.ox0);
   if (M <= 0) return TS_OK;
@@ -358,6 +359,7 @@ bool conv_direct_supported(const ConvOp& op) {
 }
 
 int launch_conv_direct(const ConvOp& op, void* stream) {
+  if (op.in.planes || op.out.planes) return TS_E_INVALID;  // fp32 activations only
   if (op.batch <= 0 || op.oy1 <= op.oy0 || op.ox1 <= op.ox0) return TS_OK;
   size_t smem;
   const DirectGeom g = direct_geom(op, &smem);

@@ -286,12 +286,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
       const int64_t gm = mt * BM + q * 32 + (tid & 31);
       const bool valid = gm < M;
       float* o = nullptr;
+      float* oblk = nullptr;
+      int ochan = 0;
       if (valid) {
         const int b = (int)(gm / ((int64_t)wy * wx));
         const int r = (int)(gm - (int64_t)b * wy * wx);
         const int y = op.oy0 + r / wx, x = op.ox0 + r % wx;
         o = op.out.base + (((int64_t)b * op.out.H + y) * op.out.W + x) * op.out.cstride +
             op.out.coff;
+        int64_t blk;
+        act_block(op.out, b, y, x, blk, ochan);
+        oblk = op.out.base + blk;
       }
       mbar_wait(acc_full + acc, (lt >> 1) & 1);
       tc_fence_after();
@@ -312,7 +317,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
             if (op.lrelu) x = x >= 0.f ? x : 0.01f * x;
             v[i] = x;
           }
-          if (vec && n0 + c + 16 <= Cout) {
+          if (op.out.planes) {
+            if (n0 + c + 16 <= Cout) store16_planes(oblk, op.out.cstride, ochan + n0 + c, v);
+          } else if (vec && n0 + c + 16 <= Cout) {
 #pragma unroll
             for (int i = 0; i < 4; ++i)
               *reinterpret_cast<float4*>(o + n0 + c + 4 * i) =
@@ -825,6 +832,11 @@ int tc_weight_layout(const ConvOp& shape, int precision) {
 
 int launch_conv_tc(const ConvOp& op, int precision, void* stream) {
   if (op.w_layout == 2) return launch_conv_tc_halo2(op, precision, stream);
+  // the regular / halo kernels read fp32 activations only; planes outputs
+  // only from the regular kernel (16-channel groups)
+  if (op.in.planes || (op.out.planes && (op.w_layout != 0 || op.out.C % 16 ||
+                                         op.out.cstride % 8 || op.out.coff % 8)))
+    return TS_E_INVALID;
   if (op.out.s2d) return TS_E_INVALID;  // s2d outputs: direct / halo2 kernels only
   if (op.w_layout == 1) {
     if (!conv_tc_halo_eligible(op, precision)) return TS_E_INVALID;

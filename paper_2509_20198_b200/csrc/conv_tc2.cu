@@ -181,6 +181,39 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
       for (int c = 0; c < T.cchunks; ++c) {
         mbar_wait(hempty + hb, ((hph >> hb) & 1u) ^ 1u);
         uint8_t* sa = halo + hb * halo_bytes;
+        if (op.in.planes) {
+          // pre-split input: 16-byte piece p of a row is 8 channels of plane
+          // p >> 2, copied as is (no conversion)
+          const int piece = tid & 7, pl = piece >> 2, sub = piece & 3;
+          const int ch = c * kKC + 8 * sub;
+          const bool ok = ch < Cin && pl < PA;
+          const uint8_t* src = reinterpret_cast<const uint8_t*>(op.in.base) +
+                               2 * (ch - op.in.coff) + 2 * (int64_t)pl * op.in.cstride;
+          const int row0 = tid >> 3;
+          uint8_t* dst0 = sa + pl * plane_a + row0 * kRow;
+          const int swz = sub ^ ((row0 >> 1) & 3);
+          constexpr int kRowStep = kProdT / PPR;  // rows per pass (multiple of 8)
+          if (pl < PA) {
+            for (int r0 = row0; r0 < L; r0 += kRowStep * kInflight) {
+              uint4 v[kInflight];
+#pragma unroll
+              for (int u = 0; u < kInflight; ++u) {
+                const int row = r0 + u * kRowStep;
+                v[u] = make_uint4(0u, 0u, 0u, 0u);
+                if (row < L) {
+                  const int64_t off = ro[row];
+                  if (off >= 0 && ok)
+                    v[u] = __ldg(reinterpret_cast<const uint4*>(src + 4 * off));
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < kInflight; ++u)
+                if (r0 + u * kRowStep < L)
+                  *reinterpret_cast<uint4*>(dst0 + (r0 - row0 + u * kRowStep) * kRow + (swz << 4)) =
+                      v[u];
+            }
+          }
+        } else {
         // each thread owns one 16-byte piece column (kProdT % 8 == 0): its
         // channel, validity and swizzled byte offset within a row are fixed,
         // and rows advance by kProdT / 8 = 32 (the swizzle phase repeats)
@@ -216,6 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
                 store_split2(d, plane_a, a);
             }
           }
+        }
         }
         fence_proxy_async();
         __syncwarp();
@@ -330,6 +364,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
       for (int u = 0; u < SUB; ++u) {
         const int64_t pos = mt * MT + u * 128 + q * 32 + (tid & 31);
         float* o = nullptr;
+        float* oblk = nullptr;
+        int ochan = 0;
         if (pos < T.positions) {
           const int64_t b = (int64_t)((uint32_t)pos / (uint32_t)img_pos);
           const int r = (int)(pos - b * img_pos);
@@ -338,6 +374,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
             const int oy = op.ph ? 2 * (op.oy0 + y) + op.ph_y : op.oy0 + y;
             const int ox = op.ph ? 2 * (op.ox0 + x) + op.ph_x : op.ox0 + x;
             o = op.out.base + act_off(op.out, b, oy, ox);
+            int64_t blk;
+            act_block(op.out, b, oy, ox, blk, ochan);
+            oblk = op.out.base + blk;
           }
         }
         for (int c = 16 * half; c < BN; c += 32) {
@@ -358,7 +397,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
             if (op.lrelu) x = x >= 0.f ? x : 0.01f * x;
             v[i] = x;
           }
-          if (o) {
+          if (o && op.out.planes) {
+            if (n0 + c + 16 <= Cout) store16_planes(oblk, op.out.cstride, ochan + n0 + c, v);
+          } else if (o) {
             if (vec && n0 + c + 16 <= Cout) {
 #pragma unroll
               for (int i = 0; i < 4; ++i)
@@ -403,6 +444,8 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
   // tile); opt in with TS_H2_1X1=1
   if (op.k == 1 && !(getenv("TS_H2_1X1") && getenv("TS_H2_1X1")[0] == '1')) return false;
   if (op.in.C % 4 || op.in.cstride % 4 || op.in.coff % 4) return false;
+  if (op.in.planes && (op.in.C % 8 || op.in.cstride % 8 || op.in.coff % 8)) return false;
+  if (op.out.planes && (op.out.C % 16 || op.out.cstride % 8 || op.out.coff % 8)) return false;
   Halo2Plan p{};
   p.pa = precision == 2 ? 1 : 2;
   p.pb = precision == 2 ? 1 : precision == 4 ? 2 : 3;

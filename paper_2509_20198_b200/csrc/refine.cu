@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "conv.cuh"
+#include "tc_ptx.cuh"
 #include "ts_common.cuh"
 
 namespace ts {
@@ -74,6 +75,8 @@ struct ConvLayer {
   bool poly = false;
   const uint8_t* w_ph[4] = {nullptr, nullptr, nullptr, nullptr};
   Win ph_win[4];
+  bool h2 = false;          // executed on the wide-M halo kernel (or phases)
+  bool out_planes = false;  // writes pre-split planes (conv.cuh ActView)
 };
 
 // low-resolution window of output phase p (0/1) of a high-res window
@@ -96,6 +99,7 @@ struct ts_weights {
   int enc_hw = 0;
   size_t cat_off = 0, fuse_in_off = 0;
   bool enc0_fused = false;  // the four encoders' first layers in one launch
+  bool fuse_in_planes = false;  // fuse-input buffer (raw inputs + decoders)
   std::vector<void*> device_allocs;
 };
 
@@ -181,13 +185,19 @@ Win unite(const Win& a, const Win& b) {
 }
 
 __global__ void copy_inputs_kernel(const float* __restrict__ in, int64_t pixels,
-                                   float* __restrict__ out, int cstride) {
+                                   float* __restrict__ out, int cstride, int planes) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pixels;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float4* s = reinterpret_cast<const float4*>(in + 8 * i);
-    float4* d = reinterpret_cast<float4*>(out + (int64_t)cstride * i);
-    d[0] = s[0];
-    d[1] = s[1];
+    if (planes) {  // pre-split channels 0..7 of the fuse input
+      const float4 a = s[0], b = s[1];
+      const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      tcx::store8_planes(out + (int64_t)cstride * i, cstride, 0, v);
+    } else {
+      float4* d = reinterpret_cast<float4*>(out + (int64_t)cstride * i);
+      d[0] = s[0];
+      d[1] = s[1];
+    }
   }
 }
 
@@ -603,6 +613,45 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
   }
   (void)params;
   if (tensors.size() != (size_t)nL * 2) return TS_E_SHAPE;  // unexpected tensors
+  // Which layers run on the wide-M halo kernel (mirrors ts_refine's
+  // dispatch), and which outputs are stored pre-split: those whose every
+  // consumer is such a layer, so its producers only copy.
+  for (auto& L : layers)
+    L.h2 = L.poly || (L.w_tc && L.w_layout == 2 && L.dexec.ci > 4);
+  {
+    // measured: the epilogue's split costs more than the producers save
+    // (12.96 vs 11.88 ms per 1,024 tiles), so pre-split storage is opt-in
+    // (TS_PLANES=1); results are bit-identical either way
+    const char* e = getenv("TS_PLANES");
+    const bool on = (W->precision >= 2 && W->precision <= 4) && (e && e[0] == '1');
+    auto fmt_ok = [](const ConvLayer& L) {
+      return L.d.co % 16 == 0 && L.out_cstride % 8 == 0 && L.out_coff % 8 == 0;
+    };
+    for (int i = 0; i < nL && on; ++i) {
+      ConvLayer& L = layers[i];
+      const bool last = i == stage_last[L.stage];
+      bool all_h2 = false;
+      if (!last) {
+        all_h2 = layers[i + 1].h2 && layers[i + 1].dexec.ci % 8 == 0;
+      } else if (L.stage == 4) {  // merge output -> both decoders' first layers
+        const ConvLayer& a = layers[stage_first[5]];
+        const ConvLayer& b = layers[stage_first[6]];
+        all_h2 = a.h2 && b.h2 && a.dexec.ci % 8 == 0;
+      }
+      // writers that can emit planes: halo2 / phase layers, the regular
+      // tensor-core kernel, the fused first encoder layers
+      const bool writer = L.h2 || (L.w_tc && L.w_layout == 0 && L.dexec.ci > 4) ||
+                          (W->enc0_fused && L.stage < 4 && L.index == 0);
+      L.out_planes = all_h2 && writer && fmt_ok(L);
+    }
+    // fuse input: raw-input copy + both decoders' last layers -> fuse.0
+    const ConvLayer& f0 = layers[stage_first[7]];
+    W->fuse_in_planes = on && f0.h2 && fin % 8 == 0 && dec_c_out[0] % 16 == 0 &&
+                        dec_c_out[1] % 16 == 0 && layers[stage_last[5]].h2 &&
+                        layers[stage_last[6]].h2;
+    layers[stage_last[5]].out_planes = W->fuse_in_planes;
+    layers[stage_last[6]].out_planes = W->fuse_in_planes;
+  }
   W->per_tile_floats = off;
   W->layers = std::move(layers);
   return TS_OK;
@@ -703,13 +752,14 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
     {
       const int64_t px = (int64_t)B * kRes * kRes;
       ts::count_launch(), copy_inputs_kernel<<<(int)std::min<int64_t>(ceil_div<int64_t>(px, 256), 148 * 16),
-                           256, 0, s>>>(in, px, buf(W->fuse_in_off), W->fuse_in_c);
+                           256, 0, s>>>(in, px, buf(W->fuse_in_off), W->fuse_in_c,
+                                        W->fuse_in_planes ? 1 : 0);
       TS_LAUNCH_CHECK();
     }
     const int enc_ch0[4] = {0, 1, 2, 5};
     const int enc_cin[4] = {1, 1, 3, 3};
     const float* prev_base = nullptr;
-    int prev_H = 0, prev_cs = 0, prev_coff = 0, prev_C = 0;
+    int prev_H = 0, prev_cs = 0, prev_coff = 0, prev_C = 0, prev_planes = 0;
     int prev_stage = -1;
     for (size_t i = 0; i < W->layers.size(); ++i) {
       const ConvLayer& L = W->layers[i];
@@ -728,21 +778,24 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
           for (size_t j = 0; j < W->layers.size(); ++j)
             if (W->layers[j].stage == 4) mi = j;
           const ConvLayer& M = W->layers[mi];
-          op.in = ActView{buf(M.out_off), M.Hout, M.Wout, M.out_cstride, M.out_coff, M.d.co};
+          op.in = ActView{buf(M.out_off), M.Hout, M.Wout, M.out_cstride, M.out_coff, M.d.co,
+                          0, M.out_planes ? 1 : 0};
         } else {
-          op.in = ActView{buf(W->fuse_in_off), kRes, kRes, W->fuse_in_c, 0, W->fuse_in_c};
+          op.in = ActView{buf(W->fuse_in_off), kRes, kRes, W->fuse_in_c, 0, W->fuse_in_c,
+                          0, W->fuse_in_planes ? 1 : 0};
         }
       } else {
         op.in = ActView{const_cast<float*>(prev_base), prev_H, prev_H, prev_cs, prev_coff,
-                        prev_C};
+                        prev_C, 0, prev_planes};
       }
       if (L.s2d_in) {
         // previous layer wrote s2d: half-resolution pixels of 4 C channels
         if (prev_coff != 0 || prev_cs != prev_C) return TS_E_INVALID;
         op.in = ActView{const_cast<float*>(prev_base), prev_H / 2, prev_H / 2, 4 * prev_C, 0,
-                        4 * prev_C};
+                        4 * prev_C, 0, prev_planes};
       }
-      op.out = ActView{buf(L.out_off), L.Hout, L.Wout, L.out_cstride, L.out_coff, L.d.co};
+      op.out = ActView{buf(L.out_off), L.Hout, L.Wout, L.out_cstride, L.out_coff, L.d.co, 0,
+                       L.out_planes ? 1 : 0};
       if (L.s2d_out) {
         if (L.out_coff != 0 || L.out_cstride != L.d.co) return TS_E_INVALID;
         op.out.cstride = 4 * L.d.co;
@@ -782,7 +835,8 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
             if (F.stage != e || F.index != 0) continue;
             E.ch0[e] = enc_ch0[e]; E.cin[e] = enc_cin[e]; E.lrelu[e] = F.d.lrelu;
             E.w[e] = F.w; E.bias[e] = F.b;
-            E.out[e] = ActView{buf(F.out_off), F.Hout, F.Wout, 4 * F.d.co, 0, F.d.co, 1};
+            E.out[e] = ActView{buf(F.out_off), F.Hout, F.Wout, 4 * F.d.co, 0, F.d.co, 1,
+                               F.out_planes ? 1 : 0};
             ++e;
           }
           E.oy0 = L.out_win.y0; E.oy1 = L.out_win.y1; E.ox0 = L.out_win.x0; E.ox1 = L.out_win.x1;
@@ -790,7 +844,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
           if (st != TS_OK) return st;
         }
         prev_base = buf(L.out_off); prev_H = L.Hout; prev_cs = L.out_cstride;
-        prev_coff = L.out_coff; prev_C = L.d.co;
+        prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? 1 : 0;
         prev_stage = L.stage;
         continue;
       }
@@ -807,7 +861,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
           if (st != TS_OK) return st;
         }
         prev_base = op.out.base; prev_H = L.Hout; prev_cs = L.out_cstride;
-        prev_coff = L.out_coff; prev_C = L.d.co;
+        prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? 1 : 0;
         prev_stage = L.stage;
         continue;
       }
@@ -827,7 +881,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
         st = launch_conv_simt(op, stream);
       if (st != TS_OK) return st;
       prev_base = op.out.base; prev_H = L.Hout; prev_cs = L.out_cstride;
-      prev_coff = L.out_coff; prev_C = L.d.co;
+      prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? 1 : 0;
       prev_stage = L.stage;
     }
     const ConvLayer& last = W->layers.back();

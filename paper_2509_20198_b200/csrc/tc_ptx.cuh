@@ -213,6 +213,40 @@ __device__ __forceinline__ void store_split2(uint8_t* dst, int plane_bytes, floa
   *reinterpret_cast<uint2*>(dst + plane_bytes) = make_uint2(l01, l23);
 }
 
+// 16 consecutive channels (chan % 8 == 0) into a planes = 1 pixel block
+// (conv.cuh ActView): 32 bytes of hi, 32 bytes of lo, 16-byte stores
+__device__ __forceinline__ void store16_planes(float* block, int cstride, int chan,
+                                               const float* v) {
+  uint32_t h[8], l[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    h[i] = pack_bf2(v[2 * i], v[2 * i + 1]);
+    l[i] = pack_bf2(v[2 * i] - __uint_as_float(h[i] << 16),
+                    v[2 * i + 1] - __uint_as_float(h[i] & 0xFFFF0000u));
+  }
+  uint4* hp = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(block) + 2 * chan);
+  uint4* lp = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(block) + 2 * (cstride + chan));
+  hp[0] = make_uint4(h[0], h[1], h[2], h[3]);
+  hp[1] = make_uint4(h[4], h[5], h[6], h[7]);
+  lp[0] = make_uint4(l[0], l[1], l[2], l[3]);
+  lp[1] = make_uint4(l[4], l[5], l[6], l[7]);
+}
+// 8 channels (chan % 8 == 0): 16 bytes of hi, 16 of lo
+__device__ __forceinline__ void store8_planes(float* block, int cstride, int chan,
+                                              const float* v) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    h[i] = pack_bf2(v[2 * i], v[2 * i + 1]);
+    l[i] = pack_bf2(v[2 * i] - __uint_as_float(h[i] << 16),
+                    v[2 * i + 1] - __uint_as_float(h[i] & 0xFFFF0000u));
+  }
+  *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(block) + 2 * chan) =
+      make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(block) + 2 * (cstride + chan)) =
+      make_uint4(l[0], l[1], l[2], l[3]);
+}
+
 // integer-ALU form of store_split2 (same values)
 __device__ __forceinline__ void store_split2_alu(uint8_t* dst, int plane_bytes, float4 a) {
   const float x0 = bf_keep(rn_bf(a.x)), y0 = bf_keep(rn_bf(a.y)), z0 = bf_keep(rn_bf(a.z)),
