@@ -158,10 +158,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     uint32_t hph = 0;
     constexpr int PPR = kKC / 4;  // float4 pieces per row
     const int pad_y = op.ph ? 1 - op.ph_y : op.pad, pad_x = op.ph ? 1 - op.ph_x : op.pad;
-    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
-      const int64_t mt = tile / T.n_tiles;
-      const int64_t j0 = mt * MT;
-      int64_t* ro = rowoff + (lt & 1) * L;
+    // row table of this CTA's tile lt_ (parity lt_ & 1); with pf, the first
+    // chunk's row lines are prefetched into L2 as they are computed
+    auto build_rows = [&](int lt_, bool pf) {
+      const int64_t tile_ = blockIdx.x + (int64_t)lt_ * gridDim.x;
+      const int64_t j0 = (tile_ / T.n_tiles) * MT;
+      int64_t* ro_ = rowoff + (lt_ & 1) * L;
       for (int j = tid; j < L; j += kProdT) {
         const int64_t pos = j0 + j;
         int64_t off = -1;
@@ -175,10 +177,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
             off = ((b * op.in.H + (iy >> sh)) * op.in.W + (ix >> sh)) * op.in.cstride +
                   op.in.coff;
         }
-        ro[j] = off;
+        ro_[j] = off;
+        if (pf && off >= 0 && !op.in.planes)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(op.in.base + off));
       }
+    };
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+      int64_t* ro = rowoff + (lt & 1) * L;
+      if (lt == 0) build_rows(0, false);
       prod_sync();
       for (int c = 0; c < T.cchunks; ++c) {
+        // during the last chunk, the next tile's row table (other parity)
+        // and an L2 prefetch of its first chunk
+        if (c == T.cchunks - 1 && tile + gridDim.x < total_tiles) build_rows(lt + 1, true);
         mbar_wait(hempty + hb, ((hph >> hb) & 1u) ^ 1u);
         uint8_t* sa = halo + hb * halo_bytes;
         if (op.in.planes) {
@@ -220,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
         const int piece = tid & 7;
         const int ch = c * kKC + 4 * piece;
         const bool ch_ok = ch < Cin;
+        const bool pf_ok = c + 1 < T.cchunks && ch + kKC < Cin;
         const float* src = op.in.base + ch;
         const int row0 = tid >> 3;
         const int obase = row0 * kRow + (((piece >> 1) ^ ((row0 >> 1) & 3)) << 4) +
@@ -234,6 +246,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
             if (row < L) {
               const int64_t off = ro[row];
               if (off >= 0 && ch_ok) v[u] = __ldg(reinterpret_cast<const float4*>(src + off));
+              // the next chunk's piece of this row into L2 while this one
+              // is converted (the fill is otherwise one DRAM latency per
+              // chunk)
+              if (off >= 0 && pf_ok)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(src + off + kKC));
             }
           }
           uint8_t* so = sa + obase + (r0 - row0) * kRow;
