@@ -5,7 +5,7 @@
 // The four layers read disjoint channels of the same B x 96 x 96 x 8 CNN
 // input, so one CTA stages the input halo of a 4 x 16 output tile ONCE for
 // all of them (the per-layer direct kernel read it four times) and its 16
-// warps split as 4 encoders x 2 row pairs.  fp32 CUDA-core FMAs (thin K: 9
+// warps split as 4 encoders x 2 output-channel halves (each thread: 2 pixels x C_out/2).  fp32 CUDA-core FMAs (thin K: 9
 // or 27 MACs per output channel), outputs written straight into the
 // space-to-depth layout the stride-2 tensor-core layers consume (a pixel's
 // C_out channels are one contiguous run there: float4 stores).  Two
@@ -27,14 +27,16 @@ constexpr int kETY = 4, kETX = 16;          // output tile
 constexpr int kEHY = 2 * kETY + 1;          // 9 halo rows
 constexpr int kEPitch = 20;                 // floats per parity row (>= 17; 4*pitch = 16 mod 32)
 constexpr int kEPlane = kEHY * 2 * kEPitch; // floats per channel
-constexpr int kEThreads = 256;  // 4 encoders x 2 row pairs; 2 CTAs per SM
+constexpr int kEThreads = 256;  // 4 encoders x 2 channel halves; 2 CTAs per SM
 
 __device__ __forceinline__ float lrelu(float v) { return v >= 0.f ? v : 0.01f * v; }
 
-template <int CIN, int CO>
+// Two output pixels (rows ty and ty + 2 of the tile) x CH consecutive
+// output channels per thread: every broadcast weight load feeds 8 FMAs.
+template <int CIN, int CO, int CH>
 __device__ __forceinline__ void enc0_accumulate(const float* __restrict__ halo, int ch0,
                                                 const float* __restrict__ w, int ty, int tx,
-                                                float* acc) {
+                                                float (&acc)[2][CH]) {
 #pragma unroll
   for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
@@ -43,15 +45,20 @@ __device__ __forceinline__ void enc0_accumulate(const float* __restrict__ halo, 
       const float* hp = halo + (2 * ty + ky) * 2 * kEPitch + (kx & 1) * kEPitch + tx + (kx >> 1);
 #pragma unroll
       for (int ci = 0; ci < CIN; ++ci) {
-        const float x = hp[(ch0 + ci) * kEPlane];
+        const float x0 = hp[(ch0 + ci) * kEPlane];
+        const float x1 = hp[(ch0 + ci) * kEPlane + 4 * 2 * kEPitch];  // two output rows on
         const float4* w4 = reinterpret_cast<const float4*>(w + ((ky * 3 + kx) * CIN + ci) * CO);
 #pragma unroll
-        for (int o = 0; o < CO / 4; ++o) {
+        for (int o = 0; o < CH / 4; ++o) {
           const float4 q = w4[o];
-          acc[4 * o] = fmaf(x, q.x, acc[4 * o]);
-          acc[4 * o + 1] = fmaf(x, q.y, acc[4 * o + 1]);
-          acc[4 * o + 2] = fmaf(x, q.z, acc[4 * o + 2]);
-          acc[4 * o + 3] = fmaf(x, q.w, acc[4 * o + 3]);
+          acc[0][4 * o] = fmaf(x0, q.x, acc[0][4 * o]);
+          acc[0][4 * o + 1] = fmaf(x0, q.y, acc[0][4 * o + 1]);
+          acc[0][4 * o + 2] = fmaf(x0, q.z, acc[0][4 * o + 2]);
+          acc[0][4 * o + 3] = fmaf(x0, q.w, acc[0][4 * o + 3]);
+          acc[1][4 * o] = fmaf(x1, q.x, acc[1][4 * o]);
+          acc[1][4 * o + 1] = fmaf(x1, q.y, acc[1][4 * o + 1]);
+          acc[1][4 * o + 2] = fmaf(x1, q.z, acc[1][4 * o + 2]);
+          acc[1][4 * o + 3] = fmaf(x1, q.w, acc[1][4 * o + 3]);
         }
       }
     }
@@ -74,7 +81,9 @@ __global__ void __launch_bounds__(kEThreads, 2) conv_enc0_kernel(Enc0Op E) {
   const float* sbias = sw + ((woff[3] + 9 * E.cin[3] * CO + 3) & ~3);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int e = warp & 3;                             // encoder of this warp
-  const int ty = 2 * (warp >> 2) + (lane >> 4), tx = lane & 15;
+  constexpr int CH = CO / 2;                          // channels per thread
+  const int chalf = (warp >> 2) * CH;                 // which half of C_out
+  const int ty = lane >> 4, tx = lane & 15;           // rows ty and ty + 2
   const int wy = E.oy1 - E.oy0, wx = E.ox1 - E.ox0;
   const int ntx = (wx + kETX - 1) / kETX, nty = (wy + kETY - 1) / kETY;
   const int64_t tiles = (int64_t)E.batch * nty * ntx;
@@ -95,30 +104,35 @@ __global__ void __launch_bounds__(kEThreads, 2) conv_enc0_kernel(Enc0Op E) {
       d[0] = v.x; d[kEPlane] = v.y; d[2 * kEPlane] = v.z; d[3 * kEPlane] = v.w;
     }
     __syncthreads();
-    float acc[CO];
+    float acc[2][CH];
 #pragma unroll
-    for (int o = 0; o < CO; ++o) acc[o] = sbias[e * CO + o];
-    if (E.cin[e] == 1) enc0_accumulate<1, CO>(halo, E.ch0[e], sw + woff[e], ty, tx, acc);
-    else enc0_accumulate<3, CO>(halo, E.ch0[e], sw + woff[e], ty, tx, acc);
+    for (int o = 0; o < CH; ++o) acc[0][o] = acc[1][o] = sbias[e * CO + chalf + o];
+    if (E.cin[e] == 1)
+      enc0_accumulate<1, CO, CH>(halo, E.ch0[e], sw + woff[e] + chalf, ty, tx, acc);
+    else
+      enc0_accumulate<3, CO, CH>(halo, E.ch0[e], sw + woff[e] + chalf, ty, tx, acc);
     // space-to-depth store: the pixel's C_out channels are contiguous
-    const int y = y0 + ty, x = x0 + tx;
-    if (y < E.oy1 && x < E.ox1) {
+    const ActView& ov = E.out[e];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int y = y0 + ty + 2 * r, x = x0 + tx;
+      if (y >= E.oy1 || x >= E.ox1) continue;
       if (E.lrelu[e])
 #pragma unroll
-        for (int o = 0; o < CO; ++o) acc[o] = lrelu(acc[o]);
-      const ActView& ov = E.out[e];
+        for (int o = 0; o < CH; ++o) acc[r][o] = lrelu(acc[r][o]);
       if (ov.planes) {  // pre-split for the tensor-core consumer
         int64_t blk;
         int chan;
         act_block(ov, b, y, x, blk, chan);
 #pragma unroll
-        for (int o = 0; o < CO; o += 16)
-          tcx::store16_planes(ov.base + blk, ov.cstride, chan + o, acc + o);
+        for (int o = 0; o < CH; o += 8)
+          tcx::store8_planes(ov.base + blk, ov.cstride, chan + chalf + o, acc[r] + o);
       } else {
-        float4* o4 = reinterpret_cast<float4*>(ov.base + act_off(ov, b, y, x));
+        float4* o4 = reinterpret_cast<float4*>(ov.base + act_off(ov, b, y, x) + chalf);
 #pragma unroll
-        for (int o = 0; o < CO / 4; ++o)
-          o4[o] = make_float4(acc[4 * o], acc[4 * o + 1], acc[4 * o + 2], acc[4 * o + 3]);
+        for (int o = 0; o < CH / 4; ++o)
+          o4[o] = make_float4(acc[r][4 * o], acc[r][4 * o + 1], acc[r][4 * o + 2],
+                              acc[r][4 * o + 3]);
       }
     }
   }
