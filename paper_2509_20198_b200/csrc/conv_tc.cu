@@ -59,6 +59,8 @@ struct TcArgs {
   const uint8_t* wpk;   // [n_tile][kiter][plane][BN][128 B]
   int bn, stages, kiters, cchunks, n_tiles;
   int64_t m_tiles;
+  int wide;  // MODE 4 with BN > 128: the three products accumulate into the
+             // same BN columns (no plane stacking), N up to 256 per MMA
 };
 
 // Row table of one tile: input pixel origin of every output pixel.
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
   // MODE 4 stacks the two weight planes along N (one MMA per A plane,
   // N = 2 BN; the epilogue adds the halves): half the A-operand shared
   // memory reads of one MMA per plane pair
-  constexpr int NST = MODE == 4 ? 2 : 1;
+  const int NST = (MODE == 4 && !T.wide) ? 2 : 1;
   uint32_t ncols = 32;
   while ((int)ncols < 2 * NST * BN) ncols <<= 1;
 
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
     // ------------------------------ MMA issuer -----------------------------
     // The whole warp walks the loop (uniform registers), one elected lane
     // issues; descriptors are integer offsets from precomputed bases.
-    const uint32_t idesc = make_idesc(Md::tf32 ? 2u : 1u, NST * BN);
+    const uint32_t idesc = make_idesc(Md::tf32 ? 2u : 1u, (NST * BN) > 256 ? 256 : NST * BN);
     const uint32_t idesc_b0 = make_idesc(1u, BN);
     (void)idesc_b0;
     const uint64_t d_smem = sw128_desc(su32(smem));
@@ -253,8 +255,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
             } else if (MODE == 4) {
               // a0 . [b0 | b1] (N = 2 BN), then a1 . b0 (N = BN): the
               // a1 . b1 term (<= 2^-18 |ab|, the size of the split
-              // residual) is dropped
-              umma<false>(d, ak, bk, idesc, first);
+              // residual) is dropped.  Wide tiles: the same three
+              // products, each N = BN, into the same columns.
+              if (T.wide) {
+                umma<false>(d, ak, bk, idesc_b0, first);
+                umma<false>(d, ak, bk + pb, idesc_b0, 1u);
+              } else {
+                umma<false>(d, ak, bk, idesc, first);
+              }
               umma<false>(d, ak + pa, bk, idesc_b0, 1u);
             } else {
               umma<false>(d, ak + pa, bk + pb, idesc, first);  // small terms first
@@ -654,7 +662,7 @@ uint16_t f2bf16_rn(float x) { return f2bf16_rn_host(x); }
 float bf16_to_f(uint16_t h) { return bf16_to_f_host(h); }
 
 struct TcPlan {
-  int bn, stages, kiters, cchunks, ntiles, pa, pb, kc;
+  int bn, stages, kiters, cchunks, ntiles, pa, pb, kc, wide;
   size_t smem;
 };
 
@@ -664,9 +672,15 @@ TcPlan plan_for(const ConvOp& op, int precision) {
   p.pb = precision == 1 ? 2 : precision == 2 ? 1 : precision == 4 ? 2 : 3;
   p.kc = precision == 1 ? 32 : 64;
   const int n16 = (op.out.C + 15) / 16 * 16;
-  const int cap = 128;
+  // BF16X4 1x1 layers (the merge GEMMs) take N tiles of up to 256 without
+  // plane stacking: every N tile re-gathers and re-splits A, so fewer tiles
+  // halve the producers' work
+  const char* e = getenv("TS_TC_WIDE");
+  const bool wide_ok = precision == 4 && op.k == 1 && !(e && e[0] == '0');
+  const int cap = wide_ok ? 256 : 128;
   p.ntiles = (n16 + cap - 1) / cap;
   p.bn = ((n16 + p.ntiles - 1) / p.ntiles + 15) / 16 * 16;
+  p.wide = wide_ok && p.bn > 128;
   p.cchunks = (op.in.C + p.kc - 1) / p.kc;
   p.kiters = op.k * op.k * p.cchunks;
   const size_t stage = ((size_t)BM * p.pa + (size_t)p.bn * p.pb) * kRowBytes;
@@ -846,7 +860,7 @@ int launch_conv_tc(const ConvOp& op, int precision, void* stream) {
   const int64_t M = (int64_t)op.batch * (op.oy1 - op.oy0) * (op.ox1 - op.ox0);
   if (M <= 0) return TS_OK;
   TcArgs a{op, op.w_tc, p.bn, p.stages, p.kiters, p.cchunks, p.ntiles,
-           ceil_div<int64_t>(M, BM)};
+           ceil_div<int64_t>(M, BM), p.wide};
   const int64_t tiles = a.m_tiles * p.ntiles;
   static int sms = 0;
   if (!sms) {
