@@ -128,11 +128,9 @@ __global__ void __launch_bounds__(kEThreads, 2) conv_enc0_kernel(Enc0Op E) {
         for (int o = 0; o < CH; o += 8)
           tcx::store8_planes(ov.base + blk, ov.cstride, chan + chalf + o, acc[r] + o);
       } else {
-        float4* o4 = reinterpret_cast<float4*>(ov.base + act_off(ov, b, y, x) + chalf);
+        float* op_ = ov.base + act_off(ov, b, y, x) + chalf;
 #pragma unroll
-        for (int o = 0; o < CH / 4; ++o)
-          o4[o] = make_float4(acc[r][4 * o], acc[r][4 * o + 1], acc[r][4 * o + 2],
-                              acc[r][4 * o + 3]);
+        for (int o = 0; o < CH; o += 8) tcx::st_v8(op_ + o, acc[r] + o);
       }
     }
   }

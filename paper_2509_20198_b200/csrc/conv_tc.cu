@@ -285,6 +285,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
     const int q = warp & 3;  // TMEM lane quadrant of this warp
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const bool vec = (op.out.cstride % 4 == 0) && (op.out.coff % 4 == 0);
+    const bool vec8 = (op.out.cstride % 8 == 0) && (op.out.coff % 8 == 0) &&
+                      ((reinterpret_cast<uintptr_t>(op.out.base) & 31) == 0);
     int lt = 0;
     for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
       const int acc = lt & 1;
@@ -327,6 +329,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
           }
           if (op.out.planes) {
             if (n0 + c + 16 <= Cout) store16_planes(oblk, op.out.cstride, ochan + n0 + c, v);
+          } else if (vec8 && n0 + c + 16 <= Cout) {
+            st_v8(o + n0 + c, v);
+            st_v8(o + n0 + c + 8, v + 8);
           } else if (vec && n0 + c + 16 <= Cout) {
 #pragma unroll
             for (int i = 0; i < 4; ++i)

@@ -368,6 +368,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     const int half = (warp - kEpiW0) >> 2;  // which 16-column groups
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const bool vec = (op.out.cstride % 4 == 0) && (op.out.coff % 4 == 0);
+    const bool vec8 = (op.out.cstride % 8 == 0) && (op.out.coff % 8 == 0) &&
+                      (op.out.C % 8 == 0) && ((reinterpret_cast<uintptr_t>(op.out.base) & 31) == 0);
     int lt = 0;
     for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
       const int acc = lt % AB;
@@ -417,7 +419,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
           if (o && op.out.planes) {
             if (n0 + c + 16 <= Cout) store16_planes(oblk, op.out.cstride, ochan + n0 + c, v);
           } else if (o) {
-            if (vec && n0 + c + 16 <= Cout) {
+            if (vec8 && n0 + c + 16 <= Cout) {
+              st_v8(o + n0 + c, v);
+              st_v8(o + n0 + c + 8, v + 8);
+            } else if (vec && n0 + c + 16 <= Cout) {
 #pragma unroll
               for (int i = 0; i < 4; ++i)
                 *reinterpret_cast<float4*>(o + n0 + c + 4 * i) =

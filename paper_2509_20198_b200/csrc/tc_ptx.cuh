@@ -194,6 +194,13 @@ __device__ __forceinline__ float bf_keep(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xFFFF0000u);
 }
 
+// 32-byte global store (STG.256, sm_100): one full sector per lane
+__device__ __forceinline__ void st_v8(float* p, const float* v) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]),
+               "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+
 // {bf16_rn(lo), bf16_rn(hi)} packed (lo in the low half): one F2FP
 __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
   uint32_t r;
