@@ -158,6 +158,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     uint32_t hph = 0;
     constexpr int PPR = kKC / 4;  // float4 pieces per row
     const int pad_y = op.ph ? 1 - op.ph_y : op.pad, pad_x = op.ph ? 1 - op.ph_x : op.pad;
+    // 32-byte aligned 8-channel pieces available
+    const bool v8in = Cin % 8 == 0 && op.in.cstride % 8 == 0 && op.in.coff % 8 == 0 &&
+                      (reinterpret_cast<uintptr_t>(op.in.base) & 31) == 0;
     // row table of this CTA's tile lt_ (parity lt_ & 1); with pf, the first
     // chunk's row lines are prefetched into L2 as they are computed
     auto build_rows = [&](int lt_, bool pf) {
@@ -222,6 +225,53 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
                 if (r0 + u * kRowStep < L)
                   *reinterpret_cast<uint4*>(dst0 + (r0 - row0 + u * kRowStep) * kRow + (swz << 4)) =
                       v[u];
+            }
+          }
+        } else if (v8in) {
+          // 32-byte pieces (8 channels): LDG.256, one STS.128 per plane.
+          // Each thread owns one piece column (kProdT % 4 == 0); rows advance
+          // by kProdT / 4 (a multiple of 8: the swizzle phase repeats).
+          const int piece = tid & 3;
+          const int ch = c * kKC + 8 * piece;
+          const bool ch_ok = ch < Cin;
+          const bool pf_ok = c + 1 < T.cchunks && ch + kKC < Cin;
+          const float* src = op.in.base + ch;
+          const int row0 = tid >> 2;
+          const int obase = row0 * kRow + ((piece ^ ((row0 >> 1) & 3)) << 4);
+          constexpr int kStep8 = kProdT / 4;
+          constexpr int kIn8 = 4;
+          for (int r0 = row0; r0 < L; r0 += kStep8 * kIn8) {
+            float v[kIn8][8];
+#pragma unroll
+            for (int u = 0; u < kIn8; ++u) {
+              const int row = r0 + u * kStep8;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[u][i] = 0.f;
+              if (row < L) {
+                const int64_t off = ro[row];
+                if (off >= 0 && ch_ok) ld_v8(src + off, v[u]);
+                if (off >= 0 && pf_ok)
+                  asm volatile("prefetch.global.L2 [%0];" ::"l"(src + off + kKC));
+              }
+            }
+            uint8_t* so = sa + obase + (r0 - row0) * kRow;
+#pragma unroll
+            for (int u = 0; u < kIn8; ++u) {
+              if (r0 + u * kStep8 < L) {
+                uint8_t* d = so + u * kStep8 * kRow;
+                uint32_t h[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) h[i] = pack_bf2(v[u][2 * i], v[u][2 * i + 1]);
+                *reinterpret_cast<uint4*>(d) = make_uint4(h[0], h[1], h[2], h[3]);
+                if (MODE != 2) {
+                  uint32_t l[4];
+#pragma unroll
+                  for (int i = 0; i < 4; ++i)
+                    l[i] = pack_bf2(v[u][2 * i] - __uint_as_float(h[i] << 16),
+                                    v[u][2 * i + 1] - __uint_as_float(h[i] & 0xFFFF0000u));
+                  *reinterpret_cast<uint4*>(d + plane_a) = make_uint4(l[0], l[1], l[2], l[3]);
+                }
+              }
             }
           }
         } else {

@@ -201,6 +201,14 @@ __device__ __forceinline__ void st_v8(float* p, const float* v) {
                : "memory");
 }
 
+// 32-byte read-only global load (LDG.256)
+__device__ __forceinline__ void ld_v8(const float* p, float* v) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]),
+                 "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+
 // {bf16_rn(lo), bf16_rn(hi)} packed (lo in the low half): one F2FP
 __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
   uint32_t r;
