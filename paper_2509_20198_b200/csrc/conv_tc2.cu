@@ -357,6 +357,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
         hph ^= 1u << hb;
         tc_fence_after();
         const uint64_t d_hb = d_halo + (uint64_t)(hb * h_step);
+        // the last chunk may hold <= 16 real channels (fuse.0: 72 = 2 x 32
+        // + 8): its second K step would multiply zeros
+        const int nk = (c == T.cchunks - 1 && Cin - c * kKC <= 16) ? 1 : 2;
         for (; s_chunk[si] == c; ++si) {
           mbar_wait(bfull + s, bph);
           tc_fence_after();
@@ -366,6 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
             const uint32_t first = si ? 1u : 0u;
 #pragma unroll
             for (int k = 0; k < 2; ++k) {  // 2 x 32-byte K steps per row
+              if (k >= nk) break;
 #pragma unroll
               for (int u = 0; u < SUB; ++u) {
                 const uint64_t ak = a0 + (uint64_t)(u * (128 * kRow >> 4) + 2 * k);
