@@ -21,6 +21,7 @@
 #include <cfloat>
 #include <climits>
 
+#include "tc_ptx.cuh"
 #include "ts_common.cuh"
 
 namespace ts {
@@ -378,9 +379,8 @@ raster_kernel(RasterArgs A) {
       }
       const int64_t o = (int64_t)p * kCells + j;
       if (A.cnn_in) {
-        float4* d = reinterpret_cast<float4*>(A.cnn_in + 8 * o);
-        d[0] = make_float4(fnn, flin, rn[0], rn[1]);
-        d[1] = make_float4(rn[2], rli[0], rli[1], rli[2]);
+        const float cell[8] = {fnn, flin, rn[0], rn[1], rn[2], rli[0], rli[1], rli[2]};
+        tcx::st_v8(A.cnn_in + 8 * o, cell);  // one 32-byte sector per cell
       }
       if (A.hm_nn) A.hm_nn[o] = fnn;
       if (A.hm_lin) A.hm_lin[o] = flin;

@@ -188,15 +188,15 @@ __global__ void copy_inputs_kernel(const float* __restrict__ in, int64_t pixels,
                                    float* __restrict__ out, int cstride, int planes) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pixels;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const float4* s = reinterpret_cast<const float4*>(in + 8 * i);
+    float v[8];
+    tcx::ld_v8(in + 8 * i, v);
     if (planes) {  // pre-split channels 0..7 of the fuse input
-      const float4 a = s[0], b = s[1];
-      const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
       tcx::store8_planes(out + (int64_t)cstride * i, cstride, 0, v);
+    } else if (cstride % 8 == 0) {
+      tcx::st_v8(out + (int64_t)cstride * i, v);
     } else {
-      float4* d = reinterpret_cast<float4*>(out + (int64_t)cstride * i);
-      d[0] = s[0];
-      d[1] = s[1];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) out[(int64_t)cstride * i + c] = v[c];
     }
   }
 }
