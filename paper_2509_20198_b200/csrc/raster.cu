@@ -133,6 +133,7 @@ raster_kernel(RasterArgs A) {
   __shared__ double s_shift;
   __shared__ int s_total;
   __shared__ int s_wsum[kThreads / 32];
+  __shared__ int s_cur[kThreads];
 
   const int p = blockIdx.x;
   const int tid = threadIdx.x;
@@ -320,18 +321,38 @@ raster_kernel(RasterArgs A) {
     }
     return bi;
   };
-  if (cached) {  // counting sort of point ids into bins (ascending ids)
-    if (tid == 0) {
-      for (int b = 0; b <= kBins * kBins; ++b) s_bstart[b] = 0;
-      for (int i = 0; i < n; ++i)
-        ++s_bstart[bin_of(xy[2 * i + 1]) * kBins + bin_of(xy[2 * i]) + 1];
-      for (int b = 0; b < kBins * kBins; ++b) s_bstart[b + 1] += s_bstart[b];
-      for (int i = 0; i < n; ++i) {
-        const int b = bin_of(xy[2 * i + 1]) * kBins + bin_of(xy[2 * i]);
-        s_bid[s_bstart[b]++] = (short)i;
+  if (cached) {
+    // counting sort of point ids into bins, block-parallel: counts by
+    // shared atomics, one 256-bin scan, placement by per-bin cursors (the
+    // order inside a bin is free: nn_of breaks d^2 ties by lowest id)
+    static_assert(kBins * kBins == kThreads, "one bin per thread in the scan");
+    s_bstart[tid + 1] = 0;
+    if (tid == 0) s_bstart[0] = 0;
+    __syncthreads();
+    for (int i = tid; i < n; i += kThreads)
+      atomicAdd(&s_bstart[bin_of(xy[2 * i + 1]) * kBins + bin_of(xy[2 * i]) + 1], 1);
+    __syncthreads();
+    {  // inclusive scan of the 256 counts (warp shuffles + warp totals)
+      int v = s_bstart[tid + 1];
+      const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, v, o);
+        if (lane >= o) v += y;
       }
-      for (int b = kBins * kBins; b > 0; --b) s_bstart[b] = s_bstart[b - 1];
-      s_bstart[0] = 0;
+      if (lane == 31) s_wsum[wid] = v;
+      __syncthreads();
+      int base = 0;
+      for (int w = 0; w < wid; ++w) base += s_wsum[w];
+      __syncthreads();
+      const int prev = __shfl_up_sync(0xFFFFFFFFu, v, 1);  // all lanes take part
+      s_bstart[tid + 1] = base + v;
+      s_cur[tid] = base + (lane ? prev : 0);  // start of bin tid
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += kThreads) {
+      const int b = bin_of(xy[2 * i + 1]) * kBins + bin_of(xy[2 * i]);
+      s_bid[atomicAdd(&s_cur[b], 1)] = (short)i;
     }
     __syncthreads();
   }
