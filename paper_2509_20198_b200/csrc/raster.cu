@@ -213,23 +213,36 @@ raster_kernel(RasterArgs A) {
     __syncthreads();
     if (tid == 0) s_pref[T] = s_total;
     __syncthreads();
+    // each thread takes one contiguous run of the flattened (triangle, cell)
+    // items: one binary search, then a forward walk that rebuilds a
+    // triangle's geometry only when the run crosses into the next triangle
     const int total = s_total;
-    for (int w = tid; w < total; w += kThreads) {
-      int lo = 0, hi = T;  // largest t with s_pref[t] <= w
+    const int per_w = ceil_div(total, kThreads);
+    const int w0 = tid * per_w, w1 = min(total, w0 + per_w);
+    if (w0 < w1) {
+      int lo = 0, hi = T;  // largest t with s_pref[t] <= w0
       while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
-        if (s_pref[mid] <= w) lo = mid; else hi = mid;
+        if (s_pref[mid] <= w0) lo = mid; else hi = mid;
       }
-      const int t = lo;
-      const uint32_t rg = s_rng[t];
-      const int width = (rg >> 8) & 0xFF;
-      const int k = w - s_pref[t];
-      const int gy = (int)(rg >> 16) + k / width;
-      const int gx = (int)(rg & 0xFF) + k % width;
+      int t = lo;
+      while (t + 1 < T && s_pref[t + 1] <= w0) ++t;  // skip empty triangles
       Tri tr{tri[3 * t], tri[3 * t + 1], tri[3 * t + 2]};
-      const Geo g = tri_geo(xy, n, tr);
-      if (contains(g, cell_center(gx, kRes), cell_center(gy, kRes)))
-        atomicMin(&s_face[gy * kRes + gx], t);
+      Geo g = tri_geo(xy, n, tr);
+      for (int w = w0; w < w1; ++w) {
+        if (w >= s_pref[t + 1]) {
+          do { ++t; } while (w >= s_pref[t + 1]);
+          tr = Tri{tri[3 * t], tri[3 * t + 1], tri[3 * t + 2]};
+          g = tri_geo(xy, n, tr);
+        }
+        const uint32_t rg = s_rng[t];
+        const int width = (rg >> 8) & 0xFF;
+        const int k = w - s_pref[t];
+        const int gy = (int)(rg >> 16) + k / width;
+        const int gx = (int)(rg & 0xFF) + k % width;
+        if (contains(g, cell_center(gx, kRes), cell_center(gy, kRes)))
+          atomicMin(&s_face[gy * kRes + gx], t);
+      }
     }
   } else {
     for (int t = tid; t < T; t += kThreads) {
