@@ -236,20 +236,63 @@ def run_ours(args, rank, world, local_rank):
     value = total_maps / (ms_max / 1e3)
 
     # ---- end to end: pinned host tile bytes in, refined rasters out ----
-    out_host = torch.empty((P, 64, 64, 4), dtype=torch.float32).pin_memory()
-    e2e_times = []
-    for i in range(args.steps + 1):
+    # Streamed the way a serving loop runs the public pipeline API: every
+    # step copies its tile images host->device on a copy stream into one of
+    # two device buffers and its refined tiles device->host into one of two
+    # pinned buffers, so step i+1's upload and step i-1's download overlap
+    # step i's kernels.  Timed on the device from the first upload to the
+    # last download (both streams joined).
+    import copy as _copy
+    out_host = [torch.empty((P, 64, 64, 4), dtype=torch.float32).pin_memory()
+                for _ in range(2)]
+    tbs = [tb, _copy.copy(tb)]
+    tbs[1].bytes = torch.empty_like(tb.bytes)
+    copy_s = torch.cuda.Stream(device=dev)
+    n_e2e = args.steps + 2
+    for rep in range(2):  # a warm-up pass, then the timed pass
+        ev_in = [ev(), ev()]
+        ev_comp = [None, None]
         torch.cuda.synchronize()
-        s, e = ev(), ev()
-        s.record(stream)
-        tb.bytes.copy_(host_bytes, non_blocking=True)
-        out, o, nf = step()
-        out_host.copy_(out, non_blocking=True)
-        e.record(stream)
+        if world > 1:
+            dist.barrier()
+        t_start, t_end = ev(), ev()
+        t_start.record(stream)
+        copy_s.wait_event(t_start)
+        for i in range(n_e2e):
+            b = i & 1
+            with torch.cuda.stream(copy_s):
+                if ev_comp[b] is not None:
+                    copy_s.wait_event(ev_comp[b])   # step i-2 done with buffer b
+                tbs[b].bytes.copy_(host_bytes, non_blocking=True)
+                ev_in[b].record(copy_s)
+            stream.wait_event(ev_in[b])
+            _tables, _cp, idx = pipe.overview(tbs[b], cell_range)
+            _g, _t, _o, cnn_in = pipe.patches(idx, centers)
+            out, _nf = pipe.refine(cnn_in, P)
+            done = ev()
+            done.record(stream)
+            ev_comp[b] = done
+            # the previous step's download is queued only now, after this
+            # step's small host-side sizing reads: queued earlier it would
+            # hold the copy engine in front of them and stall the host
+            if i:
+                pb, pout, pdone = pending
+                with torch.cuda.stream(copy_s):
+                    copy_s.wait_event(pdone)
+                    out_host[pb].copy_(pout, non_blocking=True)
+                    pout.record_stream(copy_s)
+            pending = (b, out, done)
+        pb, pout, pdone = pending
+        with torch.cuda.stream(copy_s):
+            copy_s.wait_event(pdone)
+            out_host[pb].copy_(pout, non_blocking=True)
+            pout.record_stream(copy_s)
+        last = ev()
+        last.record(copy_s)
+        stream.wait_event(last)
+        t_end.record(stream)
         torch.cuda.synchronize()
-        if i:
-            e2e_times.append(s.elapsed_time(e))
-    e2e_ms = float(np.mean(e2e_times))
+    e2e_ms = t_start.elapsed_time(t_end) / n_e2e
     e2e_t = torch.tensor([e2e_ms], device=dev)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
@@ -313,7 +356,10 @@ def run_ours(args, rank, world, local_rank):
                                          "profiles/r01_traffic.json)"},
             "e2e": {"value": round(e2e_value, 2), "unit": "heightmaps/s",
                     "h2d_bytes_per_step": int(host_bytes.numel()),
-                    "d2h_bytes_per_step": int(out_host.numel() * 4)},
+                    "d2h_bytes_per_step": int(out_host[0].numel() * 4),
+                    "mode": "streamed: per-step H2D of the tile images and "
+                            "D2H of the refined tiles on a copy stream, "
+                            "double-buffered against the kernels"},
             "gpu_launches": int(launches),
             "wall_s_timed": round(wall, 3),
         }
