@@ -18,7 +18,7 @@
 namespace ts {
 namespace {
 
-constexpr int kMaxCavity = 256;
+constexpr int kMaxCavity = 176;  // with the mesh: 31.5 KB, 7 patch-warps per SM
 // Patches up to kSmemPoints keep their whole mesh (triangles + circumcircle
 // cache, SoA) in shared memory: every insertion rewrites a few slots and the
 // next one re-reads them, so a global-memory mesh turns each step into a
@@ -28,7 +28,8 @@ constexpr int kMaxCavity = 256;
 constexpr int kSmemPoints = 384;
 constexpr int kSmemSlots = 2 * kSmemPoints + 8;
 constexpr size_t kDelaunaySmem = (size_t)kSmemSlots * (3 * sizeof(int) + 3 * sizeof(double)) +
-                                 kMaxCavity * sizeof(int) + (kMaxCavity + 8) * sizeof(int2);
+                                 kMaxCavity * sizeof(int) + (kMaxCavity + 8) * sizeof(int2) +
+                                 3 * kMaxCavity * sizeof(int);
 
 struct PatchPts {
   const double* xy;
@@ -82,10 +83,6 @@ struct Mesh {
   }
 };
 
-__device__ __forceinline__ bool has_edge(const int* t, int a, int b) {
-  return (t[0] == a && t[1] == b) || (t[1] == a && t[2] == b) ||
-         (t[2] == a && t[0] == b);
-}
 
 __global__ void __launch_bounds__(32)
 delaunay_kernel(const double* __restrict__ xy_all,
@@ -99,6 +96,7 @@ delaunay_kernel(const double* __restrict__ xy_all,
   int* s_tri = reinterpret_cast<int*>(s_r2 + kSmemSlots);
   int* bad = s_tri + 3 * kSmemSlots;
   int2* edge = reinterpret_cast<int2*>(bad + kMaxCavity);
+  int* ekey = reinterpret_cast<int*>(edge + kMaxCavity + 8);  // [3 * kMaxCavity]
   const int lane = threadIdx.x;
   const int p = blockIdx.x;
   const int64_t off = pts_off[p];
@@ -142,20 +140,28 @@ delaunay_kernel(const double* __restrict__ xy_all,
     if (nb == 0) continue;  // exact duplicate of an inserted vertex
     if (nb > kMaxCavity) { st = TS_E_INVALID; break; }
     __syncwarp();
-    // 2. boundary edges of the cavity (edges without a bad twin)
+    // 2. boundary edges of the cavity (edges without a bad twin): every
+    //    directed cavity edge is published as a key (u << 16 | w); an edge
+    //    is interior iff its reverse key is present (vertex ids < 2^16)
+    for (int e = lane; e < 3 * nb; e += 32) {
+      const int i = e / 3, j = e - 3 * i;
+      const int* t = M.tri + 3 * bad[i];
+      ekey[e] = (t[j] << 16) | t[j == 2 ? 0 : j + 1];
+    }
+    __syncwarp();
     int ne = 0;
     for (int e0 = 0; e0 < 3 * nb; e0 += 32) {
       const int e = e0 + lane;
       bool keep = false;
       int u = 0, w = 0;
       if (e < 3 * nb) {
-        const int i = e / 3, j = e - 3 * i;
-        const int* t = M.tri + 3 * bad[i];
-        u = t[j];
-        w = t[j == 2 ? 0 : j + 1];
+        const int key = ekey[e];
+        u = key >> 16;
+        w = key & 0xFFFF;
+        const int twin = (w << 16) | u;
         keep = true;
-        for (int k = 0; k < nb && keep; ++k)
-          if (k != i && has_edge(M.tri + 3 * bad[k], w, u)) keep = false;
+        for (int k = 0; k < 3 * nb; ++k)
+          if (ekey[k] == twin) { keep = false; break; }
         if (keep) {
           double ux, uy, wx, wy;
           P.get(u, ux, uy);
