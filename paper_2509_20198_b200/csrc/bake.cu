@@ -18,22 +18,22 @@
 // against the reference's sequential fp64 bincount sums that is a mean
 // difference <= 2e-9 m in height and <= 3e-8 in colour.
 //
-// One persistent CTA per SM walks a contiguous range of whole 2,048-point
-// batches (two points per thread); positions are staged into shared memory
-// one batch ahead by cp.async.bulk (mbarrier complete_tx), colours are read
-// directly (coalesced) before the wait.  The CTA's shared memory also holds the
-// accumulators of ONE "hot" patch (count, z as lo/hi 32-bit words with the
-// lo carry folded into hi, r/g/b u32 = 24 B x 4096 texels = 96 KB);
-// (point, key) pairs of the hot patch accumulate there with native 32-bit
-// shared atomics, all others go straight to the global int64 accumulators.
-// A u32 colour sum that wraps adds its carry (2^32) to the global sum, so
-// the shared sums are exact.  After each batch the CTA counts the threads
-// that missed the hot patch (the barrier that also frees the staging
-// buffer); if they are the majority, the hot patch is flushed (global
-// atomics of the non-empty texels) and replaced by the patch of the batch's
-// last point.  Input grouped by patch (engine._bake_one order, configs[2])
-// runs ~98% in shared memory; shuffled input degrades to global atomics
-// without flush churn.
+// One persistent CTA per SM walks a contiguous range of whole 1,984-point
+// batches: 31 worker warps (two points per thread) and one staging warp.
+// The staging warp bulk-copies positions into a double buffer
+// (cp.async.bulk, mbarrier complete_tx) and, one batch ahead of the
+// workers, decides whether a batch switches the CTA's "hot" patch (its
+// first and last points belong to the same patch, not the current one);
+// workers read the decision behind a per-buffer "ready" mbarrier and
+// release buffers with per-warp arrivals, so there is no block-wide barrier
+// per batch, only at the (rare) switches.  The hot patch's accumulators
+// (count, z as lo/hi 32-bit words with the lo carry folded into hi, r/g/b
+// u32 = 24 B x 4096 texels = 96 KB) live in shared memory and take native
+// 32-bit shared atomics; other (point, key) pairs go straight to the global
+// int64 accumulators.  A u32 colour sum that wraps adds its carry (2^32) to
+// the global sum, so the shared sums are exact.  Input grouped by patch
+// (engine._bake_one order, configs[2]) runs ~96% in shared memory;
+// shuffled input never switches and degrades to global atomics.
 #include <algorithm>
 
 #include "tc_ptx.cuh"
@@ -43,10 +43,11 @@ namespace ts {
 namespace {
 
 constexpr int kTex = kOut * kOut;  // 4096 texels per patch
-constexpr int kBakeThreads = 1024;  // one CTA per SM
-constexpr int kBakeU = 2;            // points per thread per batch
-constexpr int kBatch = kBakeU * kBakeThreads;
-constexpr int kBufs = 2;             // staged xyz batches (48 KB each)
+constexpr int kBakeThreads = 1024;  // one CTA per SM: 31 worker warps + 1 staging warp
+constexpr int kWorkers = kBakeThreads - 32;
+constexpr int kBakeU = 2;            // points per worker thread per batch
+constexpr int kBatch = kBakeU * kWorkers;   // 1,984 points (even: 16-byte aligned)
+constexpr int kBufs = 2;             // staged xyz batches (46.5 KB each)
 constexpr double kZScale = 268435456.0;          // 2^28
 constexpr double kZInv = 1.0 / 268435456.0;
 constexpr float kCScale = 16777216.0f;            // 2^24
@@ -119,9 +120,24 @@ struct HotSmem {
   // (the lo word's carry goes into the hi word), colour sums
   uint32_t cnt[kTex], zlo[kTex], zhi[kTex], c[3][kTex];
   double xyz[kBufs][kBatch * 3];  // staged positions (bulk copies)
-  uint64_t full[kBufs];
-  int last_key[2];  // by batch parity (a fast thread may write the next one)
+  uint64_t full[kBufs], ready[kBufs], empty[kBufs];
+  int dec[kBufs];  // per staged batch: patch to switch the hot set to, or -1
 };
+
+__device__ __forceinline__ void worker_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kWorkers) : "memory");
+}
+
+// first key whose window holds point i (-1: none)
+__device__ __forceinline__ int first_key_of(const BakeArgs& A, double x, double y) {
+  int32_t k0, k1;
+  if (!candidates(A, x, y, k0, k1)) return -1;
+  for (int32_t k = k0; k < k1; ++k) {
+    int key;
+    if (texel_of(A, k, x, y, key) >= 0) return key;
+  }
+  return -1;
+}
 
 __global__ void __launch_bounds__(kBakeThreads, 1) bake_splat_kernel(BakeArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -132,32 +148,89 @@ __global__ void __launch_bounds__(kBakeThreads, 1) bake_splat_kernel(BakeArgs A)
   }
   // CTA ranges are whole batches, so every staged batch starts 16-byte
   // aligned (given 16-byte aligned arrays, checked by the host)
-  const int64_t nb = ceil_div<int64_t>(A.m, kBatch);
-  const int64_t per = ceil_div<int64_t>(nb, gridDim.x) * kBatch;
+  const int64_t nbt = ceil_div<int64_t>(A.m, kBatch);
+  const int64_t per = ceil_div<int64_t>(nbt, gridDim.x) * kBatch;
   const int64_t lo = (int64_t)blockIdx.x * per;
   const int64_t hi = min(A.m, lo + per);
+  const int64_t nb = hi > lo ? ceil_div<int64_t>(hi - lo, kBatch) : 0;
   const bool has_rgb = A.rgb != nullptr;
-  // full batches come in by cp.async.bulk, kBufs ahead; a ragged last
-  // batch (or unaligned arrays) is read straight from global memory
-  auto staged = [&](int64_t base) { return A.bulk && base + kBatch <= hi; };
-  auto issue = [&](int64_t base, int buf) {
-    if (base < hi && staged(base)) {
-      const uint32_t bx = kBatch * 3 * sizeof(double);
-      tcx::fence_proxy_async();
-      tcx::mbar_arrive_tx(&S.full[buf], bx);
-      tcx::bulk_g2s(S.xyz[buf], A.xyz + 3 * base, bx, &S.full[buf]);
-    }
-  };
+  // full batches come in by cp.async.bulk; a ragged last batch (or
+  // unaligned arrays) is read straight from global memory
+  auto staged = [&](int64_t i) { return A.bulk && lo + (i + 1) * kBatch <= hi; };
   if (tid == 0) {
-    S.last_key[0] = S.last_key[1] = -1;
-    for (int b = 0; b < kBufs; ++b) tcx::mbar_init(&S.full[b], 1);
+    for (int b = 0; b < kBufs; ++b) {
+      tcx::mbar_init(&S.full[b], 1);
+      tcx::mbar_init(&S.ready[b], 1);
+      tcx::mbar_init(&S.empty[b], kWorkers / 32);
+    }
     tcx::fence_barrier_init();
   }
   __syncthreads();
-  if (tid == 0)
-    for (int b = 0; b < kBufs; ++b) issue(lo + (int64_t)b * kBatch, b);
+
+  if (tid >= kWorkers) {
+    // ---------------- staging + hot-patch decisions (one warp) ----------------
+    const int lane = tid & 31;
+    auto issue = [&](int64_t i) {
+      if (i < nb && staged(i) && lane == 0) {
+        const int b = (int)(i & 1);
+        const uint32_t bx = kBatch * 3 * sizeof(double);
+        tcx::fence_proxy_async();
+        tcx::mbar_arrive_tx(&S.full[b], bx);
+        tcx::bulk_g2s(S.xyz[b], A.xyz + 3 * (lo + i * kBatch), bx, &S.full[b]);
+      }
+    };
+    int hot = -1;
+    // batch i switches the hot patch when its first and last points belong
+    // to the same patch, not the current one (grouped input: once per
+    // patch; shuffled input: never, everything goes to global atomics)
+    auto decide = [&](int64_t i) {
+      const int b = (int)(i & 1);
+      const int64_t base = lo + i * kBatch, last = min(hi, base + kBatch) - 1;
+      // buffer b's previous batch (i - 2) must be fully consumed before its
+      // decision slot and ready phase are reused (staged batches already
+      // waited for that before their copy was issued)
+      if (i >= 2 && !staged(i) && lane == 0)
+        tcx::mbar_wait(&S.empty[b], (uint32_t)(((i - 2) >> 1) & 1));
+      __syncwarp();
+      int key = -1;
+      if (lane < 2) {
+        const int64_t q = lane ? last : base;
+        double x, y;
+        if (staged(i)) {
+          tcx::mbar_wait(&S.full[b], (uint32_t)((i >> 1) & 1));
+          const int j = (int)(q - base);
+          x = S.xyz[b][3 * j]; y = S.xyz[b][3 * j + 1];
+        } else {
+          x = A.xyz[3 * q]; y = A.xyz[3 * q + 1];
+        }
+        key = first_key_of(A, x, y);
+      }
+      const int ka = __shfl_sync(0xFFFFFFFFu, key, 0), kz = __shfl_sync(0xFFFFFFFFu, key, 1);
+      const int sw = (ka >= 0 && ka == kz && ka != hot) ? ka : -1;
+      if (sw >= 0) hot = sw;
+      if (lane == 0) {
+        S.dec[b] = sw;
+        tcx::mbar_arrive(&S.ready[b]);  // release: dec[b] and the staged data
+      }
+      __syncwarp();
+    };
+    issue(0);
+    issue(1);
+    if (nb > 0) decide(0);
+    for (int64_t i = 0; i < nb; ++i) {
+      if (i + 1 < nb) decide(i + 1);
+      if (i + 2 < nb && staged(i + 2)) {
+        if (lane == 0) tcx::mbar_wait(&S.empty[i & 1], (uint32_t)((i >> 1) & 1));
+        __syncwarp();
+        issue(i + 2);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------ workers ------------------------------
   auto flush = [&](int hot) {
-    for (int t = tid; t < kTex; t += kBakeThreads) {
+    for (int t = tid; t < kTex; t += kWorkers) {
       const uint32_t n = S.cnt[t];
       if (n) {
         atomicAdd(A.cnt + (int64_t)hot * kTex + t, n);
@@ -172,93 +245,82 @@ __global__ void __launch_bounds__(kBakeThreads, 1) bake_splat_kernel(BakeArgs A)
       S.cnt[t] = 0; S.zlo[t] = 0; S.zhi[t] = 0; S.c[0][t] = 0; S.c[1][t] = 0; S.c[2][t] = 0;
     }
   };
-  int hot = -1, par = 0, buf = 0;
-  uint32_t phase = 0;
-  for (int64_t base = lo; base < hi; base += kBatch, par ^= 1) {
-    const int64_t last = min(hi, base + kBatch) - 1;
+  int hot = -1;
+  for (int64_t i = 0; i < nb; ++i) {
+    const int b = (int)(i & 1);
+    const int64_t base = lo + i * kBatch;
     // colours straight from global (coalesced 12-byte runs), issued before
-    // the staged positions are waited for
+    // the batch is waited for
     float cv[kBakeU][3];
 #pragma unroll
     for (int u = 0; u < kBakeU; ++u) {
-      const int64_t i = base + u * kBakeThreads + tid;
+      const int64_t q = base + u * kWorkers + tid;
       cv[u][0] = cv[u][1] = cv[u][2] = 0.f;
-      if (has_rgb && i < hi) {
-        cv[u][0] = __ldg(A.rgb + 3 * i); cv[u][1] = __ldg(A.rgb + 3 * i + 1);
-        cv[u][2] = __ldg(A.rgb + 3 * i + 2);
+      if (has_rgb && q < hi) {
+        cv[u][0] = __ldg(A.rgb + 3 * q); cv[u][1] = __ldg(A.rgb + 3 * q + 1);
+        cv[u][2] = __ldg(A.rgb + 3 * q + 2);
       }
     }
-    const bool stg = staged(base);
-    if (stg) tcx::mbar_wait(&S.full[buf], phase);
-    int miss = 0;
+    tcx::mbar_wait(&S.ready[b], (uint32_t)((i >> 1) & 1));
+    const int sw = S.dec[b];
+    if (sw >= 0) {  // known to every worker: switch the hot patch
+      worker_sync();  // all workers are done with the previous batch
+      if (hot >= 0) flush(hot);
+      worker_sync();
+      hot = sw;
+    }
+    const bool stg = staged(i);
 #pragma unroll
     for (int u = 0; u < kBakeU; ++u) {
-      const int j = u * kBakeThreads + tid;
-      const int64_t i = base + j;
-      if (i >= hi) continue;
+      const int j = u * kWorkers + tid;
+      const int64_t q = base + j;
+      if (q >= hi) continue;
       double x, y, z;
-      if (stg) { x = S.xyz[buf][3 * j]; y = S.xyz[buf][3 * j + 1]; z = S.xyz[buf][3 * j + 2]; }
-      else { x = A.xyz[3 * i]; y = A.xyz[3 * i + 1]; z = A.xyz[3 * i + 2]; }
+      if (stg) { x = S.xyz[b][3 * j]; y = S.xyz[b][3 * j + 1]; z = S.xyz[b][3 * j + 2]; }
+      else { x = A.xyz[3 * q]; y = A.xyz[3 * q + 1]; z = A.xyz[3 * q + 2]; }
       int32_t k0 = 0, k1 = 0;
-      int first = -1;
-      if (candidates(A, x, y, k0, k1)) {
-        const long long zf = __double2ll_rn(dmul(z, kZScale));
-        for (int32_t k = k0; k < k1; ++k) {
-          int key;
-          const int t = texel_of(A, k, x, y, key);
-          if (t < 0) continue;
-          if (first < 0) first = key;
-          if (key == hot) {
-            atomicAdd(&S.cnt[t], 1u);
-            const uint32_t zl = (uint32_t)zf;
-            const uint32_t old = atomicAdd(&S.zlo[t], zl);
-            atomicAdd(&S.zhi[t], (uint32_t)((unsigned long long)zf >> 32) + (old + zl < old ? 1u : 0u));
-            if (has_rgb) {
+      if (!candidates(A, x, y, k0, k1)) continue;
+      const long long zf = __double2ll_rn(dmul(z, kZScale));
+      for (int32_t k = k0; k < k1; ++k) {
+        int key;
+        const int t = texel_of(A, k, x, y, key);
+        if (t < 0) continue;
+        if (key == hot) {
+          atomicAdd(&S.cnt[t], 1u);
+          const uint32_t zl = (uint32_t)zf;
+          const uint32_t old = atomicAdd(&S.zlo[t], zl);
+          atomicAdd(&S.zhi[t], (uint32_t)((unsigned long long)zf >> 32) + (old + zl < old ? 1u : 0u));
+          if (has_rgb) {
 #pragma unroll
-              for (int ch = 0; ch < 3; ++ch) {
-                const float v = cv[u][ch];
-                if (v >= 0.f && v < 256.f) {
-                  const uint32_t q = __float2uint_rn(v * kCScale);
-                  const uint32_t o = atomicAdd(&S.c[ch][t], q);
-                  if (o + q < o)  // carry out of the 32-bit shared sum
-                    atomicAdd(A.sum + ((int64_t)key * 4 + ch + 1) * kTex + t, 1ull << 32);
-                } else {
-                  atomicAdd(A.sum + ((int64_t)key * 4 + ch + 1) * kTex + t,
-                            (unsigned long long)__double2ll_rn((double)v * (double)kCScale));
-                }
+            for (int ch = 0; ch < 3; ++ch) {
+              const float v = cv[u][ch];
+              if (v >= 0.f && v < 256.f) {
+                const uint32_t qv = __float2uint_rn(v * kCScale);
+                const uint32_t o = atomicAdd(&S.c[ch][t], qv);
+                if (o + qv < o)  // carry out of the 32-bit shared sum
+                  atomicAdd(A.sum + ((int64_t)key * 4 + ch + 1) * kTex + t, 1ull << 32);
+              } else {
+                atomicAdd(A.sum + ((int64_t)key * 4 + ch + 1) * kTex + t,
+                          (unsigned long long)__double2ll_rn((double)v * (double)kCScale));
               }
             }
-          } else {
-            ++miss;
-            unsigned long long* gs = A.sum + (int64_t)key * 4 * kTex + t;
-            atomicAdd(A.cnt + (int64_t)key * kTex + t, 1u);
-            atomicAdd(gs, (unsigned long long)zf);
-            if (has_rgb)
-#pragma unroll
-              for (int ch = 0; ch < 3; ++ch)
-                atomicAdd(gs + (ch + 1) * kTex,
-                          (unsigned long long)__double2ll_rn((double)cv[u][ch] * (double)kCScale));
           }
+        } else {
+          unsigned long long* gs = A.sum + (int64_t)key * 4 * kTex + t;
+          atomicAdd(A.cnt + (int64_t)key * kTex + t, 1u);
+          atomicAdd(gs, (unsigned long long)zf);
+          if (has_rgb)
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch)
+              atomicAdd(gs + (ch + 1) * kTex,
+                        (unsigned long long)__double2ll_rn((double)cv[u][ch] * (double)kCScale));
         }
       }
-      if (i == last) S.last_key[par] = first;
     }
-    // every thread is done with this buffer: refill it kBufs batches ahead;
-    // switch the hot patch when most of the batch missed it (grouped input:
-    // once per patch)
-    const int nmiss = __syncthreads_count(2 * miss > kBakeU);
-    if (tid == 0) issue(base + (int64_t)kBufs * kBatch, buf);
-    if (++buf == kBufs) { buf = 0; phase ^= 1; }
-    if (nmiss * 2 > kBakeThreads) {
-      const int next = S.last_key[par];
-      if (next >= 0 && next != hot) {  // block-uniform
-        if (hot >= 0) flush(hot);
-        hot = next;
-        __syncthreads();
-      }
-    }
+    __syncwarp();
+    if ((tid & 31) == 0) tcx::mbar_arrive(&S.empty[b]);  // this warp is done with buffer b
   }
-  __syncthreads();
+  worker_sync();
   if (hot >= 0) flush(hot);
 }
 
