@@ -124,6 +124,17 @@ struct HotSmem {
   int dec[kBufs];  // per staged batch: patch to switch the hot set to, or -1
 };
 
+// shared-window atomics on explicit shared addresses (no generic-address
+// conversion per operation)
+__device__ __forceinline__ void red_sh(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_sh(uint32_t a, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ void worker_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kWorkers) : "memory");
 }
@@ -246,6 +257,8 @@ __global__ void __launch_bounds__(kBakeThreads, 1) bake_splat_kernel(BakeArgs A)
     }
   };
   int hot = -1;
+  const uint32_t sh_cnt = tcx::su32(S.cnt), sh_zlo = tcx::su32(S.zlo), sh_zhi = tcx::su32(S.zhi),
+                 sh_c = tcx::su32(S.c[0]);
   for (int64_t i = 0; i < nb; ++i) {
     const int b = (int)(i & 1);
     const int64_t base = lo + i * kBatch;
@@ -286,17 +299,17 @@ __global__ void __launch_bounds__(kBakeThreads, 1) bake_splat_kernel(BakeArgs A)
         const int t = texel_of(A, k, x, y, key);
         if (t < 0) continue;
         if (key == hot) {
-          atomicAdd(&S.cnt[t], 1u);
+          red_sh(sh_cnt + 4 * t, 1u);
           const uint32_t zl = (uint32_t)zf;
-          const uint32_t old = atomicAdd(&S.zlo[t], zl);
-          atomicAdd(&S.zhi[t], (uint32_t)((unsigned long long)zf >> 32) + (old + zl < old ? 1u : 0u));
+          const uint32_t old = atom_sh(sh_zlo + 4 * t, zl);
+          red_sh(sh_zhi + 4 * t, (uint32_t)((unsigned long long)zf >> 32) + (old + zl < old ? 1u : 0u));
           if (has_rgb) {
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) {
               const float v = cv[u][ch];
               if (v >= 0.f && v < 256.f) {
                 const uint32_t qv = __float2uint_rn(v * kCScale);
-                const uint32_t o = atomicAdd(&S.c[ch][t], qv);
+                const uint32_t o = atom_sh(sh_c + 4 * (ch * kTex + t), qv);
                 if (o + qv < o)  // carry out of the 32-bit shared sum
                   atomicAdd(A.sum + ((int64_t)key * 4 + ch + 1) * kTex + t, 1ull << 32);
               } else {
