@@ -29,7 +29,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kCells = kRes * kRes;
-constexpr int kSmemPts = 512;          // points cached in shared memory
+constexpr int kSmemPts = 384;          // points cached in shared memory (4 CTAs per SM)
 constexpr int kSmemTri = 2 * kSmemPts + 8;
 constexpr int kBins = 16;              // NN bin grid over [-1,1]^2
 
@@ -120,7 +120,7 @@ struct RasterArgs {
   int32_t* status;
 };
 
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 4)
 raster_kernel(RasterArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   int* s_face = reinterpret_cast<int*>(smem);                       // 9216
