@@ -77,9 +77,12 @@ __global__ void chunk_count_kernel(const uint8_t* __restrict__ bytes,
   status[i] = st;
 }
 
-constexpr uint32_t kDecodeSmemWords = 12 * 1024;  // 24 KB of models per thread
-constexpr int kDecodeBlock = 8;                     // 192 KB shared per CTA
+constexpr uint32_t kDecodeSmemWords = 12 * 1024;  // 24 KB of models per tile (warp)
+constexpr int kDecodeWarps = 8;                     // 192 KB shared per CTA
 
+// One warp per tile: the table is decoded by the 32 lanes in lockstep
+// (laz::WChunkTableCoder), which rebuild each adaptive model's tables
+// together; lane 0 writes the results.
 __global__ void chunk_decode_kernel(const uint8_t* __restrict__ bytes,
                                     const ts_tile_desc* __restrict__ tiles,
                                     int n_tiles,
@@ -90,38 +93,37 @@ __global__ void chunk_decode_kernel(const uint8_t* __restrict__ bytes,
                                     int32_t* status, uint16_t* scratch,
                                     uint32_t scratch_words) {
   extern __shared__ __align__(16) uint16_t s_pool[];
-  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
-  laz::ChunkTableCoder coder;
-  for (int i = gtid; i < n_tiles; i += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int gwarp = blockIdx.x * kDecodeWarps + wib;
+  const int nwarps = gridDim.x * kDecodeWarps;
+  laz::WChunkTableCoder coder;
+  for (int i = gwarp; i < n_tiles; i += nwarps) {
     if (status[i] != TS_OK) continue;
     const ts_tile_desc t = tiles[i];
     const int64_t b0 = base[i];
     const int64_t n = base[i + 1] - b0;
     int32_t st = TS_OK;
     if (!t.compressed) {
-      int64_t left = t.point_count;
-      for (int64_t k = 0; k < n; ++k) {
-        const int64_t c = left < t.las_stride ? left : t.las_stride;
+      for (int64_t k = lane; k < n; k += 32) {
+        const int64_t left = t.point_count - k * (int64_t)t.las_stride;
         offsets[b0 + k] = t.point_data_offset + k * t.las_stride * t.record_length;
-        counts[b0 + k] = c;
-        left -= c;
+        counts[b0 + k] = left < t.las_stride ? left : t.las_stride;
       }
-      if (chunk_end) chunk_end[i] = t.point_data_offset + t.point_count * t.record_length;
+      if (chunk_end && lane == 0)
+        chunk_end[i] = t.point_data_offset + t.point_count * t.record_length;
       continue;
     }
     const uint8_t* f = bytes + t.file_offset;
     const int64_t pos = table_position(f, t, &st);
     const bool variable = t.chunk_size == 0xFFFFFFFFu;
+    int64_t off = t.point_data_offset + 8;
     if (st == TS_OK && n > 0) {
       laz::Decoder dec;
-      // model tables live in shared memory (every symbol decode reads and
-      // adapts them; a global-memory pool made each step an L1/L2 round
-      // trip), overflowing to the per-thread global scratch
-      coder.init(s_pool + (size_t)threadIdx.x * kDecodeSmemWords, kDecodeSmemWords,
-                 scratch + (size_t)gtid * scratch_words);
+      coder.init(s_pool + (size_t)wib * kDecodeSmemWords, kDecodeSmemWords,
+                 scratch + (size_t)gwarp * scratch_words, lane);
       if (!dec.start(f, pos + 8, t.file_size)) st = TS_E_CORRUPT_TABLE;
       int32_t pc = 0, ps = 0;
-      int64_t off = t.point_data_offset + 8, total = 0;
+      int64_t total = 0;
       int64_t left = t.point_count;
       for (int64_t k = 0; k < n && st == TS_OK; ++k) {
         int64_t cnt;
@@ -135,18 +137,21 @@ __global__ void chunk_decode_kernel(const uint8_t* __restrict__ bytes,
         ps = coder.decompress(dec, ps, 1);
         if (dec.desync) { st = TS_E_CORRUPT_TABLE; break; }
         if (ps <= 0) { st = TS_E_CORRUPT_TABLE; break; }
-        offsets[b0 + k] = off;
-        counts[b0 + k] = cnt;
+        if (lane == 0) {
+          offsets[b0 + k] = off;
+          counts[b0 + k] = cnt;
+        }
         off += ps;
         total += cnt;
       }
       if (st == TS_OK && (total != t.point_count || off > pos))
         st = TS_E_CORRUPT_TABLE;
-      if (chunk_end) chunk_end[i] = off;
+      if (chunk_end && lane == 0) chunk_end[i] = off;
     } else if (st == TS_OK && t.point_count != 0) {
       st = TS_E_CORRUPT_TABLE;  // zero chunks but points declared
     }
-    status[i] = st;
+    if (lane == 0) status[i] = st;
+    __syncwarp();
   }
 }
 
@@ -311,7 +316,7 @@ __global__ void colors_kernel(const uint8_t* __restrict__ rec, int64_t n, int rs
   }
 }
 
-constexpr int kDecodeThreads = 148 * kDecodeBlock;
+constexpr int kDecodeThreads = 148 * kDecodeWarps;  // decoding warps
 
 uint32_t decode_pool_words() {
   // mirror of ChunkTableCoder::pool_words() on the host
@@ -353,16 +358,16 @@ extern "C" int ts_chunk_decode(const uint8_t* d_bytes, const ts_tile_desc* d_til
                                int64_t* d_chunk_end, int32_t* d_status, void* d_scratch,
                                void* stream) {
   if (n_tiles <= 0) return n_tiles == 0 ? TS_OK : TS_E_INVALID;
-  const int threads = n_tiles < kDecodeThreads ? n_tiles : kDecodeThreads;
-  const int block = kDecodeBlock;
-  const size_t smem = (size_t)block * kDecodeSmemWords * sizeof(uint16_t);
+  const int threads = n_tiles < kDecodeThreads ? n_tiles : kDecodeThreads;  // warps
+  const int block = 32 * kDecodeWarps;
+  const size_t smem = (size_t)kDecodeWarps * kDecodeSmemWords * sizeof(uint16_t);
   static bool configured = false;
   if (!configured) {
     TS_CUDA_TRY(cudaFuncSetAttribute(chunk_decode_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
-  ts::count_launch(), chunk_decode_kernel<<<ceil_div(threads, block), block, smem, as_stream(stream)>>>(
+  ts::count_launch(), chunk_decode_kernel<<<ceil_div(threads, kDecodeWarps), block, smem, as_stream(stream)>>>(
       d_bytes, d_tiles, n_tiles, d_chunk_base, d_chunk_offset, d_chunk_points,
       d_chunk_end, d_status, reinterpret_cast<uint16_t*>(d_scratch), decode_pool_words());
   TS_LAUNCH_CHECK();

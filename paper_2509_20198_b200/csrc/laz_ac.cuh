@@ -240,5 +240,176 @@ struct ChunkTableCoder {
   }
 };
 
+
+// ---------------------------------------------------------------------
+// Warp-cooperative flavour (device only).  The 32 lanes of a warp hold
+// identical decoder state in registers and take identical branches; the
+// adaptive symbol models' tables (shared memory) are rebuilt by all lanes
+// together (counts halving, the prefix sum behind dist[], the decode lookup
+// table by binary search), and the decode path's count update is written
+// by lane 0.  Produces exactly the serial coder's tables.
+struct WSymModel {
+  uint32_t n, tot, cyc, left, tbits, tshift;
+  uint16_t* dist;
+  uint16_t* cnt;
+  uint16_t* table;
+  __device__ void init(uint32_t nsym, uint16_t* mem, int lane) {
+    n = nsym;
+    tbits = SymModel::table_bits(n);
+    tshift = tbits ? 15 - tbits : 0;
+    dist = mem;
+    cnt = mem + n;
+    table = tbits ? mem + 2 * n : nullptr;
+    for (uint32_t k = lane; k < n; k += 32) cnt[k] = 1;
+    __syncwarp();
+    tot = 0;
+    cyc = n;
+    update(lane);
+    cyc = left = (n + 6) >> 1;
+  }
+  __device__ void update(int lane) {
+    tot += cyc;
+    if (tot > 32768u) {
+      uint32_t part = 0;
+      for (uint32_t k = lane; k < n; k += 32) {
+        const uint32_t c = (cnt[k] + 1u) >> 1;
+        cnt[k] = (uint16_t)c;
+        part += c;
+      }
+      tot = __reduce_add_sync(0xFFFFFFFFu, part);
+      __syncwarp();
+    }
+    const uint32_t scale = 0x80000000u / tot;
+    uint32_t carry = 0;
+    for (uint32_t b = 0; b < n; b += 32) {
+      const uint32_t k = b + lane;
+      const uint32_t c = k < n ? cnt[k] : 0u;
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (k < n) dist[k] = (uint16_t)((scale * (carry + incl - c)) >> 16);
+      carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    }
+    __syncwarp();
+    if (tbits) {
+      // table[j] = (first k with dist[k] >> tshift >= j) - 1, or n - 1;
+      // table[0] = 0 (the serial fill loop's result)
+      const uint32_t size = 1u << tbits;
+      for (uint32_t j = lane; j <= size + 1; j += 32) {
+        uint32_t v;
+        if (j == 0) {
+          v = 0;
+        } else {
+          uint32_t lo = 0, hi = n;  // first k in [0, n] with w_k >= j
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (((uint32_t)dist[mid] >> tshift) >= j) hi = mid; else lo = mid + 1;
+          }
+          v = lo < n ? lo - 1 : n - 1;
+        }
+        table[j] = (uint16_t)v;
+      }
+      __syncwarp();
+    }
+    cyc = min((5u * cyc) >> 2, (n + 6) << 3);
+    left = cyc;
+  }
+};
+
+__device__ __forceinline__ uint32_t wsymbol(Decoder& d, WSymModel& m, int lane) {
+  uint32_t hi = d.length;
+  uint32_t lo, s;
+  const uint32_t unit = d.length >> 15;
+  d.length = unit;
+  if (m.tbits) {
+    const uint32_t dv = d.value / unit;
+    const uint32_t t = dv >> m.tshift;
+    s = m.table[t];
+    uint32_t n = (uint32_t)m.table[t + 1] + 1;
+    while (n > s + 1) {
+      const uint32_t k = (s + n) >> 1;
+      if (m.dist[k] > dv) n = k; else s = k;
+    }
+    lo = m.dist[s] * unit;
+    if (s != m.n - 1) hi = m.dist[s + 1] * unit;
+  } else {
+    lo = 0; s = 0;
+    uint32_t n = m.n, k = n >> 1;
+    do {
+      const uint32_t z = unit * m.dist[k];
+      if (z > d.value) { n = k; hi = z; } else { s = k; lo = z; }
+      k = (s + n) >> 1;
+    } while (k != s);
+  }
+  d.value -= lo;
+  d.length = hi - lo;
+  if (d.length < kMinLen) d.renorm();
+  __syncwarp();  // every lane has read the model before it changes
+  if (lane == 0) ++m.cnt[s];
+  __syncwarp();
+  if (--m.left == 0) m.update(lane);
+  return s;
+}
+
+struct WChunkTableCoder {
+  WSymModel kmod[2];
+  bool kmod_live[2];
+  BitModel cbit;
+  bool cbit_live;
+  WSymModel cmod[32];
+  bool cmod_live[32];
+  uint16_t* pool;
+  uint16_t* overflow;
+  uint32_t used, budget, used_over;
+  int lane;
+
+  __device__ void init(uint16_t* fast, uint32_t fast_words, uint16_t* over, int ln) {
+    pool = fast; budget = fast_words; overflow = over; used = 0; used_over = 0; lane = ln;
+    kmod_live[0] = kmod_live[1] = false;
+    cbit_live = false;
+    for (int k = 0; k < 32; ++k) cmod_live[k] = false;
+  }
+  __device__ WSymModel& alloc(WSymModel& m, bool& live, uint32_t n) {
+    if (!live) {
+      const uint32_t w = SymModel::words16(n);
+      if (used + w <= budget) {
+        m.init(n, pool + used, lane);
+        used += w;
+      } else {
+        m.init(n, overflow + used_over, lane);
+        used_over += w;
+      }
+      live = true;
+    }
+    return m;
+  }
+  __device__ int32_t decompress(Decoder& d, int32_t pred, int ctx) {
+    const uint32_t k = wsymbol(d, alloc(kmod[ctx], kmod_live[ctx], 33), lane);
+    int64_t c;
+    if (k == 0) {
+      if (!cbit_live) { cbit.init(); cbit_live = true; }
+      c = d.bit(cbit);
+    } else if (k < 32) {
+      WSymModel& m = alloc(cmod[k], cmod_live[k], 1u << (k < 8 ? k : 8));
+      if (k <= 8) {
+        c = wsymbol(d, m, lane);
+      } else {
+        const uint32_t lowb = k - 8;
+        const uint32_t hi = wsymbol(d, m, lane);
+        const uint32_t lo = d.raw_bits(lowb);
+        c = ((int64_t)hi << lowb) | lo;
+      }
+      if (c >= (int64_t(1) << (k - 1))) c += 1;
+      else c -= (int64_t(1) << k) - 1;
+    } else {
+      c = -(int64_t)0x80000000LL;
+    }
+    return (int32_t)(uint32_t)((int64_t)pred + c);
+  }
+};
+
 }  // namespace laz
 }  // namespace ts
