@@ -5,11 +5,12 @@
 // The four layers read disjoint channels of the same B x 96 x 96 x 8 CNN
 // input, so one CTA stages the input halo of a 4 x 16 output tile ONCE for
 // all of them (the per-layer direct kernel read it four times) and its 16
-// warps split as 4 encoders x 2 output-channel halves (each thread: 2 pixels x C_out/2).  fp32 CUDA-core FMAs (thin K: 9
+// warps split as 4 encoders x C_out/16 output-channel groups (each thread: 2 pixels x 16 channels).  fp32 CUDA-core FMAs (thin K: 9
 // or 27 MACs per output channel), outputs written straight into the
 // space-to-depth layout the stride-2 tensor-core layers consume (a pixel's
-// C_out channels are one contiguous run there: float4 stores).  Two
-// 256-thread CTAs per SM so one CTA's halo load overlaps the other's FMAs.
+// C_out channels are one contiguous run there: 32-byte stores).
+// CTAs of 4 x C_out/16 warps, two per SM, so one CTA's halo load overlaps the
+// other's FMAs.
 //
 // Shared memory: halo [8 ch][9 rows][2 column parities][20] (stride-2
 // reads become stride-1 per parity plane: bank-conflict free), weights
@@ -27,7 +28,9 @@ constexpr int kETY = 4, kETX = 16;          // output tile
 constexpr int kEHY = 2 * kETY + 1;          // 9 halo rows
 constexpr int kEPitch = 20;                 // floats per parity row (>= 17; 4*pitch = 16 mod 32)
 constexpr int kEPlane = kEHY * 2 * kEPitch; // floats per channel
-constexpr int kEThreads = 256;  // 4 encoders x 2 channel halves; 2 CTAs per SM
+// threads per CTA: 4 encoders x C_out/16 channel groups of 16 (one warp each)
+template <int CO>
+__host__ __device__ constexpr int enc0_threads() { return 4 * (CO / 16) * 32; }
 
 __device__ __forceinline__ float lrelu(float v) { return v >= 0.f ? v : 0.01f * v; }
 
@@ -65,7 +68,8 @@ __device__ __forceinline__ void enc0_accumulate(const float* __restrict__ halo, 
 }
 
 template <int CO>
-__global__ void __launch_bounds__(kEThreads, 2) conv_enc0_kernel(Enc0Op E) {
+__global__ void __launch_bounds__(enc0_threads<CO>(), 2) conv_enc0_kernel(Enc0Op E) {
+  constexpr int kEThreads = enc0_threads<CO>();
   extern __shared__ __align__(16) float sm[];
   float* halo = sm;                                   // 8 * kEPlane
   float* sw = halo + 8 * kEPlane;                     // weights, 4 encoders
@@ -81,8 +85,8 @@ __global__ void __launch_bounds__(kEThreads, 2) conv_enc0_kernel(Enc0Op E) {
   const float* sbias = sw + ((woff[3] + 9 * E.cin[3] * CO + 3) & ~3);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int e = warp & 3;                             // encoder of this warp
-  constexpr int CH = CO / 2;                          // channels per thread
-  const int chalf = (warp >> 2) * CH;                 // which half of C_out
+  constexpr int CH = 16;                              // channels per thread
+  const int chalf = (warp >> 2) * CH;                 // which channel group
   const int ty = lane >> 4, tx = lane & 15;           // rows ty and ty + 2
   const int wy = E.oy1 - E.oy0, wx = E.ox1 - E.ox0;
   const int ntx = (wx + kETX - 1) / kETX, nty = (wy + kETY - 1) / kETY;
@@ -173,7 +177,7 @@ int launch_conv_enc0(const Enc0Op& E, int co, void* stream) {
     TS_CUDA_TRY(cudaFuncSetAttribute(conv_enc0_kernel<CO>,                             \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,      \
                                      (int)smem));                                      \
-    ts::count_launch(), conv_enc0_kernel<CO><<<grid, kEThreads, smem, s>>>(E);         \
+    ts::count_launch(), conv_enc0_kernel<CO><<<grid, enc0_threads<CO>(), smem, s>>>(E); \
   } while (0)
   if (co == 48) TS_ENC0(48);
   else if (co == 32) TS_ENC0(32);
