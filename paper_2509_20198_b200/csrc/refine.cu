@@ -100,6 +100,7 @@ struct ts_weights {
   size_t cat_off = 0, fuse_in_off = 0;
   bool enc0_fused = false;  // the four encoders' first layers in one launch
   bool fuse_in_planes = false;  // fuse-input buffer (raw inputs + decoders)
+  ts::Win fuse_in_win{0, 0, 0, 0};  // the part of it fuse.0 reads (crop-aware)
   std::vector<void*> device_allocs;
 };
 
@@ -184,10 +185,16 @@ Win unite(const Win& a, const Win& b) {
              std::max(a.x1, b.x1)};
 }
 
-__global__ void copy_inputs_kernel(const float* __restrict__ in, int64_t pixels,
-                                   float* __restrict__ out, int cstride, int planes) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pixels;
-       i += (int64_t)gridDim.x * blockDim.x) {
+// raw inputs -> channels [0, 8) of the fuse input, over the window
+// [y0, y0 + wy) x [x0, x0 + wx) that fuse.0 reads
+__global__ void copy_inputs_kernel(const float* __restrict__ in, int64_t n_win,
+                                   float* __restrict__ out, int cstride, int planes,
+                                   int y0, int x0, int wy, int wx) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n_win;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = w / ((int64_t)wy * wx);
+    const int r = (int)(w - b * wy * wx);
+    const int64_t i = (b * kRes + y0 + r / wx) * kRes + x0 + r % wx;  // pixel
     float v[8];
     tcx::ld_v8(in + 8 * i, v);
     if (planes) {  // pre-split channels 0..7 of the fuse input
@@ -377,6 +384,7 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
   Win crop{kCrop, kCrop + kOut, kCrop, kCrop + kOut};
   auto propagate = [&]() {
     const Win fuse_in_need = back(7, crop);
+    W->fuse_in_win = fuse_in_need;
     Win merge_need = unite(back(5, fuse_in_need), back(6, fuse_in_need));
     Win enc_need = back(4, merge_need);
     for (int s = 0; s < 4; ++s) back(s, enc_need);
@@ -750,10 +758,12 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
     auto buf = [&](size_t off) { return ws + off * B; };
     // raw inputs -> channels [0, 8) of the fuse input (skip concat)
     {
-      const int64_t px = (int64_t)B * kRes * kRes;
+      const Win& fw = W->fuse_in_win;
+      const int wy = fw.y1 - fw.y0, wx = fw.x1 - fw.x0;
+      const int64_t px = (int64_t)B * wy * wx;
       ts::count_launch(), copy_inputs_kernel<<<(int)std::min<int64_t>(ceil_div<int64_t>(px, 256), 148 * 16),
                            256, 0, s>>>(in, px, buf(W->fuse_in_off), W->fuse_in_c,
-                                        W->fuse_in_planes ? 1 : 0);
+                                        W->fuse_in_planes ? 1 : 0, fw.y0, fw.x0, wy, wx);
       TS_LAUNCH_CHECK();
     }
     const int enc_ch0[4] = {0, 1, 2, 5};
