@@ -589,9 +589,19 @@ def run_reference(args, rank, world):
         "unit": "heightmaps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32 CNN, f64 geometry", "data": "synthetic",
-        "config": {"workload": "configs[1] sample: "
-                               f"{args.cpu_sample} patches per step"},
+        "dtype": "f32 CNN, f64 geometry",
+        "data": "synthetic (seeded FractalTerrain stub-body LAZ tiles, "
+                "random He weights seed 3)",
+        "config": {"workload": "configs[1]: 1,024-tile synthetic "
+                               "terrain per GPU, chunk-point extraction "
+                               "+ rasterise + CNN refine",
+                   "tiles_per_gpu": TILES_PER_GPU_SIDE ** 2,
+                   "chunks_per_tile": CHUNKS_PER_TILE,
+                   "points_per_chunk": POINTS_PER_CHUNK,
+                   "sample": f"each step: {args.cpu_sample} patches of the "
+                             "workload (8x8 tile corner) through the "
+                             "reference algorithm on all host cores",
+                   "parallelism": "CPU process pool (rank 0 only)"},
         "cpu_baseline": {"value": round(value, 3), "unit": "heightmaps/s",
                          "cores": cores, "kind": "port",
                          "sample": f"{args.cpu_sample} patches per step"},
