@@ -294,6 +294,22 @@ def test_random_patches_vs_oracle():
         assert np.abs(raw.hm_lin - want["hm_lin"]).max() <= 1e-6, trial
 
 
+def test_large_patches_use_the_global_mesh_paths():
+    """Patches beyond the shared-memory caches (Delaunay 384 points, raster
+    384 points) take the global-memory mesh / point paths."""
+    from paper_2509_20198_b200.patches import (PatchSpacePoints,
+                                               interpolate_patch)
+    rng = np.random.default_rng(77)
+    for n in (385, 900, 1500):
+        xy = rng.uniform(-1, 1, (n, 2))
+        h = rng.uniform(-0.7, 0.7, n)
+        raw = interpolate_patch(PatchSpacePoints(xy, h, None))
+        want = opatch.interpolate(xy, h, None, 0.0)
+        assert np.array_equal(raw.hm_nn, want["hm_nn"]), n
+        assert np.array_equal(raw.face_map.cells >= 0, want["face"] >= 0), n
+        assert np.abs(raw.hm_lin - want["hm_lin"]).max() <= 1e-6, n
+
+
 def test_nearest_neighbor_query():
     from paper_2509_20198_b200.errors import EmptySet
     from paper_2509_20198_b200.patches import (PatchSpacePoints,
