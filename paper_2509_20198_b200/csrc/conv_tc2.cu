@@ -61,13 +61,11 @@ struct Halo2Args {
   ConvOp op;
   const uint8_t* wpk;  // packed weights: kHdr-byte stage list, then
                        // [n_tile][stage][plane][BN][64 B] SW64 images
-  int bn, sub, hbufs, bstages, cchunks, taps, wp, lrows, n_tiles, accbufs, nstg;
+  int bn, sub, hbufs, bstages, cchunks, taps, wp, lrows, n_tiles, accbufs;
   int stack;  // 1: B planes stacked along N (PB*BN columns per sub-tile);
               // 0: every product accumulates into the same BN columns
   int64_t m_tiles, positions;
   unsigned long long* dbg;  // TS_H2_DBG timestamps (CTA 0), or null
-  int exp;  // timing experiments only (TS_H2_EXP bits): 1 weights once, 2 no halo
-           // fill, 4 no epilogue work, 8 no MMAs
 };
 
 __device__ __forceinline__ void prod_sync() {
@@ -505,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
 }
 
 struct Halo2Plan {
-  int bn, ntiles, pa, pb, sub, hbufs, bstages, cchunks, wp, lrows, accbufs, nstg, stack;
+  int bn, ntiles, pa, pb, sub, hbufs, bstages, cchunks, wp, lrows, accbufs, stack;
   size_t smem;
   int64_t positions;
 };
@@ -555,19 +553,16 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
     const size_t fixed = 1024 + 8 * 40 + 16 + 16 * (size_t)L + 6 * kMaxStages + 64 +
                          4 * (size_t)p.ntiles * p.bn + 16;
     for (int hb : {3, 2}) {
-      for (int ns : {0}) {
-        const size_t used = hb * hbuf + fixed;
-        if (used + 3 * bst > cap) continue;
-        p.sub = sub;
-        p.accbufs = ab;
-        p.hbufs = hb;
-        p.nstg = ns;
-        p.lrows = L;
-        p.bstages = (int)std::min<size_t>(8, (cap - used) / bst);
-        p.smem = used + p.bstages * bst;
-        *out = p;
-        return true;
-      }
+      const size_t used = hb * hbuf + fixed;
+      if (used + 3 * bst > cap) continue;
+      p.sub = sub;
+      p.accbufs = ab;
+      p.hbufs = hb;
+      p.lrows = L;
+      p.bstages = (int)std::min<size_t>(8, (cap - used) / bst);
+      p.smem = used + p.bstages * bst;
+      *out = p;
+      return true;
     }
   }
   return false;
@@ -650,14 +645,8 @@ int launch_conv_tc_halo2(const ConvOp& op, int precision, void* stream) {
   if (!plan2(op, precision, &p)) return TS_E_INVALID;
   if (p.positions + 128 * p.sub + p.lrows >= (int64_t)INT32_MAX) return TS_E_INVALID;
   Halo2Args a{op, op.w_tc, p.bn, p.sub, p.hbufs, p.bstages, p.cchunks, op.k * op.k, p.wp,
-              p.lrows, p.ntiles, p.accbufs, p.nstg, p.stack,
-              ceil_div<int64_t>(p.positions, 128 * p.sub), p.positions, nullptr, 0};
-  static int exp = -1;
-  if (exp < 0) {
-    const char* e = getenv("TS_H2_EXP");
-    exp = e ? atoi(e) : 0;
-  }
-  a.exp = exp;
+              p.lrows, p.ntiles, p.accbufs, p.stack,
+              ceil_div<int64_t>(p.positions, 128 * p.sub), p.positions, nullptr};
   const int64_t tiles = a.m_tiles * p.ntiles;
   if (tiles <= 0) return TS_OK;
   static int dbg_at = -2, launch_no = 0;

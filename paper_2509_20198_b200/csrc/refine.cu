@@ -59,10 +59,6 @@ struct ConvLayer {
   const uint8_t* w_tc = nullptr;  // tensor-core packed weights (or null)
   int w_layout = 0;               // which TC kernel the packed weights serve
   size_t out_off = 0;   // workspace offset (floats) of the output buffer
-  bool materialize = false;  // tensor-core mode: up2 input copied once, then a
-                             // stride-1 halo conv (conv_tc.cu)
-  size_t up_off = 0;         // workspace offset of the upsampled input
-  Win up_win{0, 0, 0, 0};    // upsampled-coordinate window that is copied
   int out_cstride = 0, out_coff = 0;
   int in_src = -1;      // -1: external/concat buffers handled by the planner
   // space-to-depth execution of a stride-2 3x3 layer (conv.cuh ActView):
@@ -205,27 +201,6 @@ __global__ void copy_inputs_kernel(const float* __restrict__ in, int64_t n_win,
 #pragma unroll
       for (int c = 0; c < 8; ++c) out[(int64_t)cstride * i + c] = v[c];
     }
-  }
-}
-
-// Nearest x2 upsample (refiner.py:395) of the window a following stride-1
-// conv reads; lets the tensor-core halo kernel run up2 convolutions.
-__global__ void upsample2_window_kernel(ActView src, float* __restrict__ dst, int64_t n4,
-                                        int H2, int W2, int C, int y0, int y1, int x0,
-                                        int x1) {
-  const int C4 = C / 4, wx = x1 - x0, wy = y1 - y0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int c4 = (int)(i % C4);
-    int64_t r = i / C4;
-    const int X = x0 + (int)(r % wx);
-    r /= wx;
-    const int Y = y0 + (int)(r % wy);
-    const int64_t b = r / wy;
-    const float4 v = *reinterpret_cast<const float4*>(
-        src.base + ((b * src.H + (Y >> 1)) * src.W + (X >> 1)) * src.cstride + src.coff +
-        4 * c4);
-    *reinterpret_cast<float4*>(dst + ((b * H2 + Y) * W2 + X) * C + 4 * c4) = v;
   }
 }
 
@@ -510,13 +485,6 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
       L.out_off = alloc((size_t)L.Hout * L.Wout * L.d.co);
       L.out_cstride = L.d.co; L.out_coff = 0;
     }
-    if (false) {  // up2 is folded into the halo kernel's row table now
-      L.materialize = true;
-      L.up_off = alloc((size_t)4 * L.Hin * L.Win_ * L.d.ci);
-      LayerDesc flat = L.d;
-      flat.up2 = false;
-      L.up_win = need_in(L.out_win, flat, 2 * L.Hin, 2 * L.Win_);
-    }
     const std::string base = std::string(kStages[L.stage]) + "." + std::to_string(L.index);
     auto wi = tensors.find(base + ".weight");
     auto bi = tensors.find(base + ".bias");
@@ -601,7 +569,7 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
       shape.k = dx.k;
       shape.stride = dx.s;
       shape.pad = dx.p;
-      shape.up2 = L.up2 && !L.materialize;
+      shape.up2 = L.up2;
       shape.oy0 = L.out_win.y0; shape.oy1 = L.out_win.y1;
       shape.ox0 = L.out_win.x0; shape.ox1 = L.out_win.x1;
       shape.in.C = dx.ci; shape.in.cstride = dx.ci; shape.out.C = Co;
@@ -812,20 +780,6 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
         op.out.s2d = 1;
       }
       op.up2 = L.up2;
-      if (L.materialize) {
-        float* ub = buf(L.up_off);
-        const int H2 = 2 * op.in.H, W2 = 2 * op.in.W;
-        const int64_t n4 = (int64_t)B * (L.up_win.y1 - L.up_win.y0) *
-                           (L.up_win.x1 - L.up_win.x0) * (L.d.ci / 4);
-        ts::count_launch(),
-            upsample2_window_kernel<<<(int)std::min<int64_t>(ceil_div<int64_t>(n4, 256),
-                                                             148 * 16),
-                                      256, 0, s>>>(op.in, ub, n4, H2, W2, L.d.ci, L.up_win.y0,
-                                                   L.up_win.y1, L.up_win.x0, L.up_win.x1);
-        TS_LAUNCH_CHECK();
-        op.in = ActView{ub, H2, W2, L.d.ci, 0, L.d.ci};
-        op.up2 = 0;
-      }
       op.k = L.dexec.k; op.stride = L.dexec.s; op.pad = L.dexec.p;
       op.lrelu = L.d.lrelu;
       op.oy0 = L.out_win.y0; op.oy1 = L.out_win.y1;

@@ -37,24 +37,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// mbar_wait for warps that can tolerate wake-up latency (epilogue, loader):
-// non-blocking probes with a nanosleep back-off keep them off the issue
-// slots the MMA issuer and the producers need
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
-  uint32_t ok = 0, ns = 32;
-  for (;;) {
-    asm volatile(
-        "{\n.reg .pred P1;\n"
-        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
-        "selp.b32 %0, 1, 0, P1;\n}\n"
-        : "=r"(ok)
-        : "r"(su32(b)), "r"(parity)
-        : "memory");
-    if (ok) return;
-    __nanosleep(ns);
-    if (ns < 256) ns <<= 1;
-  }
-}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
   asm volatile(
