@@ -126,16 +126,25 @@ delaunay_kernel(const double* __restrict__ xy_all,
     double px, py;
     P.get(v, px, py);
     // 1. cavity: triangles whose circumcircle strictly contains v
+    //    (two triangles per lane per pass: independent circle tests in
+    //    flight; cavity order stays ascending)
     int nb = 0;
-    for (int b0 = 0; b0 < ntri; b0 += 32) {
-      const int t = b0 + lane;
-      const bool in = t < ntri && M.in_circle(P, t, px, py) > 0;
-      const unsigned m = __ballot_sync(0xFFFFFFFFu, in);
-      if (in) {
-        const int slot = nb + __popc(m & ((1u << lane) - 1));
-        if (slot < kMaxCavity) bad[slot] = t;
+    for (int b0 = 0; b0 < ntri; b0 += 64) {
+      const int t0 = b0 + lane, t1 = t0 + 32;
+      const bool in0 = t0 < ntri && M.in_circle(P, t0, px, py) > 0;
+      const bool in1 = t1 < ntri && M.in_circle(P, t1, px, py) > 0;
+      const unsigned m0 = __ballot_sync(0xFFFFFFFFu, in0);
+      const unsigned m1 = __ballot_sync(0xFFFFFFFFu, in1);
+      const unsigned below = (1u << lane) - 1;
+      if (in0) {
+        const int slot = nb + __popc(m0 & below);
+        if (slot < kMaxCavity) bad[slot] = t0;
       }
-      nb += __popc(m);
+      if (in1) {
+        const int slot = nb + __popc(m0) + __popc(m1 & below);
+        if (slot < kMaxCavity) bad[slot] = t1;
+      }
+      nb += __popc(m0) + __popc(m1);
     }
     if (nb == 0) continue;  // exact duplicate of an inserted vertex
     if (nb > kMaxCavity) { st = TS_E_INVALID; break; }
