@@ -62,7 +62,10 @@ struct Mesh {
     const double D = 2.0 * (p1 - p2);
     const bool ok = fabs(D) > 1e-6 * (fabs(p1) + fabs(p2)) && fabs(D) > 1e-200;
     const double l1 = ux * ux + uy * uy, l2 = vx * vx + vy * vy;
-    const double ox = (vy * l1 - uy * l2) / D, oy = (ux * l2 - vx * l1) / D;
+    // one divide: the cache only feeds the filter, whose 1e-6 relative
+    // margin dwarfs the extra rounding
+    const double inv = 1.0 / D;
+    const double ox = (vy * l1 - uy * l2) * inv, oy = (ux * l2 - vx * l1) * inv;
     cx[slot] = ax + ox;
     cy[slot] = ay + oy;
     r2[slot] = ok ? ox * ox + oy * oy : __longlong_as_double(0x7ff8000000000000LL);
