@@ -377,7 +377,7 @@ constexpr int kHThreads = (kProdWarps + 1 + 4 + 1) * 32;  // + B-loader warp 13
 struct HaloArgs {
   ConvOp op;
   const uint8_t* wpk;   // [n_tile][chunk][tap][plane][BN][128 B]
-  int bn, bstages, cchunks, taps, wp, lrows, n_tiles, bofs;
+  int bn, bstages, cchunks, taps, wp, lrows, n_tiles;
   int64_t m_tiles, positions;
 };
 
@@ -723,7 +723,6 @@ bool halo_plan(const ConvOp& op, int precision, HaloPlan* hp) {
   return true;
 }
 
-int g_halo_bofs = -1;
 
 }  // namespace
 
@@ -805,12 +804,8 @@ std::vector<uint8_t> pack_tc_weights(const float* w_oikk, int co, int ci, int k,
 int launch_conv_tc_halo(const ConvOp& op, int precision, void* stream) {
   HaloPlan h;
   if (!halo_plan(op, precision, &h)) return TS_E_INVALID;
-  if (g_halo_bofs < 0) {
-    const char* e = getenv("TS_HALO_BOFS");
-    g_halo_bofs = (e && e[0] == '1') ? 1 : 0;
-  }
   HaloArgs a{op, op.w_tc, h.base.bn, h.bstages, h.base.cchunks, op.k * op.k, h.wp,
-             h.lrows, h.base.ntiles, g_halo_bofs,
+             h.lrows, h.base.ntiles,
              ceil_div<int64_t>(h.positions, BM), h.positions};
   const int64_t tiles = a.m_tiles * h.base.ntiles;
   if (tiles <= 0) return TS_OK;
