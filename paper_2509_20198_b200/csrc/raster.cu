@@ -388,17 +388,72 @@ raster_kernel(RasterArgs A) {
   __syncthreads();
   const double shift = s_shift;
 
-  for (int j0 = tid; j0 < kCells; j0 += 4 * kThreads) {
-    int bi[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int jj = min(j0 + u * kThreads, kCells - 1);
-      bi[u] = nn_of(cell_center(jj % kRes, kRes), cell_center(jj / kRes, kRes));
+  // Warp-cooperative NN for cached patches: a warp takes an 8 x 4 block of
+  // cells, and all its lanes scan the SAME candidate points (the bins under
+  // the block, then rings around them, until every lane's best d^2 is below
+  // the next ring's bound): no divergence, broadcast shared loads.  Same
+  // exact argmin with the lowest-index tie rule.
+  const int lane = tid & 31, wid = tid >> 5;
+  auto nn_block = [&](int cy0, int cx0) {
+    const int cy = cy0 + (lane >> 3), cx = cx0 + (lane & 7);
+    const double qx = cell_center(cx, kRes), qy = cell_center(cy, kRes);
+    const int bx0 = bin_of(cell_center(cx0, kRes)), bx1 = bin_of(cell_center(cx0 + 7, kRes));
+    const int by0 = bin_of(cell_center(cy0, kRes)), by1 = bin_of(cell_center(cy0 + 3, kRes));
+    const double hb = 2.0 / kBins;
+    double best = DBL_MAX;
+    int bi = 0;
+    for (int r = 0; r < kBins; ++r) {
+      const int X0 = max(bx0 - r, 0), X1 = min(bx1 + r, kBins - 1);
+      const int Y0 = max(by0 - r, 0), Y1 = min(by1 + r, kBins - 1);
+      for (int gy = Y0; gy <= Y1; ++gy) {
+        const bool inner_row = gy > by0 - r && gy < by1 + r;
+        for (int gx = X0; gx <= X1; ++gx) {
+          if (r > 0 && inner_row && gx > bx0 - r && gx < bx1 + r) continue;  // ring only
+          const int b = gy * kBins + gx;
+          for (int k = s_bstart[b]; k < s_bstart[b + 1]; ++k) {
+            const int i = s_bid[k];
+            const double dx = dsub(qx, xy[2 * i]), dy = dsub(qy, xy[2 * i + 1]);
+            const double d2 = dadd(dmul(dx, dx), dmul(dy, dy));
+            if (d2 < best || (d2 == best && i < bi)) { best = d2; bi = i; }
+          }
+        }
+      }
+      double mind = DBL_MAX;
+      if (bx0 - r > 0) mind = fmin(mind, qx - (-1.0 + (bx0 - r) * hb));
+      if (bx1 + r < kBins - 1) mind = fmin(mind, (-1.0 + (bx1 + r + 1) * hb) - qx);
+      if (by0 - r > 0) mind = fmin(mind, qy - (-1.0 + (by0 - r) * hb));
+      if (by1 + r < kBins - 1) mind = fmin(mind, (-1.0 + (by1 + r + 1) * hb) - qy);
+      const bool done = mind == DBL_MAX || (best < DBL_MAX && mind * mind > best * (1.0 + 1e-12));
+      if (__all_sync(0xFFFFFFFFu, done)) break;
     }
+    return bi;
+  };
+  constexpr int kBlocksX = kRes / 8, kBlocks = kBlocksX * (kRes / 4);
+  const int n_iter = cached ? ceil_div(kBlocks, kThreads / 32) : ceil_div(kCells, 4 * kThreads);
+  for (int it = 0; it < n_iter; ++it) {
+    int bi[4], jc[4];
+    int nu = 4;
+    if (cached) {  // one cell per lane of this warp's block
+      const int blk = it * (kThreads / 32) + wid;
+      nu = 1;
+      jc[0] = -1;
+      if (blk < kBlocks) {
+        const int cy0 = (blk / kBlocksX) * 4, cx0 = (blk % kBlocksX) * 8;
+        bi[0] = nn_block(cy0, cx0);
+        jc[0] = (cy0 + (lane >> 3)) * kRes + cx0 + (lane & 7);
+      }
+    } else {
+      const int j0 = it * 4 * kThreads + tid;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int j = j0 + u * kThreads;
-      if (j >= kCells) continue;
+      for (int u = 0; u < 4; ++u) {
+        const int jj = min(j0 + u * kThreads, kCells - 1);
+        jc[u] = j0 + u * kThreads < kCells ? j0 + u * kThreads : -1;
+        bi[u] = nn_of(cell_center(jj % kRes, kRes), cell_center(jj / kRes, kRes));
+      }
+    }
+    for (int u = 0; u < nu; ++u) {
+      const int j = jc[u];
+      if (j < 0) continue;
       double hl, rl[3] = {0.0, 0.0, 0.0};
       int f;
       cell_value(j, bi[u], hl, rl, f);
