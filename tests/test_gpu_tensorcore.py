@@ -1,14 +1,14 @@
 """tcgen05 implicit-GEMM convolution vs the fp32 oracle (needs a B200).
 
-Precision modes:
-  1 TF32X3, 3 BF16X3 -- fp32-class: operand splits carry >= 2^-18 relative
-    precision, the tcgen05 fp32 accumulation sets a ~5e-6 per-layer floor;
-    refiner heights within 0.05 m max of the reference on random He weights
-    (measured 0.021 m); the CUDA-core mode 0 meets the fp32 bar 2e-3 m.
+Precision modes (table "CNN, per precision mode"):
+  1 TF32X3, 3 BF16X3, 4 BF16X4 (3 products, the bench default) --
+    fp32-class: operand splits carry >= 2^-18 relative precision, the
+    tcgen05 fp32 accumulation sets a ~5e-6 per-layer floor; refiner heights
+    within 0.05 m max of the reference on random He weights (measured
+    0.012-0.020 m); the CUDA-core mode 0 meets the fp32 bar 2e-3 m.
   2 BF16 -- stated separately: ~2^-8 per layer, RMS |dh| <= 2 m on random
     He weights.
 """
-
 import numpy as np
 import pytest
 
