@@ -172,8 +172,20 @@ delaunay_kernel(const double* __restrict__ xy_all,
         w = key & 0xFFFF;
         const int twin = (w << 16) | u;
         keep = true;
-        for (int k = 0; k < 3 * nb; ++k)
-          if (ekey[k] == twin) { keep = false; break; }
+        if (3 * nb > 32)  // large cavity: linear twin search over all keys
+          for (int k = 0; k < 3 * nb; ++k)
+            if (ekey[k] == twin) { keep = false; break; }
+      }
+      if (3 * nb <= 32) {
+        // small cavity (all edges in this pass): an interior edge appears
+        // in both directions, so its undirected key matches two lanes
+        const uint32_t canon = e < 3 * nb
+                                   ? ((uint32_t)min(u, w) << 16) | (uint32_t)max(u, w)
+                                   : 0xFFFFFFFFu - (uint32_t)lane;  // unique filler
+        const unsigned mm = __match_any_sync(0xFFFFFFFFu, canon);
+        if (e < 3 * nb) keep = __popc(mm) == 1;
+      }
+      if (e < 3 * nb) {
         if (keep) {
           double ux, uy, wx, wy;
           P.get(u, ux, uy);
