@@ -158,10 +158,18 @@ def run_ours(args, rank, world, local_rank):
                                                default_descriptor,
                                                random_weights)
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # TS_BENCH_BACKEND=gloo / TS_BENCH_DEVICE=<i>: exercise the multi-rank
+    # code path on a single-GPU box (every rank on device i, gloo) -- for
+    # testing the harness only; measurements use one GPU per rank + NCCL
+    gpu = int(os.environ.get("TS_BENCH_DEVICE", local_rank))
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("TS_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     precision = PRECISION_BF16X4 if args.precision is None else args.precision
     tiles, own = band_tiles(rank, world)
     images = [t.data for t in tiles]
@@ -228,7 +236,8 @@ def run_ours(args, rank, world, local_rank):
     wall = time.perf_counter() - wall0
     launches = (lib().ts_launch_count() - launches0) // args.steps
     ms = float(np.sum(times)) / args.steps
-    ms_t = torch.tensor([ms], device=dev)
+    red_dev = dev if (world == 1 or dist.get_backend() == "nccl") else "cpu"
+    ms_t = torch.tensor([ms], device=red_dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
@@ -293,7 +302,7 @@ def run_ours(args, rank, world, local_rank):
         t_end.record(stream)
         torch.cuda.synchronize()
     e2e_ms = t_start.elapsed_time(t_end) / n_e2e
-    e2e_t = torch.tensor([e2e_ms], device=dev)
+    e2e_t = torch.tensor([e2e_ms], device=red_dev)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = total_maps / (float(e2e_t.item()) / 1e3)

@@ -34,6 +34,8 @@ def ptr(t) -> C.c_void_p | None:
 
 def upload(a: np.ndarray) -> torch.Tensor:
     a = np.ascontiguousarray(a)
+    if not a.flags.writeable:  # e.g. np.frombuffer over bytes: copy, torch
+        a = a.copy()           # cannot wrap a read-only buffer
     return torch.from_numpy(a).to(device())
 
 

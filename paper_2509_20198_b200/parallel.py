@@ -54,6 +54,9 @@ def gather_tiles(out: torch.Tensor, dst: int = 0):
         return [out]
     world = dist.get_world_size()
     rank = dist.get_rank()
+    if dist.get_backend() == "gloo" and out.is_cuda:  # gloo gathers host tensors
+        res = gather_tiles(out.cpu(), dst)
+        return None if res is None else [r.to(out.device) for r in res]
     n = torch.tensor([out.shape[0]], dtype=torch.int64, device=out.device)
     sizes = [torch.zeros_like(n) for _ in range(world)]
     dist.all_gather(sizes, n)
