@@ -708,6 +708,35 @@ extern "C" size_t ts_refine_workspace(const ts_weights* w, int batch) {
   return (w->per_tile_floats * (size_t)std::max(sb, 1)) * sizeof(float) + 256;
 }
 
+namespace ts {
+namespace {
+// Independent branches of the network (the four encoders, the two
+// decoders) run on forked streams so one branch's persistent-kernel tail
+// is filled by the next branch's tiles.  Per host thread and device.
+struct Branches {
+  cudaStream_t side[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t fork = nullptr, join[3] = {nullptr, nullptr, nullptr};
+  int device = -1;
+};
+int branches_for(Branches*& out) {
+  thread_local Branches cache[8];
+  int dev = 0;
+  TS_CUDA_TRY(cudaGetDevice(&dev));
+  Branches& b = cache[dev & 7];
+  if (b.device != dev) {
+    for (int i = 0; i < 3; ++i) {
+      TS_CUDA_TRY(cudaStreamCreateWithFlags(&b.side[i], cudaStreamNonBlocking));
+      TS_CUDA_TRY(cudaEventCreateWithFlags(&b.join[i], cudaEventDisableTiming));
+    }
+    TS_CUDA_TRY(cudaEventCreateWithFlags(&b.fork, cudaEventDisableTiming));
+    b.device = dev;
+  }
+  out = &b;
+  return TS_OK;
+}
+}  // namespace
+}  // namespace ts
+
 extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, float* d_out,
                          uint8_t* d_nonfinite, void* d_workspace, void* stream) {
   if (!W || batch < 0) return TS_E_INVALID;
@@ -720,6 +749,28 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
   }
   float* ws = reinterpret_cast<float*>(d_workspace);
   const int fcs = W->layers.back().d.co;
+  Branches* br = nullptr;
+  {
+    const char* e = getenv("TS_BRANCH_STREAMS");
+    if (!(e && e[0] == '0')) {
+      const int st = branches_for(br);
+      if (st != TS_OK) return st;
+    }
+  }
+  // region 0: encoder branches (stages 0-3), region 1: decoders (5, 6)
+  auto nside = [](int region) { return region == 0 ? 3 : 1; };
+  auto fork = [&](int region) -> int {
+    TS_CUDA_TRY(cudaEventRecord(br->fork, s));
+    for (int k = 0; k < nside(region); ++k) TS_CUDA_TRY(cudaStreamWaitEvent(br->side[k], br->fork, 0));
+    return TS_OK;
+  };
+  auto join = [&](int region) -> int {
+    for (int k = 0; k < nside(region); ++k) {
+      TS_CUDA_TRY(cudaEventRecord(br->join[k], br->side[k]));
+      TS_CUDA_TRY(cudaStreamWaitEvent(s, br->join[k], 0));
+    }
+    return TS_OK;
+  };
   for (int b0 = 0; b0 < batch; b0 += kSubBatch) {
     const int B = std::min(kSubBatch, batch - b0);
     const float* in = d_in + (size_t)b0 * kRes * kRes * 8;
@@ -739,10 +790,25 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
     const float* prev_base = nullptr;
     int prev_H = 0, prev_cs = 0, prev_coff = 0, prev_C = 0, prev_planes = 0;
     int prev_stage = -1;
+    int region = -1;
     for (size_t i = 0; i < W->layers.size(); ++i) {
       const ConvLayer& L = W->layers[i];
       ConvOp op{};
       const bool first = (int)L.stage != prev_stage;
+      void* lstream = stream;
+      if (br) {
+        const bool fused0 = W->enc0_fused && L.stage < 4 && L.index == 0;
+        int want = region;
+        if (!(fused0 && L.stage > 0))  // skipped fused layers keep the region
+          want = (L.stage < 4 && !fused0) ? 0 : (L.stage == 5 || L.stage == 6) ? 1 : -1;
+        if (want != region) {
+          if (region >= 0 && join(region) != TS_OK) return TS_E_CUDA;
+          if (want >= 0 && fork(want) != TS_OK) return TS_E_CUDA;
+          region = want;
+        }
+        const int branch = region == 0 ? L.stage : region == 1 ? L.stage - 5 : 0;
+        if (region >= 0 && branch > 0) lstream = br->side[branch - 1];
+      }
       if (first) {
         if (L.stage < 4) {
           op.in = ActView{const_cast<float*>(in), kRes, kRes, 8, enc_ch0[L.stage],
@@ -804,7 +870,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
             ++e;
           }
           E.oy0 = L.out_win.y0; E.oy1 = L.out_win.y1; E.ox0 = L.out_win.x0; E.ox1 = L.out_win.x1;
-          st = launch_conv_enc0(E, L.d.co, stream);
+          st = launch_conv_enc0(E, L.d.co, lstream);
           if (st != TS_OK) return st;
         }
         prev_base = buf(L.out_off); prev_H = L.Hout; prev_cs = L.out_cstride;
@@ -821,7 +887,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
           q.ph = 1; q.ph_y = p >> 1; q.ph_x = p & 1;
           q.oy0 = w.y0; q.oy1 = w.y1; q.ox0 = w.x0; q.ox1 = w.x1;
           q.w_tc = L.w_ph[p]; q.w_layout = 2;
-          st = launch_conv_tc_halo2(q, W->precision, stream);
+          st = launch_conv_tc_halo2(q, W->precision, lstream);
           if (st != TS_OK) return st;
         }
         prev_base = op.out.base; prev_H = L.Hout; prev_cs = L.out_cstride;
@@ -838,16 +904,17 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
                            !op.out.s2d;
       if (conv_direct_supported(op) && !thin_tc &&
           (op.in.C <= 4 || op.out.C <= 16 || W->precision == 0))
-        st = launch_conv_direct(op, stream);
+        st = launch_conv_direct(op, lstream);
       else if (L.w_tc && conv_tc_supported(op, W->precision))
-        st = launch_conv_tc(op, W->precision, stream);
+        st = launch_conv_tc(op, W->precision, lstream);
       else
-        st = launch_conv_simt(op, stream);
+        st = launch_conv_simt(op, lstream);
       if (st != TS_OK) return st;
       prev_base = op.out.base; prev_H = L.Hout; prev_cs = L.out_cstride;
       prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? 1 : 0;
       prev_stage = L.stage;
     }
+    if (br && region >= 0 && join(region) != TS_OK) return TS_E_CUDA;
     const ConvLayer& last = W->layers.back();
     ts::count_launch(), refine_epilogue_kernel<<<B, 256, 0, s>>>(buf(last.out_off), fcs, 0, in,
                                              d_out + (size_t)b0 * kOut * kOut * 4,
