@@ -775,16 +775,21 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
     const int B = std::min(kSubBatch, batch - b0);
     const float* in = d_in + (size_t)b0 * kRes * kRes * 8;
     auto buf = [&](size_t off) { return ws + off * B; };
-    // raw inputs -> channels [0, 8) of the fuse input (skip concat)
-    {
+    // raw inputs -> channels [0, 8) of the fuse input (skip concat); with
+    // branch streams it runs beside the encoders (joined before the merge)
+    bool copied = false;
+    auto copy_inputs = [&](cudaStream_t cs) -> int {
       const Win& fw = W->fuse_in_win;
       const int wy = fw.y1 - fw.y0, wx = fw.x1 - fw.x0;
       const int64_t px = (int64_t)B * wy * wx;
       ts::count_launch(), copy_inputs_kernel<<<(int)std::min<int64_t>(ceil_div<int64_t>(px, 256), 148 * 16),
-                           256, 0, s>>>(in, px, buf(W->fuse_in_off), W->fuse_in_c,
-                                        W->fuse_in_planes ? 1 : 0, fw.y0, fw.x0, wy, wx);
+                           256, 0, cs>>>(in, px, buf(W->fuse_in_off), W->fuse_in_c,
+                                         W->fuse_in_planes ? 1 : 0, fw.y0, fw.x0, wy, wx);
       TS_LAUNCH_CHECK();
-    }
+      copied = true;
+      return TS_OK;
+    };
+    if (!br && copy_inputs(s) != TS_OK) return TS_E_CUDA;
     const int enc_ch0[4] = {0, 1, 2, 5};
     const int enc_cin[4] = {1, 1, 3, 3};
     const float* prev_base = nullptr;
@@ -804,6 +809,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
         if (want != region) {
           if (region >= 0 && join(region) != TS_OK) return TS_E_CUDA;
           if (want >= 0 && fork(want) != TS_OK) return TS_E_CUDA;
+          if (want == 0 && !copied && copy_inputs(br->side[2]) != TS_OK) return TS_E_CUDA;
           region = want;
         }
         const int branch = region == 0 ? L.stage : region == 1 ? L.stage - 5 : 0;
@@ -915,6 +921,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
       prev_stage = L.stage;
     }
     if (br && region >= 0 && join(region) != TS_OK) return TS_E_CUDA;
+    if (!copied) return TS_E_INVALID;  // every plan has an encoder region
     const ConvLayer& last = W->layers.back();
     ts::count_launch(), refine_epilogue_kernel<<<B, 256, 0, s>>>(buf(last.out_off), fcs, 0, in,
                                              d_out + (size_t)b0 * kOut * kOut * 4,
