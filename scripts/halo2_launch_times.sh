@@ -1,0 +1,9 @@
+# per-launch ncu times of the 35 wide-M halo launches of one bench step
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:conv_tc_halo2 -s 35 -c 35 --csv --log-file gpurun_out/h2_times.csv python bench.py --steps 1 --warmup 1 --no-cpu --no-splat --no-sweep > /dev/null 2>&1
+python - <<'PY'
+import csv
+r=list(csv.reader(open('gpurun_out/h2_times.csv')))
+hi=next(i for i,x in enumerate(r) if 'Metric Value' in x); h=r[hi]; vi=h.index('Metric Value')
+v=[float(x[vi].replace(',',''))/1e3 for x in r[hi+1:]]
+print(' '.join(f'{t:.0f}' for t in v), ' total', round(sum(v)))
+PY
