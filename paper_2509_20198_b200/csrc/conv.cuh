@@ -103,6 +103,12 @@ struct Enc0Op {
 bool conv_enc0_supported(const Enc0Op& e, int co);
 int launch_conv_enc0(const Enc0Op& e, int co, void* stream);
 
+// fuse.2-shaped layers (3x3 s1 p1, 32 -> 4): fp32 CUDA cores with the
+// weights in the kernel parameters (conv_final.cu)
+bool conv_final_supported(const ConvOp& op);
+int launch_conv_final(const ConvOp& op, const float* w_packed, const float* bias_host,
+                      void* stream);
+
 int launch_conv_simt(const ConvOp& op, void* stream);
 bool conv_direct_supported(const ConvOp& op);
 int launch_conv_direct(const ConvOp& op, void* stream);

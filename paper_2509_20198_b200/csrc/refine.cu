@@ -71,6 +71,7 @@ struct ConvLayer {
   bool poly = false;
   const uint8_t* w_ph[4] = {nullptr, nullptr, nullptr, nullptr};
   Win ph_win[4];
+  std::vector<float> w_host, b_host;  // final-layer kernel: weights as parameters
   bool h2 = false;          // executed on the wide-M halo kernel (or phases)
   bool out_planes = false;  // writes pre-split planes (conv.cuh ActView)
 };
@@ -522,6 +523,16 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
             packed[(size_t)((ky * dx.k + kx) * dx.ci + ci) * Co + o] =
                 src[(((size_t)o * dx.ci + ci) * dx.k + ky) * dx.k + kx];
     params += packed.size() + Co;
+    {  // the last layer (fuse.2 shape) runs on conv_final.cu when it fits
+      ConvOp fs{};
+      fs.k = dx.k; fs.stride = dx.s; fs.pad = dx.p; fs.up2 = L.up2;
+      fs.in.C = dx.ci; fs.in.cstride = dx.ci; fs.out.C = Co; fs.out.cstride = Co;
+      const char* e = getenv("TS_FINAL");
+      if (i == nL - 1 && conv_final_supported(fs) && !(e && e[0] == '0')) {
+        L.w_host = packed;
+        L.b_host = bi->second.second;
+      }
+    }
     TS_CUDA_TRY(cudaMalloc(&L.w, packed.size() * sizeof(float)));
     TS_CUDA_TRY(cudaMalloc(&L.b, Co * sizeof(float)));
     W->device_allocs.push_back(L.w);
@@ -904,6 +915,14 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
       // thin layers (few input or output channels: an MMA tile would be
       // mostly padding) -> fp32 direct kernel; the rest -> tensor cores (or
       // the fp32 CUDA-core GEMM in precision mode 0)
+      if (!L.w_host.empty() && conv_final_supported(op)) {
+        st = launch_conv_final(op, L.w_host.data(), L.b_host.data(), lstream);
+        if (st != TS_OK) return st;
+        prev_base = op.out.base; prev_H = L.Hout; prev_cs = L.out_cstride;
+        prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? 1 : 0;
+        prev_stage = L.stage;
+        continue;
+      }
       // (thin outputs with a wide input, e.g. fuse.2 32 -> 4, stay on the
       // wide-M halo kernel: N = 16 columns per plane, K = 9 x 32)
       const bool thin_tc = op.out.C <= 16 && op.in.C > 4 && L.w_tc && L.w_layout == 2 &&
