@@ -395,8 +395,8 @@ extern "C" int ts_bake(const double* d_xyz, const float* d_rgb, int64_t m,
     const int bulk = ((uintptr_t)d_xyz % 16 == 0) && ((uintptr_t)d_rgb % 16 == 0);
     BakeArgs a{d_xyz, d_rgb, m, d_keys, n_patches, d_cell_keys_off, d_cell_keys,
                d_cell_inner, gx0, gy0, gnx, gny, bulk, cnt, sum};
-    static int sms = 0;
-    if (!sms) {
+    int sms = 0;
+    {  // per call: the SM count and the attribute are per device
       int dev = 0;
       TS_CUDA_TRY(cudaGetDevice(&dev));
       TS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

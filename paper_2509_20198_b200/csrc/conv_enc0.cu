@@ -162,12 +162,8 @@ int launch_conv_enc0(const Enc0Op& E, int co, void* stream) {
   if (!conv_enc0_supported(E, co)) return TS_E_INVALID;
   if (E.batch <= 0 || E.oy1 <= E.oy0 || E.ox1 <= E.ox0) return TS_OK;
   const size_t smem = enc0_smem(E, co);
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    TS_CUDA_TRY(cudaGetDevice(&dev));
-    TS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
+  const int sms = sm_count();
+  if (!sms) return TS_E_CUDA;
   const int64_t tiles = (int64_t)E.batch * ((E.oy1 - E.oy0 + kETY - 1) / kETY) *
                         ((E.ox1 - E.ox0 + kETX - 1) / kETX);
   const int grid = (int)std::min<int64_t>(tiles, 2 * sms);

@@ -809,12 +809,8 @@ int launch_conv_tc_halo(const ConvOp& op, int precision, void* stream) {
              ceil_div<int64_t>(h.positions, BM), h.positions};
   const int64_t tiles = a.m_tiles * h.base.ntiles;
   if (tiles <= 0) return TS_OK;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    TS_CUDA_TRY(cudaGetDevice(&dev));
-    TS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
+  const int sms = sm_count();
+  if (!sms) return TS_E_CUDA;
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
   cudaStream_t s = as_stream(stream);
 #define TS_TCH_LAUNCH(MD)                                                             \
@@ -862,12 +858,8 @@ int launch_conv_tc(const ConvOp& op, int precision, void* stream) {
   TcArgs a{op, op.w_tc, p.bn, p.stages, p.kiters, p.cchunks, p.ntiles,
            ceil_div<int64_t>(M, BM), p.wide};
   const int64_t tiles = a.m_tiles * p.ntiles;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    TS_CUDA_TRY(cudaGetDevice(&dev));
-    TS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
+  const int sms = sm_count();
+  if (!sms) return TS_E_CUDA;
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
   cudaStream_t s = as_stream(stream);
 #define TS_TC_LAUNCH(MD)                                                              \

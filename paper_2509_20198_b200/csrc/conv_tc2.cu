@@ -659,12 +659,8 @@ int launch_conv_tc_halo2(const ConvOp& op, int precision, void* stream) {
     TS_CUDA_TRY(cudaMalloc(&a.dbg, 5 * 4096 * sizeof(unsigned long long)));
     TS_CUDA_TRY(cudaMemset(a.dbg, 0, 5 * 4096 * sizeof(unsigned long long)));
   }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    TS_CUDA_TRY(cudaGetDevice(&dev));
-    TS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
+  const int sms = sm_count();
+  if (!sms) return TS_E_CUDA;
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
   cudaStream_t s = as_stream(stream);
 #define TS_TCH2_LAUNCH(MD, SB_)                                                       \

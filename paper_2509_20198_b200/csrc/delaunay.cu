@@ -238,14 +238,12 @@ extern "C" int ts_triangulate(const double* d_xy, const int64_t* d_pts_off,
                               int32_t* d_status, void* d_scratch, void* stream) {
   if (n_patches <= 0) return TS_OK;
   if (!d_scratch) return TS_E_INVALID;
-  static bool configured = false;
-  if (!configured) {
+  {  // per call: the attribute is per device (one process may drive several)
     TS_CUDA_TRY(cudaFuncSetAttribute(delaunay_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kDelaunaySmem));
     TS_CUDA_TRY(cudaFuncSetAttribute(delaunay_kernel,
                                      cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    configured = true;
   }
   ts::count_launch(),
       delaunay_kernel<<<n_patches, 32, kDelaunaySmem, as_stream(stream)>>>(

@@ -361,11 +361,9 @@ extern "C" int ts_chunk_decode(const uint8_t* d_bytes, const ts_tile_desc* d_til
   const int threads = n_tiles < kDecodeThreads ? n_tiles : kDecodeThreads;  // warps
   const int block = 32 * kDecodeWarps;
   const size_t smem = (size_t)kDecodeWarps * kDecodeSmemWords * sizeof(uint16_t);
-  static bool configured = false;
-  if (!configured) {
+  {  // per call: the attribute is per device (one process may drive several)
     TS_CUDA_TRY(cudaFuncSetAttribute(chunk_decode_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
   }
   ts::count_launch(), chunk_decode_kernel<<<ceil_div(threads, kDecodeWarps), block, smem, as_stream(stream)>>>(
       d_bytes, d_tiles, n_tiles, d_chunk_base, d_chunk_offset, d_chunk_points,

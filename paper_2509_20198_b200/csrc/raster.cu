@@ -502,14 +502,12 @@ extern "C" int ts_raster(const double* d_xy, const double* d_h, const float* d_p
                          float* d_rgb_nn, float* d_rgb_lin, int32_t* d_face,
                          double* d_cz_out, int32_t* d_status, void* stream) {
   if (n_patches <= 0) return TS_OK;
-  static bool configured = false;
-  if (!configured) {
+  {  // per call: the attribute is per device (one process may drive several)
     TS_CUDA_TRY(cudaFuncSetAttribute(raster_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kRasterSmem));
     TS_CUDA_TRY(cudaFuncSetAttribute(raster_kernel,
                                      cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    configured = true;
   }
   RasterArgs a{d_xy, d_h, d_prgb, d_pts_off, d_tri, d_tri_off, d_ntri, d_cz_in,
                recenter, d_cnn_in, d_hm_nn, d_hm_lin, d_rgb_nn, d_rgb_lin, d_face,
