@@ -97,3 +97,40 @@ def test_tensor_core_refine_batch_invariance_at_scale():
         n1 = torch.zeros(1, dtype=torch.uint8, device="cuda")
         w.run(x[i:i + 1].contiguous(), 1, o1, n1)
         assert torch.equal(o1[0], out[i]), i
+
+
+@pytest.mark.parametrize("precision", [0, 4])
+def test_colourless_tiles_through_the_pipeline(precision):
+    """Point format 0 (no RGB): the CNN sees zero colour channels
+    (refiner.py:458-468) and heights still match the oracle."""
+    from paper_2509_20198_b200 import _device as D
+    from paper_2509_20198_b200 import synth
+    from paper_2509_20198_b200.lasio import parse_header
+    from paper_2509_20198_b200.pipeline import HeightmapPipeline
+    from paper_2509_20198_b200.refiner import default_descriptor, random_weights
+    tiles = synth.chunked_terrain_tiles(3, 3, chunks_per_tile=150, point_format=0)
+    descs = np.concatenate([D.tile_desc(parse_header(t.data)) for t in tiles])
+    tb = D.TileBatch([t.data for t in tiles], descs)
+    bundle = random_weights(default_descriptor(), seed=3)
+    pipe = HeightmapPipeline(bundle, precision)
+    centers = np.array([[t.x0 + 320.0, t.y0 + 320.0] for t in tiles])
+    res = pipe.run(tb, centers)
+    out = res["out"].cpu().numpy()
+    cnn_in = res["cnn_in"].cpu().numpy()
+    assert (cnn_in[..., 2:] == 0).all()
+    index = opatch.Index()
+    for t in tiles:
+        r = olaz.chunk_points(t.data)
+        hf = olaz.header_fields(t.data)
+        assert olaz.colors(r) is None
+        index.add(olaz.positions(r, hf["scale"], hf["offset"]), None)
+    layers = oref.text_to_layers(bundle.descriptor.to_text())
+    tensors = oref.random_tensors(layers, seed=3)
+    tol = 2e-3 if precision == 0 else 5e-2
+    for p in (0, 4, 8):
+        want = opatch.reconstruct(tuple(centers[p]), index)
+        assert want["rgb_nn"] is None
+        ref = oref.refine(layers, tensors, oref.stage_inputs(
+            want["hm_nn"], want["hm_lin"], None, None)[None], [want["hm_lin"]],
+            [None], has_rgb=False)[0]
+        assert np.abs(out[p, :, :, 0] - ref[0]).max() <= tol, p
