@@ -55,7 +55,7 @@ constexpr int kEpiW0 = kProdW + 2, kEpiWarps = 8;
 static_assert(kProdW % 2 == 0, "row stride must keep the swizzle phase");
 constexpr int kThreads = (kEpiW0 + kEpiWarps) * 32;
 constexpr int kHdr = 1024;         // packed-weight header: u32 count, u32 0, u16 list
-constexpr int kMaxStages = (kHdr - 8) / 2 - 1;  // + sentinel  // 16-byte loads in flight per producer thread
+constexpr int kMaxStages = (kHdr - 8) / 2 - 1;  // + sentinel
 
 struct Halo2Args {
   ConvOp op;
@@ -98,13 +98,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
   uint32_t* s_aoff = reinterpret_cast<uint32_t*>(rowoff + 2 * L);  // [nst]
   uint16_t* s_chunk = reinterpret_cast<uint16_t*>(s_aoff + kMaxStages);
   const int nst = (int)reinterpret_cast<const uint32_t*>(T.wpk)[0];
+  const int G = op_groups(op);  // output phases of this launch
   {
+    // entry = (chunk * G + phase) * taps + tap, bit 15 = the phase's first
+    // stage (its MMAs overwrite the accumulator); decoded into the A
+    // descriptor offset (bits 0-27), the phase (28-29) and that flag (30)
     const uint16_t* gl = reinterpret_cast<const uint16_t*>(T.wpk + 8);
     for (int i = threadIdx.x; i < nst; i += blockDim.x) {
-      const int e = gl[i], c = e / T.taps, t = e - c * T.taps;
+      const int e = gl[i] & 0x7FFF, c = e / (G * T.taps);
+      const int g = (e - c * G * T.taps) / T.taps, t = e % T.taps;
       const int ky = t / op.k, kx = t - ky * op.k;
       s_chunk[i] = (uint16_t)c;
-      s_aoff[i] = (uint32_t)((ky * T.wp + kx) * (kRow >> 4));
+      s_aoff[i] = (uint32_t)((ky * T.wp + kx) * (kRow >> 4)) | ((uint32_t)g << 28) |
+                  ((uint32_t)(gl[i] >> 15) << 30);
     }
     s_chunk[nst] = 0xFFFF;  // sentinel
   }
@@ -123,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
   const int64_t total_tiles = T.m_tiles * T.n_tiles;
   const int AB = T.accbufs;
   const int PBS = T.stack ? PB : 1;     // accumulator column blocks per sub
-  const int acc_cols = SUB * PBS * BN;  // per accumulator buffer
+  const int acc_cols = SUB * G * PBS * BN;  // per accumulator buffer
   uint32_t ncols = 32;
   while ((int)ncols < AB * acc_cols) ncols <<= 1;
 
@@ -362,16 +368,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
           mbar_wait(bfull + s, bph);
           tc_fence_after();
           if (elect_one()) {
-            const uint64_t a0 = d_hb + (uint64_t)s_aoff[si];
+            const uint32_t ent = s_aoff[si];
+            const uint64_t a0 = d_hb + (uint64_t)(ent & 0x0FFFFFFFu);
             const uint64_t b0 = d_ring + (uint64_t)(s * b_step);
-            const uint32_t first = si ? 1u : 0u;
+            const uint32_t first = (ent >> 30) ? 0u : 1u;  // accumulate flag of K step 0
+            const uint32_t dg = d + ((ent >> 28) & 3u) * PBS * BN;
 #pragma unroll
             for (int k = 0; k < 2; ++k) {  // 2 x 32-byte K steps per row
               if (k >= nk) break;
 #pragma unroll
               for (int u = 0; u < SUB; ++u) {
                 const uint64_t ak = a0 + (uint64_t)(u * (128 * kRow >> 4) + 2 * k);
-                const uint32_t du = d + u * PBS * BN;
+                const uint32_t du = dg + u * G * PBS * BN;
                 if (T.stack) {
                   umma<false>(du, ak, b0 + 2 * k, idesc, k ? 1u : first);
                 } else {  // a0 . b_p for every plane into the same columns
@@ -432,7 +440,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
       if (T.dbg && blockIdx.x == 0 && tid == kEpiW0 * 32 && lt < 4096)
         T.dbg[2 * 4096 + lt] = clock64();
       tc_fence_after();
-      for (int u = 0; u < SUB; ++u) {
+      for (int ug = 0; ug < SUB * G; ++ug) {
+        const int u = ug / G, g = ug - u * G;
         const int64_t pos = mt * MT + u * 128 + q * 32 + (tid & 31);
         float* o = nullptr;
         float* oblk = nullptr;
@@ -442,17 +451,27 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
           const int r = (int)(pos - b * img_pos);
           const int y = r / Wp, x = r % Wp;
           if (y < wy && x < wx) {
-            const int oy = op.ph ? 2 * (op.oy0 + y) + op.ph_y : op.oy0 + y;
-            const int ox = op.ph ? 2 * (op.ox0 + x) + op.ph_x : op.ox0 + x;
-            o = op.out.base + act_off(op.out, b, oy, ox);
-            int64_t blk;
-            act_block(op.out, b, oy, ox, blk, ochan);
-            oblk = op.out.base + blk;
+            int oy = op.oy0 + y, ox = op.ox0 + x;
+            bool in = true;
+            if (op.ph == 1) {
+              oy = 2 * oy + op.ph_y;
+              ox = 2 * ox + op.ph_x;
+            } else if (op.ph == 2) {
+              oy = 2 * oy + (op.phl[g] >> 1);
+              ox = 2 * ox + (op.phl[g] & 1);
+              in = oy >= op.hy0 && oy < op.hy1 && ox >= op.hx0 && ox < op.hx1;
+            }
+            if (in) {
+              o = op.out.base + act_off(op.out, b, oy, ox);
+              int64_t blk;
+              act_block(op.out, b, oy, ox, blk, ochan);
+              oblk = op.out.base + blk;
+            }
           }
         }
         for (int c = 16 * half; c < BN; c += 32) {
           uint32_t r[PB][16];
-          const uint32_t ta = tmem + lane_base + acc * acc_cols + u * PBS * BN + c;
+          const uint32_t ta = tmem + lane_base + acc * acc_cols + ug * PBS * BN + c;
 #pragma unroll
           for (int p = 0; p < PB; ++p)
             if (p < PBS) tmem_ld16_nw(ta + p * BN, r[p]);
@@ -514,6 +533,8 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
   // 1x1 layers stay on the regular kernel (no halo to reuse, and their
   // multi-N-tile shapes re-read A per N tile here)
   if (op.stride != 1 || op.k < 1 || op.pad < 0 || op.pad >= op.k) return false;
+  const int G = op_groups(op);
+  if (op.ph == 2 && (op.k != 3 || op.pad != 1 || op.up2 || G < 1 || G > 4)) return false;
   // 1x1 layers: measured slower than the regular kernel (A re-read per N
   // tile); opt in with TS_H2_1X1=1
   if (op.k == 1 && !(getenv("TS_H2_1X1") && getenv("TS_H2_1X1")[0] == '1')) return false;
@@ -540,10 +561,11 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
   // per TMEM buffer and amortises the MMA issuer's per-stage overhead.
   {
     const char* e = getenv("TS_H2_STACK");
-    p.stack = e ? (e[0] == '1') : (p.pb * p.bn <= 64);
+    // (a phase group stacks only if two sub-tiles still get two buffers)
+    p.stack = e ? (e[0] == '1') : (p.pb * p.bn <= 64 && 4 * G * p.pb * p.bn <= 512);
     if (p.pb * p.bn > 256) p.stack = 0;  // MMA N limit
   }
-  const int cols = p.stack ? p.pb * p.bn : p.bn;
+  const int cols = G * (p.stack ? p.pb * p.bn : p.bn);
   const int cand[5][2] = {{4, 2}, {2, 2}, {1, 2}, {4, 1}, {2, 1}};
   for (const auto& cb : cand) {
     const int sub = cb[0], ab = cb[1];
@@ -575,6 +597,11 @@ bool conv_tc_halo2_eligible(const ConvOp& op, int precision) {
   return plan2(op, precision, &p);
 }
 
+int conv_tc_halo2_accbufs(const ConvOp& op, int precision) {
+  Halo2Plan p;
+  return plan2(op, precision, &p) ? p.accbufs : 0;
+}
+
 std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, int k,
                                            int precision, const ConvOp& op) {
   Halo2Plan p;
@@ -582,22 +609,29 @@ std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, 
   const size_t plane = (size_t)p.bn * kRow;
   const size_t b_bytes = plane * p.pb;
   const int taps = k * k;
-  // (chunk, tap) stages whose weights are all zero in every n-tile are
-  // skipped (the space-to-depth form of a stride-2 3x3 layer has 7 such
-  // taps of 16 per 4 channel groups)
+  const int G = op_groups(op);
+  const size_t wg = (size_t)co * ci * taps;  // floats per phase tensor
+  // (chunk, phase, tap) stages whose weights are all zero in every n-tile
+  // are skipped (the space-to-depth form of a stride-2 3x3 layer has 7 such
+  // taps of 16 per 4 channel groups; a phase of a group uses 4 of 9 taps)
   std::vector<uint16_t> list;
+  std::vector<char> seen(G, 0);
   for (int c = 0; c < p.cchunks; ++c)
-    for (int t = 0; t < taps; ++t) {
-      const int ky = t / k, kx = t % k;
-      bool nz = false;
-      for (int n = 0; n < co && !nz; ++n)
-        for (int e = 0; e < kKC && !nz; ++e) {
-          const int ch = c * kKC + e;
-          if (ch < ci && w_oikk[(((size_t)n * ci + ch) * k + ky) * k + kx] != 0.f) nz = true;
-        }
-      if (nz) list.push_back((uint16_t)(c * taps + t));
-    }
-  if (list.empty()) list.push_back(0);  // all-zero layer: keep one stage
+    for (int g = 0; g < G; ++g)
+      for (int t = 0; t < taps; ++t) {
+        const int ky = t / k, kx = t % k;
+        bool nz = false;
+        for (int n = 0; n < co && !nz; ++n)
+          for (int e = 0; e < kKC && !nz; ++e) {
+            const int ch = c * kKC + e;
+            if (ch < ci && w_oikk[g * wg + (((size_t)n * ci + ch) * k + ky) * k + kx] != 0.f)
+              nz = true;
+          }
+        // an all-zero phase keeps one (zero) stage so its columns are written
+        if (!nz && (c != p.cchunks - 1 || t != taps - 1 || seen[g])) continue;
+        list.push_back((uint16_t)(((c * G + g) * taps + t) | (seen[g] ? 0 : 0x8000)));
+        seen[g] = 1;
+      }
   if ((int)list.size() > kMaxStages) return {};
   const int nst = (int)list.size();
   std::vector<uint8_t> out(kHdr + (size_t)p.ntiles * nst * b_bytes, 0);
@@ -606,7 +640,8 @@ std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, 
   memcpy(out.data() + 8, list.data(), 2 * list.size());
   for (int nt = 0; nt < p.ntiles; ++nt)
     for (int i = 0; i < nst; ++i) {
-      const int c = list[i] / taps, t = list[i] % taps;
+      const int e = list[i] & 0x7FFF, c = e / (G * taps);
+      const int g = (e - c * G * taps) / taps, t = e % taps;
       const int ky = t / k, kx = t % k;
       uint8_t* base = out.data() + kHdr + ((size_t)nt * nst + i) * b_bytes;
       for (int r = 0; r < p.bn; ++r) {
@@ -614,7 +649,8 @@ std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, 
         for (int e = 0; e < kKC; ++e) {
           const int ch = c * kKC + e;
           const float v =
-              (n < co && ch < ci) ? w_oikk[(((size_t)n * ci + ch) * k + ky) * k + kx] : 0.f;
+              (n < co && ch < ci) ? w_oikk[g * wg + (((size_t)n * ci + ch) * k + ky) * k + kx]
+                                  : 0.f;
           const int byte = 2 * e;
           const size_t off =
               (size_t)r * kRow + (size_t)((((byte >> 4) ^ ((r >> 1) & 3))) << 4) + (byte & 15);

@@ -71,6 +71,12 @@ struct ConvLayer {
   bool poly = false;
   const uint8_t* w_ph[4] = {nullptr, nullptr, nullptr, nullptr};
   Win ph_win[4];
+  // phase groups (conv.cuh ConvOp::ph == 2): ph_G phases per launch, 4 / ph_G
+  // launches; group i = phases i*ph_G .. (i+1)*ph_G - 1, low-res window the
+  // union of theirs
+  int ph_G = 1;
+  const uint8_t* w_grp[4] = {nullptr, nullptr, nullptr, nullptr};
+  Win grp_win[4];
   std::vector<float> w_host, b_host;  // final-layer kernel: weights as parameters
   bool h2 = false;          // executed on the wide-M halo kernel (or phases)
   bool out_planes = false;  // writes pre-split planes (conv.cuh ActView)
@@ -436,6 +442,37 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
         ok = conv_tc_halo2_eligible(o, W->precision);
       }
       L.poly = ok;
+      // TS_PHGROUP=2/4: the phases of a group share one halo fill and one
+      // launch (input read once instead of per phase); a group must still
+      // get two TMEM accumulator buffers.  Measured slower (dec*.2 4 x 146
+      // -> 649 us, dec*.1 4 x 87 -> 408 us, dec*.0 4 x 126 -> 2 x 275 us):
+      // the group's accumulators leave room for one sub-tile, not four, so
+      // every weight stage feeds 4x fewer MMAs.  Off by default.
+      const char* eg = getenv("TS_PHGROUP");
+      const int want = eg ? atoi(eg) : 1;
+      L.ph_G = 1;
+      for (int G : {4, 2}) {
+        if (!ok || G > want) continue;
+        bool fit = true;
+        for (int gi = 0; gi < 4 / G && fit; ++gi) {
+          Win u = L.ph_win[gi * G];
+          for (int j = 1; j < G; ++j) {
+            const Win& w = L.ph_win[gi * G + j];
+            u.y0 = std::min(u.y0, w.y0); u.y1 = std::max(u.y1, w.y1);
+            u.x0 = std::min(u.x0, w.x0); u.x1 = std::max(u.x1, w.x1);
+          }
+          L.grp_win[gi] = u;
+          ConvOp o{};
+          o.k = 3; o.stride = 1; o.pad = 1; o.ph = 2; o.nph = G;
+          o.oy0 = u.y0; o.oy1 = u.y1; o.ox0 = u.x0; o.ox1 = u.x1;
+          o.in.C = d.ci; o.in.cstride = d.ci; o.out.C = d.co; o.out.cstride = d.co;
+          o.in.H = L.Hin; o.in.W = L.Win_;
+          o.batch = 1;
+          const int ab = conv_tc_halo2_accbufs(o, W->precision);
+          fit = ab == 2 || (eg && ab > 0);
+        }
+        if (fit) { L.ph_G = G; break; }
+      }
     }
   }
 
@@ -542,6 +579,8 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
     TS_CUDA_TRY(cudaMemcpy(L.b, bi->second.second.data(), Co * sizeof(float),
                            cudaMemcpyHostToDevice));
     if (L.poly) {
+      std::vector<float> w3;  // phase groups: [G][Co][ci][3][3]
+      if (L.ph_G > 1) w3.assign((size_t)4 * Co * dx.ci * 9, 0.f);
       for (int p = 0; p < 4; ++p) {
         // folded 2x2 weights of phase p: sums of the 3x3 taps each low-res
         // tap collects (fp64 sums rounded once)
@@ -557,7 +596,11 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
                     if (phase_tap(py, ty, ky) && phase_tap(px, tx, kx))
                       acc += src[(((size_t)o * dx.ci + ci) * 3 + ky) * 3 + kx];
                 w2[(((size_t)o * dx.ci + ci) * 2 + ty) * 2 + tx] = (float)acc;
+                if (L.ph_G > 1)  // the phase's 2x2 taps at (ty + py, tx + px) of 3x3
+                  w3[((((size_t)p * Co + o) * dx.ci + ci) * 3 + ty + py) * 3 + tx + px] =
+                      (float)acc;
               }
+        if (L.ph_G > 1) continue;
         ConvOp shape{};
         shape.k = 2; shape.stride = 1; shape.pad = 1; shape.ph = 1; shape.ph_y = py;
         shape.ph_x = px;
@@ -574,6 +617,23 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
         W->device_allocs.push_back(dp);
         TS_CUDA_TRY(cudaMemcpy(dp, pk.data(), pk.size(), cudaMemcpyHostToDevice));
         L.w_ph[p] = reinterpret_cast<const uint8_t*>(dp);
+      }
+      for (int gi = 0; L.ph_G > 1 && gi < 4 / L.ph_G; ++gi) {
+        ConvOp shape{};
+        shape.k = 3; shape.stride = 1; shape.pad = 1; shape.ph = 2; shape.nph = L.ph_G;
+        shape.oy0 = L.grp_win[gi].y0; shape.oy1 = L.grp_win[gi].y1;
+        shape.ox0 = L.grp_win[gi].x0; shape.ox1 = L.grp_win[gi].x1;
+        shape.in.C = dx.ci; shape.in.cstride = dx.ci; shape.out.C = Co; shape.out.cstride = Co;
+        shape.in.H = L.Hin; shape.in.W = L.Win_;
+        shape.batch = 1;
+        const std::vector<uint8_t> pk = pack_tc_weights_halo2(
+            w3.data() + (size_t)gi * L.ph_G * Co * dx.ci * 9, Co, dx.ci, 3, W->precision, shape);
+        if (pk.empty()) return TS_E_INVALID;
+        void* dp = nullptr;
+        TS_CUDA_TRY(cudaMalloc(&dp, pk.size()));
+        W->device_allocs.push_back(dp);
+        TS_CUDA_TRY(cudaMemcpy(dp, pk.data(), pk.size(), cudaMemcpyHostToDevice));
+        L.w_grp[gi] = reinterpret_cast<const uint8_t*>(dp);
       }
     } else if (W->precision != 0 && dx.ci % 4 == 0) {
       ConvOp shape{};
@@ -891,6 +951,25 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
           if (st != TS_OK) return st;
         }
         prev_base = buf(L.out_off); prev_H = L.Hout; prev_cs = L.out_cstride;
+        prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? 1 : 0;
+        prev_stage = L.stage;
+        continue;
+      }
+      if (L.poly && L.ph_G > 1) {
+        for (int gi = 0; gi < 4 / L.ph_G; ++gi) {
+          const Win& w = L.grp_win[gi];
+          if (w.y1 <= w.y0 || w.x1 <= w.x0) continue;
+          ConvOp q = op;
+          q.k = 3; q.stride = 1; q.pad = 1; q.up2 = 0;
+          q.ph = 2; q.nph = L.ph_G;
+          for (int j = 0; j < L.ph_G; ++j) q.phl[j] = gi * L.ph_G + j;
+          q.hy0 = L.out_win.y0; q.hy1 = L.out_win.y1; q.hx0 = L.out_win.x0; q.hx1 = L.out_win.x1;
+          q.oy0 = w.y0; q.oy1 = w.y1; q.ox0 = w.x0; q.ox1 = w.x1;
+          q.w_tc = L.w_grp[gi]; q.w_layout = 2;
+          st = launch_conv_tc_halo2(q, W->precision, lstream);
+          if (st != TS_OK) return st;
+        }
+        prev_base = op.out.base; prev_H = L.Hout; prev_cs = L.out_cstride;
         prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? 1 : 0;
         prev_stage = L.stage;
         continue;
