@@ -16,6 +16,7 @@
 // reads become stride-1 per parity plane: bank-conflict free), weights
 // [K][C_out] per encoder.
 #include <algorithm>
+#include <cstdlib>
 
 #include "conv.cuh"
 #include "tc_ptx.cuh"
@@ -140,6 +141,129 @@ __global__ void __launch_bounds__(enc0_threads<CO>(), 2) conv_enc0_kernel(Enc0Op
   }
 }
 
+// Store two pixels (rows y and y + 2) x CH channels starting at channel c0.
+template <int CH>
+__device__ __forceinline__ void enc0_store(const ActView& ov, int64_t b, int y, int x, int oy1,
+                                           int ox1, int c0, bool lr, float (&acc)[2][CH]) {
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int yy = y + 2 * r;
+    if (yy >= oy1 || x >= ox1) continue;
+    if (lr)
+#pragma unroll
+      for (int o = 0; o < CH; ++o) acc[r][o] = lrelu(acc[r][o]);
+    if (ov.planes) {
+      int64_t blk;
+      int chan;
+      act_block(ov, b, yy, x, blk, chan);
+#pragma unroll
+      for (int o = 0; o < CH; o += 8)
+        tcx::store8_planes(ov.base + blk, ov.cstride, chan + c0 + o, acc[r] + o);
+    } else {
+      float* op_ = ov.base + act_off(ov, b, yy, x) + c0;
+#pragma unroll
+      for (int o = 0; o < CH; o += 8) tcx::st_v8(op_ + o, acc[r] + o);
+    }
+  }
+}
+
+// Work-balanced variant for C_out = 48 and encoders of 1, 1, 3, 3 input
+// channels (any order): a 1-channel encoder's 9 MACs per output take 2
+// warps of CO/2 channels, a 3-channel encoder's 27 take 6 warps of CO/6,
+// so all 16 warps do 216 MACs per pixel (the per-encoder mapping above
+// leaves the 1-channel warps idle 2/3 of the time at every tile barrier).
+// One CTA per SM; the next tile's halo is loaded into registers before this
+// tile's FMAs (the loads' latency hides behind the compute).
+constexpr int kBalWarps = 16, kBalThreads = kBalWarps * 32;
+
+template <int CO>
+__global__ void __launch_bounds__(kBalThreads, 1) conv_enc0_bal_kernel(Enc0Op E) {
+  constexpr int CH1 = CO / 2, CH3 = CO / 6;
+  extern __shared__ __align__(16) float sm[];
+  float* halo = sm;                                   // 8 * kEPlane
+  float* sw = halo + 8 * kEPlane;                     // weights, 4 encoders
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int e = 0, wi = warp, woff = 0, o = 0;
+  for (int j = 0; j < 4; ++j) {
+    for (int i = threadIdx.x; i < 9 * E.cin[j] * CO; i += kBalThreads) sw[o + i] = E.w[j][i];
+    o += 9 * E.cin[j] * CO;
+  }
+  o = (o + 3) & ~3;
+  float* sbias = sw + o;
+  for (int i = threadIdx.x; i < 4 * CO; i += kBalThreads) sbias[i] = E.bias[i / CO][i % CO];
+  for (; e < 3; ++e) {
+    const int nw = E.cin[e] == 1 ? 2 : 6;
+    if (wi < nw) break;
+    wi -= nw;
+    woff += 9 * E.cin[e] * CO;
+  }
+  const bool one = E.cin[e] == 1;
+  const int c0 = wi * (one ? CH1 : CH3);
+  const int ty = lane >> 4, tx = lane & 15;           // rows ty and ty + 2
+  const int wy = E.oy1 - E.oy0, wx = E.ox1 - E.ox0;
+  const int ntx = (wx + kETX - 1) / kETX, nty = (wy + kETY - 1) / kETY;
+  const int64_t tiles = (int64_t)E.batch * nty * ntx;
+  constexpr int kHaloPieces = kEHY * 33 * 2;
+  constexpr int kPre = (kHaloPieces + kBalThreads - 1) / kBalThreads;
+  float4 pre[kPre];
+  auto load_halo = [&](int64_t t) {
+    const int64_t b = t / (nty * ntx);
+    const int r = (int)(t - b * nty * ntx);
+    const int y0 = E.oy0 + (r / ntx) * kETY, x0 = E.ox0 + (r % ntx) * kETX;
+    const float* inb = E.in + b * (int64_t)E.H * E.W * 8;
+#pragma unroll
+    for (int j = 0; j < kPre; ++j) {
+      const int i = threadIdx.x + j * kBalThreads;
+      pre[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t < tiles && i < kHaloPieces) {
+        const int hy = i / 66, rem = i - hy * 66, hx = rem >> 1, half = rem & 1;
+        const int iy = 2 * y0 - 1 + hy, ix = 2 * x0 - 1 + hx;
+        if (iy >= 0 && iy < E.H && ix >= 0 && ix < E.W)
+          pre[j] = __ldg(reinterpret_cast<const float4*>(inb + ((int64_t)iy * E.W + ix) * 8) + half);
+      }
+    }
+  };
+  load_halo(blockIdx.x);
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t b = tile / (nty * ntx);
+    const int r = (int)(tile - b * nty * ntx);
+    const int y0 = E.oy0 + (r / ntx) * kETY, x0 = E.ox0 + (r % ntx) * kETX;
+    __syncthreads();  // previous tile's halo reads done
+#pragma unroll
+    for (int j = 0; j < kPre; ++j) {
+      const int i = threadIdx.x + j * kBalThreads;
+      if (i < kHaloPieces) {
+        const int hy = i / 66, rem = i - hy * 66, hx = rem >> 1, half = rem & 1;
+        float* d = halo + hy * 2 * kEPitch + (hx & 1) * kEPitch + (hx >> 1) + 4 * half * kEPlane;
+        d[0] = pre[j].x; d[kEPlane] = pre[j].y; d[2 * kEPlane] = pre[j].z; d[3 * kEPlane] = pre[j].w;
+      }
+    }
+    __syncthreads();
+    load_halo(tile + gridDim.x);
+    if (one) {
+      float acc[2][CH1];
+#pragma unroll
+      for (int q = 0; q < CH1; ++q) acc[0][q] = acc[1][q] = sbias[e * CO + c0 + q];
+      enc0_accumulate<1, CO, CH1>(halo, E.ch0[e], sw + woff + c0, ty, tx, acc);
+      enc0_store<CH1>(E.out[e], b, y0 + ty, x0 + tx, E.oy1, E.ox1, c0, E.lrelu[e], acc);
+    } else {
+      float acc[2][CH3];
+#pragma unroll
+      for (int q = 0; q < CH3; ++q) acc[0][q] = acc[1][q] = sbias[e * CO + c0 + q];
+      enc0_accumulate<3, CO, CH3>(halo, E.ch0[e], sw + woff + c0, ty, tx, acc);
+      enc0_store<CH3>(E.out[e], b, y0 + ty, x0 + tx, E.oy1, E.ox1, c0, E.lrelu[e], acc);
+    }
+  }
+}
+
+bool enc0_balanced(const Enc0Op& E, int co) {
+  const char* v = getenv("TS_ENC0_BAL");
+  if (v && v[0] == '0') return false;
+  int ones = 0;
+  for (int e = 0; e < 4; ++e) ones += E.cin[e] == 1;
+  return co == 48 && ones == 2;
+}
+
 size_t enc0_smem(const Enc0Op& E, int co) {
   int k = 0;
   for (int e = 0; e < 4; ++e) k += 9 * E.cin[e] * co;
@@ -166,8 +290,16 @@ int launch_conv_enc0(const Enc0Op& E, int co, void* stream) {
   if (!sms) return TS_E_CUDA;
   const int64_t tiles = (int64_t)E.batch * ((E.oy1 - E.oy0 + kETY - 1) / kETY) *
                         ((E.ox1 - E.ox0 + kETX - 1) / kETX);
-  const int grid = (int)std::min<int64_t>(tiles, 2 * sms);
   cudaStream_t s = as_stream(stream);
+  if (enc0_balanced(E, co)) {
+    TS_CUDA_TRY(cudaFuncSetAttribute(conv_enc0_bal_kernel<48>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int g1 = (int)std::min<int64_t>(tiles, sms);
+    ts::count_launch(), conv_enc0_bal_kernel<48><<<g1, kBalThreads, smem, s>>>(E);
+    TS_LAUNCH_CHECK();
+    return TS_OK;
+  }
+  const int grid = (int)std::min<int64_t>(tiles, 2 * sms);
 #define TS_ENC0(CO)                                                                    \
   do {                                                                                 \
     TS_CUDA_TRY(cudaFuncSetAttribute(conv_enc0_kernel<CO>,                             \

@@ -12,6 +12,8 @@
 //
 // Compiled with --fmad=false: the predicate error bounds assume one
 // rounding per operation.
+#include <cstdlib>
+
 #include "predicates.cuh"
 #include "ts_common.cuh"
 
@@ -27,6 +29,7 @@ constexpr int kMaxCavity = 176;  // with the mesh: 31.5 KB, 7 patch-warps per SM
 // 1,024 patches of a configs[1] batch (N ~ 310-340) run in ONE wave.
 constexpr int kSmemPoints = 384;
 constexpr int kSmemSlots = 2 * kSmemPoints + 8;
+
 constexpr size_t kDelaunaySmem = (size_t)kSmemSlots * (3 * sizeof(int) + 3 * sizeof(double)) +
                                  kMaxCavity * sizeof(int) + (kMaxCavity + 8) * sizeof(int2) +
                                  3 * kMaxCavity * sizeof(int);
@@ -70,14 +73,16 @@ struct Mesh {
     cy[slot] = ay + oy;
     r2[slot] = ok ? ox * ox + oy * oy : __longlong_as_double(0x7ff8000000000000LL);
   }
-  // > 0 strictly inside, < 0 outside, == 0 on the circle (exact when unsure)
-  __device__ __forceinline__ int in_circle(const PatchPts& P, int t, double px,
-                                           double py) const {
+  // filter only (branch-free, so several tests overlap): 1 strictly inside,
+  // -1 outside, 0 unsure (then in_circle_exact decides)
+  __device__ __forceinline__ int in_circle_fast(int t, double px, double py) const {
     const double dx = px - cx[t], dy = py - cy[t], rr = r2[t];
     const double d2 = dx * dx + dy * dy;
     const double m = 1e-6 * (d2 + rr);
-    if (d2 < rr - m) return 1;
-    if (d2 > rr + m) return -1;
+    return (d2 < rr - m) ? 1 : (d2 > rr + m) ? -1 : 0;
+  }
+  __device__ __forceinline__ int in_circle_exact(const PatchPts& P, int t, double px,
+                                                 double py) const {
     double ax, ay, bx, by, qx, qy;
     P.get(tri[3 * t], ax, ay);
     P.get(tri[3 * t + 1], bx, by);
@@ -87,12 +92,14 @@ struct Mesh {
 };
 
 
-__global__ void __launch_bounds__(32)
-delaunay_kernel(const double* __restrict__ xy_all,
-                const int64_t* __restrict__ pts_off, int n_patches,
-                int32_t* tri_all, int32_t* ntri_out, int32_t* status,
-                double* circ_all) {
-  extern __shared__ __align__(16) unsigned char smem[];
+// SMEM: the mesh lives in shared memory (the instance's pointers all derive
+// from the shared array, so its loads compile to LDS, not generic loads)
+template <bool SMEM, int kScanIlp>  // kScanIlp: circle tests per lane per scan pass
+__device__ __forceinline__ void triangulate_patch(unsigned char* smem,
+                                                  const double* __restrict__ xy_all,
+                                                  const int64_t* __restrict__ pts_off,
+                                                  int32_t* tri_all, int32_t* ntri_out,
+                                                  int32_t* status, double* circ_all) {
   double* s_cx = reinterpret_cast<double*>(smem);
   double* s_cy = s_cx + kSmemSlots;
   double* s_r2 = s_cy + kSmemSlots;
@@ -106,15 +113,11 @@ delaunay_kernel(const double* __restrict__ xy_all,
   const int n = (int)(pts_off[p + 1] - off);
   const int64_t base = 2 * off + 8 * (int64_t)p;  // first triangle slot
   int* tri_out = tri_all + 3 * base;
-  if (n == 0) {
-    if (lane == 0) { ntri_out[p] = 0; status[p] = TS_E_EMPTY_PATCH; }
-    return;
-  }
   const PatchPts P{xy_all + 2 * off, n};
   const int cap = 2 * n + 8;
-  const bool in_smem = n <= kSmemPoints;
+  constexpr bool in_smem = SMEM;
   Mesh M;
-  if (in_smem) {
+  if (SMEM) {
     M = Mesh{s_tri, s_cx, s_cy, s_r2};
   } else {
     double* g = circ_all + 3 * base;
@@ -129,25 +132,33 @@ delaunay_kernel(const double* __restrict__ xy_all,
     double px, py;
     P.get(v, px, py);
     // 1. cavity: triangles whose circumcircle strictly contains v
-    //    (two triangles per lane per pass: independent circle tests in
-    //    flight; cavity order stays ascending)
+    //    (kScanIlp triangles per lane per pass: independent circle tests
+    //    in flight; cavity order stays ascending)
     int nb = 0;
-    for (int b0 = 0; b0 < ntri; b0 += 64) {
-      const int t0 = b0 + lane, t1 = t0 + 32;
-      const bool in0 = t0 < ntri && M.in_circle(P, t0, px, py) > 0;
-      const bool in1 = t1 < ntri && M.in_circle(P, t1, px, py) > 0;
-      const unsigned m0 = __ballot_sync(0xFFFFFFFFu, in0);
-      const unsigned m1 = __ballot_sync(0xFFFFFFFFu, in1);
-      const unsigned below = (1u << lane) - 1;
-      if (in0) {
-        const int slot = nb + __popc(m0 & below);
-        if (slot < kMaxCavity) bad[slot] = t0;
+    const unsigned below = (1u << lane) - 1;
+    for (int b0 = 0; b0 < ntri; b0 += 32 * kScanIlp) {
+      bool in[kScanIlp];
+      int f[kScanIlp];
+#pragma unroll
+      for (int j = 0; j < kScanIlp; ++j) {  // slots >= ntri hold stale data: masked
+        const int t = min(b0 + lane + 32 * j, ntri - 1);
+        f[j] = M.in_circle_fast(t, px, py);
       }
-      if (in1) {
-        const int slot = nb + __popc(m0) + __popc(m1 & below);
-        if (slot < kMaxCavity) bad[slot] = t1;
+#pragma unroll
+      for (int j = 0; j < kScanIlp; ++j) {
+        const int t = b0 + lane + 32 * j;
+        if (f[j] == 0 && t < ntri) f[j] = M.in_circle_exact(P, t, px, py);
+        in[j] = t < ntri && f[j] > 0;
       }
-      nb += __popc(m0) + __popc(m1);
+#pragma unroll
+      for (int j = 0; j < kScanIlp; ++j) {
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, in[j]);
+        if (in[j]) {
+          const int slot = nb + __popc(m & below);
+          if (slot < kMaxCavity) bad[slot] = b0 + lane + 32 * j;
+        }
+        nb += __popc(m);
+      }
     }
     if (nb == 0) continue;  // exact duplicate of an inserted vertex
     if (nb > kMaxCavity) { st = TS_E_INVALID; break; }
@@ -224,6 +235,25 @@ delaunay_kernel(const double* __restrict__ xy_all,
   }
 }
 
+template <int ILP>
+__global__ void __launch_bounds__(32)
+delaunay_kernel(const double* __restrict__ xy_all,
+                const int64_t* __restrict__ pts_off, int n_patches,
+                int32_t* tri_all, int32_t* ntri_out, int32_t* status,
+                double* circ_all) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int p = blockIdx.x;
+  const int n = (int)(pts_off[p + 1] - pts_off[p]);
+  if (n == 0) {
+    if (threadIdx.x == 0) { ntri_out[p] = 0; status[p] = TS_E_EMPTY_PATCH; }
+    return;
+  }
+  if (n <= kSmemPoints)
+    triangulate_patch<true, ILP>(smem, xy_all, pts_off, tri_all, ntri_out, status, circ_all);
+  else
+    triangulate_patch<false, ILP>(smem, xy_all, pts_off, tri_all, ntri_out, status, circ_all);
+}
+
 }  // namespace
 }  // namespace ts
 
@@ -238,17 +268,26 @@ extern "C" int ts_triangulate(const double* d_xy, const int64_t* d_pts_off,
                               int32_t* d_status, void* d_scratch, void* stream) {
   if (n_patches <= 0) return TS_OK;
   if (!d_scratch) return TS_E_INVALID;
-  {  // per call: the attribute is per device (one process may drive several)
-    TS_CUDA_TRY(cudaFuncSetAttribute(delaunay_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)kDelaunaySmem));
-    TS_CUDA_TRY(cudaFuncSetAttribute(delaunay_kernel,
-                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  }
-  ts::count_launch(),
-      delaunay_kernel<<<n_patches, 32, kDelaunaySmem, as_stream(stream)>>>(
-          d_xy, d_pts_off, n_patches, d_tri, d_ntri, d_status,
-          reinterpret_cast<double*>(d_scratch));
+  static const int ilp = [] {
+    const char* e = getenv("TS_DL_ILP");
+    return e ? atoi(e) : 4;
+  }();
+#define TS_DL_LAUNCH(I)                                                                   \
+  do {                                                                                    \
+    /* per call: the attribute is per device (one process may drive several) */          \
+    TS_CUDA_TRY(cudaFuncSetAttribute(delaunay_kernel<I>,                                  \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                                     (int)kDelaunaySmem));                                \
+    TS_CUDA_TRY(cudaFuncSetAttribute(delaunay_kernel<I>,                                  \
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100)); \
+    ts::count_launch(), delaunay_kernel<I><<<n_patches, 32, kDelaunaySmem, as_stream(stream)>>>( \
+                            d_xy, d_pts_off, n_patches, d_tri, d_ntri, d_status,          \
+                            reinterpret_cast<double*>(d_scratch));                        \
+  } while (0)
+  if (ilp == 2) TS_DL_LAUNCH(2);
+  else if (ilp == 8) TS_DL_LAUNCH(8);
+  else TS_DL_LAUNCH(4);
+#undef TS_DL_LAUNCH
   TS_LAUNCH_CHECK();
   return TS_OK;
 }
