@@ -29,6 +29,7 @@ constexpr int kMaxCavity = 176;  // with the mesh: 31.5 KB, 7 patch-warps per SM
 // 1,024 patches of a configs[1] batch (N ~ 310-340) run in ONE wave.
 constexpr int kSmemPoints = 384;
 constexpr int kSmemSlots = 2 * kSmemPoints + 8;
+constexpr int kScanIlp = 4;  // circle tests per lane per cavity-scan pass (2: +6%, 8: +7% time)
 
 constexpr size_t kDelaunaySmem = (size_t)kSmemSlots * (3 * sizeof(int) + 3 * sizeof(double)) +
                                  kMaxCavity * sizeof(int) + (kMaxCavity + 8) * sizeof(int2) +
@@ -94,7 +95,7 @@ struct Mesh {
 
 // SMEM: the mesh lives in shared memory (the instance's pointers all derive
 // from the shared array, so its loads compile to LDS, not generic loads)
-template <bool SMEM, int kScanIlp>  // kScanIlp: circle tests per lane per scan pass
+template <bool SMEM>
 __device__ __forceinline__ void triangulate_patch(unsigned char* smem,
                                                   const double* __restrict__ xy_all,
                                                   const int64_t* __restrict__ pts_off,
@@ -183,18 +184,12 @@ __device__ __forceinline__ void triangulate_patch(unsigned char* smem,
         w = key & 0xFFFF;
         const int twin = (w << 16) | u;
         keep = true;
-        if (3 * nb > 32)  // large cavity: linear twin search over all keys
-          for (int k = 0; k < 3 * nb; ++k)
-            if (ekey[k] == twin) { keep = false; break; }
-      }
-      if (3 * nb <= 32) {
-        // small cavity (all edges in this pass): an interior edge appears
-        // in both directions, so its undirected key matches two lanes
-        const uint32_t canon = e < 3 * nb
-                                   ? ((uint32_t)min(u, w) << 16) | (uint32_t)max(u, w)
-                                   : 0xFFFFFFFFu - (uint32_t)lane;  // unique filler
-        const unsigned mm = __match_any_sync(0xFFFFFFFFu, canon);
-        if (e < 3 * nb) keep = __popc(mm) == 1;
+        // linear twin search over all keys (broadcast reads; measured
+        // faster than __match_any_sync on the undirected keys)
+        int hit = 0;
+#pragma unroll 4
+        for (int k = 0; k < 3 * nb; ++k) hit |= ekey[k] == twin;
+        keep = !hit;
       }
       if (e < 3 * nb) {
         if (keep) {
@@ -235,7 +230,6 @@ __device__ __forceinline__ void triangulate_patch(unsigned char* smem,
   }
 }
 
-template <int ILP>
 __global__ void __launch_bounds__(32)
 delaunay_kernel(const double* __restrict__ xy_all,
                 const int64_t* __restrict__ pts_off, int n_patches,
@@ -249,9 +243,9 @@ delaunay_kernel(const double* __restrict__ xy_all,
     return;
   }
   if (n <= kSmemPoints)
-    triangulate_patch<true, ILP>(smem, xy_all, pts_off, tri_all, ntri_out, status, circ_all);
+    triangulate_patch<true>(smem, xy_all, pts_off, tri_all, ntri_out, status, circ_all);
   else
-    triangulate_patch<false, ILP>(smem, xy_all, pts_off, tri_all, ntri_out, status, circ_all);
+    triangulate_patch<false>(smem, xy_all, pts_off, tri_all, ntri_out, status, circ_all);
 }
 
 }  // namespace
@@ -268,26 +262,15 @@ extern "C" int ts_triangulate(const double* d_xy, const int64_t* d_pts_off,
                               int32_t* d_status, void* d_scratch, void* stream) {
   if (n_patches <= 0) return TS_OK;
   if (!d_scratch) return TS_E_INVALID;
-  static const int ilp = [] {
-    const char* e = getenv("TS_DL_ILP");
-    return e ? atoi(e) : 4;
-  }();
-#define TS_DL_LAUNCH(I)                                                                   \
-  do {                                                                                    \
-    /* per call: the attribute is per device (one process may drive several) */          \
-    TS_CUDA_TRY(cudaFuncSetAttribute(delaunay_kernel<I>,                                  \
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,         \
-                                     (int)kDelaunaySmem));                                \
-    TS_CUDA_TRY(cudaFuncSetAttribute(delaunay_kernel<I>,                                  \
-                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100)); \
-    ts::count_launch(), delaunay_kernel<I><<<n_patches, 32, kDelaunaySmem, as_stream(stream)>>>( \
-                            d_xy, d_pts_off, n_patches, d_tri, d_ntri, d_status,          \
-                            reinterpret_cast<double*>(d_scratch));                        \
-  } while (0)
-  if (ilp == 2) TS_DL_LAUNCH(2);
-  else if (ilp == 8) TS_DL_LAUNCH(8);
-  else TS_DL_LAUNCH(4);
-#undef TS_DL_LAUNCH
+  // per call: the attribute is per device (one process may drive several)
+  TS_CUDA_TRY(cudaFuncSetAttribute(delaunay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kDelaunaySmem));
+  TS_CUDA_TRY(cudaFuncSetAttribute(delaunay_kernel,
+                                   cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  ts::count_launch(),
+      delaunay_kernel<<<n_patches, 32, kDelaunaySmem, as_stream(stream)>>>(
+          d_xy, d_pts_off, n_patches, d_tri, d_ntri, d_status,
+          reinterpret_cast<double*>(d_scratch));
   TS_LAUNCH_CHECK();
   return TS_OK;
 }
