@@ -93,8 +93,9 @@ __global__ void __launch_bounds__(enc0_threads<CO>(), 2) conv_enc0_kernel(Enc0Op
   const int ntx = (wx + kETX - 1) / kETX, nty = (wy + kETY - 1) / kETY;
   const int64_t tiles = (int64_t)E.batch * nty * ntx;
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const int64_t b = tile / (nty * ntx);
-    const int r = (int)(tile - b * nty * ntx);
+    // tiles < 2^31 (checked by the host): 32-bit division
+    const int64_t b = (int)tile / (nty * ntx);
+    const int r = (int)tile - (int)b * nty * ntx;
     const int y0 = E.oy0 + (r / ntx) * kETY, x0 = E.ox0 + (r % ntx) * kETX;
     __syncthreads();  // previous tile's halo reads done
     // halo: input rows 2 y0 - 1 .. + 16, columns 2 x0 - 1 .. + 32, 8 channels
@@ -207,8 +208,8 @@ __global__ void __launch_bounds__(kBalThreads, 1) conv_enc0_bal_kernel(Enc0Op E)
   constexpr int kPre = (kHaloPieces + kBalThreads - 1) / kBalThreads;
   float4 pre[kPre];
   auto load_halo = [&](int64_t t) {
-    const int64_t b = t / (nty * ntx);
-    const int r = (int)(t - b * nty * ntx);
+    const int64_t b = (int)t / (nty * ntx);
+    const int r = (int)t - (int)b * nty * ntx;
     const int y0 = E.oy0 + (r / ntx) * kETY, x0 = E.ox0 + (r % ntx) * kETX;
     const float* inb = E.in + b * (int64_t)E.H * E.W * 8;
 #pragma unroll
@@ -225,8 +226,9 @@ __global__ void __launch_bounds__(kBalThreads, 1) conv_enc0_bal_kernel(Enc0Op E)
   };
   load_halo(blockIdx.x);
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const int64_t b = tile / (nty * ntx);
-    const int r = (int)(tile - b * nty * ntx);
+    // tiles < 2^31 (checked by the host): 32-bit division
+    const int64_t b = (int)tile / (nty * ntx);
+    const int r = (int)tile - (int)b * nty * ntx;
     const int y0 = E.oy0 + (r / ntx) * kETY, x0 = E.ox0 + (r % ntx) * kETX;
     __syncthreads();  // previous tile's halo reads done
 #pragma unroll
@@ -290,6 +292,7 @@ int launch_conv_enc0(const Enc0Op& E, int co, void* stream) {
   if (!sms) return TS_E_CUDA;
   const int64_t tiles = (int64_t)E.batch * ((E.oy1 - E.oy0 + kETY - 1) / kETY) *
                         ((E.ox1 - E.ox0 + kETX - 1) / kETX);
+  if (tiles + 2 * (int64_t)sms >= (int64_t)INT32_MAX) return TS_E_INVALID;
   cudaStream_t s = as_stream(stream);
   if (enc0_balanced(E, co)) {
     TS_CUDA_TRY(cudaFuncSetAttribute(conv_enc0_bal_kernel<48>,

@@ -86,3 +86,32 @@ def test_refine_tc_vs_golden(golden, precision):
     # batch invariance holds on the tensor-core path as well
     solo = R.refine_batch(raws[:1], bundle, precision=precision)[0]
     assert np.array_equal(solo.heights_rel, res[0].heights_rel)
+
+
+@pytest.mark.parametrize("group", ["2", "4"])
+@pytest.mark.parametrize("precision", [2, 4])
+def test_phase_groups_bit_identical(monkeypatch, group, precision):
+    """TS_PHGROUP (several decoder output phases per wide-M launch over one
+    halo fill) gives every phase the same MMA sequence as its own launch, so
+    the refined tiles are bit-identical to the per-phase default."""
+    from paper_2509_20198_b200.refiner import (default_descriptor,
+                                               device_weights,
+                                               random_weights)
+    bundle = random_weights(default_descriptor(), seed=3)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    B = 5
+    x = torch.randn((B, 96, 96, 8), generator=g, device="cuda") * 0.1
+    x[..., 2:] = torch.rand((B, 96, 96, 6), generator=g, device="cuda")
+    outs = []
+    for env in (None, group):
+        if env is None:
+            monkeypatch.delenv("TS_PHGROUP", raising=False)
+        else:
+            monkeypatch.setenv("TS_PHGROUP", env)
+        w = device_weights(bundle, precision)
+        out = torch.empty((B, 64, 64, 4), device="cuda")
+        nf = torch.zeros(B, dtype=torch.uint8, device="cuda")
+        w.run(x, B, out, nf)
+        torch.cuda.synchronize()
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
