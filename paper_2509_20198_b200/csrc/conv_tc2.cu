@@ -566,8 +566,16 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
     if (p.pb * p.bn > 256) p.stack = 0;  // MMA N limit
   }
   const int cols = G * (p.stack ? p.pb * p.bn : p.bn);
-  const int cand[5][2] = {{4, 2}, {2, 2}, {1, 2}, {4, 1}, {2, 1}};
+  int cand[6][2] = {{4, 2}, {2, 2}, {1, 2}, {4, 1}, {2, 1}, {1, 1}};
+  {  // TS_H2_SUBAB=<sub>,<accbufs>: try that candidate first (A/B measurement)
+    const char* e = getenv("TS_H2_SUBAB");
+    if (e && e[0] >= '1' && e[0] <= '4' && e[1] == ',' && (e[2] == '1' || e[2] == '2')) {
+      cand[5][0] = cand[0][0]; cand[5][1] = cand[0][1];
+      cand[0][0] = e[0] - '0'; cand[0][1] = e[2] - '0';
+    }
+  }
   for (const auto& cb : cand) {
+    if (cb[0] == 3) continue;
     const int sub = cb[0], ab = cb[1];
     if (ab * sub * cols > 512) continue;
     const int L = (128 * sub + (op.k - 1) * (p.wp + 1) + 7) / 8 * 8;
