@@ -101,12 +101,45 @@ class ClockSampler:
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
+        # nvidia-smi / NVML count physical GPUs: map through CUDA_VISIBLE_DEVICES
+        vis = [v.strip() for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")
+               if v.strip()]
+        if index < len(vis) and vis[index].isdigit():
+            index = int(vis[index])
         self.index = index
         self.samples = []
         self._stop = threading.Event()
         self._t = None
 
+    def _run_nvml(self):
+        """NVML queries take microseconds (nvidia-smi ~100 ms), so even a
+        ~0.1 s timed region gets many samples; same fields and format."""
+        import pynvml as N
+        N.nvmlInit()
+        try:
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            get_r = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons
+            bits = (N.nvmlClocksEventReasonHwSlowdown,
+                    N.nvmlClocksEventReasonHwThermalSlowdown,
+                    N.nvmlClocksEventReasonSwThermalSlowdown,
+                    N.nvmlClocksEventReasonSwPowerCap)
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                r = get_r(h)
+                self.samples.append([str(sm), str(mx)] +
+                                    ["Active" if r & b else "Not Active" for b in bits])
+                self._stop.wait(0.01)
+        finally:
+            N.nvmlShutdown()
+
     def _run(self):
+        try:
+            self._run_nvml()
+            return
+        except Exception:  # noqa: BLE001 - fall back to nvidia-smi
+            self.samples = []
         while not self._stop.is_set():
             try:
                 out = subprocess.run(

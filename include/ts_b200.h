@@ -226,6 +226,19 @@ int ts_bake(const double* d_xyz, const float* d_rgb, int64_t m,
             const double* d_key_cz, const float* d_prior_rgb,
             float* d_out_h, float* d_out_rgb, void* d_accum, void* stream);
 
+/* ---- WireHeightmap records (server.py:126-142 wire_heightmap,
+ *      docs/wire.md "WireHeightmap") -------------------------------------
+ * Per patch p, back to back at d_wire + p * ts_wire_record_size(has_rgb):
+ *   i32 d_ij[2p], i32 d_ij[2p+1], f32 (float)d_cz[p], u8 d_stage[p],
+ *   u8 flags (bit 0 = has_rgb), f32[64*64] heights_rel,
+ *   u8[64*64*3] clip(round_half_even(f32(rgb*255)), 0, 255) if has_rgb.
+ * d_out: B x 64 x 64 x 4 float32 (heights_rel, r, g, b) as ts_refine and
+ * the bake leave it (16-byte aligned); d_wire 2-byte aligned.            */
+size_t ts_wire_record_size(int has_rgb);
+int ts_wire_heightmaps(const float* d_out, const double* d_cz, const int32_t* d_ij,
+                       const uint8_t* d_stage, int has_rgb, int batch,
+                       uint8_t* d_wire, void* stream);
+
 /* ---- test hooks (host-callable, no GPU needed) ------------------------ */
 /* Sign of the exact incircle / orientation determinants used by
  * ts_triangulate: returns -1, 0, +1.                                     */

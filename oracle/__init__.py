@@ -14,7 +14,7 @@ Pinning: ``tests/golden/make_golden.py`` imports the real reference in the
 build container and writes seeded input/output vectors to
 ``tests/golden/*.npz``; ``tests/test_oracle_golden.py`` checks this oracle
 against every one of them (chunk points, positions/colours, Algorithm 1
-rasters incl. face maps, conv/refine outputs, bake outputs).
+rasters incl. face maps, conv/refine outputs, bake outputs, wire records).
 
 Third-party arithmetic the reference delegates to (not under
 /root/reference): scipy.spatial.Delaunay (Qhull) and cKDTree, numpy/OpenBLAS

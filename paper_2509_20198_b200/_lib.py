@@ -65,6 +65,8 @@ SIGNATURES = {
     "ts_bake_workspace": (SZ, [I32]),
     "ts_bake": (I32, [P, P, I64, P, I32, P, P, P, F64, F64, I32, I32, P, P, P,
                       P, P, P, P, P]),
+    "ts_wire_record_size": (SZ, [I32]),
+    "ts_wire_heightmaps": (I32, [P, P, P, P, I32, I32, P, P]),
     "ts_incircle_sign": (I32, [P, P, P, P]),
     "ts_orient_sign": (I32, [P, P, P]),
     "ts_predicates_device": (I32, [P, I64, I32, P, P]),

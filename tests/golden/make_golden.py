@@ -318,6 +318,47 @@ def gold_bake():
     _save("bake.npz", **out)
 
 
+def gold_wire():
+    """server.wire_heightmap on a stand-in engine holding RefinedPatches."""
+    import threading
+    from terrascout.server import wire_heightmap
+    rng = np.random.default_rng(2024)
+    ties = ((np.arange(64 * 64 * 3) % 255 + 0.5) / 255).astype(np.float32)
+    out = {}
+    for name, colour in (("rgb", True), ("nocol", False)):
+        eng = type("E", (), {})()
+        eng.lock = threading.Lock()
+        eng.refined, eng.patches = {}, {}
+        recs, hs, rgbs, czs, ijs, stages = [], [], [], [], [], []
+        for p, (i, j) in enumerate([(0, 0), (7, 3), (-2, 5)]):
+            h = rng.normal(0, 40, (64, 64)).astype(np.float32)
+            if colour:
+                rgb = rng.uniform(-0.2, 1.2, (64, 64, 3)).astype(np.float32)
+                if p == 2:
+                    rgb = ties.reshape(64, 64, 3)      # x.5 products: half-even
+            else:
+                rgb = None
+            cz = 100.0 + 1234.56789 * p
+            stage = [3, 4, 2][p]
+            eng.refined[(i, j)] = RefinedPatch(
+                key=PatchKey(i, j, (i * 640.0 + 320, j * 640.0 + 320), cz),
+                heights_rel=h, rgb=rgb, provenance="refined")
+            eng.patches[(i, j)] = type("P", (), {"stage": stage})()
+            recs.append(np.frombuffer(wire_heightmap(eng, i, j), np.uint8))
+            hs.append(h)
+            rgbs.append(rgb if colour else np.zeros((64, 64, 3), np.float32))
+            czs.append(cz)
+            ijs.append((i, j))
+            stages.append(stage)
+        out[f"{name}_wire"] = np.concatenate(recs)
+        out[f"{name}_h"] = np.stack(hs)
+        out[f"{name}_rgb"] = np.stack(rgbs)
+        out[f"{name}_cz"] = np.array(czs)
+        out[f"{name}_ij"] = np.array(ijs, np.int32)
+        out[f"{name}_stage"] = np.array(stages, np.uint8)
+    _save("wire.npz", **out)
+
+
 if __name__ == "__main__":
     import tempfile
     with tempfile.TemporaryDirectory() as tmp:
@@ -326,3 +367,4 @@ if __name__ == "__main__":
         gold_interpolate()
         gold_refiner(tmp)
         gold_bake()
+        gold_wire()

@@ -129,3 +129,17 @@ def test_bake(golden):
                                float(g["base_cz"][p]), None,
                                g["centers"][p], float(g["key_cz"][p]))
         assert np.array_equal(h2, g["out_h_nocol"][p]), p
+
+
+def test_wire_records(golden):
+    """oracle.wire vs the reference's server.wire_heightmap bytes (colour,
+    clipping, half-to-even ties, negative grid indices, colourless)."""
+    from oracle import wire as owire
+    g = golden("wire.npz")
+    for name, colour in (("rgb", True), ("nocol", False)):
+        recs = b"".join(
+            owire.wire_record(int(g[f"{name}_ij"][p][0]), int(g[f"{name}_ij"][p][1]),
+                              float(g[f"{name}_cz"][p]), int(g[f"{name}_stage"][p]),
+                              g[f"{name}_h"][p], g[f"{name}_rgb"][p] if colour else None)
+            for p in range(len(g[f"{name}_cz"])))
+        assert recs == g[f"{name}_wire"].tobytes(), name
