@@ -66,9 +66,13 @@ struct Mesh {
     const double D = 2.0 * (p1 - p2);
     const bool ok = fabs(D) > 1e-6 * (fabs(p1) + fabs(p2)) && fabs(D) > 1e-200;
     const double l1 = ux * ux + uy * uy, l2 = vx * vx + vy * vy;
-    // one divide: the cache only feeds the filter, whose 1e-6 relative
-    // margin dwarfs the extra rounding
-    const double inv = 1.0 / D;
+    // no IEEE divide: the cache only feeds the filter, whose 1e-6 relative
+    // margin dwarfs the error of an approximate reciprocal refined by two
+    // Newton steps (relative error ~1e-16; ill-conditioned D is flagged)
+    double inv;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(D));
+    inv = inv * (2.0 - D * inv);
+    inv = inv * (2.0 - D * inv);
     const double ox = (vy * l1 - uy * l2) * inv, oy = (ux * l2 - vx * l1) * inv;
     cx[slot] = ax + ox;
     cy[slot] = ay + oy;
@@ -145,20 +149,29 @@ __device__ __forceinline__ void triangulate_patch(unsigned char* smem,
         const int t = min(b0 + lane + 32 * j, ntri - 1);
         f[j] = M.in_circle_fast(t, px, py);
       }
+      bool unsure = false;
+#pragma unroll
+      for (int j = 0; j < kScanIlp; ++j) unsure |= f[j] == 0 && b0 + lane + 32 * j < ntri;
+      if (__any_sync(0xFFFFFFFFu, unsure)) {  // rare: one warp-uniform branch
+#pragma unroll
+        for (int j = 0; j < kScanIlp; ++j) {
+          const int t = b0 + lane + 32 * j;
+          if (f[j] == 0 && t < ntri) f[j] = M.in_circle_exact(P, t, px, py);
+        }
+      }
+      unsigned m[kScanIlp];
 #pragma unroll
       for (int j = 0; j < kScanIlp; ++j) {
-        const int t = b0 + lane + 32 * j;
-        if (f[j] == 0 && t < ntri) f[j] = M.in_circle_exact(P, t, px, py);
-        in[j] = t < ntri && f[j] > 0;
+        in[j] = b0 + lane + 32 * j < ntri && f[j] > 0;
+        m[j] = __ballot_sync(0xFFFFFFFFu, in[j]);
       }
 #pragma unroll
       for (int j = 0; j < kScanIlp; ++j) {
-        const unsigned m = __ballot_sync(0xFFFFFFFFu, in[j]);
         if (in[j]) {
-          const int slot = nb + __popc(m & below);
+          const int slot = nb + __popc(m[j] & below);
           if (slot < kMaxCavity) bad[slot] = b0 + lane + 32 * j;
         }
-        nb += __popc(m);
+        nb += __popc(m[j]);
       }
     }
     if (nb == 0) continue;  // exact duplicate of an inserted vertex
