@@ -130,6 +130,11 @@ raster_kernel(RasterArgs A) {
   uint32_t* s_rng = reinterpret_cast<uint32_t*>(s_pref + kSmemTri + 1);  // 1032
   int* s_bstart = reinterpret_cast<int*>(s_rng + kSmemTri);  // kBins^2 + 1
   short* s_bid = reinterpret_cast<short*>(s_bstart + kBins * kBins + 2);  // kSmemPts
+  // bin-ordered copy of the cached points for the NN search; aliases
+  // s_pref / s_rng, which are dead once the face map is done (>= 6,144 B,
+  // 16-byte aligned)
+  double2* s_bxy = reinterpret_cast<double2*>(s_pref);
+  static_assert(sizeof(int) * (2 * kSmemTri + 1) >= sizeof(double2) * kSmemPts, "s_bxy alias");
   __shared__ double s_shift;
   __shared__ int s_total;
   __shared__ int s_wsum[kThreads / 32];
@@ -317,8 +322,9 @@ raster_kernel(RasterArgs A) {
           if (!edge_row && gx != bx - r && gx != bx + r) continue;  // ring only
           const int b = gy * kBins + gx;
           for (int k = s_bstart[b]; k < s_bstart[b + 1]; ++k) {
+            const double2 q = s_bxy[k];  // no id -> coordinate indirection
             const int i = s_bid[k];
-            const double dx = dsub(qx, xy[2 * i]), dy = dsub(qy, xy[2 * i + 1]);
+            const double dx = dsub(qx, q.x), dy = dsub(qy, q.y);
             const double d2 = dadd(dmul(dx, dx), dmul(dy, dy));
             if (d2 < best || (d2 == best && i < bi)) { best = d2; bi = i; }
           }
@@ -365,7 +371,9 @@ raster_kernel(RasterArgs A) {
     __syncthreads();
     for (int i = tid; i < n; i += kThreads) {
       const int b = bin_of(xy[2 * i + 1]) * kBins + bin_of(xy[2 * i]);
-      s_bid[atomicAdd(&s_cur[b], 1)] = (short)i;
+      const int slot = atomicAdd(&s_cur[b], 1);
+      s_bid[slot] = (short)i;
+      s_bxy[slot] = make_double2(xy[2 * i], xy[2 * i + 1]);
     }
     __syncthreads();
   }
@@ -411,8 +419,9 @@ raster_kernel(RasterArgs A) {
           if (r > 0 && inner_row && gx > bx0 - r && gx < bx1 + r) continue;  // ring only
           const int b = gy * kBins + gx;
           for (int k = s_bstart[b]; k < s_bstart[b + 1]; ++k) {
+            const double2 q = s_bxy[k];  // no id -> coordinate indirection
             const int i = s_bid[k];
-            const double dx = dsub(qx, xy[2 * i]), dy = dsub(qy, xy[2 * i + 1]);
+            const double dx = dsub(qx, q.x), dy = dsub(qy, q.y);
             const double d2 = dadd(dmul(dx, dx), dmul(dy, dy));
             if (d2 < best || (d2 == best && i < bi)) { best = d2; bi = i; }
           }
