@@ -113,10 +113,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
   uint64_t* acc_full = empty + S;    // [2]
   uint64_t* acc_empty = acc_full + 2;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  // bias of every output column (zero past C_out), read by the epilogue
+  // from shared memory instead of one global load per element
+  float* s_bias = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(tmem_slot + 1) + 15) & ~uintptr_t(15));
 
   const int tid = threadIdx.x, warp = tid >> 5;
   const int wy = op.oy1 - op.oy0, wx = op.ox1 - op.ox0;
   const int64_t M = (int64_t)op.batch * wy * wx;
+  for (int i = tid; i < T.n_tiles * T.bn; i += blockDim.x)
+    s_bias[i] = i < op.out.C ? __ldg(op.bias + i) : 0.f;
   const int Cin = op.in.C, Cout = op.out.C;
   const int64_t total_tiles = T.m_tiles * T.n_tiles;
   // MODE 4 stacks the two weight planes along N (one MMA per A plane,
@@ -323,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int n = n0 + c + i;
-            float x = v[i] + (n < Cout ? __ldg(op.bias + n) : 0.f);
+            float x = v[i] + s_bias[n];
             if (op.lrelu) x = x >= 0.f ? x : 0.01f * x;
             v[i] = x;
           }
@@ -692,7 +698,8 @@ TcPlan plan_for(const ConvOp& op, int precision) {
   const size_t budget = 218 * 1024;
   p.stages = (int)std::min<size_t>(6, budget / stage);
   p.stages = std::max(p.stages, 1);
-  p.smem = p.stages * stage + 1024 + 8 * (2 * p.stages + 4) + 16 + 2 * BM * 12 + 16;
+  p.smem = p.stages * stage + 1024 + 8 * (2 * p.stages + 4) + 16 + 2 * BM * 12 + 16 +
+           16 + 4 * (size_t)p.ntiles * p.bn;
   return p;
 }
 
