@@ -10,3 +10,8 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:bake_splat -s 1 -c 1 -o gpurun_out/${R}_splat python bench.py --steps 1 --warmup 1 --no-cpu --no-sweep > /dev/null 2>&1
 timeout 900 python bench.py > gpurun_out/${R}_bench.json 2> gpurun_out/${R}_bench.err
 cat gpurun_out/${R}_bench.json
+# the reference arm as the driver runs it (timed, for the record)
+T0=$(date +%s)
+timeout 900 python bench.py --impl reference > gpurun_out/${R}_bench_ref.json 2> gpurun_out/${R}_bench_ref.err
+echo "reference arm wall $(( $(date +%s) - T0 )) s"
+cat gpurun_out/${R}_bench_ref.json
