@@ -545,7 +545,13 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
   p.pa = precision == 2 ? 1 : 2;
   p.pb = precision == 2 ? 1 : precision == 4 ? 2 : 3;
   const int n16 = (op.out.C + 15) / 16 * 16;
-  p.ntiles = (n16 + 127) / 128;
+  {  // widest N tile: up to 256 (one MMA) so a layer's A halo is gathered
+     // and read once for all its columns (enc*.2, N = 192: 235 -> 192 us
+     // against two 96-column tiles); TS_H2_BNMAX overrides
+    const char* e = getenv("TS_H2_BNMAX");
+    const int bnmax = e ? std::max(16, std::min(256, atoi(e))) : 256;
+    p.ntiles = (n16 + bnmax - 1) / bnmax;
+  }
   p.bn = ((n16 + p.ntiles - 1) / p.ntiles + 15) / 16 * 16;
   p.cchunks = (op.in.C + kKC - 1) / kKC;
   const int wx = op.ox1 - op.ox0, wy = op.oy1 - op.oy0;
