@@ -48,6 +48,9 @@ constexpr int kKC = 32;    // channels per K chunk
 #define TS_H2_PRODW 10  // measured: 10 beats 8 and 12 on every layer (7.34 vs 7.40 / 7.48 ms per step)
 #endif
 constexpr int kProdW = TS_H2_PRODW;
+#ifndef TS_H2_IN8
+#define TS_H2_IN8 4
+#endif
 constexpr int kProdT = kProdW * 32;
 constexpr int kInflight = 8;  // 16-byte loads in flight per producer thread
 constexpr int kMmaW = kProdW;
@@ -244,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
           const int row0 = tid >> 2;
           const int obase = row0 * kRow + ((piece ^ ((row0 >> 1) & 3)) << 4);
           constexpr int kStep8 = kProdT / 4;
-          constexpr int kIn8 = 4;
+          constexpr int kIn8 = TS_H2_IN8;  // 32-byte loads in flight per thread
           for (int r0 = row0; r0 < L; r0 += kStep8 * kIn8) {
             float v[kIn8][8];
 #pragma unroll
