@@ -24,9 +24,10 @@
 //               store the SW64 image, arrive.
 //   warp P      MMA issuer + TMEM owner (AB x SUB x BN fp32 columns).
 //   warp P+1    weight loader: cp.async.bulk of pre-swizzled weight stages.
-//   warps P+2.. epilogue (8): two warps per TMEM lane quadrant, alternating
-//               16-column groups: tcgen05.ld of every B plane's columns,
-//               one wait, + bias (shared), leaky ReLU, fp32 NHWC store.
+//   warps P+2.. epilogue (TS_H2_EPIW = 4): one warp per TMEM lane quadrant
+//               (with 8 or 12, warps of a quadrant alternate 16-column
+//               groups): tcgen05.ld of every B plane's columns, one wait,
+//               + bias (shared), leaky ReLU, fp32 NHWC store.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -55,7 +56,11 @@ constexpr int kProdT = kProdW * 32;
 constexpr int kInflight = 8;  // 16-byte loads in flight per producer thread
 constexpr int kMmaW = kProdW;
 constexpr int kLoadW = kProdW + 1;
-constexpr int kEpiW0 = kProdW + 2, kEpiWarps = 8;
+#ifndef TS_H2_EPIW
+#define TS_H2_EPIW 4  // measured: 4 beats 8 and 12 (7.15 vs 7.38 / 7.45 ms of halo2 launches per step)
+#endif
+constexpr int kEpiW0 = kProdW + 2, kEpiWarps = TS_H2_EPIW;  // multiple of 4
+static_assert(kEpiWarps % 4 == 0, "epilogue warps cover the 4 TMEM lane quadrants");
 static_assert(kProdW % 2 == 0, "row stride must keep the swizzle phase");
 constexpr int kThreads = (kEpiW0 + kEpiWarps) * 32;
 constexpr int kHdr = 1024;         // packed-weight header: u32 count, u32 0, u16 list
@@ -473,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
             }
           }
         }
-        for (int c = 16 * half; c < BN; c += 32) {
+        for (int c = 16 * half; c < BN; c += 16 * (kEpiWarps / 4)) {
           uint32_t r[PB][16];
           const uint32_t ta = tmem + lane_base + acc * acc_cols + ug * PBS * BN + c;
 #pragma unroll
