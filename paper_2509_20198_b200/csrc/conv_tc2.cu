@@ -597,14 +597,23 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
     const size_t hbuf = (size_t)p.pa * L * kRow;
     const size_t fixed = 1024 + 8 * 40 + 16 + 16 * (size_t)L + 6 * kMaxStages + 64 +
                          4 * (size_t)p.ntiles * p.bn + 16;
+    static const int hb_env = [] {  // TS_H2_HB=2/3: force the halo buffer count
+      const char* e = getenv("TS_H2_HB");
+      return e ? atoi(e) : 0;
+    }();
+    static const int sb_env = [] {  // TS_H2_SB=<n>: cap on the weight ring stages
+      const char* e = getenv("TS_H2_SB");  // measured: 3-4 about 1% faster than 8
+      return e ? atoi(e) : 4;
+    }();
     for (int hb : {3, 2}) {
+      if (hb_env && hb != hb_env) continue;
       const size_t used = hb * hbuf + fixed;
       if (used + 3 * bst > cap) continue;
       p.sub = sub;
       p.accbufs = ab;
       p.hbufs = hb;
       p.lrows = L;
-      p.bstages = (int)std::min<size_t>(8, (cap - used) / bst);
+      p.bstages = (int)std::min<size_t>(std::max(3, std::min(8, sb_env)), (cap - used) / bst);
       p.smem = used + p.bstages * bst;
       *out = p;
       return true;
