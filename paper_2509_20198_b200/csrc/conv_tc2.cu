@@ -49,6 +49,9 @@ constexpr int kKC = 32;    // channels per K chunk
 #define TS_H2_PRODW 10  // measured: 10 beats 8 and 12 on every layer (7.34 vs 7.40 / 7.48 ms per step)
 #endif
 constexpr int kProdW = TS_H2_PRODW;
+#ifndef TS_H2_PF
+#define TS_H2_PF 1  // L2 prefetch of the next chunk / next tile's first chunk
+#endif
 #ifndef TS_H2_IN8
 #define TS_H2_IN8 4
 #endif
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
                   op.in.coff;
         }
         ro_[j] = off;
-        if (pf && off >= 0 && !op.in.planes)
+        if (TS_H2_PF && pf && off >= 0 && !op.in.planes)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(op.in.base + off));
       }
     };
@@ -263,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
               if (row < L) {
                 const int64_t off = ro[row];
                 if (off >= 0 && ch_ok) ld_v8(src + off, v[u]);
-                if (off >= 0 && pf_ok)
+                if (TS_H2_PF && off >= 0 && pf_ok)
                   asm volatile("prefetch.global.L2 [%0];" ::"l"(src + off + kKC));
               }
             }
