@@ -163,3 +163,16 @@ def test_key_grid_interior_list_of_a_tiling_is_one_key():
         assert inner[c] == 1 and ids[off[c]] == k
         assert off[c + 1] - off[c] == 9 or k in (0, 4, 15, 19) or \
             off[c + 1] - off[c] == 6
+
+
+def test_wire_record_sizes_and_split():
+    """WireHeightmap record sizes (docs/wire.md: 14 + 16,384 [+ 12,288]) and
+    the host-side split of a batch buffer (no GPU needed)."""
+    from paper_2509_20198_b200 import wire
+    assert wire.record_size(True) == 28686
+    assert wire.record_size(False) == 16398
+    buf = bytes(range(256)) * (2 * 28686 // 256) + bytes(2 * 28686 % 256)
+    recs = wire.split_records(buf, True)
+    assert len(recs) == 2 and b"".join(recs) == buf
+    with pytest.raises(ValueError):
+        wire.split_records(buf[:-1], True)
