@@ -549,7 +549,11 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
   if (op.ph == 2 && (op.k != 3 || op.pad != 1 || op.up2 || G < 1 || G > 4)) return false;
   // 1x1 layers: measured slower than the regular kernel (A re-read per N
   // tile); opt in with TS_H2_1X1=1
-  if (op.k == 1 && !(getenv("TS_H2_1X1") && getenv("TS_H2_1X1")[0] == '1')) return false;
+  static const bool h2_1x1 = [] {
+    const char* e = getenv("TS_H2_1X1");
+    return e && e[0] == '1';
+  }();
+  if (op.k == 1 && !h2_1x1) return false;
   if (op.in.C % 4 || op.in.cstride % 4 || op.in.coff % 4) return false;
   if (op.in.planes && (op.in.C % 8 || op.in.cstride % 8 || op.in.coff % 8)) return false;
   if (op.out.planes && (op.out.C % 16 || op.out.cstride % 8 || op.out.coff % 8)) return false;
@@ -560,8 +564,10 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
   {  // widest N tile: up to 256 (one MMA) so a layer's A halo is gathered
      // and read once for all its columns (enc*.2, N = 192: 235 -> 192 us
      // against two 96-column tiles); TS_H2_BNMAX overrides
-    const char* e = getenv("TS_H2_BNMAX");
-    const int bnmax = e ? std::max(16, std::min(256, atoi(e))) : 256;
+    static const int bnmax = [] {
+      const char* e = getenv("TS_H2_BNMAX");
+      return e ? std::max(16, std::min(256, atoi(e))) : 256;
+    }();
     p.ntiles = (n16 + bnmax - 1) / bnmax;
   }
   p.bn = ((n16 + p.ntiles - 1) / p.ntiles + 15) / 16 * 16;
@@ -578,15 +584,18 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
   // every product into the same BN columns, which doubles the sub-tiles
   // per TMEM buffer and amortises the MMA issuer's per-stage overhead.
   {
-    const char* e = getenv("TS_H2_STACK");
+    static const int stack_env = [] {  // -1: planner's choice
+      const char* e = getenv("TS_H2_STACK");
+      return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
     // (a phase group stacks only if two sub-tiles still get two buffers)
-    p.stack = e ? (e[0] == '1') : (p.pb * p.bn <= 64 && 4 * G * p.pb * p.bn <= 512);
+    p.stack = stack_env >= 0 ? stack_env : (p.pb * p.bn <= 64 && 4 * G * p.pb * p.bn <= 512);
     if (p.pb * p.bn > 256) p.stack = 0;  // MMA N limit
   }
   const int cols = G * (p.stack ? p.pb * p.bn : p.bn);
   int cand[6][2] = {{4, 2}, {2, 2}, {1, 2}, {4, 1}, {2, 1}, {1, 1}};
   {  // TS_H2_SUBAB=<sub>,<accbufs>: try that candidate first (A/B measurement)
-    const char* e = getenv("TS_H2_SUBAB");
+    static const char* e = getenv("TS_H2_SUBAB");
     if (e && e[0] >= '1' && e[0] <= '4' && e[1] == ',' && (e[2] == '1' || e[2] == '2')) {
       cand[5][0] = cand[0][0]; cand[5][1] = cand[0][1];
       cand[0][0] = e[0] - '0'; cand[0][1] = e[2] - '0';
