@@ -29,7 +29,10 @@ constexpr int kMaxCavity = 176;  // with the mesh: 31.5 KB, 7 patch-warps per SM
 // 1,024 patches of a configs[1] batch (N ~ 310-340) run in ONE wave.
 constexpr int kSmemPoints = 384;
 constexpr int kSmemSlots = 2 * kSmemPoints + 8;
-constexpr int kScanIlp = 4;  // circle tests per lane per cavity-scan pass (2: +6%, 8: +7% time)
+#ifndef TS_DL_ILP
+#define TS_DL_ILP 6
+#endif
+constexpr int kScanIlp = TS_DL_ILP;  // circle tests per lane per cavity-scan pass (4: +2%, 8: +1% time)
 
 constexpr size_t kDelaunaySmem = (size_t)kSmemSlots * (3 * sizeof(int) + 3 * sizeof(double)) +
                                  kMaxCavity * sizeof(int) + (kMaxCavity + 8) * sizeof(int2) +
