@@ -413,18 +413,26 @@ raster_kernel(RasterArgs A) {
     for (int r = 0; r < kBins; ++r) {
       const int X0 = max(bx0 - r, 0), X1 = min(bx1 + r, kBins - 1);
       const int Y0 = max(by0 - r, 0), Y1 = min(by1 + r, kBins - 1);
+      // points are in bin order, so a run of bins of one grid row is one
+      // contiguous candidate range: a full row of the ring is one range,
+      // an inner row its (up to) two edge bins
+      auto scan = [&](int k0, int k1) {
+#pragma unroll 2
+        for (int k = k0; k < k1; ++k) {
+          const double2 q = s_bxy[k];  // no id -> coordinate indirection
+          const int i = s_bid[k];
+          const double dx = dsub(qx, q.x), dy = dsub(qy, q.y);
+          const double d2 = dadd(dmul(dx, dx), dmul(dy, dy));
+          if (d2 < best || (d2 == best && i < bi)) { best = d2; bi = i; }
+        }
+      };
       for (int gy = Y0; gy <= Y1; ++gy) {
-        const bool inner_row = gy > by0 - r && gy < by1 + r;
-        for (int gx = X0; gx <= X1; ++gx) {
-          if (r > 0 && inner_row && gx > bx0 - r && gx < bx1 + r) continue;  // ring only
-          const int b = gy * kBins + gx;
-          for (int k = s_bstart[b]; k < s_bstart[b + 1]; ++k) {
-            const double2 q = s_bxy[k];  // no id -> coordinate indirection
-            const int i = s_bid[k];
-            const double dx = dsub(qx, q.x), dy = dsub(qy, q.y);
-            const double d2 = dadd(dmul(dx, dx), dmul(dy, dy));
-            if (d2 < best || (d2 == best && i < bi)) { best = d2; bi = i; }
-          }
+        const int row = gy * kBins;
+        if (r == 0 || gy <= by0 - r || gy >= by1 + r) {
+          scan(s_bstart[row + X0], s_bstart[row + X1 + 1]);
+        } else {
+          if (bx0 - r >= 0) scan(s_bstart[row + bx0 - r], s_bstart[row + bx0 - r + 1]);
+          if (bx1 + r < kBins) scan(s_bstart[row + bx1 + r], s_bstart[row + bx1 + r + 1]);
         }
       }
       double mind = DBL_MAX;
