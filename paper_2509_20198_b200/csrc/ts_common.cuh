@@ -41,7 +41,10 @@ __device__ __forceinline__ int64_t floor_i64(double v) { return (int64_t)floor(v
 
 // cell centre coordinate -1 + (k + 0.5) * (2 / res)  (patches.py:210)
 __device__ __forceinline__ double cell_center(int k, int res) {
-  return dadd(-1.0, dmul((double)k + 0.5, ddiv(2.0, (double)res)));
+  // 2 / 96 folded at compile time is the same correctly rounded double as
+  // numpy's (and __ddiv_rn's) quotient; other resolutions divide
+  const double step = res == kRes ? 2.0 / kRes : ddiv(2.0, (double)res);
+  return dadd(-1.0, dmul((double)k + 0.5, step));
 }
 
 template <typename T>
