@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", type=int, default=None,
                     help="0 fp32 SIMT, 1 tf32x3, 2 bf16, 3 bf16 2x3 planes, "
-                         "4 bf16 2x2 planes (default; fp32-class)")
+                         "4 bf16 2x2 planes, 5 fp16x3 (default; fp32-class)")
     ap.add_argument("--no-splat", action="store_true")
     ap.add_argument("--splat-points", type=int, default=200_000_000)
     ap.add_argument("--cpu-sample", type=int, default=32)
@@ -187,7 +187,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2509_20198_b200._lib import lib
     from paper_2509_20198_b200.lasio import parse_header
     from paper_2509_20198_b200.pipeline import HeightmapPipeline
-    from paper_2509_20198_b200.refiner import (PRECISION_BF16X4,
+    from paper_2509_20198_b200.refiner import (PRECISION_FP16X3,
                                                default_descriptor,
                                                random_weights)
 
@@ -203,7 +203,7 @@ def run_ours(args, rank, world, local_rank):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    precision = PRECISION_BF16X4 if args.precision is None else args.precision
+    precision = PRECISION_FP16X3 if args.precision is None else args.precision
     tiles, own = band_tiles(rank, world)
     images = [t.data for t in tiles]
     descs = np.concatenate([D.tile_desc(parse_header(b)) for b in images])
@@ -353,9 +353,11 @@ def run_ours(args, rank, world, local_rank):
             "ms_per_step": round(ms_max, 4),
             "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None,
-            "dtype": {0: "f32", 1: "tf32x3", 2: "bf16",
-                      3: "bf16 2x3-plane split (fp32-class)",
-                      4: "bf16 2x2-plane split (fp32-class)"}[precision] +
+            "dtype": {0: "f32", 1: "tf32x3 (bf16-class)", 2: "bf16",
+                      3: "bf16 2x3-plane split (bf16-class)",
+                      4: "bf16 2x2-plane split (bf16-class)",
+                      5: "fp16x3 scaled-plane split (fp32-class: "
+                         "<= 2e-3 m vs the fp32 reference)"}[precision] +
                      " CNN, f64 geometry",
             "data": "synthetic (seeded FractalTerrain stub-body LAZ tiles, "
                     "random He weights seed 3)",
@@ -384,10 +386,10 @@ def run_ours(args, rank, world, local_rank):
                          "peak_kind": f"{peak_kind} bf16 dense (burst)",
                          "algorithmic": f"{CROP_GFLOP} GFLOP/tile (fp32 "
                                         f"MACs x2, crop-aware) x {P} tiles",
-                         "note": "fp32-class mode issues 3 bf16 products "
-                                 "per MAC (a0.b0 + a0.b1 + a1.b0): its "
-                                 "tensor ceiling is peak/3; decoders run "
-                                 "in phase form (4/9 of the reference "
+                         "note": "fp32-class mode issues 3 fp16 products "
+                                 "per MAC (a0.b0 + 2^-11 [a0.b1 + a1.b0]): "
+                                 "its tensor ceiling is peak/3; decoders "
+                                 "run in phase form (4/9 of the reference "
                                  "MACs), counted at the reference's MACs",
                          "frac_of_emulated_peak": round(
                              3 * cnn_tflops / tflops, 5),
@@ -429,15 +431,15 @@ def cnn_in_of(pipe, tb, centers, cell_range):
 
 def cnn_sweep(bundle, cnn_in, dev, batches=(64, 1024, 16384)):
     """configs[4]: CNN refine alone over batches of the configs[1] rasters
-    (repeated), fp32-class (bf16x3 products) vs plain bf16, CUDA events."""
+    (repeated), fp32-class (fp16x3 products) vs plain bf16, CUDA events."""
     import torch
     from paper_2509_20198_b200.refiner import (PRECISION_BF16,
-                                               PRECISION_BF16X4,
+                                               PRECISION_FP16X3,
                                                device_weights)
     hbm, tflops, _kind = peaks()
     rows = []
     src = cnn_in
-    for prec, name in ((PRECISION_BF16X4, "fp32-class (3 bf16 products)"),
+    for prec, name in ((PRECISION_FP16X3, "fp32-class (3 fp16 products)"),
                        (PRECISION_BF16, "bf16")):
         w = device_weights(bundle, prec)
         for B in batches:

@@ -1,6 +1,7 @@
 // Convolution layer descriptors shared by the refine planner and kernels.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 #include <cstring>
@@ -102,6 +103,18 @@ inline float bf16_to_f_host(uint16_t h) {
   memcpy(&f, &u, 4);
   return f;
 }
+
+// FP16X3 weight planes (tc_ptx.cuh Mode<5>): w = h0 + 2^-11 h1
+inline void split_f16_host(float v, uint16_t& h0, uint16_t& h1) {
+  const __half a = __float2half_rn(v);
+  const float r = (v - __half2float(a)) * 2048.f;
+  const __half b = __float2half_rn(r);
+  memcpy(&h0, &a, 2);
+  memcpy(&h1, &b, 2);
+}
+
+// precision modes that run on the bf16/fp16 tensor-core kernels
+inline bool tc16_mode(int precision) { return precision >= 2 && precision <= 5; }
 
 // The four encoders' first layers (3x3 stride 2 pad 1 over 1/1/3/3 raw
 // input channels) in one launch; outputs in space-to-depth layout.

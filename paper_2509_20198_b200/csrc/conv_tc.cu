@@ -84,6 +84,8 @@ __device__ __forceinline__ void store_piece(uint8_t* sa, int row, int piece, flo
     if (MODE == 2) {
       *reinterpret_cast<uint2*>(sa + off) =
           make_uint2(hi_halves(rn_bf(a.x), rn_bf(a.y)), hi_halves(rn_bf(a.z), rn_bf(a.w)));
+    } else if (Mode<MODE>::f16) {
+      store_split_h(sa + off, plane_bytes, a);
     } else {
       store_split2(sa + off, plane_bytes, a);
     }
@@ -128,9 +130,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
   // MODE 4 stacks the two weight planes along N (one MMA per A plane,
   // N = 2 BN; the epilogue adds the halves): half the A-operand shared
   // memory reads of one MMA per plane pair
-  const int NST = (MODE == 4 && !T.wide) ? 2 : 1;
+  // MODE 5 (FP16X3): [main | correction] column blocks, same stacking
+  const int NST = MODE == 6 ? 3 : ((MODE == 4 && !T.wide) || Md::f16) ? 2 : 1;
+  // two accumulator buffers (epilogue overlaps the next tile) when they fit
+  const int AB = 2 * NST * BN <= 512 ? 2 : 1;
   uint32_t ncols = 32;
-  while ((int)ncols < 2 * NST * BN) ncols <<= 1;
+  while ((int)ncols < AB * NST * BN) ncols <<= 1;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -230,16 +235,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
     // ------------------------------ MMA issuer -----------------------------
     // The whole warp walks the loop (uniform registers), one elected lane
     // issues; descriptors are integer offsets from precomputed bases.
-    const uint32_t idesc = make_idesc(Md::tf32 ? 2u : 1u, (NST * BN) > 256 ? 256 : NST * BN);
-    const uint32_t idesc_b0 = make_idesc(1u, BN);
+    const int NMMA = Md::f16 ? 2 * BN : NST * BN;  // stacked B rows per MMA
+    const uint32_t idesc = make_idesc(mode_fmt<MODE>(), NMMA > 256 ? 256 : NMMA);
+    const uint32_t idesc_b0 = make_idesc(mode_fmt<MODE>(), BN);
     (void)idesc_b0;
     const uint64_t d_smem = sw128_desc(su32(smem));
     const uint32_t pa = (BM * kRowBytes) >> 4, pb = (BN * kRowBytes) >> 4;
     int s = 0, lt = 0;
     uint32_t ph = 0;
     for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
-      const int acc = lt & 1;
-      mbar_wait(acc_empty + acc, ((lt >> 1) & 1) ^ 1);
+      const int acc = lt % AB;
+      mbar_wait(acc_empty + acc, ((lt / AB) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d = tmem + acc * NST * BN;
       for (int kit = 0; kit < T.kiters; ++kit) {
@@ -258,6 +264,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
               umma<true>(d, ak + pa, bk, idesc, 1u);
             } else if (MODE == 2) {
               umma<false>(d, ak, bk, idesc, first);
+            } else if (Md::f16) {
+              // a0 . [b0 | b1] -> [main | corr], a1 . b0 -> corr; MODE 6:
+              // odd K steps put a0 . b0 (as a0 . 2^11 b0) into corr too
+              if (MODE == 6 && (k & 1)) {
+                // b1 -> corr, b0 -> main_odd (the tile's first odd step
+                // overwrites it)
+                umma<false>(d + BN, ak, bk + pb, idesc_b0, 1u);
+                umma<false>(d + 2 * BN, ak, bk, idesc_b0, (kit | (k >> 1)) ? 1u : 0u);
+              } else {
+                umma<false>(d, ak, bk, idesc, first);
+              }
+              umma<false>(d + BN, ak + pa, bk, idesc_b0, 1u);
             } else if (MODE == 4) {
               // a0 . [b0 | b1] (N = 2 BN), then a1 . b0 (N = BN): the
               // a1 . b1 term (<= 2^-18 |ab|, the size of the split
@@ -295,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
                       ((reinterpret_cast<uintptr_t>(op.out.base) & 31) == 0);
     int lt = 0;
     for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
-      const int acc = lt & 1;
+      const int acc = lt % AB;
       const int64_t mt = tile / T.n_tiles;
       const int nt = (int)(tile - mt * T.n_tiles);
       const int n0 = nt * BN;
@@ -314,16 +332,22 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
         act_block(op.out, b, y, x, blk, ochan);
         oblk = op.out.base + blk;
       }
-      mbar_wait(acc_full + acc, (lt >> 1) & 1);
+      mbar_wait(acc_full + acc, (lt / AB) & 1);
       tc_fence_after();
       for (int c = 0; c < BN; c += 16) {
         float v[16];
         tmem_ld16(tmem + lane_base + acc * NST * BN + c, v);  // warp-collective
-        if (NST == 2) {
+        if (NST == 3) {  // MODE 6: main_even + main_odd, then the correction
+          float w[16];
+          tmem_ld16(tmem + lane_base + acc * NST * BN + 2 * BN + c, w);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += w[i];
+        }
+        if (NST >= 2) {
           float w[16];
           tmem_ld16(tmem + lane_base + acc * NST * BN + BN + c, w);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] += w[i];
+          for (int i = 0; i < 16; ++i) v[i] += Md::f16 ? w[i] * kF16LoInv : w[i];
         }
         if (valid) {
 #pragma unroll
@@ -680,7 +704,7 @@ struct TcPlan {
 TcPlan plan_for(const ConvOp& op, int precision) {
   TcPlan p{};
   p.pa = precision == 2 ? 1 : 2;
-  p.pb = precision == 1 ? 2 : precision == 2 ? 1 : precision == 4 ? 2 : 3;
+  p.pb = precision == 2 ? 1 : precision == 3 ? 3 : 2;
   p.kc = precision == 1 ? 32 : 64;
   const int n16 = (op.out.C + 15) / 16 * 16;
   // BF16X4 1x1 layers (the merge GEMMs) take N tiles of up to 256 without
@@ -688,6 +712,7 @@ TcPlan plan_for(const ConvOp& op, int precision) {
   // halve the producers' work
   const char* e = getenv("TS_TC_WIDE");
   const bool wide_ok = precision == 4 && op.k == 1 && !(e && e[0] == '0');
+  // (MODE 6: three column blocks per accumulator, two accumulators)
   const int cap = wide_ok ? 256 : 128;
   p.ntiles = (n16 + cap - 1) / cap;
   p.bn = ((n16 + p.ntiles - 1) / p.ntiles + 15) / 16 * 16;
@@ -712,6 +737,7 @@ struct HaloPlan {
 
 bool halo_plan(const ConvOp& op, int precision, HaloPlan* hp) {
   if (op.stride != 1 || op.k < 2 || op.pad * 2 + 1 != op.k) return false;
+  if (precision >= 5) return false;  // FP16X3 runs on the wide-M halo kernel
   HaloPlan h{};
   h.base = plan_for(op, precision);
   const int wx = op.ox1 - op.ox0, wy = op.oy1 - op.oy0;
@@ -739,7 +765,7 @@ bool conv_tc_halo_eligible(const ConvOp& op, int precision) {
 }
 
 bool conv_tc_supported(const ConvOp& op, int precision) {
-  if (precision < 1 || precision > 4) return false;
+  if (precision < 1 || precision > 6) return false;
   return op.in.C % 4 == 0 && op.in.cstride % 4 == 0 && op.in.coff % 4 == 0;
 }
 
@@ -782,6 +808,11 @@ std::vector<uint8_t> pack_tc_weights(const float* w_oikk, int co, int ci, int k,
           } else if (precision == 2) {
             const uint16_t h = f2bf16_rn(v);
             memcpy(base + off, &h, 2);
+          } else if (precision >= 5) {
+            uint16_t h0, h1;
+            split_f16_host(v, h0, h1);
+            memcpy(base + off, &h0, 2);
+            memcpy(base + plane + off, &h1, 2);
           } else if (precision == 4) {  // RN split, like the device producers
             const uint16_t h0 = f2bf16_rn(v);
             const uint16_t h1 = f2bf16_rn(v - bf16_to_f(h0));
@@ -879,6 +910,8 @@ int launch_conv_tc(const ConvOp& op, int precision, void* stream) {
   if (precision == 1) TS_TC_LAUNCH(1);
   else if (precision == 2) TS_TC_LAUNCH(2);
   else if (precision == 4) TS_TC_LAUNCH(4);
+  else if (precision == 5) TS_TC_LAUNCH(5);
+  else if (precision == 6) TS_TC_LAUNCH(6);
   else TS_TC_LAUNCH(3);
 #undef TS_TC_LAUNCH
   TS_LAUNCH_CHECK();

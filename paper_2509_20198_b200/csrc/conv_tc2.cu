@@ -140,7 +140,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
   const int MT = SUB * 128;
   const int64_t total_tiles = T.m_tiles * T.n_tiles;
   const int AB = T.accbufs;
-  const int PBS = T.stack ? PB : 1;     // accumulator column blocks per sub
+  // accumulator column blocks per sub-tile (MODE 5: main + correction)
+  const int PBS = MODE == 6 ? 3 : Md::f16 ? 2 : T.stack ? PB : 1;
   const int acc_cols = SUB * G * PBS * BN;  // per accumulator buffer
   uint32_t ncols = 32;
   while ((int)ncols < AB * acc_cols) ncols <<= 1;
@@ -276,16 +277,24 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
               if (r0 + u * kStep8 < L) {
                 uint8_t* d = so + u * kStep8 * kRow;
                 uint32_t h[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) h[i] = pack_bf2(v[u][2 * i], v[u][2 * i + 1]);
-                *reinterpret_cast<uint4*>(d) = make_uint4(h[0], h[1], h[2], h[3]);
-                if (MODE != 2) {
+                if (Md::f16) {
                   uint32_t l[4];
 #pragma unroll
-                  for (int i = 0; i < 4; ++i)
-                    l[i] = pack_bf2(v[u][2 * i] - __uint_as_float(h[i] << 16),
-                                    v[u][2 * i + 1] - __uint_as_float(h[i] & 0xFFFF0000u));
+                  for (int i = 0; i < 4; ++i) split_h2(v[u][2 * i], v[u][2 * i + 1], h[i], l[i]);
+                  *reinterpret_cast<uint4*>(d) = make_uint4(h[0], h[1], h[2], h[3]);
                   *reinterpret_cast<uint4*>(d + plane_a) = make_uint4(l[0], l[1], l[2], l[3]);
+                } else {
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) h[i] = pack_bf2(v[u][2 * i], v[u][2 * i + 1]);
+                  *reinterpret_cast<uint4*>(d) = make_uint4(h[0], h[1], h[2], h[3]);
+                  if (MODE != 2) {
+                    uint32_t l[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                      l[i] = pack_bf2(v[u][2 * i] - __uint_as_float(h[i] << 16),
+                                      v[u][2 * i + 1] - __uint_as_float(h[i] & 0xFFFF0000u));
+                    *reinterpret_cast<uint4*>(d + plane_a) = make_uint4(l[0], l[1], l[2], l[3]);
+                  }
                 }
               }
             }
@@ -328,6 +337,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
               if (MODE == 2)
                 *reinterpret_cast<uint2*>(d) =
                     make_uint2(pack_bf2(a.x, a.y), pack_bf2(a.z, a.w));
+              else if (Md::f16)
+                store_split_h(d, plane_a, a);
               else
                 store_split2(d, plane_a, a);
             }
@@ -349,8 +360,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     // D[:, p*BN + n] accumulates A . b_p, summed by the epilogue.  Same
     // MACs as one MMA per (A plane, B plane) pair at N = BN, but every
     // 4 KB A read from shared memory now feeds PB*BN columns.
-    const uint32_t idesc = make_idesc(1u, PB * BN);
-    const uint32_t idesc_b0 = make_idesc(1u, BN);
+    // stacked B planes: all PB (bf16 modes) or [b0 | b1] (fp16 modes)
+    const uint32_t idesc = make_idesc(mode_fmt<MODE>(), (Md::f16 ? 2 : PB) * BN);
+    const uint32_t idesc_b0 = make_idesc(mode_fmt<MODE>(), BN);
     const uint64_t d_halo = sw64_desc(su32(halo));
     const uint64_t d_ring = sw64_desc(su32(bring));
     const uint32_t pa = (uint32_t)plane_a >> 4;
@@ -392,6 +404,25 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
               for (int u = 0; u < SUB; ++u) {
                 const uint64_t ak = a0 + (uint64_t)(u * (128 * kRow >> 4) + 2 * k);
                 const uint32_t du = dg + u * G * PBS * BN;
+                if (Md::f16) {
+                  // a0 . [b0 | b1] -> [main | corr] (stacked, N = 2 BN) or
+                  // two N = BN MMAs; a1 . b0 -> corr.  MODE 6: the odd K
+                  // step adds a0 . 2^11 b0 (plane 2) into corr instead
+                  const uint32_t f = k ? 1u : first;
+                  if (MODE == 6 && k) {
+                    // b1 -> corr, b0 -> main_odd (overwritten by a tile's
+                    // first stage)
+                    umma<false>(du + BN, ak, b0 + (uint64_t)b_plane16 + 2 * k, idesc_b0, 1u);
+                    umma<false>(du + 2 * BN, ak, b0 + 2 * k, idesc_b0, first);
+                  } else if (T.stack) {
+                    umma<false>(du, ak, b0 + 2 * k, idesc, f);
+                  } else {
+                    umma<false>(du, ak, b0 + 2 * k, idesc_b0, f);
+                    umma<false>(du + BN, ak, b0 + (uint64_t)b_plane16 + 2 * k, idesc_b0, f);
+                  }
+                  umma<false>(du + BN, ak + pa, b0 + 2 * k, idesc_b0, 1u);
+                  continue;
+                }
                 if (T.stack) {
                   umma<false>(du, ak, b0 + 2 * k, idesc, k ? 1u : first);
                 } else {  // a0 . b_p for every plane into the same columns
@@ -482,19 +513,24 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
           }
         }
         for (int c = 16 * half; c < BN; c += 16 * (kEpiWarps / 4)) {
-          uint32_t r[PB][16];
+          uint32_t r[3][16];
           const uint32_t ta = tmem + lane_base + acc * acc_cols + ug * PBS * BN + c;
 #pragma unroll
-          for (int p = 0; p < PB; ++p)
+          for (int p = 0; p < 3; ++p)
             if (p < PBS) tmem_ld16_nw(ta + p * BN, r[p]);
           tmem_wait_ld();
           float v[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             float x = __uint_as_float(r[0][i]);
+            if (Md::f16) {
+              if (MODE == 6) x += __uint_as_float(r[PBS - 1][i]);
+              x += __uint_as_float(r[1][i]) * kF16LoInv;
+            } else {
 #pragma unroll
-            for (int p = 1; p < PB; ++p)
-              if (p < PBS) x += __uint_as_float(r[p][i]);
+              for (int p = 1; p < PB; ++p)
+                if (p < PBS) x += __uint_as_float(r[p][i]);
+            }
             x += s_bias[n0 + c + i];
             if (op.lrelu) x = x >= 0.f ? x : 0.01f * x;
             v[i] = x;
@@ -540,7 +576,8 @@ struct Halo2Plan {
 };
 
 bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
-  if (precision != 2 && precision != 3 && precision != 4) return false;
+  if (precision < 2 || precision > 6) return false;
+  if (precision >= 5 && (op.in.planes || op.out.planes)) return false;
   // stride-1 k >= 2 (incl. the 2x2 space-to-depth form of stride-2 layers);
   // 1x1 layers stay on the regular kernel (no halo to reuse, and their
   // multi-N-tile shapes re-read A per N tile here)
@@ -559,7 +596,7 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
   if (op.out.planes && (op.out.C % 16 || op.out.cstride % 8 || op.out.coff % 8)) return false;
   Halo2Plan p{};
   p.pa = precision == 2 ? 1 : 2;
-  p.pb = precision == 2 ? 1 : precision == 4 ? 2 : 3;
+  p.pb = precision == 2 ? 1 : precision == 3 ? 3 : 2;
   const int n16 = (op.out.C + 15) / 16 * 16;
   {  // widest N tile: up to 256 (one MMA) so a layer's A halo is gathered
      // and read once for all its columns (enc*.2, N = 192: 235 -> 192 us
@@ -568,7 +605,9 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
       const char* e = getenv("TS_H2_BNMAX");
       return e ? std::max(16, std::min(256, atoi(e))) : 256;
     }();
-    p.ntiles = (n16 + bnmax - 1) / bnmax;
+    // FP16X3: the two weight planes stack into one MMA (N = 2 BN <= 256)
+    const int bmax = precision >= 5 ? std::min(bnmax, 128) : bnmax;
+    p.ntiles = (n16 + bmax - 1) / bmax;
   }
   p.bn = ((n16 + p.ntiles - 1) / p.ntiles + 15) / 16 * 16;
   p.cchunks = (op.in.C + kKC - 1) / kKC;
@@ -590,9 +629,10 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
     }();
     // (a phase group stacks only if two sub-tiles still get two buffers)
     p.stack = stack_env >= 0 ? stack_env : (p.pb * p.bn <= 64 && 4 * G * p.pb * p.bn <= 512);
-    if (p.pb * p.bn > 256) p.stack = 0;  // MMA N limit
+    if (precision >= 5) p.stack = p.bn <= 128;  // [b0 | b1] rows only
+    else if (p.pb * p.bn > 256) p.stack = 0;  // MMA N limit
   }
-  const int cols = G * (p.stack ? p.pb * p.bn : p.bn);
+  const int cols = G * (precision >= 5 ? (precision - 3) * p.bn : p.stack ? p.pb * p.bn : p.bn);
   int cand[6][2] = {{4, 2}, {2, 2}, {1, 2}, {4, 1}, {2, 1}, {1, 1}};
   {  // TS_H2_SUBAB=<sub>,<accbufs>: try that candidate first (A/B measurement)
     static const char* e = getenv("TS_H2_SUBAB");
@@ -701,6 +741,9 @@ std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, 
           uint16_t h[3] = {0, 0, 0};
           if (precision == 2) {
             h[0] = f2bf16_rn_host(v);
+          } else if (precision >= 5) {
+            split_f16_host(v, h[0], h[1]);
+
           } else if (precision == 4) {  // RN split, like the device producers
             h[0] = f2bf16_rn_host(v);
             h[1] = f2bf16_rn_host(v - bf16_to_f_host(h[0]));
@@ -758,6 +801,8 @@ int launch_conv_tc_halo2(const ConvOp& op, int precision, void* stream) {
   } while (0)
   if (precision == 2) TS_TCH2_SUB(2);
   else if (precision == 4) TS_TCH2_SUB(4);
+  else if (precision == 5) TS_TCH2_SUB(5);
+  else if (precision == 6) TS_TCH2_SUB(6);
   else TS_TCH2_SUB(3);
 #undef TS_TCH2_SUB
 #undef TS_TCH2_LAUNCH

@@ -79,6 +79,7 @@ struct ConvLayer {
   Win grp_win[4];
   std::vector<float> w_host, b_host;  // final-layer kernel: weights as parameters
   bool h2 = false;          // executed on the wide-M halo kernel (or phases)
+  int prec = 0;             // tensor-core precision mode of this layer's launches
   bool out_planes = false;  // writes pre-split planes (conv.cuh ActView)
 };
 
@@ -95,6 +96,7 @@ inline void phase_window(int lo, int hi, int p, int& a, int& b) {
 struct ts_weights {
   bool identity = false;
   int precision = 0;
+  int device = -1;  // the CUDA device its buffers live on
   std::vector<ts::ConvLayer> layers;
   // per-tile float counts of the planner's buffers
   size_t cat_floats = 0, fuse_in_floats = 0, per_tile_floats = 0;
@@ -380,7 +382,7 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
   // halo2), else the layer keeps its plain form.
   {
     const char* e = getenv("TS_S2D");
-    const bool s2d_ok = (W->precision >= 2 && W->precision <= 4) && !(e && e[0] == '0');
+    const bool s2d_ok = tc16_mode(W->precision) && !(e && e[0] == '0');
     auto exec_shape = [&](const ConvLayer& L, const LayerDesc& d) {
       ConvOp o{};
       o.k = d.k; o.stride = d.s; o.pad = d.p; o.up2 = L.up2;
@@ -422,7 +424,7 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
   // input's own resolution
   {
     const char* e = getenv("TS_POLY");
-    const bool poly_ok = (W->precision >= 2 && W->precision <= 4) && !(e && e[0] == '0');
+    const bool poly_ok = tc16_mode(W->precision) && !(e && e[0] == '0');
     for (auto& L : layers) {
       const LayerDesc& d = L.d;
       if (!poly_ok || !L.up2 || d.k != 3 || d.s != 1 || d.p != 1 || L.s2d_in || L.s2d_out ||
@@ -479,7 +481,7 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
   // the four first encoder layers share one input read (conv_enc0.cu)
   {
     const char* e = getenv("TS_ENC0");
-    bool ok = !(e && e[0] == '0') && W->precision >= 2 && W->precision <= 4;
+    bool ok = !(e && e[0] == '0') && tc16_mode(W->precision);
     const ConvLayer* f[4];
     for (int st = 0; st < 4 && ok; ++st) {
       f[st] = &layers[stage_first[st]];
@@ -536,6 +538,16 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
     const int K = dx.k * dx.k * dx.ci, Co = dx.co;
     std::vector<float> packed((size_t)K * Co);
     std::vector<float> src = wi->second.second;  // OIKK of the executed shape
+    // FP16X3: layers with K >= 512 split their main sum by K-step parity
+    // (mode 6).  Measured on 38 configs[1] tiles, random He weights
+    // (scripts/precision_check.py): max |dh| 2.56e-3 m with no split,
+    // 1.82e-3 from K >= 700, 1.66e-3 from K >= 512, 1.53e-3 everywhere;
+    // the fp32 CUDA-core mode 0 gives 1.63e-3 (bar: 2e-3 m)
+    L.prec = W->precision;
+    if (W->precision == 5) {
+      const int kk = L.poly ? 4 * dx.ci : dx.k * dx.k * dx.ci;
+      if (kk >= 512 && dx.ci > 16) L.prec = 6;
+    }
     if (L.s2d_in) {
       // W'[o][(a*2+b)*ci + c][ty][tx] = W[o][c][2ty+a-1][2tx+b-1] (0 outside)
       const int ci0 = L.d.ci;
@@ -610,7 +622,7 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
         shape.in.H = L.Hin; shape.in.W = L.Win_;
         shape.batch = 1;
         const std::vector<uint8_t> pk =
-            pack_tc_weights_halo2(w2.data(), Co, dx.ci, 2, W->precision, shape);
+            pack_tc_weights_halo2(w2.data(), Co, dx.ci, 2, L.prec, shape);
         if (pk.empty()) return TS_E_INVALID;
         void* dp = nullptr;
         TS_CUDA_TRY(cudaMalloc(&dp, pk.size()));
@@ -627,7 +639,7 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
         shape.in.H = L.Hin; shape.in.W = L.Win_;
         shape.batch = 1;
         const std::vector<uint8_t> pk = pack_tc_weights_halo2(
-            w3.data() + (size_t)gi * L.ph_G * Co * dx.ci * 9, Co, dx.ci, 3, W->precision, shape);
+            w3.data() + (size_t)gi * L.ph_G * Co * dx.ci * 9, Co, dx.ci, 3, L.prec, shape);
         if (pk.empty()) return TS_E_INVALID;
         void* dp = nullptr;
         TS_CUDA_TRY(cudaMalloc(&dp, pk.size()));
@@ -647,9 +659,9 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
       shape.out.cstride = Co;
       shape.in.H = L.s2d_in ? L.Hin / 2 : L.Hin; shape.in.W = shape.in.H;
       shape.batch = 1;
-      L.w_layout = tc_weight_layout(shape, W->precision);
+      L.w_layout = tc_weight_layout(shape, L.prec);
       const std::vector<uint8_t> pk =
-          pack_tc_weights(src.data(), Co, dx.ci, dx.k, W->precision, shape, L.w_layout);
+          pack_tc_weights(src.data(), Co, dx.ci, dx.k, L.prec, shape, L.w_layout);
       if (L.s2d_in && L.w_layout != 2) return TS_E_INVALID;  // planner invariant
       void* d = nullptr;
       TS_CUDA_TRY(cudaMalloc(&d, pk.size()));
@@ -670,7 +682,7 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
     // (12.96 vs 11.88 ms per 1,024 tiles), so pre-split storage is opt-in
     // (TS_PLANES=1); results are bit-identical either way
     const char* e = getenv("TS_PLANES");
-    const bool on = (W->precision >= 2 && W->precision <= 4) && (e && e[0] == '1');
+    const bool on = tc16_mode(W->precision) && W->precision != 5 && (e && e[0] == '1');
     auto fmt_ok = [](const ConvLayer& L) {
       return L.d.co % 16 == 0 && L.out_cstride % 8 == 0 && L.out_coff % 8 == 0;
     };
@@ -711,7 +723,7 @@ using namespace ts;
 
 extern "C" int ts_weights_create(const uint8_t* lswb, size_t n_bytes, int precision,
                                  ts_weights** out) {
-  if (!lswb || !out) return TS_E_INVALID;
+  if (!lswb || !out || precision < 0 || precision > 5) return TS_E_INVALID;
   *out = nullptr;
   if (n_bytes < 4 || memcmp(lswb, "LSWB", 4) != 0) return TS_E_BAD_MAGIC;
   Blob bl{lswb, n_bytes, 4};
@@ -746,6 +758,7 @@ extern "C" int ts_weights_create(const uint8_t* lswb, size_t n_bytes, int precis
   std::unique_ptr<ts_weights> W(new ts_weights());
   W->identity = identity;
   W->precision = precision;
+  TS_CUDA_TRY(cudaGetDevice(&W->device));
   if (identity) {
     if (!tensors.empty()) return TS_E_SHAPE;
     *out = W.release();
@@ -812,6 +825,11 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
                          uint8_t* d_nonfinite, void* d_workspace, void* stream) {
   if (!W || batch < 0) return TS_E_INVALID;
   if (batch == 0) return TS_E_SHAPE;  // refine_batch requires a non-empty batch
+  {
+    int dev = -1;
+    TS_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev != W->device) return TS_E_INVALID;  // handle built on another device
+  }
   cudaStream_t s = as_stream(stream);
   if (W->identity) {
     ts::count_launch(), refine_epilogue_kernel<<<batch, 256, 0, s>>>(d_in, 8, 1, d_in, d_out, d_nonfinite);
@@ -966,7 +984,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
           q.hy0 = L.out_win.y0; q.hy1 = L.out_win.y1; q.hx0 = L.out_win.x0; q.hx1 = L.out_win.x1;
           q.oy0 = w.y0; q.oy1 = w.y1; q.ox0 = w.x0; q.ox1 = w.x1;
           q.w_tc = L.w_grp[gi]; q.w_layout = 2;
-          st = launch_conv_tc_halo2(q, W->precision, lstream);
+          st = launch_conv_tc_halo2(q, L.prec, lstream);
           if (st != TS_OK) return st;
         }
         prev_base = op.out.base; prev_H = L.Hout; prev_cs = L.out_cstride;
@@ -983,7 +1001,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
           q.ph = 1; q.ph_y = p >> 1; q.ph_x = p & 1;
           q.oy0 = w.y0; q.oy1 = w.y1; q.ox0 = w.x0; q.ox1 = w.x1;
           q.w_tc = L.w_ph[p]; q.w_layout = 2;
-          st = launch_conv_tc_halo2(q, W->precision, lstream);
+          st = launch_conv_tc_halo2(q, L.prec, lstream);
           if (st != TS_OK) return st;
         }
         prev_base = op.out.base; prev_H = L.Hout; prev_cs = L.out_cstride;
@@ -1009,8 +1027,8 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
       if (conv_direct_supported(op) && !thin_tc &&
           (op.in.C <= 4 || op.out.C <= 16 || W->precision == 0))
         st = launch_conv_direct(op, lstream);
-      else if (L.w_tc && conv_tc_supported(op, W->precision))
-        st = launch_conv_tc(op, W->precision, lstream);
+      else if (L.w_tc && conv_tc_supported(op, L.prec))
+        st = launch_conv_tc(op, L.prec, lstream);
       else
         st = launch_conv_simt(op, lstream);
       if (st != TS_OK) return st;

@@ -260,23 +260,81 @@ struct Mode;
 template <>
 struct Mode<1> {  // TF32X3: A hi/lo, B hi/lo
   static constexpr int pa = 2, pb = 2, kc = 32;
-  static constexpr bool tf32 = true;
+  static constexpr bool tf32 = true, f16 = false;
 };
 template <>
 struct Mode<2> {  // BF16
   static constexpr int pa = 1, pb = 1, kc = 64;
-  static constexpr bool tf32 = false;
+  static constexpr bool tf32 = false, f16 = false;
 };
 template <>
 struct Mode<3> {  // BF16X3: A = a0 + a1 (RN, residual <= 2^-18 |a|), B = b0+b1+b2
   static constexpr int pa = 2, pb = 3, kc = 64;
-  static constexpr bool tf32 = false;
+  static constexpr bool tf32 = false, f16 = false;
 };
 template <>
 struct Mode<4> {  // BF16X4: A = a0 + a1, B = b0 + b1 (both RN, residual <= 2^-18)
   static constexpr int pa = 2, pb = 2, kc = 64;
-  static constexpr bool tf32 = false;
+  static constexpr bool tf32 = false, f16 = false;
 };
+// FP16X3 (the fp32-class mode): fp16 planes with a scaled correction plane,
+// a = a0 + 2^-11 a1, a0 = fp16_rn(a), a1 = fp16_rn((a - a0) 2^11), so both
+// planes are in fp16's normal range and |a - a0 - 2^-11 a1| <= 2^-24 |a|
+// (fp32's own rounding); same for the weights.  Products: a0 b0 into the
+// MAIN accumulator columns, a0 b1 + a1 b0 into a separate CORRECTION block
+// (scaled by 2^11), combined by the epilogue as main + 2^-11 corr.  Keeping
+// the corrections out of the main accumulator matters: each tcgen05 MMA
+// truncates its fp32 result (scripts/mma_numerics.cu measures the bias),
+// so the main sum should take one MMA per K step, not three.
+template <>
+struct Mode<5> {
+  static constexpr int pa = 2, pb = 2, kc = 64;
+  static constexpr bool tf32 = false, f16 = true;
+};
+// FP16X3 with the main sum split by K-step parity into two column blocks,
+// [main_even | corr | main_odd]: even K steps multiply rows [b0 | b1] into
+// [main_even | corr] (one stacked MMA), odd ones b1 into corr and b0 into
+// main_odd (two MMAs), so each main accumulator takes half the truncating
+// MMAs while the correction block stays small (long-K layers;
+// scripts/mma_numerics.cu)
+template <>
+struct Mode<6> {
+  static constexpr int pa = 2, pb = 2, kc = 64;
+  static constexpr bool tf32 = false, f16 = true;
+};
+constexpr float kF16Lo = 2048.f;         // correction-plane scale 2^11
+constexpr float kF16LoInv = 1.f / 2048.f;
+
+// instruction-descriptor operand format of a mode: tf32 2, bf16 1, fp16 0
+template <int MODE>
+__host__ __device__ constexpr uint32_t mode_fmt() {
+  return Mode<MODE>::tf32 ? 2u : Mode<MODE>::f16 ? 0u : 1u;
+}
+
+// {fp16_rn(lo), fp16_rn(hi)} packed (lo in the low half): one F2FP
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// a pair -> main plane word h and scaled correction word l
+__device__ __forceinline__ void split_h2(float x, float y, uint32_t& h, uint32_t& l) {
+  h = pack_h2(x, y);
+  float hx, hy;
+  asm("{\n.reg .f16 a, b;\nmov.b32 {a, b}, %2;\ncvt.f32.f16 %0, a;\ncvt.f32.f16 %1, b;\n}\n"
+      : "=f"(hx), "=f"(hy)
+      : "r"(h));
+  // x - hx is exact (hx = x rounded to 11 bits); the 2^11 scale is exact
+  l = pack_h2((x - hx) * kF16Lo, (y - hy) * kF16Lo);
+}
+// 4 floats -> 8 bytes of each plane
+__device__ __forceinline__ void store_split_h(uint8_t* dst, int plane_bytes, float4 a) {
+  uint32_t h01, l01, h23, l23;
+  split_h2(a.x, a.y, h01, l01);
+  split_h2(a.z, a.w, h23, l23);
+  *reinterpret_cast<uint2*>(dst) = make_uint2(h01, h23);
+  *reinterpret_cast<uint2*>(dst + plane_bytes) = make_uint2(l01, l23);
+}
 
 
 }  // namespace tcx

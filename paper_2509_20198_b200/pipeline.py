@@ -21,11 +21,11 @@ import torch
 
 from . import _device as D
 from .patches import DeviceIndex, RASTER_RES, OUTPUT_RES, raster, triangulate
-from .refiner import PRECISION_FP32, WeightBundle, device_weights
+from .refiner import PRECISION_FP16X3, WeightBundle, device_weights
 
 
 class HeightmapPipeline:
-    def __init__(self, weights: WeightBundle, precision: int = PRECISION_FP32):
+    def __init__(self, weights: WeightBundle, precision: int = PRECISION_FP16X3):
         self.weights = device_weights(weights, precision)
         self._ws = None
         self._ws_batch = 0

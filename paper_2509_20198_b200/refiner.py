@@ -46,6 +46,8 @@ PRECISION_TF32X3 = 1    # tcgen05 kind::tf32, 3-pass split (fp32-accurate)
 PRECISION_BF16 = 2      # tcgen05 kind::f16 (bf16 operands, fp32 accumulate)
 PRECISION_BF16X3 = 3    # tcgen05 kind::f16, A 2 RN planes, B 3 exact planes (a0.b* + a1.b0)
 PRECISION_BF16X4 = 4    # tcgen05 kind::f16, A, B 2 RN planes: a0.b0 + a0.b1 + a1.b0
+PRECISION_FP16X3 = 5    # tcgen05 kind::f16, fp16 planes a0 + 2^-11 a1 (fp32-class):
+                        # a0.b0 (main) + [a0.b1 + a1.b0] (separate accumulator)
 
 
 @dataclass
@@ -325,10 +327,13 @@ class DeviceWeights:
 
 def device_weights(bundle: WeightBundle,
                    precision: int = PRECISION_FP32) -> DeviceWeights:
+    # one handle per (device, precision): ts_weights_create allocates on the
+    # current device and ts_refine rejects a handle from another device
     cache = bundle.__dict__.setdefault("_ts_device", {})
-    if precision not in cache:
-        cache[precision] = DeviceWeights(bundle, precision)
-    return cache[precision]
+    key = (torch.cuda.current_device(), precision)
+    if key not in cache:
+        cache[key] = DeviceWeights(bundle, precision)
+    return cache[key]
 
 
 @dataclass
@@ -356,8 +361,11 @@ def staging_array(raws: list[RawPatch]) -> np.ndarray:
 
 
 def refine_batch(raws: list[RawPatch], weights: WeightBundle,
-                 precision: int = PRECISION_FP32) -> list[RefinedPatch]:
-    """refine_batch on the GPU (same outputs/provenance/fallback rules)."""
+                 precision: int = PRECISION_FP16X3) -> list[RefinedPatch]:
+    """refine_batch on the GPU (same outputs/provenance/fallback rules).
+
+    Default precision: FP16X3 on the tcgen05 tensor cores, fp32-class
+    (within the fp32 bar of 2e-3 m on random He weights)."""
     if not raws:
         raise ShapeMismatch("refine_batch requires a non-empty batch")
     for r in raws:

@@ -1,11 +1,11 @@
 """configs[1] at full size on the GPU (needs a B200).
 
 The whole 32 x 32-tile batch goes through the device pipeline in the bench's
-precision mode (fp32-class tensor cores); size-independent properties are
-checked on every patch (status, finiteness, re-centring identity) and a
-seeded sample of patches is checked against the oracle with the stated
-tolerances (raster 1e-6 patch units, c_z 1e-3 m, refined heights 0.05 m
-max on random He weights -- DESIGN.md §3).
+precision mode (FP16X3, fp32-class tensor cores); size-independent
+properties are checked on every patch (status, finiteness, re-centring
+identity) and a seeded sample of patches is checked against the oracle with
+the stated tolerances (raster 1e-6 patch units, c_z 1e-3 m, refined heights
+2e-3 m max on random He weights -- the fp32 bar).
 """
 
 import numpy as np
@@ -31,7 +31,7 @@ def test_configs1_full_batch_properties_and_sample_parity():
     from paper_2509_20198_b200 import synth
     from paper_2509_20198_b200.lasio import parse_header
     from paper_2509_20198_b200.pipeline import HeightmapPipeline
-    from paper_2509_20198_b200.refiner import (PRECISION_BF16X4,
+    from paper_2509_20198_b200.refiner import (PRECISION_FP16X3,
                                                default_descriptor,
                                                random_weights)
     side = 32
@@ -39,7 +39,7 @@ def test_configs1_full_batch_properties_and_sample_parity():
     descs = np.concatenate([D.tile_desc(parse_header(t.data)) for t in tiles])
     tb = D.TileBatch([t.data for t in tiles], descs)
     bundle = random_weights(default_descriptor(), seed=3)
-    pipe = HeightmapPipeline(bundle, PRECISION_BF16X4)
+    pipe = HeightmapPipeline(bundle, PRECISION_FP16X3)
     centers = np.array([[t.x0 + 320.0, t.y0 + 320.0] for t in tiles])
     res = pipe.run(tb, centers)
     torch.cuda.synchronize()
@@ -72,19 +72,19 @@ def test_configs1_full_batch_properties_and_sample_parity():
         ref = oref.refine(layers, tensors, oref.stage_inputs(
             want["hm_nn"], want["hm_lin"], want["rgb_nn"],
             want["rgb_lin"])[None], [want["hm_lin"]], [want["rgb_lin"]])[0]
-        assert np.abs(out[p, :, :, 0] - ref[0]).max() <= 5e-2, p
-        assert np.abs(out[p, :, :, 1:4] - ref[1]).max() <= 1e-3, p
+        assert np.abs(out[p, :, :, 0] - ref[0]).max() <= 2e-3, p
+        assert np.abs(out[p, :, :, 1:4] - ref[1]).max() <= 1e-4, p
 
 
 def test_tensor_core_refine_batch_invariance_at_scale():
     """Each tile's result is independent of its position in a large batch
     (different M-tile boundaries, halo splits and N-tile interleavings)."""
-    from paper_2509_20198_b200.refiner import (PRECISION_BF16X4,
+    from paper_2509_20198_b200.refiner import (PRECISION_FP16X3,
                                                default_descriptor,
                                                device_weights,
                                                random_weights)
     bundle = random_weights(default_descriptor(), seed=3)
-    w = device_weights(bundle, PRECISION_BF16X4)
+    w = device_weights(bundle, PRECISION_FP16X3)
     g = torch.Generator(device="cuda").manual_seed(5)
     B = 37
     x = torch.randn((B, 96, 96, 8), generator=g, device="cuda") * 0.1
@@ -99,7 +99,7 @@ def test_tensor_core_refine_batch_invariance_at_scale():
         assert torch.equal(o1[0], out[i]), i
 
 
-@pytest.mark.parametrize("precision", [0, 4])
+@pytest.mark.parametrize("precision", [0, 5])
 def test_colourless_tiles_through_the_pipeline(precision):
     """Point format 0 (no RGB): the CNN sees zero colour channels
     (refiner.py:458-468) and heights still match the oracle."""
@@ -126,7 +126,7 @@ def test_colourless_tiles_through_the_pipeline(precision):
         index.add(olaz.positions(r, hf["scale"], hf["offset"]), None)
     layers = oref.text_to_layers(bundle.descriptor.to_text())
     tensors = oref.random_tensors(layers, seed=3)
-    tol = 2e-3 if precision == 0 else 5e-2
+    tol = 2e-3
     for p in (0, 4, 8):
         want = opatch.reconstruct(tuple(centers[p]), index)
         assert want["rgb_nn"] is None
