@@ -12,9 +12,10 @@ Step = one pass of the hot path over the resident batch: chunk-table decode
 CNN refine (fp32-accurate path) -> epilogue.  L2 is flushed (256 MiB
 write) between timed steps, outside the per-step event window.
 
-``--impl reference`` times the reference algorithm's CPU restatement
-(oracle/, with the reference's own flood fill, Qhull and float32 im2col
-GEMMs) on the host cores, on a bounded sample of the same workload.
+``--impl reference`` times the unmodified reference package (pip-installed
+into baseline/_ref, bench_ref.py) through its own API on the host cores, on
+a bounded sample of the same workload, plus configs[0] through its
+ScoutEngine; without baseline/_ref it times the oracle/ port.
 """
 
 from __future__ import annotations
@@ -606,28 +607,66 @@ def _cpu_reconstruct(arg):
 
 
 def cpu_baseline(args):
-    rate, cores, dt = cpu_sample(args.cpu_sample)
-    return {"value": round(rate, 3), "unit": "heightmaps/s", "cores": cores,
-            "kind": "port",
+    """cpu_baseline of the GPU line: the real reference (baseline/_ref) on
+    the host cores when installed, the oracle port beside it."""
+    import bench_ref
+    port_rate, port_cores, port_dt = cpu_sample(args.cpu_sample)
+    port = {"value": round(port_rate, 3), "unit": "heightmaps/s",
+            "cores": port_cores, "kind": "port",
             "sample": f"{args.cpu_sample} patches of the configs[1] workload "
-                      f"(8x8 tile corner), extract+index+flood-fill "
-                      f"Algorithm 1 on {cores} procs + float32 im2col CNN "
-                      f"(OpenBLAS), {dt:.1f}s"}
+                      f"(8x8 tile corner) through oracle/ (flood-fill "
+                      f"Algorithm 1 on {port_cores} procs + float32 im2col "
+                      f"CNN), {port_dt:.1f}s"}
+    if not bench_ref.available():
+        return port
+    arm = bench_ref.RefArm(sample=args.cpu_sample)
+    try:
+        arm.step()                                   # warm-up (page cache)
+        dts = [arm.step() for _ in range(2)]
+    finally:
+        arm.close()
+    dt = min(dts)
+    return {"value": round(arm.sample / dt, 3), "unit": "heightmaps/s",
+            "cores": arm.cores, "kind": "reference",
+            "sample": f"{arm.sample} patches of the configs[1] workload (8x8 "
+                      f"tile corner) through the unmodified reference "
+                      f"({os.path.relpath(arm.module, ROOT)}): "
+                      f"read_chunk_points/positions/colors/ChunkPointIndex "
+                      f"for 64 tiles, reconstruct_patch on a {arm.cores}-"
+                      f"process fork pool, refine_batch (OpenBLAS); best of "
+                      f"2 steps, {dt:.1f}s",
+            "port": port}
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference's own CPU implementation of the path
+    (baseline/_ref; the oracle port when it is not installed), rank 0 only,
+    each step a bounded sample of the configs[1] workload."""
     if rank != 0:
         return
-    rates = []
+    import bench_ref
+    use_ref = bench_ref.available()
+    if use_ref:
+        arm = bench_ref.RefArm(sample=args.cpu_sample)
+        cores = arm.cores
+        run = arm.step
+        kind = "reference"
+        what = (f"the unmodified reference ({os.path.relpath(arm.module, ROOT)}"
+                f"): read_chunk_points/positions/colors/ChunkPointIndex for "
+                f"64 tiles, reconstruct_patch on a {cores}-process fork "
+                f"pool, refine_batch (OpenBLAS, all cores)")
+    else:
+        cores = len(os.sched_getaffinity(0))
+        run = lambda: args.cpu_sample / cpu_sample(args.cpu_sample)[0]  # noqa: E731
+        kind = "port"
+        what = "the oracle/ port of the reference algorithm on all host cores"
     for _ in range(args.warmup):
-        cpu_sample(4)
+        run()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        r, cores, _dt = cpu_sample(args.cpu_sample)
-        rates.append(r)
+    dts = [run() for _ in range(args.steps)]
     wall = time.perf_counter() - t0
-    value = float(np.mean(rates))
-    print(json.dumps({
+    value = args.cpu_sample * args.steps / float(np.sum(dts))
+    line = {
         "impl": "reference",
         "metric": "refined 64x64 heightmaps/sec", "value": round(value, 3),
         "unit": "heightmaps/s", "n_gpus": world, "steps": args.steps,
@@ -643,15 +682,18 @@ def run_reference(args, rank, world):
                    "chunks_per_tile": CHUNKS_PER_TILE,
                    "points_per_chunk": POINTS_PER_CHUNK,
                    "sample": f"each step: {args.cpu_sample} patches of the "
-                             "workload (8x8 tile corner) through the "
-                             "reference algorithm on all host cores",
-                   "parallelism": "CPU process pool (rank 0 only)"},
+                             f"workload (8x8 tile corner) through {what}",
+                   "parallelism": "CPU (rank 0 only)"},
         "cpu_baseline": {"value": round(value, 3), "unit": "heightmaps/s",
-                         "cores": cores, "kind": "port",
+                         "cores": cores, "kind": kind,
                          "sample": f"{args.cpu_sample} patches per step"},
         "e2e": {"value": round(value, 3), "unit": "heightmaps/s",
-                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
-        flush=True)
+                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if use_ref:
+        if not args.no_cpu:
+            line["configs0"] = arm.configs0()
+        arm.close()
+    print(json.dumps(line), flush=True)
 
 
 def main():
