@@ -15,7 +15,9 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libts_b200.so")
+# TS_LIB_PATH: a profiling build of the same sources (make PROFILE=1,
+# scripts only); the product always loads the in-tree library
+LIB_PATH = os.environ.get("TS_LIB_PATH") or os.path.join(HERE, "libts_b200.so")
 
 P = C.c_void_p
 I32 = C.c_int

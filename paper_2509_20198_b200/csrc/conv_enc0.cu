@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(enc0_threads<CO>(), 2) conv_enc0_kernel(Enc0Op
         act_block(ov, b, y, x, blk, chan);
 #pragma unroll
         for (int o = 0; o < CH; o += 8)
-          tcx::store8_planes(ov.base + blk, ov.cstride, chan + chalf + o, acc[r] + o);
+          tcx::store8_planes(ov.base + blk, ov.cstride, chan + chalf + o, acc[r] + o,
+                             ov.planes == 2);
       } else {
         float* op_ = ov.base + act_off(ov, b, y, x) + chalf;
 #pragma unroll
@@ -159,7 +160,8 @@ __device__ __forceinline__ void enc0_store(const ActView& ov, int64_t b, int y, 
       act_block(ov, b, yy, x, blk, chan);
 #pragma unroll
       for (int o = 0; o < CH; o += 8)
-        tcx::store8_planes(ov.base + blk, ov.cstride, chan + c0 + o, acc[r] + o);
+        tcx::store8_planes(ov.base + blk, ov.cstride, chan + c0 + o, acc[r] + o,
+                             ov.planes == 2);
     } else {
       float* op_ = ov.base + act_off(ov, b, yy, x) + c0;
 #pragma unroll

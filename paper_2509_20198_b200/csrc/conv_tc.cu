@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
   // N = 2 BN; the epilogue adds the halves): half the A-operand shared
   // memory reads of one MMA per plane pair
   // MODE 5 (FP16X3): [main | correction] column blocks, same stacking
-  const int NST = MODE == 6 ? 3 : ((MODE == 4 && !T.wide) || Md::f16) ? 2 : 1;
+  const int NST = ((MODE == 4 && !T.wide) || Md::f16) ? 2 : 1;
   // two accumulator buffers (epilogue overlaps the next tile) when they fit
   const int AB = 2 * NST * BN <= 512 ? 2 : 1;
   uint32_t ncols = 32;
@@ -265,16 +265,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
             } else if (MODE == 2) {
               umma<false>(d, ak, bk, idesc, first);
             } else if (Md::f16) {
-              // a0 . [b0 | b1] -> [main | corr], a1 . b0 -> corr; MODE 6:
-              // odd K steps put a0 . b0 (as a0 . 2^11 b0) into corr too
-              if (MODE == 6 && (k & 1)) {
-                // b1 -> corr, b0 -> main_odd (the tile's first odd step
-                // overwrites it)
-                umma<false>(d + BN, ak, bk + pb, idesc_b0, 1u);
-                umma<false>(d + 2 * BN, ak, bk, idesc_b0, (kit | (k >> 1)) ? 1u : 0u);
-              } else {
-                umma<false>(d, ak, bk, idesc, first);
-              }
+              // a0 . [b0 | b1] -> [main | corr], a1 . b0 -> corr
+              umma<false>(d, ak, bk, idesc, first);
               umma<false>(d + BN, ak + pa, bk, idesc_b0, 1u);
             } else if (MODE == 4) {
               // a0 . [b0 | b1] (N = 2 BN), then a1 . b0 (N = BN): the
@@ -337,12 +329,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
       for (int c = 0; c < BN; c += 16) {
         float v[16];
         tmem_ld16(tmem + lane_base + acc * NST * BN + c, v);  // warp-collective
-        if (NST == 3) {  // MODE 6: main_even + main_odd, then the correction
-          float w[16];
-          tmem_ld16(tmem + lane_base + acc * NST * BN + 2 * BN + c, w);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] += w[i];
-        }
         if (NST >= 2) {
           float w[16];
           tmem_ld16(tmem + lane_base + acc * NST * BN + BN + c, w);
@@ -358,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(TcArgs T) {
             v[i] = x;
           }
           if (op.out.planes) {
-            if (n0 + c + 16 <= Cout) store16_planes(oblk, op.out.cstride, ochan + n0 + c, v);
+            if (n0 + c + 16 <= Cout) store16_planes(oblk, op.out.cstride, ochan + n0 + c, v, op.out.planes == 2);
           } else if (vec8 && n0 + c + 16 <= Cout) {
             st_v8(o + n0 + c, v);
             st_v8(o + n0 + c + 8, v + 8);
@@ -712,7 +698,6 @@ TcPlan plan_for(const ConvOp& op, int precision) {
   // halve the producers' work
   const char* e = getenv("TS_TC_WIDE");
   const bool wide_ok = precision == 4 && op.k == 1 && !(e && e[0] == '0');
-  // (MODE 6: three column blocks per accumulator, two accumulators)
   const int cap = wide_ok ? 256 : 128;
   p.ntiles = (n16 + cap - 1) / cap;
   p.bn = ((n16 + p.ntiles - 1) / p.ntiles + 15) / 16 * 16;
@@ -765,7 +750,7 @@ bool conv_tc_halo_eligible(const ConvOp& op, int precision) {
 }
 
 bool conv_tc_supported(const ConvOp& op, int precision) {
-  if (precision < 1 || precision > 6) return false;
+  if (precision < 1 || precision > 5) return false;
   return op.in.C % 4 == 0 && op.in.cstride % 4 == 0 && op.in.coff % 4 == 0;
 }
 
@@ -911,7 +896,6 @@ int launch_conv_tc(const ConvOp& op, int precision, void* stream) {
   else if (precision == 2) TS_TC_LAUNCH(2);
   else if (precision == 4) TS_TC_LAUNCH(4);
   else if (precision == 5) TS_TC_LAUNCH(5);
-  else if (precision == 6) TS_TC_LAUNCH(6);
   else TS_TC_LAUNCH(3);
 #undef TS_TC_LAUNCH
   TS_LAUNCH_CHECK();

@@ -69,6 +69,23 @@ constexpr int kThreads = (kEpiW0 + kEpiWarps) * 32;
 constexpr int kHdr = 1024;         // packed-weight header: u32 count, u32 0, u16 list
 constexpr int kMaxStages = (kHdr - 8) / 2 - 1;  // + sentinel
 
+// Build-time wait profile (make PROFILE=1 -> -DTS_H2_PROF): cycles each
+// role spends in its mbarrier waits, summed per CTA, printed per launch by
+// ts_h2_prof_dump().  Compiled out of the product library.
+#ifdef TS_H2_PROF
+enum { kPrProdWait, kPrMmaAcc, kPrMmaHalo, kPrMmaW, kPrEpiWait, kPrLoadWait, kPrTotal, kPrN };
+__device__ unsigned long long g_h2_prof[kPrN];
+#define TS_PROF_WAIT(slot, call)                                          \
+  do {                                                                    \
+    const long long t0_ = clock64();                                      \
+    call;                                                                 \
+    if ((threadIdx.x & 31) == 0)                                          \
+      atomicAdd(&g_h2_prof[slot], (unsigned long long)(clock64() - t0_)); \
+  } while (0)
+#else
+#define TS_PROF_WAIT(slot, call) call
+#endif
+
 struct Halo2Args {
   ConvOp op;
   const uint8_t* wpk;  // packed weights: kHdr-byte stage list, then
@@ -76,8 +93,8 @@ struct Halo2Args {
   int bn, sub, hbufs, bstages, cchunks, taps, wp, lrows, n_tiles, accbufs;
   int stack;  // 1: B planes stacked along N (PB*BN columns per sub-tile);
               // 0: every product accumulates into the same BN columns
+  int cgrp;   // MODE 5: channel chunks per accumulator group (promotion unit)
   int64_t m_tiles, positions;
-  unsigned long long* dbg;  // TS_H2_DBG timestamps (CTA 0), or null
 };
 
 __device__ __forceinline__ void prod_sync() {
@@ -89,6 +106,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
   using Md = Mode<MODE>;
   constexpr int PA = Md::pa, PB = Md::pb;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+#ifdef TS_H2_PROF
+  const long long t_start = clock64();
+#endif
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   const ConvOp& op = T.op;
   const int BN = T.bn, HB = T.hbufs, SB = T.bstages, L = T.lrows;
@@ -141,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
   const int64_t total_tiles = T.m_tiles * T.n_tiles;
   const int AB = T.accbufs;
   // accumulator column blocks per sub-tile (MODE 5: main + correction)
-  const int PBS = MODE == 6 ? 3 : Md::f16 ? 2 : T.stack ? PB : 1;
+  const int PBS = Md::f16 ? 2 : T.stack ? PB : 1;
   const int acc_cols = SUB * G * PBS * BN;  // per accumulator buffer
   uint32_t ncols = 32;
   while ((int)ncols < AB * acc_cols) ncols <<= 1;
@@ -166,13 +186,22 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // FP16X3: the epilogue warp group (warps 12-15) holds each group's
+  // promoted sums in registers; the other three groups give theirs up
+  static_assert(MODE != 5 || (kEpiW0 == 12 && kEpiWarps == 4), "epilogue = warp group 3");
 
   if (warp < kProdW) {
+    if constexpr (MODE == 5) reg_dealloc<96>();
     // ------------------------- halo producers -------------------------
     // buffers are used round-robin per (tile, chunk); hph bit h = phase of
     // buffer h
     int hb = 0, lt = 0;
     uint32_t hph = 0;
+    // pre-split input: chunks whose cp.async copies are still in flight
+    // (publication lag kLag <= HB - 1, so the producer never waits on a
+    // buffer the MMA cannot yet have been handed)
+    const int lag = HB >= 3 ? 2 : 1;
+    int pend[3] = {0, 0, 0}, npend = 0;
     constexpr int PPR = kKC / 4;  // float4 pieces per row
     const int pad_y = op.ph ? 1 - op.ph_y : op.pad, pad_x = op.ph ? 1 - op.ph_x : op.pad;
     // 32-byte aligned 8-channel pieces available
@@ -202,46 +231,87 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(op.in.base + off));
       }
     };
+    // short halos (1x1 layers, small 2x2 ones: <= 2 rows per thread per
+    // chunk) fill two chunks per global round trip, else one chunk's MMAs
+    // (2-8 K steps) cannot cover the load latency
+    const bool pair = MODE == 5 && v8in && !op.in.planes && L <= 2 * (kProdT / 4) && HB >= 3;
     for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
       int64_t* ro = rowoff + (lt & 1) * L;
       if (lt == 0) build_rows(0, false);
       prod_sync();
+      if (pair) {
+        constexpr int kStep8 = kProdT / 4;
+        const int piece = tid & 3, row0 = tid >> 2;
+        const int obase = row0 * kRow + ((piece ^ ((row0 >> 1) & 3)) << 4);
+        for (int c = 0; c < T.cchunks; c += 2) {
+          const int nc = T.cchunks - c < 2 ? 1 : 2;
+          if (c + nc >= T.cchunks && tile + gridDim.x < total_tiles) build_rows(lt + 1, true);
+          const int hbs[2] = {hb, hb + 1 == HB ? 0 : hb + 1};
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            if (q < nc) TS_PROF_WAIT(kPrProdWait, mbar_wait(hempty + hbs[q], ((hph >> hbs[q]) & 1u) ^ 1u));
+          float v[2][2][8];
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[q][u][i] = 0.f;
+              const int row = row0 + u * kStep8, ch = (c + q) * kKC + 8 * piece;
+              if (q < nc && row < L) {
+                const int64_t off = ro[row];
+                if (off >= 0 && ch < Cin) ld_v8(op.in.base + ch + off, v[q][u]);
+              }
+            }
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+              if (q < nc && row0 + u * kStep8 < L) {
+                uint8_t* d = halo + hbs[q] * halo_bytes + obase + u * kStep8 * kRow;
+                uint32_t h[4], l[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) split_h2(v[q][u][2 * i], v[q][u][2 * i + 1], h[i], l[i]);
+                *reinterpret_cast<uint4*>(d) = make_uint4(h[0], h[1], h[2], h[3]);
+                *reinterpret_cast<uint4*>(d + plane_a) = make_uint4(l[0], l[1], l[2], l[3]);
+              }
+          fence_proxy_async();
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            if (q < nc) {
+              if ((tid & 31) == 0) mbar_arrive(hfull + hbs[q]);
+              hph ^= 1u << hbs[q];
+              if (++hb == HB) hb = 0;
+            }
+        }
+        continue;
+      }
       for (int c = 0; c < T.cchunks; ++c) {
         // during the last chunk, the next tile's row table (other parity)
         // and an L2 prefetch of its first chunk
         if (c == T.cchunks - 1 && tile + gridDim.x < total_tiles) build_rows(lt + 1, true);
-        mbar_wait(hempty + hb, ((hph >> hb) & 1u) ^ 1u);
+        TS_PROF_WAIT(kPrProdWait, mbar_wait(hempty + hb, ((hph >> hb) & 1u) ^ 1u));
         uint8_t* sa = halo + hb * halo_bytes;
         if (op.in.planes) {
           // pre-split input: 16-byte piece p of a row is 8 channels of plane
-          // p >> 2, copied as is (no conversion)
+          // p >> 2, copied as is by cp.async (zero-fill outside the image);
+          // the chunk is published kLag chunks later (below), so several
+          // chunks' copies are in flight per producer
           const int piece = tid & 7, pl = piece >> 2, sub = piece & 3;
           const int ch = c * kKC + 8 * sub;
           const bool ok = ch < Cin && pl < PA;
           const uint8_t* src = reinterpret_cast<const uint8_t*>(op.in.base) +
                                2 * (ch - op.in.coff) + 2 * (int64_t)pl * op.in.cstride;
           const int row0 = tid >> 3;
-          uint8_t* dst0 = sa + pl * plane_a + row0 * kRow;
-          const int swz = sub ^ ((row0 >> 1) & 3);
+          const uint32_t dst0 = su32(sa + pl * plane_a + row0 * kRow) +
+                                ((sub ^ ((row0 >> 1) & 3)) << 4);
           constexpr int kRowStep = kProdT / PPR;  // rows per pass (multiple of 8)
           if (pl < PA) {
-            for (int r0 = row0; r0 < L; r0 += kRowStep * kInflight) {
-              uint4 v[kInflight];
-#pragma unroll
-              for (int u = 0; u < kInflight; ++u) {
-                const int row = r0 + u * kRowStep;
-                v[u] = make_uint4(0u, 0u, 0u, 0u);
-                if (row < L) {
-                  const int64_t off = ro[row];
-                  if (off >= 0 && ok)
-                    v[u] = __ldg(reinterpret_cast<const uint4*>(src + 4 * off));
-                }
-              }
-#pragma unroll
-              for (int u = 0; u < kInflight; ++u)
-                if (r0 + u * kRowStep < L)
-                  *reinterpret_cast<uint4*>(dst0 + (r0 - row0 + u * kRowStep) * kRow + (swz << 4)) =
-                      v[u];
+            for (int r = row0; r < L; r += kRowStep) {
+              const int64_t off = ro[r];
+              const bool in = off >= 0 && ok;
+              cp_async16(dst0 + (r - row0) * kRow, in ? src + 4 * off : src, in ? 16u : 0u);
             }
           }
         } else if (v8in) {
@@ -345,12 +415,97 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
           }
         }
         }
-        fence_proxy_async();
-        __syncwarp();
-        if ((tid & 31) == 0) mbar_arrive(hfull + hb);
-        if (T.dbg && blockIdx.x == 0 && tid == 0 && lt * T.cchunks + c < 4096)
-          T.dbg[lt * T.cchunks + c] = clock64();
+        if (op.in.planes) {
+          // publish the chunk issued kLag chunks ago once its copies landed
+          cp_async_commit();
+          pend[npend++] = hb;
+          if (npend > lag) {
+            if (lag == 2) cp_async_wait<2>();
+            else cp_async_wait<1>();
+            fence_proxy_async();
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(hfull + pend[0]);
+            pend[0] = pend[1];
+            pend[1] = pend[2];
+            --npend;
+          }
+        } else {
+          fence_proxy_async();
+          __syncwarp();
+          if ((tid & 31) == 0) mbar_arrive(hfull + hb);
+        }
         hph ^= 1u << hb;
+        if (++hb == HB) hb = 0;
+      }
+    }
+    if (op.in.planes && npend) {
+      cp_async_wait<0>();
+      fence_proxy_async();
+      __syncwarp();
+      if ((tid & 31) == 0)
+        for (int i = 0; i < npend; ++i) mbar_arrive(hfull + pend[i]);
+    }
+  } else if (warp == kMmaW && MODE == 5) {
+    // ------------------- MMA issuer (FP16X3, promoted) -------------------
+    reg_dealloc<96>();
+    // Per sub-tile u and K step: a0 . [b0 | b1] -> [main | corr] (one
+    // stacked MMA, N = 2 BN) and a1 . b0 -> corr (N = BN).  The accumulator
+    // pair rotates per GROUP of T.cgrp channel chunks (<= 18 K steps): the
+    // group's first K step overwrites it, the epilogue promotes it.
+    const uint32_t idesc = make_idesc(mode_fmt<MODE>(), 2 * BN);
+    const uint32_t idesc_b0 = make_idesc(mode_fmt<MODE>(), BN);
+    const uint64_t d_halo = sw64_desc(su32(halo));
+    const uint64_t d_ring = sw64_desc(su32(bring));
+    const uint32_t pa = (uint32_t)plane_a >> 4;
+    const uint32_t b_step = (uint32_t)b_bytes >> 4, h_step = (uint32_t)halo_bytes >> 4;
+    int s = 0, hb = 0;
+    uint32_t bph = 0, hph = 0, gc = 0;
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      int si = 0;
+      uint32_t d = 0, acc_f = 0;
+      for (int c = 0; c < T.cchunks; ++c) {
+        const bool g_first = c % T.cgrp == 0;
+        const bool g_last = c % T.cgrp == T.cgrp - 1 || c == T.cchunks - 1;
+        if (g_first) {
+          TS_PROF_WAIT(kPrMmaAcc, mbar_wait(acc_empty + (gc & 1u), ((gc >> 1) & 1u) ^ 1u));
+          tc_fence_after();
+          d = tmem + (gc & 1u) * acc_cols;
+          acc_f = 0;
+        }
+        TS_PROF_WAIT(kPrMmaHalo, mbar_wait(hfull + hb, (hph >> hb) & 1u));
+        hph ^= 1u << hb;
+        tc_fence_after();
+        const uint64_t d_hb = d_halo + (uint64_t)(hb * h_step);
+        const int nk = (c == T.cchunks - 1 && Cin - c * kKC <= 16) ? 1 : 2;
+        for (; s_chunk[si] == c; ++si) {
+          TS_PROF_WAIT(kPrMmaW, mbar_wait(bfull + s, bph));
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t a0 = d_hb + (uint64_t)(s_aoff[si] & 0x0FFFFFFFu);
+            const uint64_t b0 = d_ring + (uint64_t)(s * b_step);
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              if (k >= nk) break;
+#pragma unroll
+              for (int u = 0; u < SUB; ++u) {
+                const uint64_t ak = a0 + (uint64_t)(u * (128 * kRow >> 4) + 2 * k);
+                const uint32_t du = d + u * 2 * BN;
+                umma<false>(du, ak, b0 + 2 * k, idesc, (acc_f | k) ? 1u : 0u);
+                umma<false>(du + BN, ak + pa, b0 + 2 * k, idesc_b0, 1u);
+              }
+            }
+            umma_commit(bempty + s);
+          }
+          __syncwarp();
+          acc_f = 1;
+          if (++s == SB) { s = 0; bph ^= 1; }
+        }
+        if (elect_one()) {
+          umma_commit(hempty + hb);
+          if (g_last) umma_commit(acc_full + (gc & 1u));
+        }
+        __syncwarp();
+        if (g_last) ++gc;
         if (++hb == HB) hb = 0;
       }
     }
@@ -373,15 +528,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
       const int acc = lt % AB;
       mbar_wait(acc_empty + acc, ((lt / AB) & 1) ^ 1);
-      if (T.dbg && blockIdx.x == 0 && (tid & 31) == 0 && lt < 4096)
-        T.dbg[4 * 4096 + lt] = clock64();
       tc_fence_after();
       const uint32_t d = tmem + acc * acc_cols;
       int si = 0;
       for (int c = 0; c < T.cchunks; ++c) {
         mbar_wait(hfull + hb, (hph >> hb) & 1u);
-        if (T.dbg && blockIdx.x == 0 && (tid & 31) == 0 && lt * T.cchunks + c < 4096)
-          T.dbg[4096 + lt * T.cchunks + c] = clock64();
         hph ^= 1u << hb;
         tc_fence_after();
         const uint64_t d_hb = d_halo + (uint64_t)(hb * h_step);
@@ -404,25 +555,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
               for (int u = 0; u < SUB; ++u) {
                 const uint64_t ak = a0 + (uint64_t)(u * (128 * kRow >> 4) + 2 * k);
                 const uint32_t du = dg + u * G * PBS * BN;
-                if (Md::f16) {
-                  // a0 . [b0 | b1] -> [main | corr] (stacked, N = 2 BN) or
-                  // two N = BN MMAs; a1 . b0 -> corr.  MODE 6: the odd K
-                  // step adds a0 . 2^11 b0 (plane 2) into corr instead
-                  const uint32_t f = k ? 1u : first;
-                  if (MODE == 6 && k) {
-                    // b1 -> corr, b0 -> main_odd (overwritten by a tile's
-                    // first stage)
-                    umma<false>(du + BN, ak, b0 + (uint64_t)b_plane16 + 2 * k, idesc_b0, 1u);
-                    umma<false>(du + 2 * BN, ak, b0 + 2 * k, idesc_b0, first);
-                  } else if (T.stack) {
-                    umma<false>(du, ak, b0 + 2 * k, idesc, f);
-                  } else {
-                    umma<false>(du, ak, b0 + 2 * k, idesc_b0, f);
-                    umma<false>(du + BN, ak, b0 + (uint64_t)b_plane16 + 2 * k, idesc_b0, f);
-                  }
-                  umma<false>(du + BN, ak + pa, b0 + 2 * k, idesc_b0, 1u);
-                  continue;
-                }
                 if (T.stack) {
                   umma<false>(du, ak, b0 + 2 * k, idesc, k ? 1u : first);
                 } else {  // a0 . b_p for every plane into the same columns
@@ -450,6 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     }
   } else if (warp == kLoadW) {
     // ------------------------- weight loader -------------------------
+    if constexpr (MODE == 5) reg_dealloc<96>();
     if ((tid & 31) == 0) {
       int s = 0;
       uint32_t bph = 0;
@@ -457,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
         const int nt = (int)(tile % T.n_tiles);
         const uint8_t* wsrc = wdata + (size_t)nt * nst * b_bytes;
         for (int kt = 0; kt < nst; ++kt) {
-          mbar_wait(bempty + s, bph ^ 1);
+          TS_PROF_WAIT(kPrLoadWait, mbar_wait(bempty + s, bph ^ 1));
           bulk_g2s(bring + s * b_bytes, wsrc + (size_t)kt * b_bytes, b_bytes, bfull + s);
           mbar_arrive_tx(bfull + s, b_bytes);
           if (++s == SB) { s = 0; bph ^= 1; }
@@ -465,7 +598,105 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
       }
     }
     __syncwarp();
-  } else {
+  } else if (MODE == 5 && warp >= kEpiW0) {
+    // -------------------- epilogue (FP16X3, promoted) --------------------
+    // Per group: main + 2^-11 corr of every column into fp32 registers (RN
+    // adds), the TMEM pair released; after the tile's last group: bias,
+    // leaky ReLU, fp32 NHWC stores.
+    reg_alloc<224>();
+    constexpr int NB = 128 / SUB / 16;  // 16-column blocks held per sub-tile
+    const int q = warp & 3;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const bool vec = (op.out.cstride % 4 == 0) && (op.out.coff % 4 == 0);
+    const bool vec8 = (op.out.cstride % 8 == 0) && (op.out.coff % 8 == 0) &&
+                      (op.out.C % 8 == 0) && ((reinterpret_cast<uintptr_t>(op.out.base) & 31) == 0);
+    const int groups = (T.cchunks + T.cgrp - 1) / T.cgrp;
+    uint32_t gc = 0;
+    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      const int64_t mt = tile / T.n_tiles;
+      const int n0 = (int)(tile - mt * T.n_tiles) * BN;
+      float R[SUB][NB][16];
+#pragma unroll
+      for (int u = 0; u < SUB; ++u)
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) R[u][j][i] = 0.f;
+      for (int g = 0; g < groups; ++g, ++gc) {
+        TS_PROF_WAIT(kPrEpiWait, mbar_wait(acc_full + (gc & 1u), (gc >> 1) & 1u));
+        tc_fence_after();
+        const uint32_t tb = tmem + lane_base + (gc & 1u) * acc_cols;
+#pragma unroll
+        for (int u = 0; u < SUB; ++u)
+#pragma unroll
+          for (int j = 0; j < NB; ++j) {
+            if (16 * j >= BN) break;
+            uint32_t m[16], r[16];
+            tmem_ld16_nw(tb + u * 2 * BN + 16 * j, m);
+            tmem_ld16_nw(tb + u * 2 * BN + BN + 16 * j, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              R[u][j][i] += __fmaf_rn(__uint_as_float(r[i]), kF16LoInv, __uint_as_float(m[i]));
+          }
+        tc_fence_before();
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(acc_empty + (gc & 1u));
+      }
+#pragma unroll
+      for (int u = 0; u < SUB; ++u) {
+        const int64_t pos = mt * MT + u * 128 + q * 32 + (tid & 31);
+        float* o = nullptr;
+        float* oblk = nullptr;
+        int ochan = 0;
+        if (pos < T.positions) {
+          const int64_t b = (int64_t)((uint32_t)pos / (uint32_t)img_pos);
+          const int r = (int)(pos - b * img_pos);
+          const int y = r / Wp, x = r % Wp;
+          if (y < wy && x < wx) {
+            int oy = op.oy0 + y, ox = op.ox0 + x;
+            if (op.ph == 1) {
+              oy = 2 * oy + op.ph_y;
+              ox = 2 * ox + op.ph_x;
+            }
+            o = op.out.base + act_off(op.out, b, oy, ox);
+            int64_t blk;
+            act_block(op.out, b, oy, ox, blk, ochan);
+            oblk = op.out.base + blk;
+          }
+        }
+        if (!o) continue;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          const int c = 16 * j;
+          if (c >= BN) break;
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float x = R[u][j][i] + s_bias[n0 + c + i];
+            if (op.lrelu) x = x >= 0.f ? x : 0.01f * x;
+            v[i] = x;
+          }
+          if (op.out.planes) {
+            if (n0 + c + 16 <= Cout)
+              store16_planes(oblk, op.out.cstride, ochan + n0 + c, v, op.out.planes == 2);
+          } else if (vec8 && n0 + c + 16 <= Cout) {
+            st_v8(o + n0 + c, v);
+            st_v8(o + n0 + c + 8, v + 8);
+          } else if (vec && n0 + c + 16 <= Cout) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              *reinterpret_cast<float4*>(o + n0 + c + 4 * i) =
+                  make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (n0 + c + i < Cout) o[n0 + c + i] = v[i];
+          }
+        }
+      }
+    }
+  } else if (MODE != 5) {
     // ------------------------- epilogue -------------------------
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int half = (warp - kEpiW0) >> 2;  // which 16-column groups
@@ -480,8 +711,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
       const int nt = (int)(tile - mt * T.n_tiles);
       const int n0 = nt * BN;
       mbar_wait(acc_full + acc, (lt / AB) & 1);
-      if (T.dbg && blockIdx.x == 0 && tid == kEpiW0 * 32 && lt < 4096)
-        T.dbg[2 * 4096 + lt] = clock64();
       tc_fence_after();
       for (int ug = 0; ug < SUB * G; ++ug) {
         const int u = ug / G, g = ug - u * G;
@@ -523,20 +752,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             float x = __uint_as_float(r[0][i]);
-            if (Md::f16) {
-              if (MODE == 6) x += __uint_as_float(r[PBS - 1][i]);
-              x += __uint_as_float(r[1][i]) * kF16LoInv;
-            } else {
 #pragma unroll
-              for (int p = 1; p < PB; ++p)
-                if (p < PBS) x += __uint_as_float(r[p][i]);
-            }
+            for (int p = 1; p < PB; ++p)
+              if (p < PBS) x += __uint_as_float(r[p][i]);
             x += s_bias[n0 + c + i];
             if (op.lrelu) x = x >= 0.f ? x : 0.01f * x;
             v[i] = x;
           }
           if (o && op.out.planes) {
-            if (n0 + c + 16 <= Cout) store16_planes(oblk, op.out.cstride, ochan + n0 + c, v);
+            if (n0 + c + 16 <= Cout) store16_planes(oblk, op.out.cstride, ochan + n0 + c, v, op.out.planes == 2);
           } else if (o) {
             if (vec8 && n0 + c + 16 <= Cout) {
               st_v8(o + n0 + c, v);
@@ -557,8 +781,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
       tc_fence_before();
       __syncwarp();
       if ((tid & 31) == 0) mbar_arrive(acc_empty + acc);
-      if (T.dbg && blockIdx.x == 0 && tid == kEpiW0 * 32 && lt < 4096)
-        T.dbg[3 * 4096 + lt] = clock64();
     }
   }
   tc_fence_before();
@@ -567,30 +789,34 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     tc_fence_after();
     tmem_dealloc(tmem, ncols);
   }
+#ifdef TS_H2_PROF
+  if (tid == 0) atomicAdd(&g_h2_prof[kPrTotal], (unsigned long long)(clock64() - t_start));
+#endif
 }
 
 struct Halo2Plan {
-  int bn, ntiles, pa, pb, sub, hbufs, bstages, cchunks, wp, lrows, accbufs, stack;
+  int bn, ntiles, pa, pb, sub, hbufs, bstages, cchunks, wp, lrows, accbufs, stack, cgrp;
   size_t smem;
   int64_t positions;
 };
 
 bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
-  if (precision < 2 || precision > 6) return false;
-  if (precision >= 5 && (op.in.planes || op.out.planes)) return false;
+  if (precision < 2 || precision > 5) return false;
   // stride-1 k >= 2 (incl. the 2x2 space-to-depth form of stride-2 layers);
   // 1x1 layers stay on the regular kernel (no halo to reuse, and their
   // multi-N-tile shapes re-read A per N tile here)
   if (op.stride != 1 || op.k < 1 || op.pad < 0 || op.pad >= op.k) return false;
   const int G = op_groups(op);
   if (op.ph == 2 && (op.k != 3 || op.pad != 1 || op.up2 || G < 1 || G > 4)) return false;
-  // 1x1 layers: measured slower than the regular kernel (A re-read per N
-  // tile); opt in with TS_H2_1X1=1
+  if (precision == 5 && G != 1) return false;  // promoted epilogue: one phase per launch
+  // 1x1 layers: the bf16-class modes measured slower here than on the
+  // regular kernel (A re-read per N tile; opt in with TS_H2_1X1=1); FP16X3
+  // runs them here for the promoted accumulation
   static const bool h2_1x1 = [] {
     const char* e = getenv("TS_H2_1X1");
     return e && e[0] == '1';
   }();
-  if (op.k == 1 && !h2_1x1) return false;
+  if (op.k == 1 && !h2_1x1 && precision != 5) return false;
   if (op.in.C % 4 || op.in.cstride % 4 || op.in.coff % 4) return false;
   if (op.in.planes && (op.in.C % 8 || op.in.cstride % 8 || op.in.coff % 8)) return false;
   if (op.out.planes && (op.out.C % 16 || op.out.cstride % 8 || op.out.coff % 8)) return false;
@@ -606,7 +832,7 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
       return e ? std::max(16, std::min(256, atoi(e))) : 256;
     }();
     // FP16X3: the two weight planes stack into one MMA (N = 2 BN <= 256)
-    const int bmax = precision >= 5 ? std::min(bnmax, 128) : bnmax;
+    const int bmax = precision == 5 ? std::min(bnmax, 128) : bnmax;
     p.ntiles = (n16 + bmax - 1) / bmax;
   }
   p.bn = ((n16 + p.ntiles - 1) / p.ntiles + 15) / 16 * 16;
@@ -629,10 +855,13 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
     }();
     // (a phase group stacks only if two sub-tiles still get two buffers)
     p.stack = stack_env >= 0 ? stack_env : (p.pb * p.bn <= 64 && 4 * G * p.pb * p.bn <= 512);
-    if (precision >= 5) p.stack = p.bn <= 128;  // [b0 | b1] rows only
+    if (precision == 5) p.stack = 1;  // [b0 | b1] rows (BN <= 128)
     else if (p.pb * p.bn > 256) p.stack = 0;  // MMA N limit
   }
-  const int cols = G * (precision >= 5 ? (precision - 3) * p.bn : p.stack ? p.pb * p.bn : p.bn);
+  const int cols = G * (precision == 5 ? 2 * p.bn : p.stack ? p.pb * p.bn : p.bn);
+  // FP16X3: promotion group = the channel chunks of <= 18 K steps (2 per
+  // 32-channel chunk and tap): 1 for 3x3, 2 for 2x2, 8 for 1x1
+  p.cgrp = precision == 5 ? std::max(1, 16 / (2 * op.k * op.k)) : 1;
   int cand[6][2] = {{4, 2}, {2, 2}, {1, 2}, {4, 1}, {2, 1}, {1, 1}};
   {  // TS_H2_SUBAB=<sub>,<accbufs>: try that candidate first (A/B measurement)
     static const char* e = getenv("TS_H2_SUBAB");
@@ -645,6 +874,8 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
     if (cb[0] == 3) continue;
     const int sub = cb[0], ab = cb[1];
     if (ab * sub * cols > 512) continue;
+    // FP16X3: two group buffers, and the epilogue holds SUB x BN sums
+    if (precision == 5 && (ab != 2 || sub * p.bn > 128)) continue;
     const int L = (128 * sub + (op.k - 1) * (p.wp + 1) + 7) / 8 * 8;
     const size_t hbuf = (size_t)p.pa * L * kRow;
     const size_t fixed = 1024 + 8 * 40 + 16 + 16 * (size_t)L + 6 * kMaxStages + 64 +
@@ -657,8 +888,12 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
       const char* e = getenv("TS_H2_SB");  // measured: 3-4 about 1% faster than 8
       return e ? atoi(e) : 4;
     }();
-    for (int hb : {3, 2}) {
-      if (hb_env && hb != hb_env) continue;
+    static const int hb_max = [] {  // TS_H2_HBMAX=<n>: most halo buffers tried
+      const char* e = getenv("TS_H2_HBMAX");
+      return e ? atoi(e) : 3;
+    }();
+    for (int hb : {8, 6, 5, 4, 3, 2}) {
+      if (hb > hb_max || (hb_env && hb != hb_env)) continue;
       const size_t used = hb * hbuf + fixed;
       if (used + 3 * bst > cap) continue;
       p.sub = sub;
@@ -701,7 +936,9 @@ std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, 
   std::vector<uint16_t> list;
   std::vector<char> seen(G, 0);
   for (int c = 0; c < p.cchunks; ++c)
-    for (int g = 0; g < G; ++g)
+    for (int g = 0; g < G; ++g) {
+      bool any = false;  // FP16X3: every chunk keeps a stage (its group's
+                         // first MMA must write the accumulators)
       for (int t = 0; t < taps; ++t) {
         const int ky = t / k, kx = t % k;
         bool nz = false;
@@ -712,10 +949,14 @@ std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, 
               nz = true;
           }
         // an all-zero phase keeps one (zero) stage so its columns are written
-        if (!nz && (c != p.cchunks - 1 || t != taps - 1 || seen[g])) continue;
+        const bool keep = precision == 5 ? (t == taps - 1 && !any)
+                                         : (c == p.cchunks - 1 && t == taps - 1 && !seen[g]);
+        if (!nz && !keep) continue;
         list.push_back((uint16_t)(((c * G + g) * taps + t) | (seen[g] ? 0 : 0x8000)));
         seen[g] = 1;
+        any = true;
       }
+    }
   if ((int)list.size() > kMaxStages) return {};
   const int nst = (int)list.size();
   std::vector<uint8_t> out(kHdr + (size_t)p.ntiles * nst * b_bytes, 0);
@@ -741,7 +982,7 @@ std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, 
           uint16_t h[3] = {0, 0, 0};
           if (precision == 2) {
             h[0] = f2bf16_rn_host(v);
-          } else if (precision >= 5) {
+          } else if (precision == 5) {
             split_f16_host(v, h[0], h[1]);
 
           } else if (precision == 4) {  // RN split, like the device producers
@@ -768,20 +1009,10 @@ int launch_conv_tc_halo2(const ConvOp& op, int precision, void* stream) {
   if (!plan2(op, precision, &p)) return TS_E_INVALID;
   if (p.positions + 128 * p.sub + p.lrows >= (int64_t)INT32_MAX) return TS_E_INVALID;
   Halo2Args a{op, op.w_tc, p.bn, p.sub, p.hbufs, p.bstages, p.cchunks, op.k * op.k, p.wp,
-              p.lrows, p.ntiles, p.accbufs, p.stack,
-              ceil_div<int64_t>(p.positions, 128 * p.sub), p.positions, nullptr};
+              p.lrows, p.ntiles, p.accbufs, p.stack, p.cgrp,
+              ceil_div<int64_t>(p.positions, 128 * p.sub), p.positions};
   const int64_t tiles = a.m_tiles * p.ntiles;
   if (tiles <= 0) return TS_OK;
-  static int dbg_at = -2, launch_no = 0;
-  if (dbg_at == -2) {
-    const char* e = getenv("TS_H2_DBG");
-    dbg_at = e ? atoi(e) : -1;
-  }
-  const bool dbg = launch_no++ == dbg_at;
-  if (dbg) {
-    TS_CUDA_TRY(cudaMalloc(&a.dbg, 5 * 4096 * sizeof(unsigned long long)));
-    TS_CUDA_TRY(cudaMemset(a.dbg, 0, 5 * 4096 * sizeof(unsigned long long)));
-  }
   const int sms = sm_count();
   if (!sms) return TS_E_CUDA;
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
@@ -802,30 +1033,28 @@ int launch_conv_tc_halo2(const ConvOp& op, int precision, void* stream) {
   if (precision == 2) TS_TCH2_SUB(2);
   else if (precision == 4) TS_TCH2_SUB(4);
   else if (precision == 5) TS_TCH2_SUB(5);
-  else if (precision == 6) TS_TCH2_SUB(6);
   else TS_TCH2_SUB(3);
 #undef TS_TCH2_SUB
 #undef TS_TCH2_LAUNCH
   TS_LAUNCH_CHECK();
-  if (dbg) {
-    std::vector<unsigned long long> h(5 * 4096);
-    TS_CUDA_TRY(cudaMemcpy(h.data(), a.dbg, h.size() * 8, cudaMemcpyDeviceToHost));
-    cudaFree(a.dbg);
-    fprintf(stderr, "h2dbg sub=%d ab=%d hb=%d sb=%d cchunks=%d nst=? ntiles=%d L=%d tiles=%lld\n",
-            p.sub, p.accbufs, p.hbufs, p.bstages, p.cchunks, p.ntiles, p.lrows, (long long)tiles);
-    const unsigned long long t0 = h[4 * 4096];
-    for (int lt = 0; lt < 12; ++lt) {
-      fprintf(stderr, "tile %d: mma_start %lld epi_start %lld epi_end %lld | prod",
-              lt, (long long)(h[4 * 4096 + lt] - t0), (long long)(h[2 * 4096 + lt] - t0),
-              (long long)(h[3 * 4096 + lt] - t0));
-      for (int c = 0; c < p.cchunks; ++c)
-        fprintf(stderr, " %lld", (long long)(h[lt * p.cchunks + c] - t0));
-      fprintf(stderr, " | mma_hfull");
-      for (int c = 0; c < p.cchunks; ++c)
-        fprintf(stderr, " %lld", (long long)(h[4096 + lt * p.cchunks + c] - t0));
-      fprintf(stderr, "\n");
-    }
+#ifdef TS_H2_PROF
+  {  // per-launch wait profile (profiling build only): cycles per CTA
+    unsigned long long h[kPrN];
+    TS_CUDA_TRY(cudaStreamSynchronize(s));
+    TS_CUDA_TRY(cudaMemcpyFromSymbol(h, g_h2_prof, sizeof(h)));
+    const unsigned long long z[kPrN] = {};
+    TS_CUDA_TRY(cudaMemcpyToSymbol(g_h2_prof, z, sizeof(z)));
+    const double n = (double)grid, tot = (double)h[kPrTotal] / n;
+    fprintf(stderr,
+            "h2prof k=%d ci=%d co=%d sub=%d bn=%d nt=%d hb=%d sb=%d L=%d cgrp=%d tiles=%lld | "
+            "total %.0f kcyc | prod-wait-buf %.2f (x%d warps) | mma: acc %.2f halo %.2f wts "
+            "%.2f | epi-wait %.2f (x4) | load-wait %.2f\n",
+            op.k, op.in.C, op.out.C, p.sub, p.bn, p.ntiles, p.hbufs, p.bstages, p.lrows, p.cgrp,
+            (long long)tiles, tot / 1e3, h[kPrProdWait] / n / kProdW / tot, kProdW,
+            h[kPrMmaAcc] / n / tot, h[kPrMmaHalo] / n / tot, h[kPrMmaW] / n / tot,
+            h[kPrEpiWait] / n / 4 / tot, h[kPrLoadWait] / n / tot);
   }
+#endif
   return TS_OK;
 }
 

@@ -105,6 +105,8 @@ struct ts_weights {
   size_t cat_off = 0, fuse_in_off = 0;
   bool enc0_fused = false;  // the four encoders' first layers in one launch
   bool fuse_in_planes = false;  // fuse-input buffer (raw inputs + decoders)
+  bool cat_planes = false;      // encoder concat buffer (merge input)
+  int plane_fmt = 1;            // ActView planes format: 1 bf16, 2 FP16X3
   ts::Win fuse_in_win{0, 0, 0, 0};  // the part of it fuse.0 reads (crop-aware)
   std::vector<void*> device_allocs;
 };
@@ -203,7 +205,7 @@ __global__ void copy_inputs_kernel(const float* __restrict__ in, int64_t n_win,
     float v[8];
     tcx::ld_v8(in + 8 * i, v);
     if (planes) {  // pre-split channels 0..7 of the fuse input
-      tcx::store8_planes(out + (int64_t)cstride * i, cstride, 0, v);
+      tcx::store8_planes(out + (int64_t)cstride * i, cstride, 0, v, planes == 2);
     } else if (cstride % 8 == 0) {
       tcx::st_v8(out + (int64_t)cstride * i, v);
     } else {
@@ -538,16 +540,10 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
     const int K = dx.k * dx.k * dx.ci, Co = dx.co;
     std::vector<float> packed((size_t)K * Co);
     std::vector<float> src = wi->second.second;  // OIKK of the executed shape
-    // FP16X3: layers with K >= 512 split their main sum by K-step parity
-    // (mode 6).  Measured on 38 configs[1] tiles, random He weights
-    // (scripts/precision_check.py): max |dh| 2.56e-3 m with no split,
-    // 1.82e-3 from K >= 700, 1.66e-3 from K >= 512, 1.53e-3 everywhere;
-    // the fp32 CUDA-core mode 0 gives 1.63e-3 (bar: 2e-3 m)
+    // FP16X3 layers run on the wide-M halo kernel with the accumulator
+    // restarted and promoted to fp32 registers every <= 18 K steps
+    // (tc_ptx.cuh Mode<5>)
     L.prec = W->precision;
-    if (W->precision == 5) {
-      const int kk = L.poly ? 4 * dx.ci : dx.k * dx.k * dx.ci;
-      if (kk >= 512 && dx.ci > 16) L.prec = 6;
-    }
     if (L.s2d_in) {
       // W'[o][(a*2+b)*ci + c][ty][tx] = W[o][c][2ty+a-1][2tx+b-1] (0 outside)
       const int ci0 = L.d.ci;
@@ -678,11 +674,16 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
   for (auto& L : layers)
     L.h2 = L.poly || (L.w_tc && L.w_layout == 2 && L.dexec.ci > 4);
   {
-    // measured: the epilogue's split costs more than the producers save
-    // (12.96 vs 11.88 ms per 1,024 tiles), so pre-split storage is opt-in
-    // (TS_PLANES=1); results are bit-identical either way
+    // Pre-split storage (TS_PLANES=1, opt-in): producing epilogues write
+    // the consumer's operand planes (bf16 RN hi/lo, or the FP16X3 scaled
+    // fp16 pair) and the halo producers only copy (cp.async for FP16X3).
+    // Measured slower in every mode: bf16-class 12.96 vs 11.88 ms per 1,024
+    // tiles, FP16X3 12.08 vs 10.04 ms (the epilogues' split and plane stores
+    // cost more than the producers save; profiles/r02_cnn_layers.md).
+    // Results are bit-identical either way.
     const char* e = getenv("TS_PLANES");
-    const bool on = tc16_mode(W->precision) && W->precision != 5 && (e && e[0] == '1');
+    W->plane_fmt = W->precision == 5 ? 2 : 1;
+    const bool on = tc16_mode(W->precision) && (e && e[0] == '1');
     auto fmt_ok = [](const ConvLayer& L) {
       return L.d.co % 16 == 0 && L.out_cstride % 8 == 0 && L.out_coff % 8 == 0;
     };
@@ -696,6 +697,9 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
         const ConvLayer& a = layers[stage_first[5]];
         const ConvLayer& b = layers[stage_first[6]];
         all_h2 = a.h2 && b.h2 && a.dexec.ci % 8 == 0;
+      } else if (L.stage < 4) {  // encoder output -> the concat -> merge.0
+        const ConvLayer& m = layers[stage_first[4]];
+        all_h2 = m.h2 && m.dexec.ci % 8 == 0;
       }
       // writers that can emit planes: halo2 / phase layers, the regular
       // tensor-core kernel, the fused first encoder layers
@@ -703,6 +707,11 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
                           (W->enc0_fused && L.stage < 4 && L.index == 0);
       L.out_planes = all_h2 && writer && fmt_ok(L);
     }
+    // the concat is pre-split only if every encoder writes it so
+    W->cat_planes = on;
+    for (int st = 0; st < 4; ++st)
+      W->cat_planes = W->cat_planes && layers[stage_last[st]].out_planes;
+    for (int st = 0; st < 4; ++st) layers[stage_last[st]].out_planes = W->cat_planes;
     // fuse input: raw-input copy + both decoders' last layers -> fuse.0
     const ConvLayer& f0 = layers[stage_first[7]];
     W->fuse_in_planes = on && f0.h2 && fin % 8 == 0 && dec_c_out[0] % 16 == 0 &&
@@ -873,7 +882,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
       const int64_t px = (int64_t)B * wy * wx;
       ts::count_launch(), copy_inputs_kernel<<<(int)std::min<int64_t>(ceil_div<int64_t>(px, 256), 148 * 16),
                            256, 0, cs>>>(in, px, buf(W->fuse_in_off), W->fuse_in_c,
-                                         W->fuse_in_planes ? 1 : 0, fw.y0, fw.x0, wy, wx);
+                                         W->fuse_in_planes ? W->plane_fmt : 0, fw.y0, fw.x0, wy, wx);
       TS_LAUNCH_CHECK();
       copied = true;
       return TS_OK;
@@ -910,7 +919,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
                           enc_cin[L.stage]};
         } else if (L.stage == 4) {
           op.in = ActView{buf(W->cat_off), W->enc_hw, W->enc_hw, W->enc_out_c, 0,
-                          W->enc_out_c};
+                          W->enc_out_c, 0, W->cat_planes ? W->plane_fmt : 0};
         } else if (L.stage == 5 || L.stage == 6) {
           // merge output = the last merge layer's buffer
           size_t mi = 0;
@@ -918,10 +927,10 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
             if (W->layers[j].stage == 4) mi = j;
           const ConvLayer& M = W->layers[mi];
           op.in = ActView{buf(M.out_off), M.Hout, M.Wout, M.out_cstride, M.out_coff, M.d.co,
-                          0, M.out_planes ? 1 : 0};
+                          0, M.out_planes ? W->plane_fmt : 0};
         } else {
           op.in = ActView{buf(W->fuse_in_off), kRes, kRes, W->fuse_in_c, 0, W->fuse_in_c,
-                          0, W->fuse_in_planes ? 1 : 0};
+                          0, W->fuse_in_planes ? W->plane_fmt : 0};
         }
       } else {
         op.in = ActView{const_cast<float*>(prev_base), prev_H, prev_H, prev_cs, prev_coff,
@@ -934,7 +943,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
                         4 * prev_C, 0, prev_planes};
       }
       op.out = ActView{buf(L.out_off), L.Hout, L.Wout, L.out_cstride, L.out_coff, L.d.co, 0,
-                       L.out_planes ? 1 : 0};
+                       L.out_planes ? W->plane_fmt : 0};
       if (L.s2d_out) {
         if (L.out_coff != 0 || L.out_cstride != L.d.co) return TS_E_INVALID;
         op.out.cstride = 4 * L.d.co;
@@ -961,7 +970,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
             E.ch0[e] = enc_ch0[e]; E.cin[e] = enc_cin[e]; E.lrelu[e] = F.d.lrelu;
             E.w[e] = F.w; E.bias[e] = F.b;
             E.out[e] = ActView{buf(F.out_off), F.Hout, F.Wout, 4 * F.d.co, 0, F.d.co, 1,
-                               F.out_planes ? 1 : 0};
+                               F.out_planes ? W->plane_fmt : 0};
             ++e;
           }
           E.oy0 = L.out_win.y0; E.oy1 = L.out_win.y1; E.ox0 = L.out_win.x0; E.ox1 = L.out_win.x1;
@@ -969,7 +978,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
           if (st != TS_OK) return st;
         }
         prev_base = buf(L.out_off); prev_H = L.Hout; prev_cs = L.out_cstride;
-        prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? 1 : 0;
+        prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? W->plane_fmt : 0;
         prev_stage = L.stage;
         continue;
       }
@@ -988,7 +997,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
           if (st != TS_OK) return st;
         }
         prev_base = op.out.base; prev_H = L.Hout; prev_cs = L.out_cstride;
-        prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? 1 : 0;
+        prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? W->plane_fmt : 0;
         prev_stage = L.stage;
         continue;
       }
@@ -1005,7 +1014,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
           if (st != TS_OK) return st;
         }
         prev_base = op.out.base; prev_H = L.Hout; prev_cs = L.out_cstride;
-        prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? 1 : 0;
+        prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? W->plane_fmt : 0;
         prev_stage = L.stage;
         continue;
       }
@@ -1016,7 +1025,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
         st = launch_conv_final(op, L.w_host.data(), L.b_host.data(), lstream);
         if (st != TS_OK) return st;
         prev_base = op.out.base; prev_H = L.Hout; prev_cs = L.out_cstride;
-        prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? 1 : 0;
+        prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? W->plane_fmt : 0;
         prev_stage = L.stage;
         continue;
       }
@@ -1033,7 +1042,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
         st = launch_conv_simt(op, lstream);
       if (st != TS_OK) return st;
       prev_base = op.out.base; prev_H = L.Hout; prev_cs = L.out_cstride;
-      prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? 1 : 0;
+      prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? W->plane_fmt : 0;
       prev_stage = L.stage;
     }
     if (br && region >= 0 && join(region) != TS_OK) return TS_E_CUDA;

@@ -45,6 +45,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(su32(bar))
       : "memory");
 }
+// 16-byte asynchronous global -> shared copy (LDGSTS); bytes = 0 zero-fills
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -114,6 +126,18 @@ __device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t* r) {
 }
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Warp-group register reallocation (setmaxnreg): every warp of a warp group
+// must execute the same instruction.  The launch-bounds budget is the
+// starting point; ptxas allocates each region within its new limit.
+template <int N>
+__device__ __forceinline__ void reg_alloc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void reg_dealloc() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N));
 }
 
 __device__ __forceinline__ bool elect_one() {
@@ -210,17 +234,18 @@ __device__ __forceinline__ void store_split2(uint8_t* dst, int plane_bytes, floa
   *reinterpret_cast<uint2*>(dst + plane_bytes) = make_uint2(l01, l23);
 }
 
-// 16 consecutive channels (chan % 8 == 0) into a planes = 1 pixel block
+// a pair -> the two plane words of an ActView planes format (1: bf16 RN
+// hi/lo, 2: FP16X3 hi / 2^11-scaled lo, the split the halo producers would
+// compute from the fp32 value)
+__device__ __forceinline__ void split_pair(float x, float y, bool f16, uint32_t& h,
+                                           uint32_t& l);
+// 16 consecutive channels (chan % 8 == 0) into a planes pixel block
 // (conv.cuh ActView): 32 bytes of hi, 32 bytes of lo, 16-byte stores
 __device__ __forceinline__ void store16_planes(float* block, int cstride, int chan,
-                                               const float* v) {
+                                               const float* v, bool f16) {
   uint32_t h[8], l[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    h[i] = pack_bf2(v[2 * i], v[2 * i + 1]);
-    l[i] = pack_bf2(v[2 * i] - __uint_as_float(h[i] << 16),
-                    v[2 * i + 1] - __uint_as_float(h[i] & 0xFFFF0000u));
-  }
+  for (int i = 0; i < 8; ++i) split_pair(v[2 * i], v[2 * i + 1], f16, h[i], l[i]);
   uint4* hp = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(block) + 2 * chan);
   uint4* lp = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(block) + 2 * (cstride + chan));
   hp[0] = make_uint4(h[0], h[1], h[2], h[3]);
@@ -230,14 +255,10 @@ __device__ __forceinline__ void store16_planes(float* block, int cstride, int ch
 }
 // 8 channels (chan % 8 == 0): 16 bytes of hi, 16 of lo
 __device__ __forceinline__ void store8_planes(float* block, int cstride, int chan,
-                                              const float* v) {
+                                              const float* v, bool f16) {
   uint32_t h[4], l[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    h[i] = pack_bf2(v[2 * i], v[2 * i + 1]);
-    l[i] = pack_bf2(v[2 * i] - __uint_as_float(h[i] << 16),
-                    v[2 * i + 1] - __uint_as_float(h[i] & 0xFFFF0000u));
-  }
+  for (int i = 0; i < 4; ++i) split_pair(v[2 * i], v[2 * i + 1], f16, h[i], l[i]);
   *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(block) + 2 * chan) =
       make_uint4(h[0], h[1], h[2], h[3]);
   *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(block) + 2 * (cstride + chan)) =
@@ -280,25 +301,15 @@ struct Mode<4> {  // BF16X4: A = a0 + a1, B = b0 + b1 (both RN, residual <= 2^-1
 // FP16X3 (the fp32-class mode): fp16 planes with a scaled correction plane,
 // a = a0 + 2^-11 a1, a0 = fp16_rn(a), a1 = fp16_rn((a - a0) 2^11), so both
 // planes are in fp16's normal range and |a - a0 - 2^-11 a1| <= 2^-24 |a|
-// (fp32's own rounding); same for the weights.  Products: a0 b0 into the
-// MAIN accumulator columns, a0 b1 + a1 b0 into a separate CORRECTION block
-// (scaled by 2^11), combined by the epilogue as main + 2^-11 corr.  Keeping
-// the corrections out of the main accumulator matters: each tcgen05 MMA
-// truncates its fp32 result (scripts/mma_numerics.cu measures the bias),
-// so the main sum should take one MMA per K step, not three.
+// (fp32's own rounding); same for the weights.  Products: a0 b0 into a MAIN
+// column block, a0 b1 + a1 b0 into a CORRECTION block (scaled by 2^11).
+// Each tcgen05 MMA truncates its fp32 accumulation (scripts/mma_numerics.cu
+// measures the bias), so a long K chain in one accumulator drifts: the
+// kernels restart both blocks every <= 18 K steps (a "group" of channel
+// chunks) and the epilogue warps promote each group's main + 2^-11 corr into
+// fp32 registers with round-to-nearest adds.
 template <>
 struct Mode<5> {
-  static constexpr int pa = 2, pb = 2, kc = 64;
-  static constexpr bool tf32 = false, f16 = true;
-};
-// FP16X3 with the main sum split by K-step parity into two column blocks,
-// [main_even | corr | main_odd]: even K steps multiply rows [b0 | b1] into
-// [main_even | corr] (one stacked MMA), odd ones b1 into corr and b0 into
-// main_odd (two MMAs), so each main accumulator takes half the truncating
-// MMAs while the correction block stays small (long-K layers;
-// scripts/mma_numerics.cu)
-template <>
-struct Mode<6> {
   static constexpr int pa = 2, pb = 2, kc = 64;
   static constexpr bool tf32 = false, f16 = true;
 };
@@ -326,6 +337,15 @@ __device__ __forceinline__ void split_h2(float x, float y, uint32_t& h, uint32_t
       : "r"(h));
   // x - hx is exact (hx = x rounded to 11 bits); the 2^11 scale is exact
   l = pack_h2((x - hx) * kF16Lo, (y - hy) * kF16Lo);
+}
+__device__ __forceinline__ void split_pair(float x, float y, bool f16, uint32_t& h,
+                                           uint32_t& l) {
+  if (f16) {
+    split_h2(x, y, h, l);
+  } else {
+    h = pack_bf2(x, y);
+    l = pack_bf2(x - __uint_as_float(h << 16), y - __uint_as_float(h & 0xFFFF0000u));
+  }
 }
 // 4 floats -> 8 bytes of each plane
 __device__ __forceinline__ void store_split_h(uint8_t* dst, int plane_bytes, float4 a) {

@@ -1,11 +1,11 @@
 """tcgen05 implicit-GEMM convolution vs the fp32 oracle (needs a B200).
 
 Precision modes (table "CNN, per precision mode"):
-  5 FP16X3 (the default; 6 = its K-parity split, chosen per layer for
-    K >= 512) -- fp32-class: fp16 planes a0 + 2^-11 a1 (split residual
-    2^-24), main products and corrections in separate TMEM accumulators;
-    the fp32 bar: refiner heights within 2e-3 m of the reference on random
-    He weights (measured 1.66e-3 m; the CUDA-core mode 0: 1.63e-3 m).
+  5 FP16X3 (the default) -- fp32-class: fp16 planes a0 + 2^-11 a1 (split
+    residual 2^-24), main and correction products in separate TMEM blocks
+    restarted every <= 18 K steps and promoted to fp32 registers; the fp32
+    bar: refiner heights within 2e-3 m of the reference on random He
+    weights (the CUDA-core fp32 mode 0 measures 1.63e-3 m).
   1 TF32X3, 3 BF16X3, 4 BF16X4 -- bf16-class splits (2^-16 residual, all
     products in one truncating accumulator): within 0.05 m (measured
     0.012-0.020 m).
@@ -41,7 +41,7 @@ SHAPES = [  # (ci, co, k, stride, pad, h, w)
 
 
 @pytest.mark.parametrize("shape", SHAPES)
-@pytest.mark.parametrize("precision", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("precision", [1, 2, 3, 4, 5])
 def test_conv_tc_vs_oracle(shape, precision):
     from paper_2509_20198_b200.refiner import conv2d
     ci, co, k, s, p, h, w = shape
@@ -55,9 +55,10 @@ def test_conv_tc_vs_oracle(shape, precision):
     got = conv2d(x, wt, b, s, p, precision=precision)
     scale = np.abs(want).max()
     err = np.abs(got - want).max() / scale
-    if precision in (5, 6):
-        # fp32 class: split residual 2^-24, one truncating MMA per K step
-        # into the main accumulator
+    if precision == 5:
+        # fp32 class: split residual 2^-24, <= 18 truncating K steps per
+        # promoted group (1x1 and 2x2 layers on the halo kernel; others on
+        # the regular kernel's unpromoted pair of blocks)
         assert err < 2e-6, err
     elif precision in (1, 3, 4):
         # the tcgen05 fp32 accumulator (every product into one truncating
