@@ -153,8 +153,10 @@ int ts_nearest(const double* d_xy, int64_t n, const double* d_q, int64_t nq,
  * orientation/incircle predicates; vertex ids 0..N-1 real, N..N+3 the
  * corners (-1,-1),(1,-1),(-1,1),(1,1).  Triangle slot p starts at
  * 2*pts_off[p] + 8*p; capacity 2N+8; d_ntri[p] gets the count.  CCW.
+ * Any patch size and insertion order: patches of <= 384 points run in
+ * shared memory and restart in global memory if a cavity outgrows it.
  * d_scratch: ts_triangulate_scratch(total points, patches) bytes (the
- * per-triangle circumcircle cache).                                      */
+ * global-memory meshes, circumcircle caches and cavities).                */
 size_t ts_triangulate_scratch(int64_t total_points, int n_patches);
 int ts_triangulate(const double* d_xy, const int64_t* d_pts_off,
                    int n_patches, int32_t* d_tri, int32_t* d_ntri,

@@ -13,6 +13,7 @@
 // Compiled with --fmad=false: the predicate error bounds assume one
 // rounding per operation.
 #include <cstdlib>
+#include <type_traits>
 
 #include "predicates.cuh"
 #include "ts_common.cuh"
@@ -100,21 +101,33 @@ struct Mesh {
 };
 
 
-// SMEM: the mesh lives in shared memory (the instance's pointers all derive
-// from the shared array, so its loads compile to LDS, not generic loads)
+constexpr int kOverflow = -1;  // shared-memory cavity full: retry in global memory
+
+// Scratch layout (ts_triangulate_scratch): patch p owns triangle slots
+// [base, base + cap), base = 2 off + 8 p, cap = 2 n + 8 (the most an n-point
+// mesh can hold), and the byte block [60 base + 64 p, 60 (base + cap) +
+// 64 (p + 1)) of the scratch:
+//   circumcircle cache  3 x cap doubles (x, y, r^2 per slot)
+//   cavity keys         3 x cap int64   (global-memory variant)
+//   cavity edges        cap + 8 int2
+//   cavity slots        cap int
+// (60 base is a multiple of 8: base is even.)
+constexpr int64_t kSlotBytes = 60, kPatchBytes = 64;
+
+// SMEM: the mesh and the cavity live in shared memory (the instance's
+// pointers all derive from the shared array, so its loads compile to LDS),
+// the cavity holds kMaxCavity triangles and edge keys are u << 16 | w (ids <
+// 2^16: n <= kSmemPoints).  Otherwise the mesh and a cavity of the mesh's
+// full capacity live in the caller's scratch and keys are 64-bit, so no
+// patch size or insertion order can overflow it.
 template <bool SMEM>
-__device__ __forceinline__ void triangulate_patch(unsigned char* smem,
-                                                  const double* __restrict__ xy_all,
-                                                  const int64_t* __restrict__ pts_off,
-                                                  int32_t* tri_all, int32_t* ntri_out,
-                                                  int32_t* status, double* circ_all) {
-  double* s_cx = reinterpret_cast<double*>(smem);
-  double* s_cy = s_cx + kSmemSlots;
-  double* s_r2 = s_cy + kSmemSlots;
-  int* s_tri = reinterpret_cast<int*>(s_r2 + kSmemSlots);
-  int* bad = s_tri + 3 * kSmemSlots;
-  int2* edge = reinterpret_cast<int2*>(bad + kMaxCavity);
-  int* ekey = reinterpret_cast<int*>(edge + kMaxCavity + 8);  // [3 * kMaxCavity]
+__device__ __forceinline__ int triangulate_patch(unsigned char* smem,
+                                                 const double* __restrict__ xy_all,
+                                                 const int64_t* __restrict__ pts_off,
+                                                 int32_t* tri_all, int32_t* ntri_out,
+                                                 int32_t* status, uint8_t* scratch) {
+  using Key = typename std::conditional<SMEM, int, long long>::type;
+  constexpr int kShift = SMEM ? 16 : 32;
   const int lane = threadIdx.x;
   const int p = blockIdx.x;
   const int64_t off = pts_off[p];
@@ -124,12 +137,27 @@ __device__ __forceinline__ void triangulate_patch(unsigned char* smem,
   const PatchPts P{xy_all + 2 * off, n};
   const int cap = 2 * n + 8;
   constexpr bool in_smem = SMEM;
+  const int max_cav = SMEM ? kMaxCavity : cap;
   Mesh M;
+  int* bad;
+  int2* edge;
+  Key* ekey;
   if (SMEM) {
+    double* s_cx = reinterpret_cast<double*>(smem);
+    double* s_cy = s_cx + kSmemSlots;
+    double* s_r2 = s_cy + kSmemSlots;
+    int* s_tri = reinterpret_cast<int*>(s_r2 + kSmemSlots);
     M = Mesh{s_tri, s_cx, s_cy, s_r2};
+    bad = s_tri + 3 * kSmemSlots;
+    edge = reinterpret_cast<int2*>(bad + kMaxCavity);
+    ekey = reinterpret_cast<Key*>(edge + kMaxCavity + 8);  // [3 * kMaxCavity]
   } else {
-    double* g = circ_all + 3 * base;
+    uint8_t* blk = scratch + kSlotBytes * base + kPatchBytes * p;
+    double* g = reinterpret_cast<double*>(blk);
     M = Mesh{tri_out, g, g + cap, g + 2 * cap};
+    ekey = reinterpret_cast<Key*>(blk + 24 * (int64_t)cap);
+    edge = reinterpret_cast<int2*>(blk + 48 * (int64_t)cap);
+    bad = reinterpret_cast<int*>(blk + 56 * (int64_t)cap + 64);
   }
   if (lane == 0) M.set(P, 0, n, n + 1, n + 3);
   if (lane == 1) M.set(P, 1, n, n + 3, n + 2);
@@ -172,21 +200,21 @@ __device__ __forceinline__ void triangulate_patch(unsigned char* smem,
       for (int j = 0; j < kScanIlp; ++j) {
         if (in[j]) {
           const int slot = nb + __popc(m[j] & below);
-          if (slot < kMaxCavity) bad[slot] = b0 + lane + 32 * j;
+          if (slot < max_cav) bad[slot] = b0 + lane + 32 * j;
         }
         nb += __popc(m[j]);
       }
     }
     if (nb == 0) continue;  // exact duplicate of an inserted vertex
-    if (nb > kMaxCavity) { st = TS_E_INVALID; break; }
+    if (nb > max_cav) { st = kOverflow; break; }  // (shared-memory cavity only)
     __syncwarp();
     // 2. boundary edges of the cavity (edges without a bad twin): every
-    //    directed cavity edge is published as a key (u << 16 | w); an edge
-    //    is interior iff its reverse key is present (vertex ids < 2^16)
+    //    directed cavity edge is published as a key (u << kShift | w); an
+    //    edge is interior iff its reverse key is present
     for (int e = lane; e < 3 * nb; e += 32) {
       const int i = e / 3, j = e - 3 * i;
       const int* t = M.tri + 3 * bad[i];
-      ekey[e] = (t[j] << 16) | t[j == 2 ? 0 : j + 1];
+      ekey[e] = ((Key)t[j] << kShift) | (Key)t[j == 2 ? 0 : j + 1];
     }
     __syncwarp();
     int ne = 0;
@@ -195,10 +223,10 @@ __device__ __forceinline__ void triangulate_patch(unsigned char* smem,
       bool keep = false;
       int u = 0, w = 0;
       if (e < 3 * nb) {
-        const int key = ekey[e];
-        u = key >> 16;
-        w = key & 0xFFFF;
-        const int twin = (w << 16) | u;
+        const Key key = ekey[e];
+        u = (int)(key >> kShift);
+        w = (int)(key & (((Key)1 << kShift) - 1));
+        const Key twin = ((Key)w << kShift) | (Key)u;
         keep = true;
         // linear twin search over all keys (broadcast reads; measured
         // faster than __match_any_sync on the undirected keys)
@@ -220,11 +248,12 @@ __device__ __forceinline__ void triangulate_patch(unsigned char* smem,
       const unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
       if (keep) {
         const int slot = ne + __popc(m & ((1u << lane) - 1));
-        if (slot < kMaxCavity + 8) edge[slot] = make_int2(u, w);
+        if (slot < max_cav + 8) edge[slot] = make_int2(u, w);
       }
       ne += __popc(m);
     }
-    if (ne < nb || ne > kMaxCavity + 8 || ntri + ne - nb > cap) {
+    if (ne > max_cav + 8) { st = kOverflow; break; }
+    if (ne < nb || ntri + ne - nb > cap) {  // impossible with exact predicates
       st = TS_E_INVALID;
       break;
     }
@@ -238,19 +267,20 @@ __device__ __forceinline__ void triangulate_patch(unsigned char* smem,
     ntri += ne - nb;
     __syncwarp();
   }
+  if (st == kOverflow) return st;  // the caller retries in global memory
   if (in_smem && st == TS_OK)
-    for (int i = lane; i < 3 * ntri; i += 32) tri_out[i] = s_tri[i];
+    for (int i = lane; i < 3 * ntri; i += 32) tri_out[i] = M.tri[i];
   if (lane == 0) {
     ntri_out[p] = st == TS_OK ? ntri : 0;
     status[p] = st;
   }
+  return st;
 }
 
 __global__ void __launch_bounds__(32)
 delaunay_kernel(const double* __restrict__ xy_all,
                 const int64_t* __restrict__ pts_off, int n_patches,
-                int32_t* tri_all, int32_t* ntri_out, int32_t* status,
-                double* circ_all) {
+                int32_t* tri_all, int32_t* ntri_out, int32_t* status, uint8_t* scratch) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int p = blockIdx.x;
   const int n = (int)(pts_off[p + 1] - pts_off[p]);
@@ -258,10 +288,14 @@ delaunay_kernel(const double* __restrict__ xy_all,
     if (threadIdx.x == 0) { ntri_out[p] = 0; status[p] = TS_E_EMPTY_PATCH; }
     return;
   }
-  if (n <= kSmemPoints)
-    triangulate_patch<true>(smem, xy_all, pts_off, tri_all, ntri_out, status, circ_all);
-  else
-    triangulate_patch<false>(smem, xy_all, pts_off, tri_all, ntri_out, status, circ_all);
+  // a cavity larger than the shared-memory one (rare insertion orders)
+  // restarts the patch with the global-memory mesh
+  if (n <= kSmemPoints &&
+      triangulate_patch<true>(smem, xy_all, pts_off, tri_all, ntri_out, status, scratch) !=
+          kOverflow)
+    return;
+  __syncwarp();
+  triangulate_patch<false>(smem, xy_all, pts_off, tri_all, ntri_out, status, scratch);
 }
 
 }  // namespace
@@ -270,7 +304,8 @@ delaunay_kernel(const double* __restrict__ xy_all,
 using namespace ts;
 
 extern "C" size_t ts_triangulate_scratch(int64_t total_points, int n_patches) {
-  return 3 * sizeof(double) * (size_t)(2 * total_points + 8 * (int64_t)n_patches + 8);
+  const int64_t slots = 2 * total_points + 8 * (int64_t)n_patches + 8;
+  return (size_t)(kSlotBytes * slots + kPatchBytes * (int64_t)(n_patches + 1));
 }
 
 extern "C" int ts_triangulate(const double* d_xy, const int64_t* d_pts_off,
@@ -286,7 +321,7 @@ extern "C" int ts_triangulate(const double* d_xy, const int64_t* d_pts_off,
   ts::count_launch(),
       delaunay_kernel<<<n_patches, 32, kDelaunaySmem, as_stream(stream)>>>(
           d_xy, d_pts_off, n_patches, d_tri, d_ntri, d_status,
-          reinterpret_cast<double*>(d_scratch));
+          reinterpret_cast<uint8_t*>(d_scratch));
   TS_LAUNCH_CHECK();
   return TS_OK;
 }
