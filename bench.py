@@ -607,6 +607,31 @@ def run_splat(args, dev, world, rank):
     hbm, _tf, kind = peaks()
     alg = M * 36 + P * 4096 * 32
     gbs = alg / (ms / 1e3) / 1e9
+    # the same points in a random order (the atomics worst case: no
+    # shared-memory hot patch ever forms)
+    perm = torch.randperm(M, device=dev, generator=torch.Generator(
+        device=dev).manual_seed(7))
+    xyz, rgb = xyz[perm], rgb[perm]
+    del perm
+    torch.cuda.empty_cache()
+    bake_device(xyz, rgb, centers, prior, cz, cz, prior_rgb, grid, accum)
+    torch.cuda.synchronize()
+    ts2 = []
+    for _ in range(3):
+        s, e = torch.cuda.Event(enable_timing=True), \
+            torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        bake_device(xyz, rgb, centers, prior, cz, cz, prior_rgb, grid, accum)
+        e.record(stream)
+        torch.cuda.synchronize()
+        ts2.append(s.elapsed_time(e))
+    ms2 = float(np.mean(ts2))
+    del xyz, rgb, accum
+    torch.cuda.empty_cache()
+    shuffled = {"ms_per_step": round(ms2, 4),
+                "value": round(M / (ms2 / 1e3) * world, 1),
+                "frac": round(alg / (ms2 / 1e3) / 1e9 / hbm, 4),
+                "config": "the same points in a random order"}
     return {"metric": "full-res splat points/sec",
             "value": round(M / (ms / 1e3) * world, 1), "unit": "points/s",
             "config": f"configs[2]: {M:,} points into {P} heightmaps per GPU,"
@@ -625,7 +650,8 @@ def run_splat(args, dev, world, rank):
                              "bake_dram_bytes_per_launch"),
                          "traffic_unit": "DRAM bytes, splat + finalize "
                                          "launches (ncu, "
-                                         "profiles/r01_traffic.json)"}}
+                                         "profiles/r01_traffic.json)"},
+            "shuffled": shuffled}
 
 
 # ------------------------------------------------------------ CPU legs
