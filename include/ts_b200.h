@@ -228,6 +228,20 @@ int ts_bake(const double* d_xyz, const float* d_rgb, int64_t m,
             const double* d_key_cz, const float* d_prior_rgb,
             float* d_out_h, float* d_out_rgb, void* d_accum, void* stream);
 
+/* Points in any order -> grouped by 640 m cell of the same key grid (a
+ * two-pass counting sort: cell rows, then cells), so ts_bake's shared-memory
+ * hot-patch accumulation applies
+ * to shuffled input too (bake_fullres accepts any point order,
+ * engine.py:416-456).  Points outside the grid are placed last.  Order
+ * within a cell is unspecified; ts_bake's fixed-point sums do not depend on
+ * it.  Grids up to 16,383 cells; m < 2^32.  d_rgb / d_rgb_out both NULL or
+ * both set.  d_scratch: ts_bake_bin_scratch(m, gnx, gny) bytes (0: grid
+ * too large, call ts_bake on the unsorted points).                        */
+size_t ts_bake_bin_scratch(int64_t m, int gnx, int gny);
+int ts_bake_bin(const double* d_xyz, const float* d_rgb, int64_t m, double gx0,
+                double gy0, int gnx, int gny, double* d_xyz_out, float* d_rgb_out,
+                void* d_scratch, void* stream);
+
 /* ---- WireHeightmap records (server.py:126-142 wire_heightmap,
  *      docs/wire.md "WireHeightmap") -------------------------------------
  * Per patch p, back to back at d_wire + p * ts_wire_record_size(has_rgb):

@@ -65,6 +65,8 @@ SIGNATURES = {
     "ts_conv2d": (I32, [P, I32, I32, I32, I32, P, I32, I32, P, I32, I32, I32, P,
                         P]),
     "ts_bake_workspace": (SZ, [I32]),
+    "ts_bake_bin_scratch": (SZ, [I64, I32, I32]),
+    "ts_bake_bin": (I32, [P, P, I64, F64, F64, I32, I32, P, P, P, P]),
     "ts_bake": (I32, [P, P, I64, P, I32, P, P, P, F64, F64, I32, I32, P, P, P,
                       P, P, P, P, P]),
     "ts_wire_record_size": (SZ, [I32]),

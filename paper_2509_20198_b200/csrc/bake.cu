@@ -36,6 +36,8 @@
 // shuffled input never switches and degrades to global atomics.
 #include <algorithm>
 
+#include <cub/device/device_scan.cuh>
+
 #include "tc_ptx.cuh"
 #include "ts_common.cuh"
 
@@ -368,10 +370,277 @@ bake_finalize_kernel(const uint32_t* __restrict__ cnt, const unsigned long long*
   }
 }
 
+// ---------------------------------------------------------------------------
+// Binning (ts_bake_bin): points in arbitrary order -> grouped by 640 m cell
+// of the key grid, so the splat's shared-memory hot patch forms again.  Two
+// counting-sort passes (most significant digit first): by cell row, then
+// by cell.  Each pass: per-CTA bin histograms in shared memory, a column
+// scan over CTAs, a scan over bins, then every CTA scatters its chunk
+// through shared-memory cursors.  One pass over all cells would keep
+// CTAs x cells partially written output lines in flight (4,357 cells x 592
+// CTAs: 10x the L2) and write-amplify 6x; by rows first, every CTA of the
+// second pass reads points of ~one row and writes ~gnx runs.  Points outside the grid go to the last bin (the
+// splat skips them).  Order inside a cell is not defined -- the splat's
+// fixed-point sums do not depend on it.
+constexpr int kBinThreads = 512;
+constexpr int kBinMaxCells = 16384;  // shared histogram: 64 KB
+
+// bin of a point: its cell (rows: its cell row), outside the grid -> last
+__device__ __forceinline__ int bin_cell(double x, double y, double gx0, double gy0, int gnx,
+                                        int gny, bool rows) {
+  const double fx = floor(dmul(dsub(x, gx0), 1.0 / kPatch));
+  const double fy = floor(dmul(dsub(y, gy0), 1.0 / kPatch));
+  if (!(fx >= 0.0 && fy >= 0.0 && fx < (double)gnx && fy < (double)gny))
+    return rows ? gny : gnx * gny;
+  return rows ? (int)fy : (int)fy * gnx + (int)fx;
+}
+
+struct BinArgs {
+  const double* xyz;
+  const float* rgb;
+  int64_t m, per;  // points, points per CTA
+  double gx0, gy0;
+  int gnx, gny, nb;  // nb bins: gnx * gny + 1 (cells) or gny + 1 (rows)
+  int rows;          // pass 1: bin by cell row only
+  uint32_t* hist;    // [grid][nb]: counts, then each CTA's offset within the bin
+  uint32_t* total;   // [nb]
+  uint32_t* start;   // [nb] exclusive scan of total
+  double* xyz_out;
+  float* rgb_out;
+};
+
+__global__ void __launch_bounds__(kBinThreads) bin_count_kernel(BinArgs A) {
+  extern __shared__ uint32_t s_h[];
+  for (int i = threadIdx.x; i < A.nb; i += kBinThreads) s_h[i] = 0;
+  __syncthreads();
+  const int64_t lo = (int64_t)blockIdx.x * A.per, hi = min(A.m, lo + A.per);
+  for (int64_t i0 = lo; i0 < hi; i0 += kBinThreads) {
+    const int64_t i = i0 + threadIdx.x;
+    const int bin = i < hi ? bin_cell(A.xyz[3 * i], A.xyz[3 * i + 1], A.gx0, A.gy0, A.gnx,
+                                      A.gny, A.rows)
+                           : -1;
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, bin);
+    if (bin >= 0 && (int)(threadIdx.x & 31) == __ffs(peers) - 1)
+      atomicAdd(s_h + bin, (uint32_t)__popc(peers));
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < A.nb; i += kBinThreads)
+    A.hist[(int64_t)blockIdx.x * A.nb + i] = s_h[i];
+}
+
+// per bin: exclusive prefix over CTAs (in place) and the bin total
+__global__ void bin_column_kernel(BinArgs A, int grid) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= A.nb) return;
+  uint32_t run = 0;
+  for (int g = 0; g < grid; ++g) {
+    uint32_t* h = A.hist + (int64_t)g * A.nb + c;
+    const uint32_t v = *h;
+    *h = run;
+    run += v;
+  }
+  A.total[c] = run;
+}
+
+// Scatter through a shared-memory staging tile: kBinTile points are sorted
+// by bin locally (counting sort), then written out run by run, so each
+// bin's points of the tile leave as one coalesced run instead of one
+// partial-line store per point.
+
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp) {
+  // exclusive scan of one value per thread across the block (kBinThreads)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t t = lane < kBinThreads / 32 ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < kBinThreads / 32) s_warp[lane] = t;  // inclusive warp totals
+  }
+  __syncthreads();
+  const uint32_t before = w ? s_warp[w - 1] : 0;
+  __syncthreads();
+  return before + x - v;
+}
+
+// kBinTile: 2,048 points for the row pass (two CTAs per SM), 4,096 for the
+// cell pass (its per-tile bin bookkeeping covers every cell); measured
+// 4.4 + 7.0 ms for 200 M points against 6.5 + 7.0 / 4.4 + 7.6
+template <int kBinTile>
+__global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(BinArgs A) {
+  extern __shared__ __align__(16) uint8_t s_raw[];
+  // [nb] global cursors, [nb] tile counts -> tile starts, [nb] tile fill
+  // cursors, staged points (xyz, rgb, bin) of one tile
+  uint32_t* s_cur = reinterpret_cast<uint32_t*>(s_raw);
+  uint32_t* s_cnt = s_cur + A.nb;
+  uint32_t* s_fill = s_cnt + A.nb;
+  double* s_xyz = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(s_fill + A.nb) + 15) & ~uintptr_t(15));
+  float* s_rgb = reinterpret_cast<float*>(s_xyz + 3 * kBinTile);
+  int* s_bin = reinterpret_cast<int*>(s_rgb + 3 * kBinTile);
+  __shared__ uint32_t s_warp[32];
+  for (int i = threadIdx.x; i < A.nb; i += kBinThreads)
+    s_cur[i] = A.start[i] + A.hist[(int64_t)blockIdx.x * A.nb + i];
+  const int64_t lo = (int64_t)blockIdx.x * A.per, hi = min(A.m, lo + A.per);
+  const int per_thread = (A.nb + kBinThreads - 1) / kBinThreads;
+  for (int64_t t0 = lo; t0 < hi; t0 += kBinTile) {
+    const int n = (int)(hi - t0 < kBinTile ? hi - t0 : kBinTile);
+    for (int i = threadIdx.x; i < A.nb; i += kBinThreads) s_cnt[i] = 0;
+    __syncthreads();
+    // 1. bins of the tile's points + local histogram
+    int bins[kBinTile / kBinThreads];
+#pragma unroll
+    for (int u = 0; u < kBinTile / kBinThreads; ++u) {
+      const int j = u * kBinThreads + threadIdx.x;
+      bins[u] = -1;
+      if (j < n) {
+        const int64_t i = t0 + j;
+        bins[u] = bin_cell(A.xyz[3 * i], A.xyz[3 * i + 1], A.gx0, A.gy0, A.gnx, A.gny, A.rows);
+        atomicAdd(s_cnt + bins[u], 1u);
+      }
+    }
+    __syncthreads();
+    // 2. tile starts per bin (block scan over nb bins, per_thread each)
+    uint32_t mine = 0;
+    for (int k = 0; k < per_thread; ++k) {
+      const int b = threadIdx.x * per_thread + k;
+      if (b < A.nb) mine += s_cnt[b];
+    }
+    uint32_t run = block_excl_scan(mine, s_warp);
+    for (int k = 0; k < per_thread; ++k) {
+      const int b = threadIdx.x * per_thread + k;
+      if (b < A.nb) {
+        const uint32_t c = s_cnt[b];
+        s_cnt[b] = run;  // tile start of bin b
+        s_fill[b] = run;
+        run += c;
+      }
+    }
+    __syncthreads();
+    // 3. stage the points in bin order
+#pragma unroll
+    for (int u = 0; u < kBinTile / kBinThreads; ++u) {
+      const int j = u * kBinThreads + threadIdx.x;
+      if (j < n) {
+        const int64_t i = t0 + j;
+        const uint32_t q = atomicAdd(s_fill + bins[u], 1u);
+        s_xyz[3 * q] = A.xyz[3 * i];
+        s_xyz[3 * q + 1] = A.xyz[3 * i + 1];
+        s_xyz[3 * q + 2] = A.xyz[3 * i + 2];
+        if (A.rgb) {
+          s_rgb[3 * q] = A.rgb[3 * i];
+          s_rgb[3 * q + 1] = A.rgb[3 * i + 1];
+          s_rgb[3 * q + 2] = A.rgb[3 * i + 2];
+        }
+        s_bin[q] = bins[u];
+      }
+    }
+    __syncthreads();
+    // 4. write runs: staged slot q of bin b -> global cursor[b] + (q - start[b])
+    for (int e = threadIdx.x; e < 3 * n; e += kBinThreads) {
+      const int q = e / 3, c = e - 3 * q, b = s_bin[q];
+      const uint32_t g = s_cur[b] + (uint32_t)(q - (int)s_cnt[b]);
+      A.xyz_out[3 * (int64_t)g + c] = s_xyz[e];
+      if (A.rgb) A.rgb_out[3 * (int64_t)g + c] = s_rgb[e];
+    }
+    __syncthreads();
+    for (int k = 0; k < per_thread; ++k) {  // advance the global cursors
+      const int b = threadIdx.x * per_thread + k;
+      if (b < A.nb) s_cur[b] += s_fill[b] - s_cnt[b];
+    }
+    __syncthreads();
+  }
+}
+
+size_t bin_scatter_smem(int nb, int tile) {
+  return (3 * (size_t)nb * 4 + 15) / 16 * 16 + (size_t)tile * (24 + 12 + 4);
+}
+
+int bin_grid(int64_t m) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(148 * 4, ceil_div<int64_t>(m, 4096)));
+}
+
+size_t bin_scan_bytes(int nb) {
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, (const uint32_t*)nullptr, (uint32_t*)nullptr, nb);
+  return (tmp + 255) & ~size_t(255);
+}
+
 }  // namespace
 }  // namespace ts
 
 using namespace ts;
+
+namespace {
+size_t bin_words(int64_t m, int nb) { return (size_t)bin_grid(m) * nb + 2 * (size_t)nb; }
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+}  // namespace
+
+extern "C" size_t ts_bake_bin_scratch(int64_t m, int gnx, int gny) {
+  if (m < 0 || gnx <= 0 || gny <= 0 || (int64_t)gnx * gny + 1 > kBinMaxCells) return 0;
+  const int nb = gnx * gny + 1;
+  // counters + scan temp (sized for the larger pass) + the pass-1 points
+  return align256(bin_words(m, nb) * sizeof(uint32_t)) + bin_scan_bytes(nb) +
+         align256((size_t)m * 3 * sizeof(double)) + align256((size_t)m * 3 * sizeof(float));
+}
+
+extern "C" int ts_bake_bin(const double* d_xyz, const float* d_rgb, int64_t m, double gx0,
+                           double gy0, int gnx, int gny, double* d_xyz_out, float* d_rgb_out,
+                           void* d_scratch, void* stream) {
+  if (m < 0 || gnx <= 0 || gny <= 0 || (int64_t)gnx * gny + 1 > kBinMaxCells) return TS_E_INVALID;
+  if (m >= ((int64_t)1 << 32)) return TS_E_INVALID;  // u32 positions
+  if (m == 0) return TS_OK;
+  if ((d_rgb == nullptr) != (d_rgb_out == nullptr)) return TS_E_INVALID;
+  cudaStream_t s = as_stream(stream);
+  const int ncell = gnx * gny + 1, grid = bin_grid(m);
+  uint8_t* q = reinterpret_cast<uint8_t*>(d_scratch);
+  uint32_t* w = reinterpret_cast<uint32_t*>(q);
+  q += align256(bin_words(m, ncell) * sizeof(uint32_t));
+  void* tmp = q;
+  const size_t tmp_cap = bin_scan_bytes(ncell);
+  q += tmp_cap;
+  double* mid_xyz = reinterpret_cast<double*>(q);
+  q += align256((size_t)m * 3 * sizeof(double));
+  float* mid_rgb = d_rgb ? reinterpret_cast<float*>(q) : nullptr;
+  for (int pass = 0; pass < 2; ++pass) {
+    BinArgs a{};
+    a.rows = pass == 0;
+    a.nb = a.rows ? gny + 1 : ncell;
+    a.xyz = pass == 0 ? d_xyz : mid_xyz;
+    a.rgb = pass == 0 ? d_rgb : mid_rgb;
+    a.xyz_out = pass == 0 ? mid_xyz : d_xyz_out;
+    a.rgb_out = pass == 0 ? mid_rgb : d_rgb_out;
+    a.m = m; a.per = ceil_div<int64_t>(m, grid);
+    a.gx0 = gx0; a.gy0 = gy0; a.gnx = gnx; a.gny = gny;
+    a.hist = w;
+    a.total = w + (size_t)grid * a.nb;
+    a.start = a.total + a.nb;
+    size_t tmp_bytes = tmp_cap;
+    const int smem = a.nb * (int)sizeof(uint32_t);
+    const int smem2 = (int)bin_scatter_smem(a.nb, a.rows ? 2048 : 4096);
+    TS_CUDA_TRY(cudaFuncSetAttribute(bin_count_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    TS_CUDA_TRY(cudaFuncSetAttribute(a.rows ? bin_scatter_kernel<2048> : bin_scatter_kernel<4096>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+    ts::count_launch(), bin_count_kernel<<<grid, kBinThreads, smem, s>>>(a);
+    ts::count_launch(), bin_column_kernel<<<ceil_div(a.nb, 256), 256, 0, s>>>(a, grid);
+    TS_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, a.total, a.start, a.nb, s));
+    if (a.rows) ts::count_launch(), bin_scatter_kernel<2048><<<grid, kBinThreads, smem2, s>>>(a);
+    else ts::count_launch(), bin_scatter_kernel<4096><<<grid, kBinThreads, smem2, s>>>(a);
+    TS_LAUNCH_CHECK();
+  }
+  return TS_OK;
+}
 
 extern "C" size_t ts_bake_workspace(int n_patches) {
   const size_t p = n_patches > 0 ? (size_t)n_patches : 1;

@@ -120,3 +120,37 @@ def test_bake_utm_seams_colourless():
     out = bake_fullres(xyz, None, bases, keys)
     _check(out, xyz, None, keys, bases)
     assert all(o.rgb is None for o in out)
+
+
+def test_bin_points_groups_by_cell_and_keeps_the_bake():
+    """ts_bake_bin: a permutation of the points, non-decreasing 640 m cell
+    of the key grid (outside points last), and the bake of the binned
+    points equals the bake of the shuffled ones bit for bit."""
+    from paper_2509_20198_b200 import _device as D
+    from paper_2509_20198_b200.engine import bake_device, bin_points, key_grid
+    rng = np.random.default_rng(21)
+    centers = np.stack(np.meshgrid(np.arange(5) * 640.0 + 320.0,
+                                   np.arange(4) * 640.0 + 320.0), -1).reshape(-1, 2)
+    m = 300_000
+    xyz = np.stack([rng.uniform(-700, 3900, m), rng.uniform(-700, 3300, m),
+                    rng.uniform(0, 100, m)], 1)
+    rgb = rng.random((m, 3)).astype(np.float32)
+    off, ids, gx0, gy0, gnx, gny, inner = key_grid(centers)
+    dx, dc = D.upload(xyz), D.upload(rgb)
+    bx, bc = bin_points(dx, dc, (gx0, gy0, gnx, gny))
+    bxh, bch = bx.cpu().numpy(), bc.cpu().numpy()
+    fx = np.floor((bxh[:, 0] - gx0) / 640.0)
+    fy = np.floor((bxh[:, 1] - gy0) / 640.0)
+    inside = (fx >= 0) & (fy >= 0) & (fx < gnx) & (fy < gny)
+    cell = np.where(inside, fy * gnx + fx, gnx * gny)
+    assert (np.diff(cell) >= 0).all()
+    a = np.lexsort(np.hstack([xyz, rgb]).T)
+    b = np.lexsort(np.hstack([bxh, bch]).T)
+    assert np.array_equal(xyz[a], bxh[b]) and np.array_equal(rgb[a], bch[b])
+    P = len(centers)
+    prior = torch.zeros((P, 64, 64), device="cuda")
+    prior_rgb = torch.zeros((P, 64, 64, 3), device="cuda")
+    cz = torch.full((P,), 10.0, dtype=torch.float64, device="cuda")
+    h1, c1 = bake_device(dx, dc, centers, prior, cz, cz, prior_rgb)
+    h2, c2 = bake_device(bx, bc, centers, prior, cz, cz, prior_rgb)
+    assert torch.equal(h1, h2) and torch.equal(c1, c2)
