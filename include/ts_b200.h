@@ -52,7 +52,15 @@ typedef struct ts_tile_desc {
   int32_t compressed;        /* 1 = LAZ (chunk table), 0 = LAS              */
   double scale[3];
   double offset[3];
+  /* Sparse images (the file is not uploaded whole): the image in d_bytes
+   * holds file bytes [image_base, image_base + image size); 0 = the whole
+   * file.  table_pos >= 0: the chunk-table position (the host read the
+   * 8-byte pointer, reader.py:146-157); < -1 (TS_TABLE_POS_IN_IMAGE): read
+   * the pointer from the image.  file_size is then the real file size.   */
+  int64_t image_base;
+  int64_t table_pos;
 } ts_tile_desc;
+#define TS_TABLE_POS_IN_IMAGE (-2)
 
 /* Patch key: centre of a 640 m patch (patches.py:33-53). */
 typedef struct ts_patch_key {

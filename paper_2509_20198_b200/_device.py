@@ -12,7 +12,7 @@ import ctypes as C
 import numpy as np
 import torch
 
-from ._lib import TILE_DESC, lib
+from ._lib import TABLE_POS_IN_IMAGE, TILE_DESC, lib
 from .errors import raise_for_status
 
 
@@ -91,7 +91,9 @@ class TileBatch:
 
     PAD = 64  # vector-window slack after the last image
 
-    def __init__(self, images, descs: np.ndarray):
+    def __init__(self, images, descs: np.ndarray, file_sizes=None):
+        """images: whole files, or (file_sizes given) sparse images whose
+        descs carry image_base / table_pos (ts_tile_desc)."""
         sizes = np.array([len(b) for b in images], np.int64)
         offs = np.zeros(len(images), np.int64)
         # 16-byte aligned images keep the window loads aligned per tile
@@ -103,7 +105,7 @@ class TileBatch:
             host_buf[o:o + len(b)] = np.frombuffer(b, np.uint8)
         descs = descs.copy()
         descs["file_offset"] = offs
-        descs["file_size"] = sizes
+        descs["file_size"] = sizes if file_sizes is None else file_sizes
         self.descs = descs
         self.n = len(images)
         self.bytes = upload(host_buf)
@@ -132,6 +134,8 @@ def tile_desc(header, las_stride: int = 50_000) -> np.ndarray:
     d["compressed"] = 1 if header.is_compressed else 0
     d["scale"] = header.scale
     d["offset"] = header.offset
+    d["image_base"] = 0
+    d["table_pos"] = TABLE_POS_IN_IMAGE
     return d
 
 

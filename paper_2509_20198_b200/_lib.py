@@ -31,8 +31,10 @@ TILE_DESC = np.dtype([
     ("point_data_offset", "<i8"), ("point_count", "<i8"),
     ("las_stride", "<i8"), ("chunk_size", "<u4"), ("format", "<i4"),
     ("record_length", "<i4"), ("compressed", "<i4"),
-    ("scale", "<f8", (3,)), ("offset", "<f8", (3,))], align=True)
-assert TILE_DESC.itemsize == 104
+    ("scale", "<f8", (3,)), ("offset", "<f8", (3,)),
+    ("image_base", "<i8"), ("table_pos", "<i8")], align=True)
+assert TILE_DESC.itemsize == 120
+TABLE_POS_IN_IMAGE = -2
 
 # name -> (restype, argtypes); every symbol include/ts_b200.h declares
 SIGNATURES = {

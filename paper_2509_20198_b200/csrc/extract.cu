@@ -35,14 +35,18 @@ __host__ __device__ __forceinline__ int rec_size(int fmt) {
 }
 
 // Validated chunk-table position of a LAZ tile, or a negative status.
+// f addresses file offsets (the image pointer minus image_base).
 __device__ int64_t table_position(const uint8_t* f, const ts_tile_desc& t,
                                   int32_t* status) {
   if (t.point_data_offset + 8 > t.file_size) {
     *status = TS_E_CORRUPT_TABLE;
     return -1;
   }
-  int64_t pos = load_i64_unaligned(f + t.point_data_offset);
-  if (pos == -1) pos = load_i64_unaligned(f + t.file_size - 8);
+  int64_t pos = t.table_pos;
+  if (pos < -1) {  // the pointer is in the image (reader.py:146-157)
+    pos = load_i64_unaligned(f + t.point_data_offset);
+    if (pos == -1) pos = load_i64_unaligned(f + t.file_size - 8);
+  }
   const int64_t start = t.point_data_offset + 8;
   if (!(start <= pos && pos <= t.file_size - 8)) {
     *status = TS_E_CORRUPT_TABLE;
@@ -65,7 +69,7 @@ __global__ void chunk_count_kernel(const uint8_t* __restrict__ bytes,
   } else if (!t.compressed) {
     n = t.las_stride > 0 ? (t.point_count + t.las_stride - 1) / t.las_stride : 0;
   } else {
-    const uint8_t* f = bytes + t.file_offset;
+    const uint8_t* f = bytes + t.file_offset - t.image_base;
     const int64_t pos = table_position(f, t, &st);
     if (pos >= 0) {
       const uint32_t version = load_u32_unaligned(f + pos);
@@ -113,7 +117,7 @@ __global__ void chunk_decode_kernel(const uint8_t* __restrict__ bytes,
         chunk_end[i] = t.point_data_offset + t.point_count * t.record_length;
       continue;
     }
-    const uint8_t* f = bytes + t.file_offset;
+    const uint8_t* f = bytes + t.file_offset - t.image_base;
     const int64_t pos = table_position(f, t, &st);
     const bool variable = t.chunk_size == 0xFFFFFFFFu;
     int64_t off = t.point_data_offset + 8;
@@ -204,7 +208,7 @@ extract_kernel(const uint8_t* __restrict__ bytes,
   const int fmt = t.format;
   const int rs = rec_size(fmt);
   const bool has_rgb = fmt == 2 || fmt == 3;
-  const uint8_t* f = bytes + t.file_offset;
+  const uint8_t* f = bytes + t.file_offset - t.image_base;
   if (status[ti] != TS_OK) return;
   if (rs < 0) { if (threadIdx.x == 0) status[ti] = TS_E_UNSUPPORTED_FORMAT; return; }
   // pass 1: bounds + the per-batch colour heuristic (records.py:81-85)

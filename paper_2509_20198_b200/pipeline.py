@@ -51,6 +51,16 @@ class HeightmapPipeline:
                           cell_range)
         return tables, cp, idx
 
+    def overview_staged(self, st, cell_range=None):
+        """load_overview from files: ``lasio.reader.StagedChunkPoints``
+        (tables decoded from the table bytes, first records from 64-byte
+        windows of the reference's 4 KiB-aligned preads)."""
+        cp = D.ChunkPoints(st.tb, st, records=False)
+        D.raise_item_status(cp.status.cpu().numpy(), "chunk points")
+        idx = DeviceIndex(cp.xyz[:max(cp.n, 1)], cp.rgb, cp.cells[:max(cp.n, 1)],
+                          cell_range)
+        return st, cp, idx
+
     def patches(self, idx: DeviceIndex, centers):
         """Gather + triangulate + rasterise every patch -> CNN input."""
         g = idx.gather(centers)
