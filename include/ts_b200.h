@@ -108,6 +108,23 @@ int ts_extract_chunk_points(const uint8_t* d_bytes,
                             uint8_t* d_records, double* d_xyz, float* d_rgb,
                             int64_t* d_cell, int32_t* d_status,
                             void* stream);
+/* Full chunk decode (reader.py:286-364 decode_chunk / load_tile_fullres,
+ * items.py:108-606 POINT10 / GPSTIME11 / RGB12 v2, codec.py:173-484): every
+ * record of every chunk of the tiles in d_bytes, bit-exact, one GPU thread
+ * per chunk.  Chunk tables from ts_chunk_counts / ts_chunk_decode (offsets,
+ * point counts, d_chunk_end); d_point_base[n_chunks + 1] = exclusive scan
+ * of the chunk point counts: chunk c's records land at d_records +
+ * d_point_base[c] * record size (all tiles must share the format).
+ * d_status[n_chunks]: TS_E_DESYNC (stream ran past the chunk), TS_E_OOB,
+ * TS_E_UNSUPPORTED_FORMAT (LAS tiles: read the records directly),
+ * TS_E_INVALID (more adaptive models than the per-chunk arena holds).
+ * d_scratch: ts_lazdec_scratch(n_chunks) bytes.                          */
+size_t ts_lazdec_scratch(int64_t n_chunks);
+int ts_lazdec(const uint8_t* d_bytes, const ts_tile_desc* d_tiles, int n_tiles,
+              const int64_t* d_chunk_base, const int64_t* d_chunk_offset,
+              const int64_t* d_chunk_points, const int64_t* d_chunk_end,
+              const int64_t* d_point_base, int64_t n_chunks, uint8_t* d_records,
+              int32_t* d_status, void* d_scratch, void* stream);
 /* positions()/colors() for records already in device memory
  * (records.py:62-86).  Records are rows of record_stride bytes with x,y,z
  * int32 at bytes 0,4,8 and red,green,blue uint16 at rgb_offset.

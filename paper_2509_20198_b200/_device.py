@@ -161,6 +161,36 @@ class ChunkTables:
              ptr(self.status), ptr(scratch), stream())
 
 
+class FullRecords:
+    """Every record of every chunk of a TileBatch of LAZ tiles, decoded on
+    the GPU (ts_lazdec; load_tile_fullres).  ``records`` is the packed
+    record_dtype(fmt) byte array, ``point_base`` the per-chunk record
+    offsets (tile t's records: chunks tables.base[t] .. base[t + 1])."""
+
+    def __init__(self, tb: TileBatch, tables: ChunkTables):
+        fmts = set(int(f) for f in tb.descs["format"])
+        if len(fmts) != 1:
+            raise_for_status(8, "mixed point formats")
+        self.format = fmts.pop()
+        rs = int(lib().ts_record_size(self.format))
+        if rs < 0:
+            raise_for_status(8, f"point format {self.format}")
+        n = tables.total
+        pts = tables.points[:max(n, 1)]
+        self.point_base = torch.zeros(n + 1, dtype=torch.int64, device=device())
+        if n:
+            torch.cumsum(pts[:n], 0, out=self.point_base[1:])
+        self.n_points = int(self.point_base[-1].item())   # sizes the output
+        self.records = empty((max(self.n_points, 1) * rs,), torch.uint8)
+        self.status = torch.zeros(max(n, 1), dtype=torch.int32, device=device())
+        scratch = empty((int(lib().ts_lazdec_scratch(n)),), torch.uint8)
+        call("ts_lazdec", ptr(tb.bytes), ptr(tb.d_desc), tb.n, ptr(tables.base),
+             ptr(tables.offsets), ptr(tables.points), ptr(tables.end),
+             ptr(self.point_base), n, ptr(self.records), ptr(self.status),
+             ptr(scratch), stream())
+        self.tables = tables
+
+
 class ChunkPoints:
     """Extracted chunk points of a TileBatch (ts_extract_chunk_points)."""
 

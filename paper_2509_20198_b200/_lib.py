@@ -46,6 +46,8 @@ SIGNATURES = {
     "ts_chunk_decode_scratch": (SZ, [I32]),
     "ts_chunk_decode": (I32, [P, P, I32, P, P, P, P, P, P, P]),
     "ts_extract_chunk_points": (I32, [P, P, I32, P, P, P, P, P, P, P, P]),
+    "ts_lazdec_scratch": (SZ, [I64]),
+    "ts_lazdec": (I32, [P, P, I32, P, P, P, P, P, I64, P, P, P, P]),
     "ts_positions": (I32, [P, I64, I32, P, P, P, P]),
     "ts_colors": (I32, [P, I64, I32, I32, P, P, P]),
     "ts_index_build": (I32, [P, I64, I64, I64, I64, I64, P, P, P, P]),

@@ -11,9 +11,10 @@ Drop-in for ``pkg/src/terrascout/lasio/reader.py``:
     (``ts_extract_chunk_points``, replacing :251-283); it returns the same
     structured record array, fills ``tile.chunk_refs`` like the reference
     and reads from them when they are already set,
-  * ``StagedChunkPoints`` is the batched form over many files.
-Full chunk decompression (``decode_chunk``/``load_tile_fullres``) is not
-part of the heightmap hot path.
+  * ``StagedChunkPoints`` is the batched form over many files,
+  * ``decode_chunk`` / ``load_tile_fullres`` (:286-364) decode whole chunks
+    on the GPU (``ts_lazdec``), reading the chunk
+    bytes only.
 """
 
 from __future__ import annotations
@@ -326,3 +327,97 @@ def read_chunk_points(tile: TileMeta,
     dt = record_dtype(fmt)
     raw = cp.records[:st.total * dt.itemsize].cpu().numpy()
     return raw.view(dt).copy()
+
+
+# ----------------------------------------------------------- full decode
+
+_ITEMS = {0: [6], 1: [6, 7], 2: [6, 8], 3: [6, 7, 8]}  # POINT10, GPSTIME11, RGB12
+
+
+def _check_items(tile: TileMeta):
+    """decode_chunk's item-layout checks (reader.py:294-314)."""
+    fmt = tile.header.point_record_format
+    if fmt not in DECODABLE_FORMATS:
+        raise UnsupportedFormat(f"compressed point format {fmt} not supported")
+    lz = tile.header.laszip
+    got = [t for t, _s, _v in lz.items]
+    if got != _ITEMS[fmt]:
+        raise UnsupportedFormat(f"unexpected LASzip item layout {lz.items}")
+    for _t, _s, version in lz.items:
+        if version != 2:
+            raise UnsupportedFormat(
+                f"LASzip item version {version}, only v2 is decodable")
+
+
+class _Tables:
+    """Chunk-table arrays of already known chunks (ChunkTables layout)."""
+
+    def __init__(self, D, offsets, counts, ends_per_tile, base):
+        import torch
+        self.base = D.upload(np.asarray(base, np.int64))
+        self.offsets = D.upload(np.asarray(offsets, np.int64))
+        self.points = D.upload(np.asarray(counts, np.int64))
+        self.end = D.upload(np.asarray(ends_per_tile, np.int64))
+        self.total = len(offsets)
+        self.status = torch.zeros(len(base) - 1, dtype=torch.int32, device=self.base.device)
+
+
+def decode_chunk(tile: TileMeta, chunk: ChunkRef) -> np.ndarray:
+    """One compressed chunk -> raw records (bit-exact), decoded on the GPU
+    from the chunk's bytes only (reader.py:286-344)."""
+    from .. import _device as D
+    _check_items(tile)
+    with open(tile.path, "rb") as fp:
+        fp.seek(chunk.byte_offset)
+        buf = fp.read(chunk.byte_size)
+        size = os.fstat(fp.fileno()).st_size
+    if len(buf) < chunk.byte_size:
+        raise OutOfBoundsRead("chunk extends beyond file end")
+    d = D.tile_desc(tile.header)
+    d["image_base"] = chunk.byte_offset
+    tb = D.TileBatch([buf], d, file_sizes=np.array([size], np.int64))
+    tab = _Tables(D, [chunk.byte_offset], [chunk.point_count],
+                  [chunk.byte_offset + chunk.byte_size], [0, 1])
+    fr = D.FullRecords(tb, tab)
+    D.raise_item_status(fr.status.cpu().numpy(), "decode_chunk")
+    dt = record_dtype(tile.header.point_record_format)
+    return fr.records[:fr.n_points * dt.itemsize].cpu().numpy().view(dt).copy()
+
+
+def load_tile_fullres(tile: TileMeta, max_workers: int = 4) -> np.ndarray:
+    """Every record of the tile (reader.py:347-364): LAS point block read
+    directly, LAZ chunks decoded on the GPU in parallel (one thread per
+    chunk); max_workers is accepted for the reference's signature."""
+    header = tile.header
+    if not tile.is_compressed:
+        fmt = header.point_record_format
+        dtype = record_dtype(fmt, header.point_record_length)
+        with open(tile.path, "rb") as fp:
+            fp.seek(header.point_data_offset)
+            buf = fp.read(header.point_count * dtype.itemsize)
+        if len(buf) < header.point_count * dtype.itemsize:
+            raise OutOfBoundsRead("point data truncated")
+        return np.frombuffer(buf, dtype=dtype)
+    from .. import _device as D
+    _check_laz(tile)
+    _check_items(tile)
+    refs = ensure_chunk_refs(tile)
+    if not refs:
+        return np.empty(0, dtype=record_dtype(header.point_record_format))
+    lo = refs[0].byte_offset
+    hi = max(r.byte_offset + r.byte_size for r in refs)
+    with open(tile.path, "rb") as fp:
+        size = os.fstat(fp.fileno()).st_size
+        fp.seek(lo)
+        buf = fp.read(hi - lo)   # the chunks only (header and table excluded)
+    if len(buf) < hi - lo:
+        raise OutOfBoundsRead("chunk extends beyond file end")
+    d = D.tile_desc(header)
+    d["image_base"] = lo
+    tb = D.TileBatch([buf], d, file_sizes=np.array([size], np.int64))
+    tab = _Tables(D, [r.byte_offset for r in refs], [r.point_count for r in refs],
+                  [refs[-1].byte_offset + refs[-1].byte_size], [0, len(refs)])
+    fr = D.FullRecords(tb, tab)
+    D.raise_item_status(fr.status.cpu().numpy(), "load_tile_fullres")
+    dt = record_dtype(header.point_record_format)
+    return fr.records[:fr.n_points * dt.itemsize].cpu().numpy().view(dt).copy()

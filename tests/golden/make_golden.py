@@ -359,9 +359,93 @@ def gold_wire():
     _save("wire.npz", **out)
 
 
+# ------------------------------------------------------ full chunk decode
+
+def gold_fullres(tmp):
+    """Reference-compressed LAZ files (write_laz encodes every point with the
+    reference's POINT10 / GPSTIME11 / RGB12 v2 encoders) and their
+    load_tile_fullres records (reader.py:286-364), formats 0-3, covering the
+    item coders' branches: varying returns / classes / user data / point
+    source ids (changed_values), two interleaved GPS sequences with jumps,
+    repeats and exact duplicates (the four-sequence GPS state), grey and
+    8-bit colours (RGB byte masks), fixed and variable chunking."""
+    from terrascout.lasio import load_tile_fullres
+    terrain = rsynth.FractalTerrain(seed=31)
+    rng = np.random.default_rng(31)
+    out = {}
+    k = 0
+    for i in range(8):
+        fmt = i % 4
+        n = int(rng.integers(1500, 4000))
+        rec = rsynth.sample_tile_records(terrain, 640.0 * i, 640.0, 640.0, n,
+                                         fmt, rng)
+        if i >= 4:
+            # branchy content: per-point return/class/user/source changes
+            n_ret = rng.integers(1, 4, n)
+            ret = np.minimum(n_ret, rng.integers(1, 4, n))
+            rec["bitfield"] = (ret | (n_ret << 3) |
+                               (rng.integers(0, 2, n) << 6)).astype(np.uint8)
+            rec["classification"] = rng.choice([1, 2, 3, 6, 9], n).astype(np.uint8)
+            rec["user_data"] = rng.choice([0, 0, 0, 7], n).astype(np.uint8)
+            rec["point_source_id"] = rng.choice([7, 7, 7, 8, 300], n).astype(np.uint16)
+        if fmt in (1, 3) and i >= 4:
+            # two flight lines interleaved in blocks, repeats and jumps
+            t = np.where((np.arange(n) // 37) % 2 == 0,
+                         1.0e5 + np.arange(n) * 1e-3,
+                         3.7e5 + np.arange(n) * 7e-4)
+            t[::11] = t[np.maximum(np.arange(0, n, 11) - 1, 0)]
+            t[5::97] += rng.uniform(1e3, 1e5, len(t[5::97]))
+            rec["gps_time"] = t.view(np.uint64)
+        if fmt in (2, 3) and i >= 4:
+            grey = rng.random(n) < 0.3
+            for ch in ("green", "blue"):
+                rec[ch] = np.where(grey, rec["red"], rec[ch])
+            if i == 6:
+                for ch in ("red", "green", "blue"):
+                    rec[ch] = rec[ch] >> 8
+        path = os.path.join(tmp, f"full{i}.laz")
+        if i == 5:
+            write_laz(path, rec, fmt, chunk_sizes=[400, 1, 999, n - 1400])
+        else:
+            write_laz(path, rec, fmt, chunk_size=int(rng.integers(500, 2500)))
+        tile = scan_tile(path, i)
+        full = load_tile_fullres(tile, max_workers=1)
+        assert full.tobytes() == rec.tobytes()
+        out[f"file{k}"] = np.frombuffer(open(path, "rb").read(), np.uint8)
+        out[f"rec{k}"] = np.frombuffer(full.tobytes(), np.uint8)
+        out[f"fmt{k}"] = np.array(fmt)
+        k += 1
+    out["n_files"] = np.array(k)
+    _save("fullres.npz", **out)
+
+
+def gold_fullres_big(tmp):
+    """One realistic tile for decode throughput: 4 chunks x 50,000 format-2
+    points (the reference's chunk size), compressed by the reference; the
+    expected records are pinned by their SHA-256 (5.2 MB raw)."""
+    from terrascout.lasio import load_tile_fullres
+    terrain = rsynth.FractalTerrain(seed=11)
+    rng = np.random.default_rng(12)
+    rec = rsynth.sample_tile_records(terrain, 0.0, 0.0, 640.0, 200_000, 2, rng)
+    path = os.path.join(tmp, "big.laz")
+    write_laz(path, rec, 2, chunk_size=50_000)
+    full = load_tile_fullres(scan_tile(path, 0), max_workers=1)
+    assert full.tobytes() == rec.tobytes()
+    _save("fullres_big.npz", laz=np.frombuffer(open(path, "rb").read(), np.uint8),
+          sha256=np.frombuffer(hashlib.sha256(full.tobytes()).digest(), np.uint8),
+          n=np.array(len(full)))
+
+
 if __name__ == "__main__":
     import tempfile
     with tempfile.TemporaryDirectory() as tmp:
+        if len(sys.argv) > 1:  # only the named fixtures
+            for name in sys.argv[1:]:
+                f = globals()[f"gold_{name}"]
+                f(tmp) if f.__code__.co_argcount else f()
+            sys.exit(0)
+        gold_fullres(tmp)
+        gold_fullres_big(tmp)
         gold_chunk_points(tmp)
         gold_reconstruct(tmp)
         gold_interpolate()

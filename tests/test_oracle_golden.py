@@ -143,3 +143,14 @@ def test_wire_records(golden):
                               g[f"{name}_h"][p], g[f"{name}_rgb"][p] if colour else None)
             for p in range(len(g[f"{name}_cz"])))
         assert recs == g[f"{name}_wire"].tobytes(), name
+
+
+def test_oracle_full_chunk_decode_matches_reference(golden):
+    """oracle.lazdec restates decode_chunk + the POINT10 / GPSTIME11 /
+    RGB12 v2 item decoders: bit-exact with the reference's
+    load_tile_fullres on reference-compressed files (formats 0-3)."""
+    from oracle import lazdec
+    g = golden("fullres.npz")
+    for k in range(int(g["n_files"])):
+        rec = lazdec.load_fullres(g[f"file{k}"].tobytes())
+        assert rec.tobytes() == g[f"rec{k}"].tobytes(), k
