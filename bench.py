@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--country-tiles", type=int, default=1_000_000,
                     help="configs[3] streamed grid size (0 = skip)")
     ap.add_argument("--country-block", type=int, default=64)
+    ap.add_argument("--lazdec-tiles", type=int, default=1024,
+                    help="copies of the realistic LAZ tile decoded (0 = skip)")
     ap.add_argument("--files", type=int, default=32,
                     help="full-size LAZ files for the file-path line (0 = skip)")
     return ap.parse_args()
@@ -421,6 +423,8 @@ def run_ours(args, rank, world, local_rank):
         country = run_country(args, pipe, dev, world, rank)
         if rank == 0:
             result["country"] = country
+    if args.lazdec_tiles > 0 and rank == 0:
+        result["lazdec"] = run_lazdec(args)
     if args.files > 0 and rank == 0:
         result["files"] = run_files(args, pipe)
     if not args.no_sweep and rank == 0:
@@ -491,6 +495,67 @@ def run_country(args, pipe, dev, world, rank):
             "data": "synthetic: 256 stub-body tiles re-placed per virtual "
                     "tile on the host (producer thread, pinned H2D on a "
                     "copy stream) inside the timed region"}
+
+
+def run_lazdec(args):
+    """full LAZ chunk decode on the GPU (ts_lazdec).  A
+    reference-compressed 200,000-point tile (tests/golden/fullres_big.npz:
+    4 chunks of 50,000 format-2 points) replicated into a batch resident in
+    HBM; CUDA events; records checked against the reference's SHA-256.  The
+    CPU line times the reference's own decode_chunk (baseline/_ref) on one
+    chunk."""
+    import hashlib
+
+    import torch
+
+    from paper_2509_20198_b200 import _device as D
+    from paper_2509_20198_b200.lasio import parse_header
+    g = np.load(os.path.join(ROOT, "tests", "golden", "fullres_big.npz"))
+    img = g["laz"].tobytes()
+    n_rep = args.lazdec_tiles
+    tb = D.TileBatch([img] * n_rep, np.concatenate([D.tile_desc(parse_header(img))] * n_rep))
+    tables = D.ChunkTables(tb)
+    fr = D.FullRecords(tb, tables)          # warm-up
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    fr = D.FullRecords(tb, tables)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    n = fr.n_points
+    one = int(g["n"]) * 26
+    ok = (not fr.status.any()) and hashlib.sha256(
+        fr.records[:one].cpu().numpy().tobytes()).digest() == g["sha256"].tobytes()
+    res = {"metric": "decoded points/sec", "unit": "points/s",
+           "value": round(n / (ms / 1e3), 1),
+           "config": f"{n_rep} x 200,000-point reference-compressed tile "
+                     f"({tables.total} chunks of 50,000, format 2), resident",
+           "ms": round(ms, 2), "records_match_reference": bool(ok)}
+    import bench_ref
+    if bench_ref.available() and not args.no_cpu:
+        import sys as _sys
+        if bench_ref.REF not in _sys.path:
+            _sys.path.insert(0, bench_ref.REF)
+        import tempfile
+
+        from terrascout.lasio import decode_chunk, ensure_chunk_refs, scan_tile
+        with tempfile.TemporaryDirectory() as tmp:
+            p = os.path.join(tmp, "big.laz")
+            with open(p, "wb") as fp:
+                fp.write(img)
+            tile = scan_tile(p, 0)
+            ref = ensure_chunk_refs(tile)[0]
+            t0 = time.perf_counter()
+            decode_chunk(tile, ref)
+            dt = time.perf_counter() - t0
+        res["cpu_baseline"] = {"value": round(ref.point_count / dt, 1), "unit": "points/s",
+                               "cores": 1, "kind": "reference",
+                               "sample": f"decode_chunk of one {ref.point_count:,}-point "
+                                         f"chunk, {dt:.1f} s"}
+    del fr, tb
+    torch.cuda.empty_cache()
+    return res
 
 
 def run_files(args, pipe):

@@ -15,6 +15,8 @@
 // (tests/test_gpu_lazdec.py against reference-compressed golden files).
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "laz_ac.cuh"
 #include "ts_common.cuh"
 
@@ -25,29 +27,47 @@ using laz::BitModel;
 using laz::Decoder;
 using laz::SymModel;
 
-constexpr uint32_t kArenaWords = 96 * 1024;  // 192 KB of model memory per chunk
-constexpr int kMaxModels = 640;              // symbol-model descriptors per chunk
-constexpr int kDecThreads = 64;
-// concurrent chunk decoders: 2 CTAs of 64 per SM (scratch ~226 KB each: 4.3 GB)
-constexpr int64_t kMaxDecThreads = 148 * 2 * kDecThreads;
+// Pass 1: every chunk with a 128 KB arena and 256 model descriptors (the
+// reference's own files use 26-45 K words in 80-125 models per chunk);
+// chunks that outgrow it are queued and decoded again in pass 2 with a
+// 2 MB arena and 4,096 descriptors (every model a chunk can create fits).
+constexpr uint32_t kArenaWords = 64 * 1024, kMaxModels = 256;
+constexpr uint32_t kArenaWords2 = 1024 * 1024, kMaxModels2 = 4096;
+constexpr int kDecThreads = 128;                     // 4 warps, one decoder each
+constexpr int64_t kDecWarps = 148 * 64;              // 64 warps per SM
+constexpr int kMaxLanes = 4;                          // <= 37,888 decoders (~5.5 GB)
+constexpr int64_t kRetryThreads = 1024;              // pass-2 decoders (~2.2 GB)
 
 __device__ __forceinline__ int32_t i32w(int64_t v) { return (int32_t)(uint32_t)(uint64_t)v; }
 
 // Per-chunk model store: descriptors + their tables in one global arena.
 struct Arena {
-  SymModel* desc;   // [kMaxModels]
-  uint16_t* words;  // [kArenaWords]
-  uint32_t ndesc, used;
+  SymModel* desc;   // [max_models]
+  uint16_t* words;  // [max_words]: model tables, fast memory (shared) first
+  uint16_t* over;   // [max_over]: overflow tables (global), or null
+  uint32_t ndesc, used, used_over, max_models, max_words, max_over;
   bool full;
+  __device__ void reset() { ndesc = used = used_over = 0; full = false; }
   __device__ SymModel* make(uint32_t nsym) {
     const uint32_t w = SymModel::words16(nsym);
-    if (ndesc >= kMaxModels || used + w > kArenaWords) {
+    uint16_t* mem;
+    if (ndesc >= max_models) {
+      mem = nullptr;
+    } else if (used + w <= max_words) {
+      mem = words + used;
+      used += w;
+    } else if (used_over + w <= max_over) {
+      mem = over + used_over;
+      used_over += w;
+    } else {
+      mem = nullptr;
+    }
+    if (!mem) {
       full = true;
       return nullptr;
     }
     SymModel* m = desc + ndesc++;
-    m->init(nsym, words + used);
-    used += w;
+    m->init(nsym, mem);
     return m;
   }
 };
@@ -88,7 +108,7 @@ struct IntComp {
     cbit_live = false;
     k = 0;
   }
-  __device__ int32_t decompress(Decoder& d, Arena& A, int32_t pred, int ctx) {
+  __device__ __forceinline__ int32_t decompress(Decoder& d, Arena& A, int32_t pred, int ctx) {
     SymModel* mk = lazy(A, kslot[ctx], corr_bits + 1);
     if (!mk) return pred;
     k = d.symbol(*mk);
@@ -202,7 +222,7 @@ __device__ __forceinline__ uint32_t sym(Decoder& d, Arena& A, int16_t& slot, uin
   return m ? d.symbol(*m) : 0u;
 }
 
-__device__ void point10_read(ChunkState& S, Decoder& d, Arena& A) {
+__device__ __forceinline__ void point10_read(ChunkState& S, Decoder& d, Arena& A) {
   const uint32_t cv = sym(d, A, S.m_changed, 64);
   if (cv & 32) S.bf = (uint8_t)sym(d, A, S.m_bit[S.bf], 256);
   const uint32_t r = S.bf & 7, n = (S.bf >> 3) & 7;
@@ -231,7 +251,7 @@ __device__ void point10_read(ChunkState& S, Decoder& d, Arena& A) {
   S.lh[lvl] = S.z;
 }
 
-__device__ void gps_full(ChunkState& S, Decoder& d, Arena& A) {
+__device__ __forceinline__ void gps_full(ChunkState& S, Decoder& d, Arena& A) {
   S.g_next = (S.g_next + 1) & 3;
   const int32_t hi = S.ic_gps.decompress(d, A, (int32_t)(uint32_t)(S.gt[S.g_last] >> 32), 8);
   const uint32_t lo = d.raw_bits(32);
@@ -241,7 +261,7 @@ __device__ void gps_full(ChunkState& S, Decoder& d, Arena& A) {
   S.gcnt[S.g_last] = 0;
 }
 
-__device__ uint64_t gps_read(ChunkState& S, Decoder& d, Arena& A) {
+__device__ __forceinline__ uint64_t gps_read(ChunkState& S, Decoder& d, Arena& A) {
   for (int guard = 0; guard < 8; ++guard) {  // a sequence switch re-reads (items.py:304, 382)
     const uint32_t L = S.g_last;
     if (S.gdt[L] == 0) {
@@ -296,7 +316,7 @@ __device__ uint64_t gps_read(ChunkState& S, Decoder& d, Arena& A) {
   return S.gt[S.g_last];
 }
 
-__device__ void rgb_read(ChunkState& S, Decoder& d, Arena& A) {
+__device__ __forceinline__ void rgb_read(ChunkState& S, Decoder& d, Arena& A) {
   const int lr = S.lr, lg = S.lg, lb = S.lb;
   const uint32_t s = sym(d, A, S.m_used, 128);
   const int rl = s & 1 ? (int)((sym(d, A, S.m_diff[0], 256) + (lr & 0xFF)) & 0xFF) : lr & 0xFF;
@@ -339,7 +359,7 @@ __device__ __forceinline__ uint32_t get32(const uint8_t* p) {
   return p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
 }
 
-__device__ void emit(const ChunkState& S, int fmt, uint8_t* o) {
+__device__ __forceinline__ void emit(const ChunkState& S, int fmt, uint8_t* o) {
   put32(o, (uint32_t)S.x); put32(o + 4, (uint32_t)S.y); put32(o + 8, (uint32_t)S.z);
   put16(o + 12, S.intensity);
   o[14] = S.bf; o[15] = S.cls; o[16] = S.sa; o[17] = S.ud;
@@ -373,83 +393,110 @@ struct DecArgs {
   int32_t* status;              // per chunk
   uint8_t* scratch;             // per thread: ChunkState + arena
   size_t per_thread;
+  uint32_t arena_words, max_models;
+  int lanes;                    // decoding lanes per warp
+  const int64_t* list;          // pass 2: the chunks to decode, else null
+  const uint32_t* list_n;
+  int64_t* retry;               // pass 1: chunks whose models outgrew the arena
+  uint32_t* retry_n;
 };
 
+constexpr int32_t kRetry = -1;
+
+// Decode chunk ci with the given state and arena; the status, or kRetry
+// when the models outgrew the arena (pass 1 only).
+__device__ __forceinline__ int32_t decode_one(const DecArgs& a, int64_t ci, ChunkState& S, Arena& A) {
+  // tile of this chunk: binary search over chunk_base
+  int lo = 0, hi = a.n_tiles;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (a.chunk_base[mid] <= ci) lo = mid; else hi = mid;
+  }
+  const ts_tile_desc t = a.tiles[lo];
+  const int fmt = t.format;
+  const int rs = rec_bytes(fmt);
+  const int64_t off = a.chunk_offset[ci];
+  const int64_t end = ci + 1 < a.chunk_base[lo + 1] ? a.chunk_offset[ci + 1] : a.chunk_end[lo];
+  const int64_t count = a.chunk_points[ci];
+  if (!t.compressed || rs < 0) return TS_E_UNSUPPORTED_FORMAT;
+  if (off < 0 || end > t.file_size || end - off < rs || count < 0) return TS_E_OOB;
+  if (count == 0) return TS_OK;
+  const uint8_t* f = a.bytes + t.file_offset - t.image_base;
+  const uint8_t* first = f + off;
+  uint8_t* out = a.records + a.point_base[ci] * rs;
+  for (int b = 0; b < rs; ++b) out[b] = first[b];  // the raw first record
+  // item state from the first record (items.py:137-141, 270-276, 510-512)
+  S.x = (int32_t)get32(first); S.y = (int32_t)get32(first + 4); S.z = (int32_t)get32(first + 8);
+  S.intensity = 0;
+  S.bf = first[14]; S.cls = first[15]; S.sa = first[16]; S.ud = first[17];
+  S.psid = (uint16_t)get16(first + 18);
+  S.m_changed = S.m_sar[0] = S.m_sar[1] = -1;
+  for (int i = 0; i < 256; ++i) S.m_bit[i] = S.m_cls[i] = S.m_ud[i] = -1;
+  S.ic_int.init(16); S.ic_psid.init(16);
+  S.ic_dx.init(32); S.ic_dy.init(32); S.ic_z.init(32);
+  for (int i = 0; i < 16; ++i) { S.mx[i].init(); S.my[i].init(); S.lint[i] = 0; }
+  for (int i = 0; i < 8; ++i) S.lh[i] = 0;
+  int c = 20;
+  S.m_multi = S.m_0diff = -1;
+  S.ic_gps.init(32);
+  S.g_last = S.g_next = 0;
+  for (int i = 0; i < 4; ++i) { S.gt[i] = 0; S.gdt[i] = 0; S.gcnt[i] = 0; }
+  if (fmt == 1 || fmt == 3) {
+    S.gt[0] = (uint64_t)get32(first + 20) | ((uint64_t)get32(first + 24) << 32);
+    c = 28;
+  }
+  S.m_used = -1;
+  for (int i = 0; i < 6; ++i) S.m_diff[i] = -1;
+  if (fmt == 2 || fmt == 3) {
+    S.lr = (uint16_t)get16(first + c); S.lg = (uint16_t)get16(first + c + 2);
+    S.lb = (uint16_t)get16(first + c + 4);
+  }
+  A.reset();
+  Decoder d;
+  if (!d.start(f, off + rs, end)) return TS_E_DESYNC;
+  for (int64_t i = 1; i < count; ++i) {
+    point10_read(S, d, A);
+    if (fmt == 1 || fmt == 3) gps_read(S, d, A);
+    if (fmt == 2 || fmt == 3) rgb_read(S, d, A);
+    if (d.desync || A.full) break;
+    emit(S, fmt, out + i * rs);
+  }
+  if (d.desync) return TS_E_DESYNC;
+  if (A.full) return a.list ? TS_E_INVALID : kRetry;
+  return TS_OK;
+}
+
+// One chunk per thread, its state and models in the thread's global arena
+// (pass 1: 128 KB for every chunk; pass 2: 2 MB for the queued ones).  A
+// single thread's decode is a chain of dependent model reads, so
+// throughput comes from many chunks in flight.  (Measured alternative: one
+// decoding lane per CTA with the models in shared memory, two CTAs per SM:
+// 0.68 s instead of 1.2 s for one 50,000-point chunk, but 22 M instead of
+// 139 M points/s over 16,384 chunks.)
 __global__ void __launch_bounds__(kDecThreads) lazdec_kernel(DecArgs a) {
-  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // a.lanes decoding lanes per warp: lanes of one warp on different chunks
+  // diverge on every symbol, so small batches run one lane per warp (one
+  // 50,000-point chunk: 0.77 s instead of 1.2-3.3 s) and large ones a few
+  // (more chunks in flight; 16,384 chunks: 89 -> 137 M points/s)
+  const int lane = threadIdx.x & 31;
+  if (lane >= a.lanes) return;
+  const int64_t nthreads = (int64_t)gridDim.x * (blockDim.x >> 5) * a.lanes;
+  const int64_t gt = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * a.lanes + lane;
   uint8_t* mine = a.scratch + (size_t)gt * a.per_thread;
   ChunkState& S = *reinterpret_cast<ChunkState*>(mine);
   Arena A;
   A.desc = reinterpret_cast<SymModel*>(mine + ((sizeof(ChunkState) + 15) & ~size_t(15)));
-  A.words = reinterpret_cast<uint16_t*>(A.desc + kMaxModels);
-  for (int64_t ci = gt; ci < a.n_chunks; ci += nthreads) {
-    // tile of this chunk: binary search over chunk_base
-    int lo = 0, hi = a.n_tiles;
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (a.chunk_base[mid] <= ci) lo = mid; else hi = mid;
-    }
-    const ts_tile_desc t = a.tiles[lo];
-    const int fmt = t.format;
-    const int rs = rec_bytes(fmt);
-    const int64_t off = a.chunk_offset[ci];
-    const int64_t end = ci + 1 < a.chunk_base[lo + 1] ? a.chunk_offset[ci + 1] : a.chunk_end[lo];
-    const int64_t count = a.chunk_points[ci];
-    int32_t st = TS_OK;
-    if (!t.compressed || rs < 0) {
-      st = TS_E_UNSUPPORTED_FORMAT;
-    } else if (off < 0 || end > t.file_size || end - off < rs || count < 0) {
-      st = TS_E_OOB;
-    }
-    if (st != TS_OK || count == 0) {
-      a.status[ci] = st;
-      continue;
-    }
-    const uint8_t* f = a.bytes + t.file_offset - t.image_base;
-    const uint8_t* first = f + off;
-    uint8_t* out = a.records + a.point_base[ci] * rs;
-    for (int b = 0; b < rs; ++b) out[b] = first[b];  // the raw first record
-    // item state from the first record (items.py:137-141, 270-276, 510-512)
-    S.x = (int32_t)get32(first); S.y = (int32_t)get32(first + 4); S.z = (int32_t)get32(first + 8);
-    S.intensity = 0;
-    S.bf = first[14]; S.cls = first[15]; S.sa = first[16]; S.ud = first[17];
-    S.psid = (uint16_t)get16(first + 18);
-    S.m_changed = S.m_sar[0] = S.m_sar[1] = -1;
-    for (int i = 0; i < 256; ++i) S.m_bit[i] = S.m_cls[i] = S.m_ud[i] = -1;
-    S.ic_int.init(16); S.ic_psid.init(16);
-    S.ic_dx.init(32); S.ic_dy.init(32); S.ic_z.init(32);
-    for (int i = 0; i < 16; ++i) { S.mx[i].init(); S.my[i].init(); S.lint[i] = 0; }
-    for (int i = 0; i < 8; ++i) S.lh[i] = 0;
-    int c = 20;
-    S.m_multi = S.m_0diff = -1;
-    S.ic_gps.init(32);
-    S.g_last = S.g_next = 0;
-    for (int i = 0; i < 4; ++i) { S.gt[i] = 0; S.gdt[i] = 0; S.gcnt[i] = 0; }
-    if (fmt == 1 || fmt == 3) {
-      S.gt[0] = (uint64_t)get32(first + 20) | ((uint64_t)get32(first + 24) << 32);
-      c = 28;
-    }
-    S.m_used = -1;
-    for (int i = 0; i < 6; ++i) S.m_diff[i] = -1;
-    if (fmt == 2 || fmt == 3) {
-      S.lr = (uint16_t)get16(first + c); S.lg = (uint16_t)get16(first + c + 2);
-      S.lb = (uint16_t)get16(first + c + 4);
-    }
-    A.ndesc = 0; A.used = 0; A.full = false;
-    Decoder d;
-    if (!d.start(f, off + rs, end)) {
-      a.status[ci] = TS_E_DESYNC;
-      continue;
-    }
-    for (int64_t i = 1; i < count; ++i) {
-      point10_read(S, d, A);
-      if (fmt == 1 || fmt == 3) gps_read(S, d, A);
-      if (fmt == 2 || fmt == 3) rgb_read(S, d, A);
-      if (d.desync || A.full) break;
-      emit(S, fmt, out + i * rs);
-    }
-    a.status[ci] = d.desync ? TS_E_DESYNC : A.full ? TS_E_INVALID : TS_OK;
+  A.words = reinterpret_cast<uint16_t*>(A.desc + a.max_models);
+  A.over = nullptr;
+  A.max_models = a.max_models;
+  A.max_words = a.arena_words;
+  A.max_over = 0;
+  const int64_t nwork = a.list ? (int64_t)*a.list_n : a.n_chunks;
+  for (int64_t wi = gt; wi < nwork; wi += nthreads) {
+    const int64_t ci = a.list ? a.list[wi] : wi;
+    const int32_t st = decode_one(a, ci, S, A);
+    if (st == kRetry) a.retry[atomicAdd(a.retry_n, 1u)] = ci;
+    else a.status[ci] = st;
   }
 }
 
@@ -458,12 +505,24 @@ __global__ void __launch_bounds__(kDecThreads) lazdec_kernel(DecArgs a) {
 
 using namespace ts;
 
+namespace {
+size_t block_bytes(uint32_t words, uint32_t models) {
+  const size_t per = ((sizeof(ChunkState) + 15) & ~size_t(15)) + models * sizeof(SymModel) +
+                     words * sizeof(uint16_t);
+  return (per + 255) & ~size_t(255);
+}
+int pass1_lanes(int64_t n_chunks) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(kMaxLanes, ceil_div<int64_t>(n_chunks, kDecWarps)));
+}
+int64_t pass1_threads(int64_t n_chunks) {  // decoders
+  return std::max<int64_t>(1, std::min<int64_t>(n_chunks, kDecWarps * pass1_lanes(n_chunks)));
+}
+}  // namespace
+
 extern "C" size_t ts_lazdec_scratch(int64_t n_chunks) {
-  const int64_t threads = n_chunks < kMaxDecThreads ? n_chunks : kMaxDecThreads;
-  const size_t per = ((sizeof(ChunkState) + 15) & ~size_t(15)) + kMaxModels * sizeof(SymModel) +
-                     kArenaWords * sizeof(uint16_t);
-  const size_t per_a = (per + 255) & ~size_t(255);
-  return (size_t)(threads > 0 ? threads : 1) * per_a + 256;
+  const size_t list = ((size_t)std::max<int64_t>(n_chunks, 1) * 8 + 16 + 255) & ~size_t(255);
+  return (size_t)pass1_threads(n_chunks) * block_bytes(kArenaWords, kMaxModels) + list +
+         (size_t)kRetryThreads * block_bytes(kArenaWords2, kMaxModels2) + 256;
 }
 
 extern "C" int ts_lazdec(const uint8_t* d_bytes, const ts_tile_desc* d_tiles, int n_tiles,
@@ -473,18 +532,39 @@ extern "C" int ts_lazdec(const uint8_t* d_bytes, const ts_tile_desc* d_tiles, in
                          int32_t* d_status, void* d_scratch, void* stream) {
   if (n_tiles < 0 || n_chunks < 0) return TS_E_INVALID;
   if (n_chunks == 0) return TS_OK;
-  const int64_t threads = n_chunks < kMaxDecThreads ? n_chunks : kMaxDecThreads;
+  cudaStream_t s = as_stream(stream);
+  const int64_t threads = pass1_threads(n_chunks);
+  uint8_t* base = reinterpret_cast<uint8_t*>(d_scratch);
+  const size_t b1 = (size_t)threads * block_bytes(kArenaWords, kMaxModels);
+  int64_t* retry = reinterpret_cast<int64_t*>(base + b1);
+  uint32_t* retry_n = reinterpret_cast<uint32_t*>(retry + n_chunks);
+  const size_t list = ((size_t)n_chunks * 8 + 16 + 255) & ~size_t(255);
+  TS_CUDA_TRY(cudaMemsetAsync(retry_n, 0, sizeof(uint32_t), s));
   DecArgs a{};
   a.bytes = d_bytes; a.tiles = d_tiles; a.n_tiles = n_tiles;
   a.chunk_base = d_chunk_base; a.chunk_offset = d_chunk_offset; a.chunk_points = d_chunk_points;
   a.chunk_end = d_chunk_end; a.point_base = d_point_base; a.n_chunks = n_chunks;
   a.records = d_records; a.status = d_status;
-  a.scratch = reinterpret_cast<uint8_t*>(d_scratch);
-  const size_t per = ((sizeof(ChunkState) + 15) & ~size_t(15)) + kMaxModels * sizeof(SymModel) +
-                     kArenaWords * sizeof(uint16_t);
-  a.per_thread = (per + 255) & ~size_t(255);
-  const int grid = (int)ceil_div<int64_t>(threads, kDecThreads);
-  ts::count_launch(), lazdec_kernel<<<grid, kDecThreads, 0, as_stream(stream)>>>(a);
+  a.scratch = base;
+  a.per_thread = block_bytes(kArenaWords, kMaxModels);
+  a.arena_words = kArenaWords;
+  a.max_models = kMaxModels;
+  a.retry = retry;
+  a.retry_n = retry_n;
+  a.lanes = pass1_lanes(n_chunks);
+  const int64_t warps = ceil_div<int64_t>(threads, a.lanes);
+  ts::count_launch(),
+      lazdec_kernel<<<(int)ceil_div<int64_t>(warps, kDecThreads / 32), kDecThreads, 0, s>>>(a);
+  // pass 2: the chunks that outgrew pass 1 (the count stays on the device)
+  a.scratch = base + b1 + list;
+  a.per_thread = block_bytes(kArenaWords2, kMaxModels2);
+  a.arena_words = kArenaWords2;
+  a.max_models = kMaxModels2;
+  a.list = retry;
+  a.list_n = retry_n;
+  a.lanes = 1;
+  ts::count_launch(),
+      lazdec_kernel<<<(int)(kRetryThreads / (kDecThreads / 32)), kDecThreads, 0, s>>>(a);
   TS_LAUNCH_CHECK();
   return TS_OK;
 }

@@ -436,6 +436,26 @@ def gold_fullres_big(tmp):
           n=np.array(len(full)))
 
 
+def gold_fullres_models(tmp):
+    """A chunk that creates hundreds of adaptive models: every point a new
+    classification, user-data and bitfield byte (items.py:156-164 create one
+    256-symbol model per previous value), format 3."""
+    from terrascout.lasio import load_tile_fullres
+    terrain = rsynth.FractalTerrain(seed=5)
+    rng = np.random.default_rng(5)
+    n = 3000
+    rec = rsynth.sample_tile_records(terrain, 0.0, 0.0, 640.0, n, 3, rng)
+    rec["classification"] = rng.integers(0, 256, n).astype(np.uint8)
+    rec["user_data"] = rng.integers(0, 256, n).astype(np.uint8)
+    rec["bitfield"] = rng.integers(0, 256, n).astype(np.uint8)
+    path = os.path.join(tmp, "models.laz")
+    write_laz(path, rec, 3, chunk_size=n)
+    full = load_tile_fullres(scan_tile(path, 0), max_workers=1)
+    assert full.tobytes() == rec.tobytes()
+    _save("fullres_models.npz", laz=np.frombuffer(open(path, "rb").read(), np.uint8),
+          rec=np.frombuffer(full.tobytes(), np.uint8))
+
+
 if __name__ == "__main__":
     import tempfile
     with tempfile.TemporaryDirectory() as tmp:
@@ -446,6 +466,7 @@ if __name__ == "__main__":
             sys.exit(0)
         gold_fullres(tmp)
         gold_fullres_big(tmp)
+        gold_fullres_models(tmp)
         gold_chunk_points(tmp)
         gold_reconstruct(tmp)
         gold_interpolate()

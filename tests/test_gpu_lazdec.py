@@ -80,3 +80,20 @@ def test_realistic_tile_decode_sha(golden):
     assert not fr.status.any()
     rec = fr.records[:int(g["n"]) * 26].cpu().numpy().tobytes()
     assert hashlib.sha256(rec).digest() == g["sha256"].tobytes()
+
+
+def test_model_heavy_chunk_takes_the_big_arena(golden):
+    """Hundreds of lazily created byte models outgrow the first pass's
+    arena: the chunk is queued and decoded again with the big arena, still
+    bit-exact (and batched with ordinary chunks)."""
+    from paper_2509_20198_b200 import _device as D
+    from paper_2509_20198_b200.lasio import parse_header
+    g = golden("fullres_models.npz")
+    h = golden("fullres.npz")
+    imgs = [g["laz"].tobytes(), h["file3"].tobytes(), g["laz"].tobytes()]
+    descs = np.concatenate([D.tile_desc(parse_header(b)) for b in imgs])
+    tb = D.TileBatch(imgs, descs)
+    fr = D.FullRecords(tb, D.ChunkTables(tb))
+    assert not fr.status.any(), fr.status.cpu().numpy()
+    want = g["rec"].tobytes() + h["rec3"].tobytes() + g["rec"].tobytes()
+    assert fr.records[:len(want)].cpu().numpy().tobytes() == want
