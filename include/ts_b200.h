@@ -280,6 +280,41 @@ int ts_wire_heightmaps(const float* d_out, const double* d_cz, const int32_t* d_
                        const uint8_t* d_stage, int has_rgb, int batch,
                        uint8_t* d_wire, void* stream);
 
+/* ---- rendering (render.py:25-268, geometry.py:71-102) ------------------
+ * A framebuffer is width x height uint64 min keys (EMPTY = all ones):
+ * key = depth_key(eye depth) << 32 | 0xRRGGBBAA, merged with atomicMin, so
+ * the image is independent of submission order.  The camera is the
+ * reference's CameraState reduced on the host: position, the basis() unit
+ * vectors, f = 1/tan(fov_y/2), f / aspect, near, far, viewport.          */
+typedef struct ts_camera {
+  double pos[3], right[3], up[3], fwd[3];
+  double f, f_over_aspect, near, far;
+  int32_t width, height;
+} ts_camera;
+/* rasterize_points (render.py:55-98): one fragment per in-frustum point;
+ * d_rgb (n,3) float32 in [0,1] or NULL (every point grey_color, the
+ * reference's pack_color(0.85 grey)).                                    */
+int ts_render_points(const double* d_xyz, const float* d_rgb, int64_t n,
+                     const ts_camera* cam, uint32_t grey_color, uint64_t* d_fb,
+                     void* stream);
+/* rasterize_heightmaps (render.py:101-239): patch_mesh triangles of each
+ * refined patch (heights_rel P x 64 x 64 float32 + c_z, centres P x 2),
+ * quad colours from rgb (P x 64 x 64 x 3, used where d_has_rgb[p]) or the
+ * height shade; small / large triangle paths with identical per-pixel
+ * arithmetic.  d_scratch: ts_render_heightmaps_scratch(P) bytes.         */
+size_t ts_render_heightmaps_scratch(int n_patches);
+int ts_render_heightmaps(const float* d_heights, const float* d_rgb,
+                         const uint8_t* d_has_rgb, const double* d_center,
+                         const double* d_cz, int n_patches, const ts_camera* cam,
+                         uint64_t* d_fb, void* d_scratch, void* stream);
+/* resolve (render.py:254-268): colour bytes of each key through the sRGB
+ * table (the reference's _srgb_lut), background where empty; RGBA8.      */
+typedef struct ts_srgb_lut {
+  uint8_t v[256];
+} ts_srgb_lut;
+int ts_render_resolve(const uint64_t* d_fb, int64_t n_cells, const ts_srgb_lut* lut,
+                      const uint8_t background[3], uint8_t* d_rgba, void* stream);
+
 /* ---- test hooks (host-callable, no GPU needed) ------------------------ */
 /* Sign of the exact incircle / orientation determinants used by
  * ts_triangulate: returns -1, 0, +1.                                     */

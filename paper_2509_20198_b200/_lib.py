@@ -75,6 +75,10 @@ SIGNATURES = {
                       P, P, P, P, P]),
     "ts_wire_record_size": (SZ, [I32]),
     "ts_wire_heightmaps": (I32, [P, P, P, P, I32, I32, P, P]),
+    "ts_render_points": (I32, [P, P, I64, P, C.c_uint32, P, P]),
+    "ts_render_heightmaps_scratch": (SZ, [I32]),
+    "ts_render_heightmaps": (I32, [P, P, P, P, P, I32, P, P, P, P]),
+    "ts_render_resolve": (I32, [P, I64, P, P, P, P]),
     "ts_incircle_sign": (I32, [P, P, P, P]),
     "ts_orient_sign": (I32, [P, P, P]),
     "ts_predicates_device": (I32, [P, I64, I32, P, P]),

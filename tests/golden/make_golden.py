@@ -456,6 +456,68 @@ def gold_fullres_models(tmp):
           rec=np.frombuffer(full.tobytes(), np.uint8))
 
 
+def gold_render(tmp):
+    """Framebuffers of the reference renderer (render.py:55-239, geometry.py
+    projection / depth keys): random points (with and without colour) and
+    refined heightmaps (coloured and shaded) under a top-down, an oblique
+    and a close-up camera, plus resolve()."""
+    from terrascout.geometry import CameraState, fit_overview
+    from terrascout.patches import PatchKey
+    from terrascout.refiner import RefinedPatch
+    from terrascout.render import (Framebuffer, rasterize_heightmaps,
+                                   rasterize_points, resolve)
+    rng = np.random.default_rng(2024)
+    cams = {
+        "top": fit_overview((0, 0, 0), (1280, 1280, 120), (128, 96)),
+        "oblique": CameraState.from_yaw_pitch((-300.0, -250.0, 420.0),
+                                              np.deg2rad(40), np.deg2rad(-35),
+                                              np.deg2rad(55), (160, 120)),
+        "close": CameraState.from_yaw_pitch((300.0, 280.0, 95.0),
+                                            np.deg2rad(15), np.deg2rad(-60),
+                                            np.deg2rad(70), (200, 150),
+                                            near=0.5, far=5000.0),
+    }
+    out = {}
+    pts = np.stack([rng.uniform(-100, 1400, 30000), rng.uniform(-100, 1400, 30000),
+                    rng.uniform(0, 140, 30000)], 1)
+    rgb = rng.random((30000, 3)).astype(np.float32)
+    out["pts"] = pts
+    out["rgb"] = rgb
+    patches = []
+    for j in range(2):
+        for i in range(2):
+            c_z = float(40 + 10 * i + 5 * j)
+            xs = (np.arange(64) + 0.5) * 10.0
+            h = (20 * np.sin(xs[None, :] / 90.0 + i) * np.cos(xs[:, None] / 70.0 + j)
+                 + rng.normal(0, 0.5, (64, 64))).astype(np.float32)
+            col = rng.random((64, 64, 3)).astype(np.float32) if (i + j) % 2 == 0 else None
+            key = PatchKey(i, j, (640.0 * i + 320.0, 640.0 * j + 320.0), c_z)
+            patches.append(RefinedPatch(key=key, heights_rel=h, rgb=col, provenance="refined"))
+            out[f"hm{2 * j + i}"] = h
+            out[f"cz{2 * j + i}"] = np.array(c_z)
+            out[f"key{2 * j + i}"] = np.array([i, j, 640.0 * i + 320.0, 640.0 * j + 320.0])
+            if col is not None:
+                out[f"col{2 * j + i}"] = col
+    for name, cam in cams.items():
+        out[f"cam_{name}"] = np.concatenate([cam.position, cam.direction,
+                                             [cam.fov_y, cam.viewport[0], cam.viewport[1],
+                                              cam.near, cam.far]])
+        w, h = cam.viewport
+        fb = Framebuffer(w, h)
+        rasterize_points(pts, rgb, cam, fb)
+        out[f"fb_pts_{name}"] = fb.cells.copy()
+        fb = Framebuffer(w, h)
+        rasterize_points(pts[:5000], None, cam, fb)
+        out[f"fb_grey_{name}"] = fb.cells.copy()
+        fb = Framebuffer(w, h)
+        rasterize_heightmaps(patches, cam, fb)
+        out[f"fb_hm_{name}"] = fb.cells.copy()
+        rasterize_points(pts, rgb, cam, fb)
+        out[f"fb_both_{name}"] = fb.cells.copy()
+        out[f"img_{name}"] = resolve(fb)
+    _save("render.npz", **out)
+
+
 if __name__ == "__main__":
     import tempfile
     with tempfile.TemporaryDirectory() as tmp:
@@ -467,6 +529,7 @@ if __name__ == "__main__":
         gold_fullres(tmp)
         gold_fullres_big(tmp)
         gold_fullres_models(tmp)
+        gold_render(tmp)
         gold_chunk_points(tmp)
         gold_reconstruct(tmp)
         gold_interpolate()

@@ -154,3 +154,35 @@ def test_oracle_full_chunk_decode_matches_reference(golden):
     for k in range(int(g["n_files"])):
         rec = lazdec.load_fullres(g[f"file{k}"].tobytes())
         assert rec.tobytes() == g[f"rec{k}"].tobytes(), k
+
+
+def _render_scene(g):
+    from oracle import render as orender
+    patches = []
+    for k in range(4):
+        key = g[f"key{k}"]
+        patches.append((g[f"hm{k}"], g[f"col{k}"] if f"col{k}" in g else None,
+                        (float(key[2]), float(key[3])), float(g[f"cz{k}"])))
+    return orender, patches
+
+
+def test_oracle_render_matches_reference(golden):
+    """oracle.render restates render.py / geometry.py projection with the
+    same numpy expressions: framebuffers bit-identical to the reference."""
+    g = golden("render.npz")
+    orender, patches = _render_scene(g)
+    for name in ("top", "oblique", "close"):
+        cam = orender.Camera(g[f"cam_{name}"])
+        w, h = cam.viewport
+        fb = orender.new_fb(w, h)
+        orender.rasterize_points(g["pts"], g["rgb"], cam, fb)
+        assert np.array_equal(fb, g[f"fb_pts_{name}"]), name
+        fb = orender.new_fb(w, h)
+        orender.rasterize_points(g["pts"][:5000], None, cam, fb)
+        assert np.array_equal(fb, g[f"fb_grey_{name}"]), name
+        fb = orender.new_fb(w, h)
+        orender.rasterize_heightmaps(patches, cam, fb)
+        assert np.array_equal(fb, g[f"fb_hm_{name}"]), name
+        orender.rasterize_points(g["pts"], g["rgb"], cam, fb)
+        assert np.array_equal(fb, g[f"fb_both_{name}"]), name
+        assert np.array_equal(orender.resolve(fb), g[f"img_{name}"]), name
