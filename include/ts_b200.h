@@ -315,6 +315,18 @@ typedef struct ts_srgb_lut {
 int ts_render_resolve(const uint64_t* d_fb, int64_t n_cells, const ts_srgb_lut* lut,
                       const uint8_t background[3], uint8_t* d_rgba, void* stream);
 
+/* projected_bbox_area (geometry.py:128-164) of n boxes (n x 6 float64:
+ * min xyz, max xyz) -> screen-space AABB area and diagonal, 0 for boxes
+ * outside the frustum (the six inward planes of frustum_planes,
+ * geometry.py:105-125, computed on the host).  The scheduler's viewpoint
+ * priorities (engine.py:185-202) for every patch and tile in one launch. */
+typedef struct ts_frustum {
+  double plane[6][4];
+} ts_frustum;
+int ts_bbox_areas(const double* d_boxes, int64_t n, const ts_camera* cam,
+                  const ts_frustum* frustum, double* d_area, double* d_diag,
+                  void* stream);
+
 /* ---- test hooks (host-callable, no GPU needed) ------------------------ */
 /* Sign of the exact incircle / orientation determinants used by
  * ts_triangulate: returns -1, 0, +1.                                     */

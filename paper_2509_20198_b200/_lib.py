@@ -79,6 +79,7 @@ SIGNATURES = {
     "ts_render_heightmaps_scratch": (SZ, [I32]),
     "ts_render_heightmaps": (I32, [P, P, P, P, P, I32, P, P, P, P]),
     "ts_render_resolve": (I32, [P, I64, P, P, P, P]),
+    "ts_bbox_areas": (I32, [P, I64, P, P, P, P, P]),
     "ts_incircle_sign": (I32, [P, P, P, P]),
     "ts_orient_sign": (I32, [P, P, P]),
     "ts_predicates_device": (I32, [P, I64, I32, P, P]),

@@ -236,10 +236,70 @@ __global__ void resolve_kernel(const unsigned long long* __restrict__ fb, int64_
   }
 }
 
+// projected_bbox_area (geometry.py:128-164) for many boxes: 0 when all
+// eight corners are behind one frustum plane, else the screen-space AABB
+// of the corners (depth clamped to near) -> (area, diagonal)
+__global__ void bbox_area_kernel(const double* __restrict__ boxes, int64_t n, ts_camera c,
+                                 ts_frustum fr, double* __restrict__ area,
+                                 double* __restrict__ diag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double* b = boxes + 6 * i;
+    double cx[8], cy[8], cz[8];
+    for (int k = 0; k < 8; ++k) {  // meshgrid(..., indexing="ij") corner order
+      cx[k] = b[(k >> 2) & 1 ? 3 : 0];
+      cy[k] = b[(k >> 1) & 1 ? 4 : 1];
+      cz[k] = b[k & 1 ? 5 : 2];
+    }
+    bool outside = false;
+    for (int p = 0; p < 6 && !outside; ++p) {
+      bool all_behind = true;
+      for (int k = 0; k < 8; ++k) {
+        const double v = dadd(dadd(dadd(dmul(cx[k], fr.plane[p][0]), dmul(cy[k], fr.plane[p][1])),
+                                   dmul(cz[k], fr.plane[p][2])),
+                              fr.plane[p][3]);
+        all_behind = all_behind && v < 0.0;
+      }
+      outside = all_behind;
+    }
+    if (outside) {
+      area[i] = 0.0;
+      diag[i] = 0.0;
+      continue;
+    }
+    double xlo = 1e308, xhi = -1e308, ylo = 1e308, yhi = -1e308;
+    for (int k = 0; k < 8; ++k) {
+      const double d[3] = {dsub(cx[k], c.pos[0]), dsub(cy[k], c.pos[1]), dsub(cz[k], c.pos[2])};
+      const double xe = dot3(d, c.right), ye = dot3(d, c.up);
+      const double ze = fmax(dot3(d, c.fwd), c.near);
+      const double px = dmul(dadd(dmul(ddiv(dmul(xe, c.f_over_aspect), ze), 0.5), 0.5),
+                             (double)c.width);
+      const double py = dmul(dsub(0.5, dmul(ddiv(dmul(ye, c.f), ze), 0.5)), (double)c.height);
+      xlo = fmin(xlo, px); xhi = fmax(xhi, px);
+      ylo = fmin(ylo, py); yhi = fmax(yhi, py);
+    }
+    const double w = dsub(xhi, xlo), h = dsub(yhi, ylo);
+    area[i] = dmul(w, h);
+    diag[i] = hypot(w, h);
+  }
+}
+
 }  // namespace
 }  // namespace ts
 
 using namespace ts;
+
+extern "C" int ts_bbox_areas(const double* d_boxes, int64_t n, const ts_camera* cam,
+                             const ts_frustum* frustum, double* d_area, double* d_diag,
+                             void* stream) {
+  if (!cam || !frustum || n < 0) return TS_E_INVALID;
+  if (n == 0) return TS_OK;
+  const int grid = (int)std::min<int64_t>(ceil_div<int64_t>(n, 256), 148 * 16);
+  ts::count_launch(), bbox_area_kernel<<<grid, 256, 0, as_stream(stream)>>>(
+      d_boxes, n, *cam, *frustum, d_area, d_diag);
+  TS_LAUNCH_CHECK();
+  return TS_OK;
+}
 
 extern "C" int ts_render_points(const double* d_xyz, const float* d_rgb, int64_t n,
                                 const ts_camera* cam, uint32_t grey_color, uint64_t* d_fb,

@@ -518,6 +518,73 @@ def gold_render(tmp):
     _save("render.npz", **out)
 
 
+def gold_engine(tmp):
+    """The reference ScoutEngine end to end on a 3 x 3 corpus of real
+    (reference-compressed) LAZ tiles, like tests/conftest.py small_dataset:
+    (A) overview camera, random seed-3 bundle, batch_max 64 -- configs[0]'s
+    driver; (B) the close-up of test_baked_patches_survive_eviction with
+    the identity bundle -- tile loads (full chunk decode), bakes, eviction.
+    Records priorities, task counts, stages, ready events and every refined
+    patch."""
+    import glob
+
+    from terrascout.engine import Dataset, EngineConfig, ScoutEngine, Stage
+    from terrascout.geometry import CameraState
+    from terrascout.synth import FractalTerrain, generate_corpus
+    d = os.path.join(tmp, "engine_corpus")
+    generate_corpus(d, n_tiles=9, points_per_tile=4000, seed=11, point_format=2,
+                    chunk_size=250, terrain=FractalTerrain(seed=11))
+    paths = sorted(glob.glob(os.path.join(d, "*.laz")))
+    out = {"n_files": np.array(len(paths))}
+    for k, pth in enumerate(paths):
+        out[f"file{k}"] = np.frombuffer(open(pth, "rb").read(), np.uint8)
+        out[f"name{k}"] = np.array(os.path.basename(pth))
+
+    def record(tag, eng, n_tasks, pre_prio):
+        pids = sorted(eng.patches)
+        out[f"{tag}_pids"] = np.array(pids, np.int64)
+        out[f"{tag}_prio"] = np.array([pre_prio[p] for p in pids])
+        out[f"{tag}_stage"] = np.array([int(eng.patches[p].stage) for p in pids])
+        out[f"{tag}_nodata"] = np.array([eng.patches[p].no_data for p in pids])
+        out[f"{tag}_tasks"] = np.array(n_tasks)
+        out[f"{tag}_events"] = np.array([(i, j, int(s)) for (i, j), s in eng.ready_events],
+                                        np.int64).reshape(-1, 3)
+        for p in pids:
+            r = eng.refined.get(p)
+            if r is not None:
+                out[f"{tag}_h_{p[0]}_{p[1]}"] = r.heights_rel
+                out[f"{tag}_prov_{p[0]}_{p[1]}"] = np.array(r.provenance)
+                if r.rgb is not None:
+                    out[f"{tag}_rgb_{p[0]}_{p[1]}"] = r.rgb
+        out[f"{tag}_tile_state"] = np.array([int(eng.tiles[t].state) for t in sorted(eng.tiles)])
+        out[f"{tag}_tile_wanted"] = np.array([eng.tiles[t].wanted for t in sorted(eng.tiles)])
+
+    ds = Dataset.scan(paths)
+    eng = ScoutEngine(ds, EngineConfig(batch_max=64), random_weights(default_descriptor(), seed=3))
+    eng.load_overview()
+    prio = {p: s.priority for p, s in eng.patches.items()}
+    n = eng.run_until_idle()
+    record("A", eng, n, prio)
+
+    ds = Dataset.scan(paths)
+    eng = ScoutEngine(ds)
+    eng.load_overview()
+    t = ds.tiles[4]
+    cx = (t.header.bbox_min[0] + t.header.bbox_max[0]) / 2
+    cy = (t.header.bbox_min[1] + t.header.bbox_max[1]) / 2
+    cam = CameraState(position=np.array([cx, cy, 100.0]), direction=np.array([0.0, 0.3, -0.95]),
+                      fov_y=np.deg2rad(60), viewport=(800, 600), near=0.5, far=10000.0)
+    out["B_cam"] = np.concatenate([cam.position, cam.direction,
+                                   [cam.fov_y, 800, 600, 0.5, 10000.0]])
+    eng.update_viewpoint(cam)
+    prio = {p: s.priority for p, s in eng.patches.items()}
+    out["B_tile_prio"] = np.array([eng.tiles[t].priority for t in sorted(eng.tiles)])
+    n = eng.run_until_idle()
+    assert any(s.stage == Stage.FULLRES_BAKED for s in eng.patches.values())
+    record("B", eng, n, prio)
+    _save("engine.npz", **out)
+
+
 if __name__ == "__main__":
     import tempfile
     with tempfile.TemporaryDirectory() as tmp:
@@ -530,6 +597,7 @@ if __name__ == "__main__":
         gold_fullres_big(tmp)
         gold_fullres_models(tmp)
         gold_render(tmp)
+        gold_engine(tmp)
         gold_chunk_points(tmp)
         gold_reconstruct(tmp)
         gold_interpolate()
