@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--country-block", type=int, default=64)
     ap.add_argument("--lazdec-tiles", type=int, default=1024,
                     help="copies of the realistic LAZ tile decoded (0 = skip)")
+    ap.add_argument("--sched-patches", type=int, default=1_000_000,
+                    help="patch grid of the scheduler line (0 = skip)")
     ap.add_argument("--files", type=int, default=32,
                     help="full-size LAZ files for the file-path line (0 = skip)")
     return ap.parse_args()
@@ -427,6 +429,8 @@ def run_ours(args, rank, world, local_rank):
         result["lazdec"] = run_lazdec(args)
     if args.files > 0 and rank == 0:
         result["files"] = run_files(args, pipe)
+    if args.sched_patches > 0 and rank == 0:
+        result["scheduler"] = run_scheduler(args)
     if not args.no_sweep and rank == 0:
         result["cnn_sweep"] = cnn_sweep(bundle, cnn_in_of(pipe, tb, centers,
                                                           cell_range), dev)
@@ -555,6 +559,80 @@ def run_lazdec(args):
                                          f"chunk, {dt:.1f} s"}
     del fr, tb
     torch.cuda.empty_cache()
+    return res
+
+
+def _sched_engine(mod, side):
+    """A scheduler-only ScoutEngine over a side x side patch grid (the
+    reference test suite's _fake_dataset_engine), for either package."""
+    import threading
+
+    class _Box:
+        pass
+    ds = _Box()
+    ds.tiles = []
+    ds.bbox_min = np.array([0.0, 0.0, 0.0])
+    ds.bbox_max = np.array([side * 640.0, side * 640.0, 100.0])
+    eng = mod.ScoutEngine.__new__(mod.ScoutEngine)
+    eng.dataset = ds
+    eng.config = mod.EngineConfig()
+    eng.grid = mod.patch_grid_for(ds.bbox_min, ds.bbox_max)
+    eng.patches = {(k.i, k.j): mod.PatchState(key=k, stage=mod.Stage.CHUNK_POINTS_ONLY)
+                   for k in eng.grid.keys()}
+    eng.tiles, eng.raw, eng.refined = {}, {}, {}
+    eng.resident_records, eng.pending_bakes = {}, {}
+    eng.frame = 0
+    eng.ready_events = []
+    eng.lock = threading.RLock()
+    eng._tile_by_id = {}
+    return eng
+
+
+def run_scheduler(args):
+    """SURVEY 8(f) rank 2 at scale: one viewpoint update (projected area of
+    every patch box, engine.py:185-202) and one next_tasks(64) (sorted
+    candidates, engine.py:218-242) on a 1,000 x 1,000 patch grid, host wall
+    clock (the scheduler is host state; the areas run in one GPU launch).
+    The reference engine (baseline/_ref) is timed on a 100 x 100 grid."""
+    from paper_2509_20198_b200 import engine as E
+    from paper_2509_20198_b200.geometry import CameraState
+    side = int(round(args.sched_patches ** 0.5))
+    eng = _sched_engine(E, side)
+    cam = CameraState.from_yaw_pitch((side * 320.0, -2000.0, 3000.0), np.deg2rad(90),
+                                     np.deg2rad(-30), np.deg2rad(60), (1280, 720),
+                                     far=1e7)
+    eng.update_viewpoint(cam)  # warm-up
+    t0 = time.perf_counter()
+    eng.update_viewpoint(cam)
+    t1 = time.perf_counter()
+    tasks = eng.next_tasks(64)
+    t2 = time.perf_counter()
+    res = {"config": f"{side}x{side} = {side * side:,} patches, oblique camera",
+           "update_viewpoint_s": round(t1 - t0, 3), "next_tasks_s": round(t2 - t1, 3),
+           "first_task": list(tasks[0].patch) if tasks else None}
+    import bench_ref
+    if bench_ref.available() and not args.no_cpu:
+        import sys as _sys
+        if bench_ref.REF not in _sys.path:
+            _sys.path.insert(0, bench_ref.REF)
+        import terrascout.engine as RE
+        from terrascout.geometry import CameraState as RC
+        from terrascout.patches import patch_grid_for as rgrid
+        RE.patch_grid_for = rgrid
+        rs = 100
+        reng = _sched_engine(RE, rs)
+        rcam = RC.from_yaw_pitch((rs * 320.0, -2000.0, 3000.0), np.deg2rad(90),
+                                 np.deg2rad(-30), np.deg2rad(60), (1280, 720), far=1e7)
+        r0 = time.perf_counter()
+        reng.update_viewpoint(rcam)
+        r1 = time.perf_counter()
+        reng.next_tasks(64)
+        r2 = time.perf_counter()
+        scale = side * side / (rs * rs)
+        res["reference"] = {"config": f"{rs}x{rs} patches, same camera, "
+                                      f"scaled x{scale:.0f} (both steps are O(P))",
+                            "update_viewpoint_s": round((r1 - r0) * scale, 2),
+                            "next_tasks_s": round((r2 - r1) * scale, 2)}
     return res
 
 
