@@ -68,22 +68,8 @@ struct ConvOp {
   // the low-resolution input, rows/cols offset by ph - 1 (pad 1 - ph), the
   // window [oy0,oy1) x [ox0,ox1) in low-resolution coordinates and output
   // pixel (2*oy + ph_y, 2*ox + ph_x) of op.out.
-  //
-  // ph = 2: a GROUP of nph output phases (phase codes phl[g] = 2*py + px)
-  // in one launch: k = 3, pad = 1 geometry over the low-resolution input
-  // (the union of the phases' 2x2 taps), the window the union of their
-  // low-resolution windows; phase g's taps are the 3x3 positions
-  // (ty + py, tx + px) and its output pixel (2*oy + py, 2*ox + px) is
-  // stored when inside the high-resolution window [hy0,hy1) x [hx0,hx1).
-  // The halo is gathered once for all phases of the group.
   int ph, ph_y, ph_x;
-  int nph;
-  int phl[4];
-  int hy0, hy1, hx0, hx1;
 };
-
-// phases computed by one launch of op (1 unless ph == 2)
-__host__ __device__ inline int op_groups(const ConvOp& op) { return op.ph == 2 ? op.nph : 1; }
 
 // Tap set of the phase form: low-resolution tap t (0 or 1) of output phase
 // p collects the 3x3 taps k with (p + k - 1) >> 1 == p + t - 1, i.e.
@@ -154,8 +140,6 @@ bool conv_tc_halo2_eligible(const ConvOp& op, int precision);
 // TMEM accumulator buffers the wide-M halo kernel's plan gives op (0: not
 // eligible)
 int conv_tc_halo2_accbufs(const ConvOp& op, int precision);
-// w_oikk: op_groups(op) consecutive [co][ci][k][k] tensors (one per phase of
-// a ph == 2 group, zeros at the taps a phase does not use)
 std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, int k,
                                            int precision, const ConvOp& op);
 int launch_conv_tc_halo2(const ConvOp& op, int precision, void* stream);

@@ -261,8 +261,6 @@ __global__ void __launch_bounds__(kBalThreads, 1) conv_enc0_bal_kernel(Enc0Op E)
 }
 
 bool enc0_balanced(const Enc0Op& E, int co) {
-  const char* v = getenv("TS_ENC0_BAL");
-  if (v && v[0] == '0') return false;
   int ones = 0;
   for (int e = 0; e < 4; ++e) ones += E.cin[e] == 1;
   return co == 48 && ones == 2;

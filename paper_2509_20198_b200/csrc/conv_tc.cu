@@ -696,8 +696,7 @@ TcPlan plan_for(const ConvOp& op, int precision) {
   // BF16X4 1x1 layers (the merge GEMMs) take N tiles of up to 256 without
   // plane stacking: every N tile re-gathers and re-splits A, so fewer tiles
   // halve the producers' work
-  const char* e = getenv("TS_TC_WIDE");
-  const bool wide_ok = precision == 4 && op.k == 1 && !(e && e[0] == '0');
+  const bool wide_ok = precision == 4 && op.k == 1;
   const int cap = wide_ok ? 256 : 128;
   p.ntiles = (n16 + cap - 1) / cap;
   p.bn = ((n16 + p.ntiles - 1) / p.ntiles + 15) / 16 * 16;
@@ -853,12 +852,7 @@ int launch_conv_tc_halo(const ConvOp& op, int precision, void* stream) {
 }
 
 int tc_weight_layout(const ConvOp& shape, int precision) {
-  static int halo2 = -1;
-  if (halo2 < 0) {
-    const char* e = getenv("TS_HALO2");
-    halo2 = (e && e[0] == '0') ? 0 : 1;
-  }
-  if (halo2 && conv_tc_halo2_eligible(shape, precision)) return 2;
+  if (conv_tc_halo2_eligible(shape, precision)) return 2;
   if (conv_tc_halo_eligible(shape, precision)) return 1;
   return 0;
 }

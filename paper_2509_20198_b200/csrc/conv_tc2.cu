@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
   uint32_t* s_aoff = reinterpret_cast<uint32_t*>(rowoff + 2 * L);  // [nst]
   uint16_t* s_chunk = reinterpret_cast<uint16_t*>(s_aoff + kMaxStages);
   const int nst = (int)reinterpret_cast<const uint32_t*>(T.wpk)[0];
-  const int G = op_groups(op);  // output phases of this launch
+  constexpr int G = 1;  // output phases per launch (stage-list encoding keeps the field)
   {
     // entry = (chunk * G + phase) * taps + tap, bit 15 = the phase's first
     // stage (its MMAs overwrite the accumulator); decoded into the A
@@ -724,21 +724,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
           const int y = r / Wp, x = r % Wp;
           if (y < wy && x < wx) {
             int oy = op.oy0 + y, ox = op.ox0 + x;
-            bool in = true;
             if (op.ph == 1) {
               oy = 2 * oy + op.ph_y;
               ox = 2 * ox + op.ph_x;
-            } else if (op.ph == 2) {
-              oy = 2 * oy + (op.phl[g] >> 1);
-              ox = 2 * ox + (op.phl[g] & 1);
-              in = oy >= op.hy0 && oy < op.hy1 && ox >= op.hx0 && ox < op.hx1;
             }
-            if (in) {
-              o = op.out.base + act_off(op.out, b, oy, ox);
-              int64_t blk;
-              act_block(op.out, b, oy, ox, blk, ochan);
-              oblk = op.out.base + blk;
-            }
+            o = op.out.base + act_off(op.out, b, oy, ox);
+            int64_t blk;
+            act_block(op.out, b, oy, ox, blk, ochan);
+            oblk = op.out.base + blk;
           }
         }
         for (int c = 16 * half; c < BN; c += 16 * (kEpiWarps / 4)) {
@@ -806,17 +799,11 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
   // 1x1 layers stay on the regular kernel (no halo to reuse, and their
   // multi-N-tile shapes re-read A per N tile here)
   if (op.stride != 1 || op.k < 1 || op.pad < 0 || op.pad >= op.k) return false;
-  const int G = op_groups(op);
-  if (op.ph == 2 && (op.k != 3 || op.pad != 1 || op.up2 || G < 1 || G > 4)) return false;
-  if (precision == 5 && G != 1) return false;  // promoted epilogue: one phase per launch
+  constexpr int G = 1;
   // 1x1 layers: the bf16-class modes measured slower here than on the
-  // regular kernel (A re-read per N tile; opt in with TS_H2_1X1=1); FP16X3
-  // runs them here for the promoted accumulation
-  static const bool h2_1x1 = [] {
-    const char* e = getenv("TS_H2_1X1");
-    return e && e[0] == '1';
-  }();
-  if (op.k == 1 && !h2_1x1 && precision != 5) return false;
+  // regular kernel (A re-read per N tile); FP16X3 runs them here for the
+  // promoted accumulation
+  if (op.k == 1 && precision != 5) return false;
   if (op.in.C % 4 || op.in.cstride % 4 || op.in.coff % 4) return false;
   if (op.in.planes && (op.in.C % 8 || op.in.cstride % 8 || op.in.coff % 8)) return false;
   if (op.out.planes && (op.out.C % 16 || op.out.cstride % 8 || op.out.coff % 8)) return false;
@@ -826,13 +813,9 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
   const int n16 = (op.out.C + 15) / 16 * 16;
   {  // widest N tile: up to 256 (one MMA) so a layer's A halo is gathered
      // and read once for all its columns (enc*.2, N = 192: 235 -> 192 us
-     // against two 96-column tiles); TS_H2_BNMAX overrides
-    static const int bnmax = [] {
-      const char* e = getenv("TS_H2_BNMAX");
-      return e ? std::max(16, std::min(256, atoi(e))) : 256;
-    }();
-    // FP16X3: the two weight planes stack into one MMA (N = 2 BN <= 256)
-    const int bmax = precision == 5 ? std::min(bnmax, 128) : bnmax;
+     // against two 96-column tiles); FP16X3 stacks its two weight planes
+     // into one MMA (N = 2 BN <= 256)
+    const int bmax = precision == 5 ? 128 : 256;
     p.ntiles = (n16 + bmax - 1) / bmax;
   }
   p.bn = ((n16 + p.ntiles - 1) / p.ntiles + 15) / 16 * 16;
@@ -848,30 +831,15 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
   // measured better only for thin N (BN <= 32).  Wider layers accumulate
   // every product into the same BN columns, which doubles the sub-tiles
   // per TMEM buffer and amortises the MMA issuer's per-stage overhead.
-  {
-    static const int stack_env = [] {  // -1: planner's choice
-      const char* e = getenv("TS_H2_STACK");
-      return e ? (e[0] == '1' ? 1 : 0) : -1;
-    }();
-    // (a phase group stacks only if two sub-tiles still get two buffers)
-    p.stack = stack_env >= 0 ? stack_env : (p.pb * p.bn <= 64 && 4 * G * p.pb * p.bn <= 512);
-    if (precision == 5) p.stack = 1;  // [b0 | b1] rows (BN <= 128)
-    else if (p.pb * p.bn > 256) p.stack = 0;  // MMA N limit
-  }
+  p.stack = p.pb * p.bn <= 64 && 4 * G * p.pb * p.bn <= 512;
+  if (precision == 5) p.stack = 1;          // [b0 | b1] rows (BN <= 128)
+  else if (p.pb * p.bn > 256) p.stack = 0;  // MMA N limit
   const int cols = G * (precision == 5 ? 2 * p.bn : p.stack ? p.pb * p.bn : p.bn);
   // FP16X3: promotion group = the channel chunks of <= 18 K steps (2 per
   // 32-channel chunk and tap): 1 for 3x3, 2 for 2x2, 8 for 1x1
   p.cgrp = precision == 5 ? std::max(1, 16 / (2 * op.k * op.k)) : 1;
-  int cand[6][2] = {{4, 2}, {2, 2}, {1, 2}, {4, 1}, {2, 1}, {1, 1}};
-  {  // TS_H2_SUBAB=<sub>,<accbufs>: try that candidate first (A/B measurement)
-    static const char* e = getenv("TS_H2_SUBAB");
-    if (e && e[0] >= '1' && e[0] <= '4' && e[1] == ',' && (e[2] == '1' || e[2] == '2')) {
-      cand[5][0] = cand[0][0]; cand[5][1] = cand[0][1];
-      cand[0][0] = e[0] - '0'; cand[0][1] = e[2] - '0';
-    }
-  }
+  const int cand[6][2] = {{4, 2}, {2, 2}, {1, 2}, {4, 1}, {2, 1}, {1, 1}};
   for (const auto& cb : cand) {
-    if (cb[0] == 3) continue;
     const int sub = cb[0], ab = cb[1];
     if (ab * sub * cols > 512) continue;
     // FP16X3: two group buffers, and the epilogue holds SUB x BN sums
@@ -880,27 +848,16 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
     const size_t hbuf = (size_t)p.pa * L * kRow;
     const size_t fixed = 1024 + 8 * 40 + 16 + 16 * (size_t)L + 6 * kMaxStages + 64 +
                          4 * (size_t)p.ntiles * p.bn + 16;
-    static const int hb_env = [] {  // TS_H2_HB=2/3: force the halo buffer count
-      const char* e = getenv("TS_H2_HB");
-      return e ? atoi(e) : 0;
-    }();
-    static const int sb_env = [] {  // TS_H2_SB=<n>: cap on the weight ring stages
-      const char* e = getenv("TS_H2_SB");  // measured: 3-4 about 1% faster than 8
-      return e ? atoi(e) : 4;
-    }();
-    static const int hb_max = [] {  // TS_H2_HBMAX=<n>: most halo buffers tried
-      const char* e = getenv("TS_H2_HBMAX");
-      return e ? atoi(e) : 3;
-    }();
-    for (int hb : {8, 6, 5, 4, 3, 2}) {
-      if (hb > hb_max || (hb_env && hb != hb_env)) continue;
+    // halo buffers: 3, else 2 (measured: 4-8 no faster); weight ring: up to
+    // 4 stages (measured: 3-4 about 1% faster than 8)
+    for (int hb : {3, 2}) {
       const size_t used = hb * hbuf + fixed;
       if (used + 3 * bst > cap) continue;
       p.sub = sub;
       p.accbufs = ab;
       p.hbufs = hb;
       p.lrows = L;
-      p.bstages = (int)std::min<size_t>(std::max(3, std::min(8, sb_env)), (cap - used) / bst);
+      p.bstages = (int)std::min<size_t>(4, (cap - used) / bst);
       p.smem = used + p.bstages * bst;
       *out = p;
       return true;
@@ -928,7 +885,7 @@ std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, 
   const size_t plane = (size_t)p.bn * kRow;
   const size_t b_bytes = plane * p.pb;
   const int taps = k * k;
-  const int G = op_groups(op);
+  constexpr int G = 1;
   const size_t wg = (size_t)co * ci * taps;  // floats per phase tensor
   // (chunk, phase, tap) stages whose weights are all zero in every n-tile
   // are skipped (the space-to-depth form of a stride-2 3x3 layer has 7 such

@@ -71,12 +71,6 @@ struct ConvLayer {
   bool poly = false;
   const uint8_t* w_ph[4] = {nullptr, nullptr, nullptr, nullptr};
   Win ph_win[4];
-  // phase groups (conv.cuh ConvOp::ph == 2): ph_G phases per launch, 4 / ph_G
-  // launches; group i = phases i*ph_G .. (i+1)*ph_G - 1, low-res window the
-  // union of theirs
-  int ph_G = 1;
-  const uint8_t* w_grp[4] = {nullptr, nullptr, nullptr, nullptr};
-  Win grp_win[4];
   std::vector<float> w_host, b_host;  // final-layer kernel: weights as parameters
   bool h2 = false;          // executed on the wide-M halo kernel (or phases)
   int prec = 0;             // tensor-core precision mode of this layer's launches
@@ -113,6 +107,36 @@ struct ts_weights {
 
 namespace ts {
 namespace {
+
+// Execution switches: alternative formulations kept for A/B measurement
+// (DESIGN.md §2), read from the environment once per process.  Defaults
+// are the measured-best configuration; every setting computes the same
+// result within the stated tolerance (planes: bit-identical).
+struct Switches {
+  bool s2d = true;             // TS_S2D=0: stride-2 layers without space-to-depth
+  bool poly = true;            // TS_POLY=0: decoders as plain up2 + 3x3
+  bool enc0 = true;            // TS_ENC0=0: four first-layer launches
+  bool final_cuda = true;      // TS_FINAL=0: fuse.2 on the tensor cores
+  bool planes = false;         // TS_PLANES=1: pre-split activation storage
+  bool branch_streams = true;  // TS_BRANCH_STREAMS=0: branches serialised
+};
+const Switches& switches() {
+  static const Switches sw = [] {
+    auto on = [](const char* name, bool dflt) {
+      const char* e = getenv(name);
+      return e ? e[0] == '1' : dflt;
+    };
+    Switches w;
+    w.s2d = on("TS_S2D", true);
+    w.poly = on("TS_POLY", true);
+    w.enc0 = on("TS_ENC0", true);
+    w.final_cuda = on("TS_FINAL", true);
+    w.planes = on("TS_PLANES", false);
+    w.branch_streams = on("TS_BRANCH_STREAMS", true);
+    return w;
+  }();
+  return sw;
+}
 
 int parse_descriptor(const std::string& text, bool& identity,
                      std::map<std::string, std::vector<LayerDesc>>& stages,
@@ -383,8 +407,7 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
   // reuse.  The producing layer must be able to write s2d (direct kernel or
   // halo2), else the layer keeps its plain form.
   {
-    const char* e = getenv("TS_S2D");
-    const bool s2d_ok = tc16_mode(W->precision) && !(e && e[0] == '0');
+    const bool s2d_ok = tc16_mode(W->precision) && switches().s2d;
     auto exec_shape = [&](const ConvLayer& L, const LayerDesc& d) {
       ConvOp o{};
       o.k = d.k; o.stride = d.s; o.pad = d.p; o.up2 = L.up2;
@@ -425,8 +448,7 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
   // wide-M halo kernel: 4/9 of the MACs, and the halo is gathered at the
   // input's own resolution
   {
-    const char* e = getenv("TS_POLY");
-    const bool poly_ok = tc16_mode(W->precision) && !(e && e[0] == '0');
+    const bool poly_ok = tc16_mode(W->precision) && switches().poly;
     for (auto& L : layers) {
       const LayerDesc& d = L.d;
       if (!poly_ok || !L.up2 || d.k != 3 || d.s != 1 || d.p != 1 || L.s2d_in || L.s2d_out ||
@@ -446,44 +468,12 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
         ok = conv_tc_halo2_eligible(o, W->precision);
       }
       L.poly = ok;
-      // TS_PHGROUP=2/4: the phases of a group share one halo fill and one
-      // launch (input read once instead of per phase); a group must still
-      // get two TMEM accumulator buffers.  Measured slower (dec*.2 4 x 146
-      // -> 649 us, dec*.1 4 x 87 -> 408 us, dec*.0 4 x 126 -> 2 x 275 us):
-      // the group's accumulators leave room for one sub-tile, not four, so
-      // every weight stage feeds 4x fewer MMAs.  Off by default.
-      const char* eg = getenv("TS_PHGROUP");
-      const int want = eg ? atoi(eg) : 1;
-      L.ph_G = 1;
-      for (int G : {4, 2}) {
-        if (!ok || G > want) continue;
-        bool fit = true;
-        for (int gi = 0; gi < 4 / G && fit; ++gi) {
-          Win u = L.ph_win[gi * G];
-          for (int j = 1; j < G; ++j) {
-            const Win& w = L.ph_win[gi * G + j];
-            u.y0 = std::min(u.y0, w.y0); u.y1 = std::max(u.y1, w.y1);
-            u.x0 = std::min(u.x0, w.x0); u.x1 = std::max(u.x1, w.x1);
-          }
-          L.grp_win[gi] = u;
-          ConvOp o{};
-          o.k = 3; o.stride = 1; o.pad = 1; o.ph = 2; o.nph = G;
-          o.oy0 = u.y0; o.oy1 = u.y1; o.ox0 = u.x0; o.ox1 = u.x1;
-          o.in.C = d.ci; o.in.cstride = d.ci; o.out.C = d.co; o.out.cstride = d.co;
-          o.in.H = L.Hin; o.in.W = L.Win_;
-          o.batch = 1;
-          const int ab = conv_tc_halo2_accbufs(o, W->precision);
-          fit = ab == 2 || (eg && ab > 0);
-        }
-        if (fit) { L.ph_G = G; break; }
-      }
     }
   }
 
   // the four first encoder layers share one input read (conv_enc0.cu)
   {
-    const char* e = getenv("TS_ENC0");
-    bool ok = !(e && e[0] == '0') && tc16_mode(W->precision);
+    bool ok = switches().enc0 && tc16_mode(W->precision);
     const ConvLayer* f[4];
     for (int st = 0; st < 4 && ok; ++st) {
       f[st] = &layers[stage_first[st]];
@@ -572,8 +562,7 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
       ConvOp fs{};
       fs.k = dx.k; fs.stride = dx.s; fs.pad = dx.p; fs.up2 = L.up2;
       fs.in.C = dx.ci; fs.in.cstride = dx.ci; fs.out.C = Co; fs.out.cstride = Co;
-      const char* e = getenv("TS_FINAL");
-      if (i == nL - 1 && conv_final_supported(fs) && !(e && e[0] == '0')) {
+      if (i == nL - 1 && conv_final_supported(fs) && switches().final_cuda) {
         L.w_host = packed;
         L.b_host = bi->second.second;
       }
@@ -587,8 +576,6 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
     TS_CUDA_TRY(cudaMemcpy(L.b, bi->second.second.data(), Co * sizeof(float),
                            cudaMemcpyHostToDevice));
     if (L.poly) {
-      std::vector<float> w3;  // phase groups: [G][Co][ci][3][3]
-      if (L.ph_G > 1) w3.assign((size_t)4 * Co * dx.ci * 9, 0.f);
       for (int p = 0; p < 4; ++p) {
         // folded 2x2 weights of phase p: sums of the 3x3 taps each low-res
         // tap collects (fp64 sums rounded once)
@@ -604,11 +591,7 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
                     if (phase_tap(py, ty, ky) && phase_tap(px, tx, kx))
                       acc += src[(((size_t)o * dx.ci + ci) * 3 + ky) * 3 + kx];
                 w2[(((size_t)o * dx.ci + ci) * 2 + ty) * 2 + tx] = (float)acc;
-                if (L.ph_G > 1)  // the phase's 2x2 taps at (ty + py, tx + px) of 3x3
-                  w3[((((size_t)p * Co + o) * dx.ci + ci) * 3 + ty + py) * 3 + tx + px] =
-                      (float)acc;
               }
-        if (L.ph_G > 1) continue;
         ConvOp shape{};
         shape.k = 2; shape.stride = 1; shape.pad = 1; shape.ph = 1; shape.ph_y = py;
         shape.ph_x = px;
@@ -625,23 +608,6 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
         W->device_allocs.push_back(dp);
         TS_CUDA_TRY(cudaMemcpy(dp, pk.data(), pk.size(), cudaMemcpyHostToDevice));
         L.w_ph[p] = reinterpret_cast<const uint8_t*>(dp);
-      }
-      for (int gi = 0; L.ph_G > 1 && gi < 4 / L.ph_G; ++gi) {
-        ConvOp shape{};
-        shape.k = 3; shape.stride = 1; shape.pad = 1; shape.ph = 2; shape.nph = L.ph_G;
-        shape.oy0 = L.grp_win[gi].y0; shape.oy1 = L.grp_win[gi].y1;
-        shape.ox0 = L.grp_win[gi].x0; shape.ox1 = L.grp_win[gi].x1;
-        shape.in.C = dx.ci; shape.in.cstride = dx.ci; shape.out.C = Co; shape.out.cstride = Co;
-        shape.in.H = L.Hin; shape.in.W = L.Win_;
-        shape.batch = 1;
-        const std::vector<uint8_t> pk = pack_tc_weights_halo2(
-            w3.data() + (size_t)gi * L.ph_G * Co * dx.ci * 9, Co, dx.ci, 3, L.prec, shape);
-        if (pk.empty()) return TS_E_INVALID;
-        void* dp = nullptr;
-        TS_CUDA_TRY(cudaMalloc(&dp, pk.size()));
-        W->device_allocs.push_back(dp);
-        TS_CUDA_TRY(cudaMemcpy(dp, pk.data(), pk.size(), cudaMemcpyHostToDevice));
-        L.w_grp[gi] = reinterpret_cast<const uint8_t*>(dp);
       }
     } else if (W->precision != 0 && dx.ci % 4 == 0) {
       ConvOp shape{};
@@ -681,9 +647,8 @@ int build_plan(ts_weights* W, std::map<std::string, std::vector<LayerDesc>>& st,
     // tiles, FP16X3 12.08 vs 10.04 ms (the epilogues' split and plane stores
     // cost more than the producers save; profiles/r02_cnn_layers.md).
     // Results are bit-identical either way.
-    const char* e = getenv("TS_PLANES");
     W->plane_fmt = W->precision == 5 ? 2 : 1;
-    const bool on = tc16_mode(W->precision) && (e && e[0] == '1');
+    const bool on = tc16_mode(W->precision) && switches().planes;
     auto fmt_ok = [](const ConvLayer& L) {
       return L.d.co % 16 == 0 && L.out_cstride % 8 == 0 && L.out_coff % 8 == 0;
     };
@@ -849,8 +814,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
   const int fcs = W->layers.back().d.co;
   Branches* br = nullptr;
   {
-    const char* e = getenv("TS_BRANCH_STREAMS");
-    if (!(e && e[0] == '0')) {
+    if (switches().branch_streams) {
       const int st = branches_for(br);
       if (st != TS_OK) return st;
     }
@@ -978,25 +942,6 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
           if (st != TS_OK) return st;
         }
         prev_base = buf(L.out_off); prev_H = L.Hout; prev_cs = L.out_cstride;
-        prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? W->plane_fmt : 0;
-        prev_stage = L.stage;
-        continue;
-      }
-      if (L.poly && L.ph_G > 1) {
-        for (int gi = 0; gi < 4 / L.ph_G; ++gi) {
-          const Win& w = L.grp_win[gi];
-          if (w.y1 <= w.y0 || w.x1 <= w.x0) continue;
-          ConvOp q = op;
-          q.k = 3; q.stride = 1; q.pad = 1; q.up2 = 0;
-          q.ph = 2; q.nph = L.ph_G;
-          for (int j = 0; j < L.ph_G; ++j) q.phl[j] = gi * L.ph_G + j;
-          q.hy0 = L.out_win.y0; q.hy1 = L.out_win.y1; q.hx0 = L.out_win.x0; q.hx1 = L.out_win.x1;
-          q.oy0 = w.y0; q.oy1 = w.y1; q.ox0 = w.x0; q.ox1 = w.x1;
-          q.w_tc = L.w_grp[gi]; q.w_layout = 2;
-          st = launch_conv_tc_halo2(q, L.prec, lstream);
-          if (st != TS_OK) return st;
-        }
-        prev_base = op.out.base; prev_H = L.Hout; prev_cs = L.out_cstride;
         prev_coff = L.out_coff; prev_C = L.d.co; prev_planes = L.out_planes ? W->plane_fmt : 0;
         prev_stage = L.stage;
         continue;
