@@ -69,13 +69,17 @@ def parse():
 
 
 def ncu_traffic():
-    """DRAM bytes per step of the CNN launches / per splat launch from the
-    committed ncu capture of this command (profiles/r01_traffic.json)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fp:
-            return json.load(fp)
-    except (OSError, ValueError):
+    """DRAM bytes of the CNN launches / the bake launches per step, from the
+    committed ncu capture of this command (the latest profiles/rNN_traffic
+    .json, written by scripts/summarize_round.py)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    if not files:
         return {}
+    with open(files[-1]) as fp:
+        d = json.load(fp)
+    d["file"] = os.path.relpath(files[-1], ROOT)
+    return d
 
 
 def peaks():
@@ -406,8 +410,8 @@ def run_ours(args, rank, world, local_rank):
                          "traffic": ncu_traffic().get(
                              "cnn_dram_bytes_per_step"),
                          "traffic_unit": "DRAM bytes per step (ncu "
-                                         "launch list, "
-                                         "profiles/r01_traffic.json)"},
+                                         "launch list, " + str(ncu_traffic().get(
+                                             "file")) + ")"},
             "e2e": {"value": round(e2e_value, 2), "unit": "heightmaps/s",
                     "h2d_bytes_per_step": int(host_bytes.numel()),
                     "d2h_bytes_per_step": int(out_host[0].numel() * 4),
@@ -879,8 +883,8 @@ def run_splat(args, dev, world, rank):
                          "traffic": ncu_traffic().get(
                              "bake_dram_bytes_per_launch"),
                          "traffic_unit": "DRAM bytes, splat + finalize "
-                                         "launches (ncu, "
-                                         "profiles/r01_traffic.json)"},
+                                         "launches (ncu, " + str(ncu_traffic().get(
+                                             "file")) + ")"},
             "shuffled": shuffled}
 
 

@@ -8,7 +8,7 @@ import os
 import subprocess
 import sys
 
-R = sys.argv[1] if len(sys.argv) > 1 else "r01"
+R = sys.argv[1] if len(sys.argv) > 1 else "r02"
 G, P = "gpurun_out", "profiles"
 
 
@@ -64,7 +64,7 @@ json.dump({"cnn_dram_bytes_per_step": cnn_b, "cnn_ncu_us_per_step": cnn_t,
            "step_ncu_us": tot, "bake_dram_bytes_per_launch": bake_b,
            "source": f"profiles/{R}_step_kernels.md (ncu launch lists of bench.py)"},
           open(f"{P}/{R}_traffic.json", "w"), indent=1)
-for cap in ("fuse0", "splat"):
+for cap in ("fuse0", "splat", "raster", "delaunay"):
     rep = f"{G}/{R}_{cap}.ncu-rep"
     if not os.path.exists(rep):
         continue
