@@ -166,13 +166,22 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
   uint32_t ncols = 32;
   while ((int)ncols < AB * acc_cols) ncols <<= 1;
 
+  // FP16X3 over 32-byte aligned fp32 input with short halos (1x1 and
+  // SUB-1 2x2 layers, L <= 160 rows): grouped producers (below).  Measured:
+  // merge.0 1127 -> 906 us, merge.1 579 -> 463 us; longer halos (SUB 2-4)
+  // got slower (dec*.2 134 -> 153 us): their chunks already outlast a round
+  // trip, and a group has half the loads in flight per chunk
+  const bool grouped = MODE == 5 && L <= 160 && !op.in.planes && Cin % 8 == 0 &&
+                       op.in.cstride % 8 == 0 && op.in.coff % 8 == 0 &&
+                       (reinterpret_cast<uintptr_t>(op.in.base) & 31) == 0;
   if (tid == 0) {
     for (int s = 0; s < SB; ++s) {
       mbar_init(bfull + s, 1);
       mbar_init(bempty + s, 1);
     }
     for (int h = 0; h < HB; ++h) {
-      mbar_init(hfull + h, kProdW);  // one arrival per producer warp
+      // one arrival per producer warp (per warp of the filling group)
+      mbar_init(hfull + h, grouped ? kProdW / 2 : kProdW);
       mbar_init(hempty + h, 1);
     }
     for (int a = 0; a < AB; ++a) {
@@ -231,62 +240,69 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(op.in.base + off));
       }
     };
-    // short halos (1x1 layers, small 2x2 ones: <= 2 rows per thread per
-    // chunk) fill two chunks per global round trip, else one chunk's MMAs
-    // (2-8 K steps) cannot cover the load latency
-    const bool pair = MODE == 5 && v8in && !op.in.planes && L <= 2 * (kProdT / 4) && HB >= 3;
+    if (grouped) {
+      // FP16X3 fp32 input: two producer groups of kProdW / 2 warps fill
+      // alternate (tile, chunk) units, so two chunks' loads are in flight
+      // per round trip (the 1x1 and 2x2 layers' MMAs per chunk are shorter
+      // than one L2 round trip); unit n uses halo buffer n % HB, phase
+      // (n / HB) & 1
+      constexpr int kGW = kProdW / 2, kGT = kGW * 32, kStep = kGT / 4;
+      static_assert(kStep % 8 == 0, "rows per pass keep the swizzle phase");
+      const int pg = warp / kGW, gt = tid - pg * kGT;
+      const int piece = gt & 3, row0 = gt >> 2;
+      const int obase = row0 * kRow + ((piece ^ ((row0 >> 1) & 3)) << 4);
+      constexpr int kIn = TS_H2_IN8;
+      int64_t n = 0;
+      for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+        const int64_t* ro = rowoff + (lt & 1) * L;
+        if (lt == 0) build_rows(0, false);
+        prod_sync();
+        for (int c = 0; c < T.cchunks; ++c, ++n) {
+          if (c == T.cchunks - 1 && tile + gridDim.x < total_tiles) build_rows(lt + 1, true);
+          if ((int)(n & 1) != pg) continue;
+          const int h = (int)(n % HB);
+          TS_PROF_WAIT(kPrProdWait, mbar_wait(hempty + h, (uint32_t)((n / HB) & 1) ^ 1u));
+          uint8_t* sa = halo + h * halo_bytes + obase;
+          const int ch = c * kKC + 8 * piece;
+          const bool ch_ok = ch < Cin;
+          const bool pf_ok = c + 1 < T.cchunks && ch + kKC < Cin;
+          const float* src = op.in.base + ch;
+          for (int r0 = row0; r0 < L; r0 += kStep * kIn) {
+            float v[kIn][8];
+#pragma unroll
+            for (int u = 0; u < kIn; ++u) {
+              const int row = r0 + u * kStep;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[u][i] = 0.f;
+              if (row < L) {
+                const int64_t off = ro[row];
+                if (off >= 0 && ch_ok) ld_v8(src + off, v[u]);
+                if (TS_H2_PF && off >= 0 && pf_ok)
+                  asm volatile("prefetch.global.L2 [%0];" ::"l"(src + off + kKC));
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < kIn; ++u) {
+              if (r0 + u * kStep < L) {
+                uint8_t* d = sa + (r0 - row0 + u * kStep) * kRow;
+                uint32_t hw[4], lw[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) split_h2(v[u][2 * i], v[u][2 * i + 1], hw[i], lw[i]);
+                *reinterpret_cast<uint4*>(d) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                *reinterpret_cast<uint4*>(d + plane_a) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+              }
+            }
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if ((tid & 31) == 0) mbar_arrive(hfull + h);
+        }
+      }
+    } else
     for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
       int64_t* ro = rowoff + (lt & 1) * L;
       if (lt == 0) build_rows(0, false);
       prod_sync();
-      if (pair) {
-        constexpr int kStep8 = kProdT / 4;
-        const int piece = tid & 3, row0 = tid >> 2;
-        const int obase = row0 * kRow + ((piece ^ ((row0 >> 1) & 3)) << 4);
-        for (int c = 0; c < T.cchunks; c += 2) {
-          const int nc = T.cchunks - c < 2 ? 1 : 2;
-          if (c + nc >= T.cchunks && tile + gridDim.x < total_tiles) build_rows(lt + 1, true);
-          const int hbs[2] = {hb, hb + 1 == HB ? 0 : hb + 1};
-#pragma unroll
-          for (int q = 0; q < 2; ++q)
-            if (q < nc) TS_PROF_WAIT(kPrProdWait, mbar_wait(hempty + hbs[q], ((hph >> hbs[q]) & 1u) ^ 1u));
-          float v[2][2][8];
-#pragma unroll
-          for (int q = 0; q < 2; ++q)
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-#pragma unroll
-              for (int i = 0; i < 8; ++i) v[q][u][i] = 0.f;
-              const int row = row0 + u * kStep8, ch = (c + q) * kKC + 8 * piece;
-              if (q < nc && row < L) {
-                const int64_t off = ro[row];
-                if (off >= 0 && ch < Cin) ld_v8(op.in.base + ch + off, v[q][u]);
-              }
-            }
-#pragma unroll
-          for (int q = 0; q < 2; ++q)
-#pragma unroll
-            for (int u = 0; u < 2; ++u)
-              if (q < nc && row0 + u * kStep8 < L) {
-                uint8_t* d = halo + hbs[q] * halo_bytes + obase + u * kStep8 * kRow;
-                uint32_t h[4], l[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) split_h2(v[q][u][2 * i], v[q][u][2 * i + 1], h[i], l[i]);
-                *reinterpret_cast<uint4*>(d) = make_uint4(h[0], h[1], h[2], h[3]);
-                *reinterpret_cast<uint4*>(d + plane_a) = make_uint4(l[0], l[1], l[2], l[3]);
-              }
-          fence_proxy_async();
-          __syncwarp();
-#pragma unroll
-          for (int q = 0; q < 2; ++q)
-            if (q < nc) {
-              if ((tid & 31) == 0) mbar_arrive(hfull + hbs[q]);
-              hph ^= 1u << hbs[q];
-              if (++hb == HB) hb = 0;
-            }
-        }
-        continue;
-      }
       for (int c = 0; c < T.cchunks; ++c) {
         // during the last chunk, the next tile's row table (other parity)
         // and an L2 prefetch of its first chunk
