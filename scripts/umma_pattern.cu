@@ -18,20 +18,26 @@ using namespace ts::tcx;
 
 constexpr int kStages = 2048;
 
-__global__ void __launch_bounds__(128, 1) pat_kernel(int bn, int sub, int commit_each,
-                                                     unsigned long long* out) {
+// align: tap slides of whole 8-row swizzle atoms instead of the 3x3
+// pattern; sts: warps 1..10 store 16-byte pieces to a separate region while
+// the MMAs run (the producers' halo stores)
+__global__ void __launch_bounds__(352, 1) pat_kernel(int bn, int sub, int commit_each, int align,
+                                                     int sts, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* a = smem;                    // 2 planes x 640 rows x 64 B
   uint8_t* b = smem + 2 * 640 * 64;     // 2 planes x 128 rows x 64 B
   __shared__ uint64_t bar[2];
   __shared__ uint32_t slot;
+  __shared__ volatile int done;
+  uint8_t* scratch = smem + (2 * 640 + 2 * 128) * 64;  // 400 rows x 128 B
   for (int i = threadIdx.x; i < (2 * 640 + 2 * 128) * 64 / 4; i += blockDim.x)
     reinterpret_cast<uint32_t*>(smem)[i] = 0x3C003C00u;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_barrier_init();
+    done = 0;
   }
   if (threadIdx.x < 32) tmem_alloc(&slot, 512);
   fence_proxy_async();
@@ -46,7 +52,7 @@ __global__ void __launch_bounds__(128, 1) pat_kernel(int bn, int sub, int commit
     unsigned long long t0 = clock64();
     if (elect_one()) {
       for (int st = 0; st < kStages; ++st) {
-        const uint64_t a0 = da + (uint64_t)((st % 9) / 3 * 70 + (st % 3)) * 4;  // tap slide
+        const uint64_t a0 = da + (uint64_t)((align ? (st % 9) * 8 : (st % 9) / 3 * 70 + (st % 3))) * 4;  // tap slide
 #pragma unroll 1
         for (int k = 0; k < 2; ++k)
           for (int u = 0; u < sub; ++u) {
@@ -68,7 +74,20 @@ __global__ void __launch_bounds__(128, 1) pat_kernel(int bn, int sub, int commit
       t1 = clock64();
     }
     (void)pb;
-    if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+    if (threadIdx.x == 0) {
+      out[blockIdx.x] = t1 - t0;
+      done = 1;
+    }
+  } else if (sts) {
+    const int t = threadIdx.x - 32;
+    uint4 v = make_uint4(t, t + 1, t + 2, t + 3);
+    while (!done) {
+#pragma unroll 4
+      for (int r = t; r < 400 * 8; r += 320) {
+        *reinterpret_cast<uint4*>(scratch + r * 16) = v;
+        v.x += 1;
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -83,23 +102,24 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   unsigned long long* d_out;
   cudaMalloc(&d_out, sms * sizeof(unsigned long long));
-  const int smem = (2 * 640 + 2 * 128) * 64 + 1024;
+  const int smem = (2 * 640 + 2 * 128) * 64 + 400 * 128 + 1024;
   cudaFuncSetAttribute(pat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   std::vector<unsigned long long> h(sms);
-  printf("BN SUB commit : cycles/stage (median SM)   model\n");
+  printf("BN SUB commit align sts : cycles/stage (median SM)   model\n");
   const int cfg[][2] = {{32, 4}, {64, 2}, {96, 1}, {128, 1}};
   for (auto& c : cfg)
-    for (int ce : {0, 1}) {
-      const int bn = c[0], sub = c[1];
+    for (int v = 0; v < 4; ++v) {
+      const int bn = c[0], sub = c[1], ce = 1, al = v & 1, sts = v >> 1;
       for (int rep = 0; rep < 2; ++rep) {
-        pat_kernel<<<sms, 128, smem>>>(bn, sub, ce, d_out);
+        pat_kernel<<<sms, 352, smem>>>(bn, sub, ce, al, sts, d_out);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
       }
       cudaMemcpy(h.data(), d_out, sms * 8, cudaMemcpyDeviceToHost);
       std::sort(h.begin(), h.end());
       const double model = 2.0 * sub * (std::max(bn, 32 + bn / 2) + std::max(bn / 2, 32 + bn / 4));
-      printf("%3d %d %d : %8.1f   %6.1f\n", bn, sub, ce, (double)h[sms / 2] / kStages, model);
+      printf("%3d %d %d %d %d : %8.1f   %6.1f\n", bn, sub, ce, al, sts, (double)h[sms / 2] / kStages,
+             model);
     }
   return 0;
 }
