@@ -26,7 +26,11 @@
 // first and last points belong to the same patch, not the current one);
 // workers read the decision behind a per-buffer "ready" mbarrier and
 // release buffers with per-warp arrivals, so there is no block-wide barrier
-// per batch, only at the (rare) switches.  The hot patch's accumulators
+// per batch, only at the (rare) switches; the staging warp sleeps in its
+// buffer waits (mbarrier suspend hint) instead of spinning on the issue
+// slots the workers need.  Points >= 2 cm inside the hot key's window skip
+// the CSR candidate walk when that window is its cell's only interior key
+// (set_hot below; instructions per point 355 -> 210).  The hot patch's accumulators
 // (count, z as lo/hi 32-bit words with the lo carry folded into hi, r/g/b
 // u32 = 24 B x 4096 texels = 96 KB) live in shared memory and take native
 // 32-bit shared atomics; other (point, key) pairs go straight to the global
@@ -45,11 +49,17 @@ namespace ts {
 namespace {
 
 constexpr int kTex = kOut * kOut;  // 4096 texels per patch
-constexpr int kBakeThreads = 1024;  // one CTA per SM: 31 worker warps + 1 staging warp
-constexpr int kWorkers = kBakeThreads - 32;
-constexpr int kBakeU = 2;            // points per worker thread per batch
-constexpr int kBatch = kBakeU * kWorkers;   // 1,984 points (even: 16-byte aligned)
-constexpr int kBufs = 2;             // staged xyz batches (46.5 KB each)
+// one CTA per SM: 31 worker warps + 1 staging warp, two points per worker
+// thread per batch, two staged batches.  Measured alternatives (r02):
+// 24 warps x 3 buffers, 31 x 1 point x 4 buffers, colours staged with the
+// positions (28 warps to fit) and decisions made a whole buffer ahead were
+// all 5-10% slower: the kernel is latency bound and wants resident warps.
+constexpr int kWorkers = 31 * 32;
+constexpr int kBakeThreads = kWorkers + 32;
+constexpr int kBakeU = 2;                   // points per worker thread per batch
+constexpr int kBatch = kBakeU * kWorkers;   // 1,984 points
+constexpr int kBufs = 2;                    // staged xyz batches (46.5 KB each)
+static_assert(kBatch % 2 == 0, "16-byte aligned batches");
 constexpr double kZScale = 268435456.0;          // 2^28
 constexpr double kZInv = 1.0 / 268435456.0;
 constexpr float kCScale = 16777216.0f;            // 2^24
@@ -185,7 +195,7 @@ __global__ void __launch_bounds__(kBakeThreads, 1) bake_splat_kernel(BakeArgs A)
     const int lane = tid & 31;
     auto issue = [&](int64_t i) {
       if (i < nb && staged(i) && lane == 0) {
-        const int b = (int)(i & 1);
+        const int b = (int)(i % kBufs);
         const uint32_t bx = kBatch * 3 * sizeof(double);
         tcx::fence_proxy_async();
         tcx::mbar_arrive_tx(&S.full[b], bx);
@@ -193,24 +203,18 @@ __global__ void __launch_bounds__(kBakeThreads, 1) bake_splat_kernel(BakeArgs A)
       }
     };
     int hot = -1;
-    // batch i switches the hot patch when its first and last points belong
-    // to the same patch, not the current one (grouped input: once per
-    // patch; shuffled input: never, everything goes to global atomics)
     auto decide = [&](int64_t i) {
-      const int b = (int)(i & 1);
+      const int b = (int)(i % kBufs);
       const int64_t base = lo + i * kBatch, last = min(hi, base + kBatch) - 1;
-      // buffer b's previous batch (i - 2) must be fully consumed before its
-      // decision slot and ready phase are reused (staged batches already
-      // waited for that before their copy was issued)
-      if (i >= 2 && !staged(i) && lane == 0)
-        tcx::mbar_wait(&S.empty[b], (uint32_t)(((i - 2) >> 1) & 1));
+      if (i >= kBufs && !staged(i) && lane == 0)
+        tcx::mbar_wait_sleep(&S.empty[b], (uint32_t)(((i - kBufs) / kBufs) & 1), 20000);
       __syncwarp();
       int key = -1;
       if (lane < 2) {
         const int64_t q = lane ? last : base;
         double x, y;
         if (staged(i)) {
-          tcx::mbar_wait(&S.full[b], (uint32_t)((i >> 1) & 1));
+          tcx::mbar_wait(&S.full[b], (uint32_t)((i / kBufs) & 1));
           const int j = (int)(q - base);
           x = S.xyz[b][3 * j]; y = S.xyz[b][3 * j + 1];
         } else {
@@ -223,19 +227,19 @@ __global__ void __launch_bounds__(kBakeThreads, 1) bake_splat_kernel(BakeArgs A)
       if (sw >= 0) hot = sw;
       if (lane == 0) {
         S.dec[b] = sw;
-        tcx::mbar_arrive(&S.ready[b]);  // release: dec[b] and the staged data
+        tcx::mbar_arrive(&S.ready[b]);
       }
       __syncwarp();
     };
-    issue(0);
-    issue(1);
+    for (int q = 0; q < kBufs; ++q) issue(q);
     if (nb > 0) decide(0);
     for (int64_t i = 0; i < nb; ++i) {
       if (i + 1 < nb) decide(i + 1);
-      if (i + 2 < nb && staged(i + 2)) {
-        if (lane == 0) tcx::mbar_wait(&S.empty[i & 1], (uint32_t)((i >> 1) & 1));
+      if (i + kBufs < nb && staged(i + kBufs)) {
+        if (lane == 0)
+          tcx::mbar_wait_sleep(&S.empty[i % kBufs], (uint32_t)((i / kBufs) & 1), 20000);
         __syncwarp();
-        issue(i + 2);
+        issue(i + kBufs);
       }
     }
     return;
@@ -259,14 +263,37 @@ __global__ void __launch_bounds__(kBakeThreads, 1) bake_splat_kernel(BakeArgs A)
     }
   };
   int hot = -1;
+  // Hot-patch fast path.  When the hot key's window lies within 5 mm of its
+  // 640 m grid cell and is that cell's only interior key, a point >= 2 cm
+  // inside the window (dx, dy as texel_of computes them) is >= 1.5 cm inside
+  // the cell, where no other key's window (+-1e-6 m) reaches: its candidate
+  // set is {hot}, so the CSR walk is skipped with the same result.
+  double hx0 = 0.0, hy0 = 0.0;
+  bool fast = false;
+  auto set_hot = [&](int h) {
+    const double2 cc = __ldg(reinterpret_cast<const double2*>(A.keys) + h);
+    hx0 = dsub(cc.x, 320.0);
+    hy0 = dsub(cc.y, 320.0);
+    fast = false;
+    if (!A.cell_inner) return;
+    const double fx = floor(dmul(dsub(cc.x, A.gx0), 1.0 / kPatch));
+    const double fy = floor(dmul(dsub(cc.y, A.gy0), 1.0 / kPatch));
+    if (!(fx >= 0.0 && fy >= 0.0 && fx < (double)A.gnx && fy < (double)A.gny)) return;
+    const int64_t c = (int64_t)fy * A.gnx + (int64_t)fx;
+    const double ox = dsub(hx0, dadd(A.gx0, dmul(fx, kPatch)));
+    const double oy = dsub(hy0, dadd(A.gy0, dmul(fy, kPatch)));
+    fast = fabs(ox) <= 0.005 && fabs(oy) <= 0.005 && __ldg(A.cell_inner + c) == 1 &&
+           __ldg(A.cell_keys + __ldg(A.cell_off + c)) == h;
+  };
   const uint32_t sh_cnt = tcx::su32(S.cnt), sh_zlo = tcx::su32(S.zlo), sh_zhi = tcx::su32(S.zhi),
                  sh_c = tcx::su32(S.c[0]);
   for (int64_t i = 0; i < nb; ++i) {
-    const int b = (int)(i & 1);
+    const int b = (int)(i % kBufs);
     const int64_t base = lo + i * kBatch;
     // colours straight from global (coalesced 12-byte runs), issued before
     // the batch is waited for
     float cv[kBakeU][3];
+    const bool stg = staged(i);
 #pragma unroll
     for (int u = 0; u < kBakeU; ++u) {
       const int64_t q = base + u * kWorkers + tid;
@@ -276,15 +303,15 @@ __global__ void __launch_bounds__(kBakeThreads, 1) bake_splat_kernel(BakeArgs A)
         cv[u][2] = __ldg(A.rgb + 3 * q + 2);
       }
     }
-    tcx::mbar_wait(&S.ready[b], (uint32_t)((i >> 1) & 1));
+    tcx::mbar_wait(&S.ready[b], (uint32_t)((i / kBufs) & 1));
     const int sw = S.dec[b];
     if (sw >= 0) {  // known to every worker: switch the hot patch
       worker_sync();  // all workers are done with the previous batch
       if (hot >= 0) flush(hot);
       worker_sync();
       hot = sw;
+      set_hot(hot);
     }
-    const bool stg = staged(i);
 #pragma unroll
     for (int u = 0; u < kBakeU; ++u) {
       const int j = u * kWorkers + tid;
@@ -293,12 +320,22 @@ __global__ void __launch_bounds__(kBakeThreads, 1) bake_splat_kernel(BakeArgs A)
       double x, y, z;
       if (stg) { x = S.xyz[b][3 * j]; y = S.xyz[b][3 * j + 1]; z = S.xyz[b][3 * j + 2]; }
       else { x = A.xyz[3 * q]; y = A.xyz[3 * q + 1]; z = A.xyz[3 * q + 2]; }
-      int32_t k0 = 0, k1 = 0;
-      if (!candidates(A, x, y, k0, k1)) continue;
       const long long zf = __double2ll_rn(dmul(z, kZScale));
+      int32_t k0 = 0, k1 = 0;
+      int tfast = -1;
+      if (fast) {
+        const double dx = dsub(x, hx0), dy = dsub(y, hy0);
+        if (dx >= 0.02 && dx <= 639.98 && dy >= 0.02 && dy <= 639.98)
+          tfast = (int)(texel_index(dy) * kOut + texel_index(dx));
+      }
+      if (tfast < 0) {
+        if (!candidates(A, x, y, k0, k1)) continue;
+      } else {
+        k1 = k0 + 1;  // one pass: the hot key, texel tfast
+      }
       for (int32_t k = k0; k < k1; ++k) {
-        int key;
-        const int t = texel_of(A, k, x, y, key);
+        int key = hot;
+        const int t = tfast >= 0 ? tfast : texel_of(A, k, x, y, key);
         if (t < 0) continue;
         if (key == hot) {
           red_sh(sh_cnt + 4 * t, 1u);

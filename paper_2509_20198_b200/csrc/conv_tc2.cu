@@ -728,8 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
       const int n0 = nt * BN;
       mbar_wait(acc_full + acc, (lt / AB) & 1);
       tc_fence_after();
-      for (int ug = 0; ug < SUB * G; ++ug) {
-        const int u = ug / G, g = ug - u * G;
+      for (int u = 0; u < SUB; ++u) {
         const int64_t pos = mt * MT + u * 128 + q * 32 + (tid & 31);
         float* o = nullptr;
         float* oblk = nullptr;
@@ -752,7 +751,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
         }
         for (int c = 16 * half; c < BN; c += 16 * (kEpiWarps / 4)) {
           uint32_t r[3][16];
-          const uint32_t ta = tmem + lane_base + acc * acc_cols + ug * PBS * BN + c;
+          const uint32_t ta = tmem + lane_base + acc * acc_cols + u * PBS * BN + c;
 #pragma unroll
           for (int p = 0; p < 3; ++p)
             if (p < PBS) tmem_ld16_nw(ta + p * BN, r[p]);
