@@ -122,6 +122,35 @@ def test_bake_utm_seams_colourless():
     assert all(o.rgb is None for o in out)
 
 
+def test_bake_fast_path_edges_and_shifted_keys():
+    """The splat's hot-patch fast path (points >= 2 cm inside a cell-aligned
+    window skip the CSR walk) against the oracle: a 3 x 3 tiling with one key
+    shifted by 3 mm (still within the 5 mm alignment tolerance) and one by
+    7 mm (outside it: its cell has two interior keys), with points packed
+    within +-3 cm of every window edge."""
+    from paper_2509_20198_b200.engine import bake_fullres
+    side = 3
+    centers = [[640.0 * i + 320.0, 640.0 * j + 320.0]
+               for j in range(side) for i in range(side)]
+    centers[4][0] += 0.003
+    centers[4][1] -= 0.002
+    centers[2][0] += 0.007
+    centers = [tuple(c) for c in centers]
+    keys, bases = _keys_and_bases(centers, seed=4)
+    xyz, rgb = _grouped_points(side, 20000, 11)
+    rng = np.random.default_rng(12)
+    n = 60000
+    ex = 640.0 * rng.integers(0, side + 1, n) + rng.uniform(-0.03, 0.03, n)
+    ey = rng.uniform(0.0, 640.0 * side, n)
+    flip = rng.random(n) < 0.5
+    ex, ey = np.where(flip, ey, ex), np.where(flip, ex, ey)
+    edge = np.stack([ex, ey, rng.uniform(90.0, 110.0, n)], 1)
+    xyz = np.concatenate([xyz, edge])
+    rgb = np.concatenate([rgb, rng.random((n, 3), dtype=np.float32)])
+    out = bake_fullres(xyz, rgb, bases, keys)
+    _check(out, xyz, rgb, keys, bases)
+
+
 def test_bin_points_groups_by_cell_and_keeps_the_bake():
     """ts_bake_bin: a permutation of the points, non-decreasing 640 m cell
     of the key grid (outside points last), and the bake of the binned
