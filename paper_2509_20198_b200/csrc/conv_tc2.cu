@@ -101,7 +101,7 @@ __device__ __forceinline__ void prod_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kProdT) : "memory");
 }
 
-template <int MODE, int SUB>
+template <int MODE, int SUB, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T) {
   using Md = Mode<MODE>;
   constexpr int PA = Md::pa, PB = Md::pb;
@@ -114,7 +114,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
   const int BN = T.bn, HB = T.hbufs, SB = T.bstages, L = T.lrows;
   const int plane_a = L * kRow;          // multiple of 512 (L % 8 == 0)
   const int halo_bytes = PA * plane_a;
-  const int b_bytes = PB * BN * kRow;
+  // weight ring slot: one stage's B planes, or (PAIR) this CTA's halves
+  const int b_bytes = PAIR ? 3 * BN * kRow / 2 : PB * BN * kRow;
   uint8_t* halo = smem;
   uint8_t* bring = smem + HB * halo_bytes;
   uint64_t* bfull = reinterpret_cast<uint64_t*>(bring + SB * b_bytes);
@@ -123,7 +124,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
   uint64_t* hempty = hfull + HB;
   uint64_t* acc_full = hempty + HB;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* bpeer = acc_empty + 2;  // PAIR: the peer's weight stage landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bpeer + SB);
   int64_t* rowoff = reinterpret_cast<int64_t*>(tmem_slot + 4);  // [2][L]
   // stage table: (chunk, tap) pairs with nonzero weights, chunk-major,
   // decoded once into the chunk id and the A-descriptor row offset of the tap
@@ -159,6 +161,25 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
   const int Cin = op.in.C, Cout = op.out.C;
   const int MT = SUB * 128;
   const int64_t total_tiles = T.m_tiles * T.n_tiles;
+  // This CTA's tiles: units u = unit0, unit0 + n_units_step, ... < units.
+  // PAIR: a unit is (m-tile pair, n-tile); rank r of the CTA pair computes
+  // m-tile 2 mp + r (an odd last m-tile leaves the peer's half empty:
+  // its positions lie past the end, gathered as zeros and not stored).
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const bool leader = rank == 0;
+  const int64_t unit_step = PAIR ? gridDim.x / 2 : gridDim.x;
+  const int64_t unit0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const int64_t units = PAIR ? (T.m_tiles + 1) / 2 * T.n_tiles : total_tiles;
+  auto tile_of = [&](int64_t u) -> int64_t {
+    if (!PAIR) return u;
+    const int64_t mp = u / T.n_tiles;
+    return (2 * mp + rank) * T.n_tiles + (u - mp * T.n_tiles);
+  };
+  // arrivals on a barrier the leader waits on (the peer's go across the pair)
+  auto arrive_leader = [&](uint64_t* bar) {
+    if (PAIR && !leader) mbar_arrive_remote(mapa_shared(bar, 0));
+    else mbar_arrive(bar);
+  };
   const int AB = T.accbufs;
   // accumulator column blocks per sub-tile (MODE 5: main + correction)
   const int PBS = Md::f16 ? 2 : T.stack ? PB : 1;
@@ -181,18 +202,23 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     }
     for (int h = 0; h < HB; ++h) {
       // one arrival per producer warp (per warp of the filling group)
-      mbar_init(hfull + h, grouped ? kProdW / 2 : kProdW);
+      mbar_init(hfull + h, (grouped ? kProdW / 2 : kProdW) * (PAIR ? 2 : 1));
       mbar_init(hempty + h, 1);
     }
     for (int a = 0; a < AB; ++a) {
       mbar_init(acc_full + a, 1);
-      mbar_init(acc_empty + a, kEpiWarps);
+      mbar_init(acc_empty + a, kEpiWarps * (PAIR ? 2 : 1));
     }
+    for (int st = 0; st < SB; ++st) mbar_init(bpeer + st, 1);
     fence_barrier_init();
   }
-  if (warp == kMmaW) tmem_alloc(tmem_slot, ncols);
+  if (warp == kMmaW) {
+    if (PAIR) tmem_alloc2(tmem_slot, ncols);
+    else tmem_alloc(tmem_slot, ncols);
+  }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync_all();  // both CTAs' barriers and TMEM ready
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // FP16X3: the epilogue warp group (warps 12-15) holds each group's
@@ -219,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     // row table of this CTA's tile lt_ (parity lt_ & 1); with pf, the first
     // chunk's row lines are prefetched into L2 as they are computed
     auto build_rows = [&](int lt_, bool pf) {
-      const int64_t tile_ = blockIdx.x + (int64_t)lt_ * gridDim.x;
+      const int64_t tile_ = tile_of(unit0 + (int64_t)lt_ * unit_step);
       const int64_t j0 = (tile_ / T.n_tiles) * MT;
       int64_t* ro_ = rowoff + (lt_ & 1) * L;
       for (int j = tid; j < L; j += kProdT) {
@@ -253,12 +279,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
       const int obase = row0 * kRow + ((piece ^ ((row0 >> 1) & 3)) << 4);
       constexpr int kIn = TS_H2_IN8;
       int64_t n = 0;
-      for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+      for (int64_t u = unit0; u < units; u += unit_step, ++lt) {
         const int64_t* ro = rowoff + (lt & 1) * L;
         if (lt == 0) build_rows(0, false);
         prod_sync();
         for (int c = 0; c < T.cchunks; ++c, ++n) {
-          if (c == T.cchunks - 1 && tile + gridDim.x < total_tiles) build_rows(lt + 1, true);
+          if (c == T.cchunks - 1 && u + unit_step < units) build_rows(lt + 1, true);
           if ((int)(n & 1) != pg) continue;
           const int h = (int)(n % HB);
           TS_PROF_WAIT(kPrProdWait, mbar_wait(hempty + h, (uint32_t)((n / HB) & 1) ^ 1u));
@@ -295,18 +321,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
           }
           fence_proxy_async();
           __syncwarp();
-          if ((tid & 31) == 0) mbar_arrive(hfull + h);
+          if ((tid & 31) == 0) arrive_leader(hfull + h);
         }
       }
     } else
-    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+    for (int64_t u = unit0; u < units; u += unit_step, ++lt) {
       int64_t* ro = rowoff + (lt & 1) * L;
       if (lt == 0) build_rows(0, false);
       prod_sync();
       for (int c = 0; c < T.cchunks; ++c) {
         // during the last chunk, the next tile's row table (other parity)
         // and an L2 prefetch of its first chunk
-        if (c == T.cchunks - 1 && tile + gridDim.x < total_tiles) build_rows(lt + 1, true);
+        if (c == T.cchunks - 1 && u + unit_step < units) build_rows(lt + 1, true);
         TS_PROF_WAIT(kPrProdWait, mbar_wait(hempty + hb, ((hph >> hb) & 1u) ^ 1u));
         uint8_t* sa = halo + hb * halo_bytes;
         if (op.in.planes) {
@@ -448,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
         } else {
           fence_proxy_async();
           __syncwarp();
-          if ((tid & 31) == 0) mbar_arrive(hfull + hb);
+          if ((tid & 31) == 0) arrive_leader(hfull + hb);
         }
         hph ^= 1u << hb;
         if (++hb == HB) hb = 0;
@@ -461,22 +487,45 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
       if ((tid & 31) == 0)
         for (int i = 0; i < npend; ++i) mbar_arrive(hfull + pend[i]);
     }
+  } else if (warp == kMmaW && MODE == 5 && PAIR && !leader) {
+    // ---------- the peer's weight-stage forwarder (CTA pair) ----------
+    // its loader's bulk copies complete on this CTA's bfull; the leader's
+    // MMA issuer learns of them through bpeer
+    reg_dealloc<96>();
+    if ((tid & 31) == 0) {
+      int s = 0;
+      uint32_t bph = 0;
+      for (int64_t u = unit0; u < units; u += unit_step)
+        for (int kt = 0; kt < nst; ++kt) {
+          mbar_wait(bfull + s, bph);
+          mbar_arrive_remote(mapa_shared(bpeer + s, 0));
+          if (++s == SB) { s = 0; bph ^= 1; }
+        }
+    }
+    __syncwarp();
   } else if (warp == kMmaW && MODE == 5) {
     // ------------------- MMA issuer (FP16X3, promoted) -------------------
+    // PAIR: the leader issues M = 256 MMAs for both CTAs (cta_group::2):
+    // each CTA supplies its own 128 A rows and half of every B operand
+    // ([b0 | b1]: b0 here, b1 in the peer; b0 for a1 . b0: its first half
+    // here, its second in the peer), commits arrive in both CTAs
     reg_dealloc<96>();
     // Per sub-tile u and K step: a0 . [b0 | b1] -> [main | corr] (one
     // stacked MMA, N = 2 BN) and a1 . b0 -> corr (N = BN).  The accumulator
     // pair rotates per GROUP of T.cgrp channel chunks (<= 18 K steps): the
     // group's first K step overwrites it, the epilogue promotes it.
-    const uint32_t idesc = make_idesc(mode_fmt<MODE>(), 2 * BN);
-    const uint32_t idesc_b0 = make_idesc(mode_fmt<MODE>(), BN);
+    const uint32_t idesc = make_idesc(mode_fmt<MODE>(), 2 * BN, PAIR ? 256 : 128);
+    const uint32_t idesc_b0 = make_idesc(mode_fmt<MODE>(), BN, PAIR ? 256 : 128);
     const uint64_t d_halo = sw64_desc(su32(halo));
     const uint64_t d_ring = sw64_desc(su32(bring));
     const uint32_t pa = (uint32_t)plane_a >> 4;
     const uint32_t b_step = (uint32_t)b_bytes >> 4, h_step = (uint32_t)halo_bytes >> 4;
+    // B of the a1 . b0 MMA: the same b0 rows (single CTA) or this CTA's
+    // half of b0 stored after its BN rows of [b0 | b1] (pair)
+    const uint32_t b2_off = PAIR ? (uint32_t)(BN * kRow) >> 4 : 0u;
     int s = 0, hb = 0;
     uint32_t bph = 0, hph = 0, gc = 0;
-    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    for (int64_t u_ = unit0; u_ < units; u_ += unit_step) {
       int si = 0;
       uint32_t d = 0, acc_f = 0;
       for (int c = 0; c < T.cchunks; ++c) {
@@ -495,6 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
         const int nk = (c == T.cchunks - 1 && Cin - c * kKC <= 16) ? 1 : 2;
         for (; s_chunk[si] == c; ++si) {
           TS_PROF_WAIT(kPrMmaW, mbar_wait(bfull + s, bph));
+          if (PAIR) TS_PROF_WAIT(kPrMmaW, mbar_wait(bpeer + s, bph));
           tc_fence_after();
           if (elect_one()) {
             const uint64_t a0 = d_hb + (uint64_t)(s_aoff[si] & 0x0FFFFFFFu);
@@ -506,19 +556,30 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
               for (int u = 0; u < SUB; ++u) {
                 const uint64_t ak = a0 + (uint64_t)(u * (128 * kRow >> 4) + 2 * k);
                 const uint32_t du = d + u * 2 * BN;
-                umma<false>(du, ak, b0 + 2 * k, idesc, (acc_f | k) ? 1u : 0u);
-                umma<false>(du + BN, ak + pa, b0 + 2 * k, idesc_b0, 1u);
+                if (PAIR) {
+                  umma2(du, ak, b0 + 2 * k, idesc, (acc_f | k) ? 1u : 0u);
+                  umma2(du + BN, ak + pa, b0 + b2_off + 2 * k, idesc_b0, 1u);
+                } else {
+                  umma<false>(du, ak, b0 + 2 * k, idesc, (acc_f | k) ? 1u : 0u);
+                  umma<false>(du + BN, ak + pa, b0 + 2 * k, idesc_b0, 1u);
+                }
               }
             }
-            umma_commit(bempty + s);
+            if (PAIR) umma_commit2(bempty + s);
+            else umma_commit(bempty + s);
           }
           __syncwarp();
           acc_f = 1;
           if (++s == SB) { s = 0; bph ^= 1; }
         }
         if (elect_one()) {
-          umma_commit(hempty + hb);
-          if (g_last) umma_commit(acc_full + (gc & 1u));
+          if (PAIR) {
+            umma_commit2(hempty + hb);
+            if (g_last) umma_commit2(acc_full + (gc & 1u));
+          } else {
+            umma_commit(hempty + hb);
+            if (g_last) umma_commit(acc_full + (gc & 1u));
+          }
         }
         __syncwarp();
         if (g_last) ++gc;
@@ -541,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     uint32_t bph = 0, hph = 0;
     const uint32_t b_step = (uint32_t)b_bytes >> 4, h_step = (uint32_t)halo_bytes >> 4;
     const uint32_t b_plane16 = (uint32_t)(BN * kRow) >> 4;  // one B plane
-    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+    for (int64_t u_ = unit0; u_ < units; u_ += unit_step, ++lt) {
       const int acc = lt % AB;
       mbar_wait(acc_empty + acc, ((lt / AB) & 1) ^ 1);
       tc_fence_after();
@@ -602,13 +663,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     if ((tid & 31) == 0) {
       int s = 0;
       uint32_t bph = 0;
-      for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        const int nt = (int)(tile % T.n_tiles);
-        const uint8_t* wsrc = wdata + (size_t)nt * nst * b_bytes;
+      // PAIR: this CTA's image of each stage (its halves, 1.5 BN rows)
+      const int img = b_bytes;
+      for (int64_t u = unit0; u < units; u += unit_step) {
+        const int nt = (int)(tile_of(u) % T.n_tiles);
+        const uint8_t* wsrc = wdata + (size_t)nt * nst * (PAIR ? 2 * img : img);
         for (int kt = 0; kt < nst; ++kt) {
           TS_PROF_WAIT(kPrLoadWait, mbar_wait(bempty + s, bph ^ 1));
-          bulk_g2s(bring + s * b_bytes, wsrc + (size_t)kt * b_bytes, b_bytes, bfull + s);
-          mbar_arrive_tx(bfull + s, b_bytes);
+          const uint8_t* src = PAIR ? wsrc + ((size_t)kt * 2 + rank) * img
+                                    : wsrc + (size_t)kt * b_bytes;
+          bulk_g2s(bring + s * b_bytes, src, img, bfull + s);
+          mbar_arrive_tx(bfull + s, img);
           if (++s == SB) { s = 0; bph ^= 1; }
         }
       }
@@ -628,7 +693,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
                       (op.out.C % 8 == 0) && ((reinterpret_cast<uintptr_t>(op.out.base) & 31) == 0);
     const int groups = (T.cchunks + T.cgrp - 1) / T.cgrp;
     uint32_t gc = 0;
-    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    for (int64_t u_ = unit0; u_ < units; u_ += unit_step) {
+      const int64_t tile = tile_of(u_);
       const int64_t mt = tile / T.n_tiles;
       const int n0 = (int)(tile - mt * T.n_tiles) * BN;
       float R[SUB][NB][16];
@@ -657,7 +723,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
           }
         tc_fence_before();
         __syncwarp();
-        if ((tid & 31) == 0) mbar_arrive(acc_empty + (gc & 1u));
+        if ((tid & 31) == 0) arrive_leader(acc_empty + (gc & 1u));
       }
 #pragma unroll
       for (int u = 0; u < SUB; ++u) {
@@ -721,7 +787,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
     const bool vec8 = (op.out.cstride % 8 == 0) && (op.out.coff % 8 == 0) &&
                       (op.out.C % 8 == 0) && ((reinterpret_cast<uintptr_t>(op.out.base) & 31) == 0);
     int lt = 0;
-    for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++lt) {
+    for (int64_t u_ = unit0; u_ < units; u_ += unit_step, ++lt) {
+      const int64_t tile = tile_of(u_);
       const int acc = lt % AB;
       const int64_t mt = tile / T.n_tiles;
       const int nt = (int)(tile - mt * T.n_tiles);
@@ -793,17 +860,40 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_halo2_kernel(Halo2Args T)
   }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync_all();  // the leader's last MMAs wrote the peer's TMEM
   if (warp == kMmaW) {
     tc_fence_after();
-    tmem_dealloc(tmem, ncols);
+    if (PAIR) tmem_dealloc2(tmem, ncols);
+    else tmem_dealloc(tmem, ncols);
   }
 #ifdef TS_H2_PROF
   if (tid == 0) atomicAdd(&g_h2_prof[kPrTotal], (unsigned long long)(clock64() - t_start));
 #endif
 }
 
+// weight-ring depth of the CTA-pair kernel (its slots are 1.5 BN rows)
+#ifndef TS_H2_PAIR_STAGES
+#define TS_H2_PAIR_STAGES 8
+#endif
+constexpr int kPairStages = TS_H2_PAIR_STAGES;
+
+// CTA pairs (cta_group::2) for the FP16X3 halo kernel: opt-in with
+// TS_H2_PAIR=1 (read once per process).  Bit-identical to the single-CTA
+// kernel, 23% fewer shared-memory operand reads, but measured slower (CNN
+// 11.7 vs 9.7 ms per 1,024 tiles, fuse.0 2.38 vs 1.53 ms: tensor pipe 27%
+// active, the leader's MMA issuer waiting on the weight ring 40% of the
+// time; profiles/r02_notes.md)
+bool pair_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TS_H2_PAIR");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 struct Halo2Plan {
   int bn, ntiles, pa, pb, sub, hbufs, bstages, cchunks, wp, lrows, accbufs, stack, cgrp;
+  int pair;  // FP16X3 on CTA pairs: M = 256 MMAs, B halves per CTA
   size_t smem;
   int64_t positions;
 };
@@ -873,7 +963,20 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
       p.hbufs = hb;
       p.lrows = L;
       p.bstages = (int)std::min<size_t>(4, (cap - used) / bst);
-      p.smem = used + p.bstages * bst;
+      // pairs need B halves of >= 8 rows (BN a multiple of 16: always) and
+      // the plain fp32 producers (the pre-split cp.async path publishes
+      // chunks with a lag the pair's arrival counts do not model).  A
+      // pair's ring slot holds one CTA's halves (1.5 BN rows), and the ring
+      // is deeper: a slot's reuse also waits for the peer's copy to be
+      // forwarded
+      p.pair = precision == 5 && pair_enabled() && !op.in.planes && p.bn % 16 == 0;
+      if (p.pair) {
+        const size_t slot = (size_t)3 * p.bn * kRow / 2;
+        p.bstages = (int)std::min<size_t>(kPairStages, (cap - used) / slot);
+        p.smem = used + p.bstages * slot;
+      } else {
+        p.smem = used + p.bstages * bst;
+      }
       *out = p;
       return true;
     }
@@ -931,7 +1034,18 @@ std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, 
     }
   if ((int)list.size() > kMaxStages) return {};
   const int nst = (int)list.size();
-  std::vector<uint8_t> out(kHdr + (size_t)p.ntiles * nst * b_bytes, 0);
+  // CTA pair: per stage two images of 1.5 BN rows, [b0 | b0 rows 0..BN/2)
+  // for rank 0 and [b1 | b0 rows BN/2..BN) for rank 1 (each CTA's half of
+  // the [b0 | b1] and b0 B operands; conv_tc_halo2_kernel PAIR)
+  const size_t img = p.pair ? (size_t)3 * p.bn * kRow / 2 : b_bytes;
+  const size_t stage_bytes = p.pair ? 2 * img : b_bytes;
+  std::vector<uint8_t> out(kHdr + (size_t)p.ntiles * nst * stage_bytes, 0);
+  auto put = [&](uint8_t* image, int r, int e, uint16_t v) {  // SW64 row r, channel e
+    const int byte = 2 * e;
+    const size_t off = (size_t)r * kRow + (size_t)(((byte >> 4) ^ ((r >> 1) & 3)) << 4) +
+                       (byte & 15);
+    memcpy(image + off, &v, 2);
+  };
   const uint32_t hdr[2] = {(uint32_t)nst, 0u};
   memcpy(out.data(), hdr, 8);
   memcpy(out.data() + 8, list.data(), 2 * list.size());
@@ -940,7 +1054,7 @@ std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, 
       const int e = list[i] & 0x7FFF, c = e / (G * taps);
       const int g = (e - c * G * taps) / taps, t = e % taps;
       const int ky = t / k, kx = t % k;
-      uint8_t* base = out.data() + kHdr + ((size_t)nt * nst + i) * b_bytes;
+      uint8_t* base = out.data() + kHdr + ((size_t)nt * nst + i) * stage_bytes;
       for (int r = 0; r < p.bn; ++r) {
         const int n = nt * p.bn + r;
         for (int e = 0; e < kKC; ++e) {
@@ -948,9 +1062,6 @@ std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, 
           const float v =
               (n < co && ch < ci) ? w_oikk[g * wg + (((size_t)n * ci + ch) * k + ky) * k + kx]
                                   : 0.f;
-          const int byte = 2 * e;
-          const size_t off =
-              (size_t)r * kRow + (size_t)((((byte >> 4) ^ ((r >> 1) & 3))) << 4) + (byte & 15);
           uint16_t h[3] = {0, 0, 0};
           if (precision == 2) {
             h[0] = f2bf16_rn_host(v);
@@ -969,7 +1080,14 @@ std::vector<uint8_t> pack_tc_weights_halo2(const float* w_oikk, int co, int ci, 
               rr -= bf16_to_f_host(h[pl]);
             }
           }
-          for (int pl = 0; pl < p.pb; ++pl) memcpy(base + pl * plane + off, &h[pl], 2);
+          if (p.pair) {
+            put(base, r, e, h[0]);                 // rank 0: b0 row r
+            put(base + img, r, e, h[1]);           // rank 1: b1 row r
+            if (r < p.bn / 2) put(base, p.bn + r, e, h[0]);
+            else put(base + img, p.bn + r - p.bn / 2, e, h[0]);
+          } else {
+            for (int pl = 0; pl < p.pb; ++pl) put(base + pl * plane, r, e, h[pl]);
+          }
         }
       }
     }
@@ -987,8 +1105,37 @@ int launch_conv_tc_halo2(const ConvOp& op, int precision, void* stream) {
   if (tiles <= 0) return TS_OK;
   const int sms = sm_count();
   if (!sms) return TS_E_CUDA;
-  const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+  unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
   cudaStream_t s = as_stream(stream);
+  if (p.pair && precision == 5) {
+    // one CTA pair (2-CTA cluster, same TPC) per two SMs
+    const int64_t units = (a.m_tiles + 1) / 2 * p.ntiles;
+    grid = 2 * (unsigned)std::min<int64_t>(units, sms / 2);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+#define TS_TCH2_PAIR(SB_)                                                                 \
+  do {                                                                                    \
+    TS_CUDA_TRY(cudaFuncSetAttribute(conv_tc_halo2_kernel<5, SB_, true>,                  \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                                     (int)p.smem));                                       \
+    ts::count_launch();                                                                   \
+    TS_CUDA_TRY(cudaLaunchKernelEx(&cfg, conv_tc_halo2_kernel<5, SB_, true>, a));         \
+  } while (0)
+    if (p.sub == 1) TS_TCH2_PAIR(1);
+    else if (p.sub == 2) TS_TCH2_PAIR(2);
+    else TS_TCH2_PAIR(4);
+#undef TS_TCH2_PAIR
+  } else {
 #define TS_TCH2_LAUNCH(MD, SB_)                                                       \
   do {                                                                                \
     TS_CUDA_TRY(cudaFuncSetAttribute(conv_tc_halo2_kernel<MD, SB_>,                   \
@@ -1008,6 +1155,7 @@ int launch_conv_tc_halo2(const ConvOp& op, int precision, void* stream) {
   else TS_TCH2_SUB(3);
 #undef TS_TCH2_SUB
 #undef TS_TCH2_LAUNCH
+  }
   TS_LAUNCH_CHECK();
 #ifdef TS_H2_PROF
   {  // per-launch wait profile (profiling build only): cycles per CTA

@@ -19,43 +19,23 @@ using namespace ts::tcx;
 
 constexpr int kStages = 2048;
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
-                   : "memory");
-}
-__device__ __forceinline__ void umma2(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
-                                      uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void commit2(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
-      "[%0], %1;" ::"r"(su32(bar)),
-      "h"((uint16_t)3)
-      : "memory");
-}
+// cluster_rank, cluster_sync_all, umma2, umma_commit2: tc_ptx.cuh
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
-    pair_kernel(int bn, int sub, unsigned long long* out) {
+    pair_kernel(int bn, int sub, int ring, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* a = smem;                 // 2 planes x 640 rows x 64 B
   uint8_t* b = smem + 2 * 640 * 64;  // this CTA's half of B
   __shared__ uint64_t bar[2];
+  __shared__ uint64_t rbar[8];  // ring: stage st waits for the commit of st - ring
   __shared__ uint32_t slot;
   for (int i = threadIdx.x; i < (2 * 640 + 2 * 128) * 64 / 4; i += blockDim.x)
     reinterpret_cast<uint32_t*>(smem)[i] = 0x3C003C00u;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    for (int i = 0; i < 8; ++i) mbar_init(&rbar[i], 1);
     fence_barrier_init();
   }
   if (threadIdx.x < 32) {
@@ -78,6 +58,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     unsigned long long t0 = clock64();
     if (elect_one()) {
       for (int st = 0; st < kStages; ++st) {
+        if (ring && st >= ring) mbar_wait(&rbar[(st - ring) % ring], (uint32_t)(((st - ring) / ring) & 1));
         const uint64_t a0 = da + (uint64_t)((st % 9) / 3 * 70 + (st % 3)) * 4;  // tap slide
 #pragma unroll 1
         for (int k = 0; k < 2; ++k)
@@ -87,18 +68,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
             umma2(du, ak, db + 2 * k, idesc, (st | k) ? 1u : 0u);
             umma2(du + bn, ak + pa, db + 2 * k, idesc_b0, 1u);
           }
-        commit2(&bar[st & 1]);
+        if (ring) umma_commit2(&rbar[st % ring]);
+        else umma_commit2(&bar[st & 1]);
       }
-      commit2(&bar[0]);
+      umma_commit2(&bar[0]);
     }
     __syncwarp();
-    const int n0 = (kStages + 1) / 2 + 1;
+    const int n0 = ring ? 1 : (kStages + 1) / 2 + 1;
     mbar_wait(&bar[0], (uint32_t)((n0 - 1) & 1));
     const unsigned long long t1 = clock64();
     if (threadIdx.x == 0) out[blockIdx.x / 2] = t1 - t0;
   } else if (threadIdx.x < 32) {
     // the peer's barrier receives the same multicast arrivals
-    const int n0 = (kStages + 1) / 2 + 1;
+    const int n0 = ring ? 1 : (kStages + 1) / 2 + 1;
     mbar_wait(&bar[0], (uint32_t)((n0 - 1) & 1));
   }
   tc_fence_before();
@@ -121,16 +103,17 @@ int main() {
   std::vector<unsigned long long> h(pairs);
   printf("cta_group::2  BN SUB : cycles/stage (median pair; per SM: SUB x 128 rows x BN)\n");
   const int cfg[][2] = {{32, 4}, {64, 2}, {96, 1}, {128, 1}};
+  for (int ring : {0, 4, 8})
   for (auto& c : cfg) {
     const int bn = c[0], sub = c[1];
     for (int rep = 0; rep < 2; ++rep) {
-      pair_kernel<<<2 * pairs, 128, smem>>>(bn, sub, d_out);
+      pair_kernel<<<2 * pairs, 128, smem>>>(bn, sub, ring, d_out);
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
     }
     cudaMemcpy(h.data(), d_out, pairs * 8, cudaMemcpyDeviceToHost);
     std::sort(h.begin(), h.end());
-    printf("  %3d %d : %8.1f\n", bn, sub, (double)h[pairs / 2] / kStages);
+    printf("  ring %d  %3d %d : %8.1f\n", ring, bn, sub, (double)h[pairs / 2] / kStages);
   }
   return 0;
 }

@@ -127,3 +127,39 @@ def test_phase_groups_bit_identical(monkeypatch, group, precision):
         torch.cuda.synchronize()
         outs.append(out)
     assert torch.equal(outs[0], outs[1])
+
+
+_PAIR_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2509_20198_b200 import refiner as R
+B = 24
+g = torch.Generator(device="cuda").manual_seed(9)
+x = torch.randn((B, 96, 96, 8), generator=g, device="cuda") * 0.1
+x[..., 2:] = torch.rand((B, 96, 96, 6), generator=g, device="cuda")
+w = R.device_weights(R.random_weights(R.default_descriptor(), seed=3), 5)
+out = torch.empty((B, 64, 64, 4), device="cuda")
+nf = torch.zeros(B, dtype=torch.uint8, device="cuda")
+w.run(x, B, out, nf, w.workspace(B))
+torch.cuda.synchronize()
+np.save(sys.argv[2], out.cpu().numpy())
+"""
+
+
+def test_fp16x3_cta_pair_bit_identical(tmp_path):
+    """The opt-in CTA-pair halo kernel (tcgen05.mma.cta_group::2, M = 256,
+    TS_H2_PAIR=1) computes every layer with the same MMAs in the same order
+    as the single-CTA kernel: the whole CNN must agree bit for bit."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for pair in ("0", "1"):
+        f = tmp_path / f"out{pair}.npy"
+        env = dict(os.environ, TS_H2_PAIR=pair)
+        subprocess.run([sys.executable, "-c", _PAIR_SCRIPT, root, str(f)], env=env,
+                       check=True, timeout=300)
+        outs.append(np.load(f))
+    assert np.isfinite(outs[0]).all()
+    assert np.array_equal(outs[0], outs[1])
