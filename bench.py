@@ -452,7 +452,7 @@ def run_country(args, pipe, dev, world, rank):
     through the pipeline in blocks with halo rings, row bands across ranks,
     refined tiles kept on each GPU and gathered to rank 0 (NCCL).  Timed on
     the device from the first block to the gather, max over ranks; tile
-    images are synthesised on the host by a producer thread overlapping the
+    images are assembled on the host by a producer thread overlapping the
     kernels (paper_2509_20198_b200/country.py)."""
     import torch
     import torch.distributed as dist
@@ -500,9 +500,10 @@ def run_country(args, pipe, dev, world, rank):
             "blocks_per_rank": blocks, "seconds": round(ms / 1e3, 3),
             "gather_ms": round(ms_gather, 2), "tiles_on_rank0": got,
             "failed_tiles": bad,
-            "data": "synthetic: 256 stub-body tiles re-placed per virtual "
-                    "tile on the host (producer thread, pinned H2D on a "
-                    "copy stream) inside the timed region"}
+            "data": "synthetic: 256 stub-body pool tiles concatenated per "
+                    "block on the host (producer thread, pinned H2D on a "
+                    "copy stream), first records moved to the virtual tile "
+                    "on the device, inside the timed region"}
 
 
 def run_lazdec(args):

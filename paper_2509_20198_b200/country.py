@@ -19,9 +19,11 @@ measured path): a pool of distinct stub-body LAZ tiles generated once
 (``synth.grid_tiles``) is re-used with every chunk's first record moved to
 the virtual tile's footprint (x, y integers shifted by whole tiles), so the
 chunk tables, record formats and per-tile point counts are those of real
-tiles.  A producer thread builds block i+1's images (numpy, releases the
-GIL) and stages them in pinned memory while the GPU runs block i; the
-upload runs on a copy stream.
+tiles.  A producer thread concatenates block i+1's pool images straight into
+pinned memory (one numpy call) while the GPU runs block i; the upload runs
+on a copy stream and the record moves are applied on the device
+(``TilePool.move_records``, byte-for-byte what ``images_for`` does on the
+host).
 """
 
 from __future__ import annotations
@@ -53,6 +55,15 @@ class TilePool:
         self.n = len(tiles)
         self.images = [np.frombuffer(t.data, np.uint8) for t in tiles]
         self.sizes = np.array([len(t.data) for t in tiles], np.int64)
+        # the images again, each zero-padded to 16 bytes, as views of one
+        # array (the block buffers are their concatenation)
+        self.aligned = (self.sizes + 15) // 16 * 16
+        flat = np.zeros(int(self.aligned.sum()), np.uint8)
+        o = np.concatenate([[0], np.cumsum(self.aligned)[:-1]])
+        for i, im in enumerate(self.images):
+            flat[o[i]:o[i] + len(im)] = im
+        self.padded = [flat[o[i]:o[i] + self.aligned[i]] for i in range(self.n)]
+        self._rec_off_dev = {}
         self.pos = np.array([[round(t.x0 / TILE), round(t.y0 / TILE)]
                              for t in tiles], np.int64)
         self.rec_off = np.stack([t.chunk_offsets for t in tiles]).astype(np.int64)
@@ -63,6 +74,49 @@ class TilePool:
 
     def pick(self, cx: np.ndarray, cy: np.ndarray) -> np.ndarray:
         return (cx * 7919 + cy * 104729) % self.n
+
+    def stage(self, cx: np.ndarray, cy: np.ndarray):
+        """Block staging for the streaming driver: the chosen pool images
+        concatenated into a pinned buffer (records NOT yet moved), the
+        descriptors, and a pinned int64 (4, n) array (pool tile, image
+        offset, x and y shift in record units) for ``move_records``."""
+        k = self.pick(cx, cy)
+        al = self.aligned[k]
+        offs = np.zeros(len(k), np.int64)
+        offs[1:] = np.cumsum(al)[:-1]
+        total = int(al.sum())
+        pinned = torch.empty(total + D.TileBatch.PAD, dtype=torch.uint8, pin_memory=True)
+        host = pinned.numpy()
+        np.concatenate([self.padded[i] for i in k], out=host[:total])
+        host[total:] = 0
+        meta = torch.empty((4, len(k)), dtype=torch.int64, pin_memory=True)
+        m = meta.numpy()
+        m[0], m[1] = k, offs
+        m[2] = (cx - self.pos[k, 0]) * self.step[0]
+        m[3] = (cy - self.pos[k, 1]) * self.step[1]
+        descs = self.desc[k].copy()
+        descs["file_offset"] = offs
+        descs["file_size"] = self.sizes[k]
+        return pinned, descs, meta
+
+    def move_records(self, d_bytes: torch.Tensor, meta: torch.Tensor) -> None:
+        """On the device: every chunk's first record of tile i moves by
+        (meta[2, i], meta[3, i]) record units in x and y (little-endian int32
+        at record bytes 0 and 4, wrapping like the host path)."""
+        dev = d_bytes.device
+        ro = self._rec_off_dev.get(dev)
+        if ro is None:
+            ro = self._rec_off_dev[dev] = torch.from_numpy(self.rec_off).to(dev)
+        nch = ro.shape[1]
+        idx = (meta[1][:, None] + ro[meta[0]]).reshape(-1)
+        for axis, shift in ((0, meta[2]), (4, meta[3])):
+            j = idx + axis
+            v = torch.zeros_like(j)
+            for t in range(4):
+                v |= d_bytes[j + t].to(torch.int64) << (8 * t)
+            v = (v + shift.repeat_interleave(nch)) & 0xFFFFFFFF
+            for t in range(4):
+                d_bytes[j + t] = ((v >> (8 * t)) & 0xFF).to(torch.uint8)
 
     def images_for(self, cx: np.ndarray, cy: np.ndarray):
         """Host image buffer (16-byte aligned tiles) + descriptors."""
@@ -112,14 +166,13 @@ class CountryRun:
         h0, h1 = max(0, r0 - 1), min(self.rows, r1 + 1)
         g0, g1 = max(0, c0 - 1), min(self.cols, c1 + 1)
         cy, cx = np.meshgrid(np.arange(h0, h1), np.arange(g0, g1), indexing="ij")
-        buf, descs = self.pool.images_for(cx.ravel(), cy.ravel())
-        pinned = torch.from_numpy(buf).pin_memory()
+        pinned, descs, meta = self.pool.stage(cx.ravel(), cy.ravel())
         oy, ox = np.meshgrid(np.arange(r0, r1), np.arange(c0, c1), indexing="ij")
         centers = np.stack([ox.ravel() * TILE + TILE / 2,
                             oy.ravel() * TILE + TILE / 2], 1)
         cr = HeightmapPipeline.cell_range((g0 * TILE, h0 * TILE),
                                           (g1 * TILE, h1 * TILE))
-        return blk, pinned, descs, centers, cr
+        return blk, pinned, descs, meta, centers, cr
 
     def run(self, on_block=None):
         """Process every block; returns host-side block count.  on_block(i)
@@ -140,12 +193,19 @@ class CountryRun:
             item = q.get()
             if item is None:
                 break
-            (c0, c1, r0, r1), pinned, descs, centers, cr = item
-            d_bytes = torch.empty(pinned.shape, dtype=torch.uint8, device=self.dev)
+            (c0, c1, r0, r1), pinned, descs, meta, centers, cr = item
+            # allocated on the copy stream (written there first); the
+            # record_stream below keeps them from being reused there until
+            # the compute stream is done with them
             with torch.cuda.stream(copy_s):
+                d_bytes = torch.empty(pinned.shape, dtype=torch.uint8, device=self.dev)
+                d_meta = torch.empty(meta.shape, dtype=torch.int64, device=self.dev)
                 d_bytes.copy_(pinned, non_blocking=True)
+                d_meta.copy_(meta, non_blocking=True)
             stream.wait_stream(copy_s)
             d_bytes.record_stream(stream)
+            d_meta.record_stream(stream)
+            self.pool.move_records(d_bytes, d_meta)
             tb = D.TileBatch.from_device(d_bytes, descs)
             res = self.pipe.run(tb, centers, cr)
             # owned tiles of the block -> row-major slots of the band
