@@ -954,8 +954,14 @@ bool plan2(const ConvOp& op, int precision, Halo2Plan* out) {
     const size_t fixed = 1024 + 8 * 40 + 16 + 16 * (size_t)L + 6 * kMaxStages + 64 +
                          4 * (size_t)p.ntiles * p.bn + 16;
     // halo buffers: 3, else 2 (measured: 4-8 no faster); weight ring: up to
-    // 4 stages (measured: 3-4 about 1% faster than 8)
-    for (int hb : {3, 2}) {
+    // 4 stages (measured: 3-4 about 1% faster than 8).  Layers the kernel
+    // fills with two producer groups (FP16X3, L <= 160, 8-channel aligned
+    // input: conv_tc_halo2_kernel `grouped`) take an even count, so each
+    // buffer is always filled by the same group's threads
+    const bool grouped = precision == 5 && L <= 160 && !op.in.planes && op.in.C % 8 == 0 &&
+                         op.in.cstride % 8 == 0 && op.in.coff % 8 == 0;
+    const int hbs[2] = {grouped ? 4 : 3, 2};  // (4 vs 3: same time, within noise)
+    for (int hb : hbs) {
       const size_t used = hb * hbuf + fixed;
       if (used + 3 * bst > cap) continue;
       p.sub = sub;
