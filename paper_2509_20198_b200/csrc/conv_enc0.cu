@@ -53,16 +53,12 @@ __device__ __forceinline__ void enc0_accumulate(const float* __restrict__ halo, 
         const float x1 = hp[(ch0 + ci) * kEPlane + 4 * 2 * kEPitch];  // two output rows on
         const float4* w4 = reinterpret_cast<const float4*>(w + ((ky * 3 + kx) * CIN + ci) * CO);
 #pragma unroll
-        for (int o = 0; o < CH / 4; ++o) {
+        for (int o = 0; o < CH / 4; ++o) {  // packed fp32 FMAs (FFMA2)
           const float4 q = w4[o];
-          acc[0][4 * o] = fmaf(x0, q.x, acc[0][4 * o]);
-          acc[0][4 * o + 1] = fmaf(x0, q.y, acc[0][4 * o + 1]);
-          acc[0][4 * o + 2] = fmaf(x0, q.z, acc[0][4 * o + 2]);
-          acc[0][4 * o + 3] = fmaf(x0, q.w, acc[0][4 * o + 3]);
-          acc[1][4 * o] = fmaf(x1, q.x, acc[1][4 * o]);
-          acc[1][4 * o + 1] = fmaf(x1, q.y, acc[1][4 * o + 1]);
-          acc[1][4 * o + 2] = fmaf(x1, q.z, acc[1][4 * o + 2]);
-          acc[1][4 * o + 3] = fmaf(x1, q.w, acc[1][4 * o + 3]);
+          tcx::ffma2(acc[0][4 * o], acc[0][4 * o + 1], x0, q.x, q.y);
+          tcx::ffma2(acc[0][4 * o + 2], acc[0][4 * o + 3], x0, q.z, q.w);
+          tcx::ffma2(acc[1][4 * o], acc[1][4 * o + 1], x1, q.x, q.y);
+          tcx::ffma2(acc[1][4 * o + 2], acc[1][4 * o + 3], x1, q.z, q.w);
         }
       }
     }

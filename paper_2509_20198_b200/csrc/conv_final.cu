@@ -11,6 +11,7 @@
 #include <algorithm>
 
 #include "conv.cuh"
+#include "tc_ptx.cuh"
 #include "ts_common.cuh"
 
 namespace ts {
@@ -62,10 +63,11 @@ __global__ void __launch_bounds__(kFT * kFT) conv_final_kernel(const __grid_cons
         const float4 v = *reinterpret_cast<const float4*>(hp + 4 * g);
         const float xs[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-          for (int o = 0; o < kFCo; ++o)
-            acc[o] = fmaf(xs[j], A.w[((ky * 3 + kx) * kFCin + 4 * g + j) * kFCo + o], acc[o]);
+        for (int j = 0; j < 4; ++j) {
+          const float* w = A.w + ((ky * 3 + kx) * kFCin + 4 * g + j) * kFCo;
+          tcx::ffma2(acc[0], acc[1], xs[j], w[0], w[1]);  // packed fp32 FMAs
+          tcx::ffma2(acc[2], acc[3], xs[j], w[2], w[3]);
+        }
       }
     }
   if (A.lrelu)

@@ -115,6 +115,18 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
           su32(bar))
       : "memory");
 }
+// Packed fp32 FMA (sm_100 FFMA2): {a0, a1} = fma({x, x}, {w0, w1}, {a0, a1}),
+// each lane an IEEE fp32 fma (the same results as two fmaf calls, in half
+// the instructions)
+__device__ __forceinline__ void ffma2(float& a0, float& a1, float x, float w0, float w1) {
+  uint64_t a = ((uint64_t)__float_as_uint(a1) << 32) | __float_as_uint(a0);
+  const uint64_t xx = ((uint64_t)__float_as_uint(x) << 32) | __float_as_uint(x);
+  const uint64_t ww = ((uint64_t)__float_as_uint(w1) << 32) | __float_as_uint(w0);
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(xx), "l"(ww));
+  a0 = __uint_as_float((uint32_t)a);
+  a1 = __uint_as_float((uint32_t)(a >> 32));
+}
+
 // ---- CTA pairs (cta_group::2): two CTAs of a 2-CTA cluster share one
 // M = 256 MMA stream.  The leader (rank 0) issues every MMA; A rows come from
 // each CTA's own shared memory, the B (N) columns are split between them,
