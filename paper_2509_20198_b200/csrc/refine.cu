@@ -221,11 +221,13 @@ Win unite(const Win& a, const Win& b) {
 __global__ void copy_inputs_kernel(const float* __restrict__ in, int64_t n_win,
                                    float* __restrict__ out, int cstride, int planes,
                                    int y0, int x0, int wy, int wx) {
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n_win;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = w / ((int64_t)wy * wx);
-    const int r = (int)(w - b * wy * wx);
-    const int64_t i = (b * kRes + y0 + r / wx) * kRes + x0 + r % wx;  // pixel
+  // n_win < 2^31 (checked by the caller): 32-bit index math
+  const uint32_t per = (uint32_t)(wy * wx);
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < (uint32_t)n_win;
+       w += gridDim.x * blockDim.x) {
+    const uint32_t b = w / per;
+    const uint32_t r = w - b * per;
+    const int64_t i = ((int64_t)b * kRes + y0 + r / wx) * kRes + x0 + r % wx;  // pixel
     float v[8];
     tcx::ld_v8(in + 8 * i, v);
     if (planes) {  // pre-split channels 0..7 of the fuse input
@@ -844,6 +846,7 @@ extern "C" int ts_refine(const ts_weights* W, const float* d_in, int batch, floa
       const Win& fw = W->fuse_in_win;
       const int wy = fw.y1 - fw.y0, wx = fw.x1 - fw.x0;
       const int64_t px = (int64_t)B * wy * wx;
+      if (px >= (int64_t)INT32_MAX) return TS_E_INVALID;
       ts::count_launch(), copy_inputs_kernel<<<(int)std::min<int64_t>(ceil_div<int64_t>(px, 256), 148 * 16),
                            256, 0, cs>>>(in, px, buf(W->fuse_in_off), W->fuse_in_c,
                                          W->fuse_in_planes ? W->plane_fmt : 0, fw.y0, fw.x0, wy, wx);
