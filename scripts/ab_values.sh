@@ -1,5 +1,5 @@
 # GPU tests, then the bench for each value of an execution switch:
-#   bash scripts/ab_values.sh TS_PHGROUP 1 4
+#   bash scripts/ab_values.sh TS_ENC0 1 0
 V=$1; shift
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/ab_tests.log 2>&1; echo "pytest exit $?"
 tail -3 gpurun_out/ab_tests.log

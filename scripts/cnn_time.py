@@ -38,7 +38,7 @@ def main():
         ms = s.elapsed_time(e) / 10
         print(f"mode {mode}: {ms:.3f} ms / {B} tiles  "
               f"{CROP_GFLOP * B / ms:.1f} TFLOP/s alg  "
-              f"[{os.environ.get('TS_KSPLIT_MIN', 'default')}]", flush=True)
+              f"[{'pair' if os.environ.get('TS_H2_PAIR') == '1' else 'default'}]", flush=True)
 
 
 if __name__ == "__main__":
