@@ -106,3 +106,28 @@ def test_fuzzed_events_monotone_and_budget_safe():
             assert state.stage >= last[pid], "stage regressed"
             last[pid] = state.stage
         events += 1
+
+
+def test_patch_table_views_stay_consistent():
+    """PatchState attributes read and write the engine's patch table once it
+    exists (structure of arrays behind the reference API): values set before
+    the table is built are kept, later writes through either side agree,
+    and replacing the patch dict rebuilds the table."""
+    eng = _fake(4, 4)
+    pids = list(eng.patches)
+    eng.patches[pids[3]].priority = 7.5
+    eng.patches[pids[5]].no_data = True
+    t = eng._table()
+    assert t.priority[3] == 7.5 and bool(t.no_data[5])
+    st = eng.patches[pids[6]]
+    st.stage = Stage.REFINED
+    assert t.stage[6] == Stage.REFINED and st.stage is Stage.REFINED
+    t.in_flight[7] = True
+    assert eng.patches[pids[7]].in_flight is True
+    assert eng.progress()["refined"] == 1 / 16
+    tasks = eng.next_tasks(100)
+    assert all(t_.patch not in (pids[5], pids[6], pids[7]) for t_ in tasks)
+    assert len(tasks) == 13
+    eng.patches = {p: PatchState(key=eng.grid.key(*p), stage=Stage.CHUNK_POINTS_ONLY)
+                   for p in pids}
+    assert len(eng.next_tasks(100)) == 16  # fresh states: a fresh table
