@@ -75,7 +75,7 @@ class TilePool:
     def pick(self, cx: np.ndarray, cy: np.ndarray) -> np.ndarray:
         return (cx * 7919 + cy * 104729) % self.n
 
-    def stage(self, cx: np.ndarray, cy: np.ndarray):
+    def stage(self, cx: np.ndarray, cy: np.ndarray, pin: bool = True):
         """Block staging for the streaming driver: the chosen pool images
         concatenated into a pinned buffer (records NOT yet moved), the
         descriptors, and a pinned int64 (4, n) array (pool tile, image
@@ -85,11 +85,11 @@ class TilePool:
         offs = np.zeros(len(k), np.int64)
         offs[1:] = np.cumsum(al)[:-1]
         total = int(al.sum())
-        pinned = torch.empty(total + D.TileBatch.PAD, dtype=torch.uint8, pin_memory=True)
+        pinned = torch.empty(total + D.TileBatch.PAD, dtype=torch.uint8, pin_memory=pin)
         host = pinned.numpy()
         np.concatenate([self.padded[i] for i in k], out=host[:total])
         host[total:] = 0
-        meta = torch.empty((4, len(k)), dtype=torch.int64, pin_memory=True)
+        meta = torch.empty((4, len(k)), dtype=torch.int64, pin_memory=pin)
         m = meta.numpy()
         m[0], m[1] = k, offs
         m[2] = (cx - self.pos[k, 0]) * self.step[0]
